@@ -1,0 +1,225 @@
+/*
+ * cdr.h — C-ABI of the B200 collocated differentiable renderer (the hot path of
+ * arXiv 2103.15208 as implemented by the reference library "collodiff").
+ *
+ * Plain C types only: pointers, sizes, PODs. Every function returns an int
+ * status (CDR_OK = 0); the message of the last failure on a context is
+ * available from cdr_last_error(). Status codes map 1:1 onto the reference's
+ * exception hierarchy (errors.hpp:8-46):
+ *   CDR_ERR_SIZE_MISMATCH  -> collodiff::SizeMismatch       (errors.hpp:24-26)
+ *   CDR_ERR_NONFINITE      -> collodiff::NonFiniteGradient  (errors.hpp:28-30)
+ *   CDR_ERR_ERROR          -> collodiff::Error              (errors.hpp:8-10)
+ *   CDR_ERR_CUDA / _NO_DEVICE / _INVALID_ARG -> collodiff::Error
+ *
+ * Each entry point names the reference interface it replaces (file:line is
+ * relative to /root/reference/proj). The reference is a C++ static library with
+ * no FFI of its own; its drop-in binding is the C++ shim described in
+ * INTEGRATION.md, which defines the reference symbols on top of these calls.
+ *
+ * Conventions
+ *   - All arithmetic is IEEE fp64 (as the reference); RNG keys are u64.
+ *   - Arrays are row-major and AoS: positions V x 3, uvs V x 2, triangles T x 3,
+ *     edges E x 4 (v0, v1, f0, f1) in the reference's build_adjacency order
+ *     (mesh.cpp:27-63: sorted by (v0, v1), v0 < v1, f1 = -1 on boundary edges).
+ *   - Images are W x H x 3 (pixel (x, y) at (y * W + x) * 3), masks W x H,
+ *     hit caches W x H x spp pixel-major (render.cpp:44-57).
+ *   - Gradients are accumulated (+=) into a caller buffer in ParamLayout order
+ *     (params.cpp:30-43); offsets are given by cdr_layout, -1 = segment absent.
+ *   - Textures are row-major, top-left origin, channels interleaved
+ *     (texture.hpp:11-28). All three maps must share one resolution.
+ *   - "view" arguments are slots into the array given to cdr_set_views; RNG
+ *     streams use the slot's global view id (render.cpp:12, diff_render.cpp:232),
+ *     so results do not depend on how views are sharded across GPUs.
+ */
+#ifndef CDR_H
+#define CDR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CDR_ABI_VERSION 1
+
+enum {
+    CDR_OK = 0,
+    CDR_ERR_SIZE_MISMATCH = 1,
+    CDR_ERR_NONFINITE = 2,
+    CDR_ERR_ERROR = 3,
+    CDR_ERR_CUDA = 4,
+    CDR_ERR_INVALID_ARG = 5,
+    CDR_ERR_NO_DEVICE = 6
+};
+
+enum { CDR_PROBE_RADIANCE = 0, CDR_PROBE_COVERAGE = 1 };  /* diff_render.hpp:38 */
+enum { CDR_LAPLACIAN_COTANGENT = 0, CDR_LAPLACIAN_UNIFORM = 1 }; /* laplacian.hpp:10 */
+
+typedef struct cdr_ctx cdr_ctx;
+
+/* Pinhole camera (camera.hpp:12-23). tan(fov/2) and the aspect ratio are
+ * evaluated on the host exactly as Camera::tan_half_fov (camera.cpp:25-27). */
+typedef struct cdr_camera {
+    double origin[3];
+    double right[3];
+    double up[3];
+    double forward[3];
+    double fov_deg;
+    int32_t width;
+    int32_t height;
+} cdr_camera;
+
+/* RenderSettings (render.hpp:27-35); `threads` has no meaning on the GPU. */
+typedef struct cdr_settings {
+    int32_t spp;
+    int32_t boundary_term;    /* 0/1 */
+    int32_t boundary_samples; /* 0 -> W*H (diff_render.cpp:300-301) */
+    int32_t reserved;
+    uint64_t seed;
+    double gamma;
+} cdr_settings;
+
+/* ParamLayout segment offsets (params.hpp:25-33, params.cpp:30-43). */
+typedef struct cdr_layout {
+    int64_t positions; /* 3V */
+    int64_t diffuse;   /* 3 * texels */
+    int64_t specular;  /* 3 * texels */
+    int64_t roughness; /* texels */
+    int64_t light;     /* 3, or -1 */
+    int64_t total;
+} cdr_layout;
+
+/* SilhouetteSegment (silhouette.hpp:14-21), 128 bytes. */
+typedef struct cdr_segment {
+    int32_t v0, v1;
+    double p0[3], p1[3];
+    double t0, t1;
+    double q0[2], q1[2];
+    double z0, z1;
+    double length_px;
+} cdr_segment;
+
+/* Work counters of the last call (the unit counts of the byte model in
+ * DESIGN.md) and the device time of its stages, in milliseconds. */
+typedef struct cdr_stats {
+    int64_t pixels;
+    int64_t samples;
+    int64_t hit_samples;
+    int64_t adjoint_samples;   /* hit samples whose pixel adjoint is non-zero */
+    int64_t boundary_samples;  /* edge samples drawn */
+    int64_t boundary_active;   /* edge samples that traced their two probes */
+    int64_t segments;
+    int32_t degenerate_skipped;
+    int32_t nonfinite;         /* 1 if a NonFiniteGradient was raised */
+    double ms_prepare;         /* normals + LBVH + t_min */
+    double ms_render;          /* fused trace/shade/loss/interior kernel */
+    double ms_silhouette;
+    double ms_boundary;
+    double ms_finalize;        /* normal chain + position gather + Laplacian */
+    double ms_total;
+} cdr_stats;
+
+int cdr_abi_version(void);
+int cdr_device_count(int* count);
+
+int cdr_create(int device, cdr_ctx** out);
+void cdr_destroy(cdr_ctx* ctx);
+const char* cdr_last_error(const cdr_ctx* ctx);
+/* cudaStream_t the context launches on (for CUDA-event timing by the caller). */
+int cdr_get_stream(cdr_ctx* ctx, void** stream);
+
+/* Mesh + adjacency (mesh.hpp:14-39). edges may be NULL (then built here with
+ * build_adjacency's ordering, mesh.cpp:27-63). Replaces the per-pass setup of
+ * SceneContext / GradContext (render.hpp:44-50, diff_render.hpp:25-31). */
+int cdr_set_mesh(cdr_ctx* ctx, const double* positions, int32_t n_vertices,
+                 const int32_t* triangles, int32_t n_triangles, const double* uvs,
+                 const int32_t* edges, int32_t n_edges);
+/* New positions, same topology (the optimiser's per-iteration apply()). */
+int cdr_update_positions(cdr_ctx* ctx, const double* positions);
+int cdr_get_edges(cdr_ctx* ctx, int32_t* edges_out /* E x 4 */, int32_t* n_edges);
+
+/* MaterialMaps (material.hpp:22-26). */
+int cdr_set_textures(cdr_ctx* ctx, const double* diffuse, const double* specular,
+                     const double* roughness, int32_t width, int32_t height);
+/* CollocatedLight::intensity, Scene::background (scene.hpp:13-23). */
+int cdr_set_light(cdr_ctx* ctx, const double intensity[3], const double background[3]);
+/* Scene::views (scene.hpp:21). global_ids may be NULL (= 0..n-1). */
+int cdr_set_views(cdr_ctx* ctx, const cdr_camera* cameras, const int32_t* global_ids,
+                  int32_t n_views);
+/* Target image of a view slot (W x H x 3) and optional mask (W x H). */
+int cdr_set_target(cdr_ctx* ctx, int32_t view, const double* rgb, const double* mask);
+
+/* vertex_normals (mesh.cpp:65-95). */
+int cdr_vertex_normals(cdr_ctx* ctx, double* normals_out /* V x 3 */);
+
+/* render (render.hpp:67-68, render.cpp:35-64). hit_cache may be NULL. */
+int cdr_render(cdr_ctx* ctx, int32_t view, const cdr_settings* settings, double* rgb_out,
+               double* mask_out, int32_t* hit_cache_out);
+
+/* radiance_at (render.hpp:61-62, render.cpp:24-33) for n continuous pixel
+ * positions xy (n x 2); tri_out (nullable) receives the hit triangle or -1. */
+int cdr_radiance_at(cdr_ctx* ctx, int32_t view, int32_t n, const double* xy, double* rgb_out,
+                    int32_t* tri_out);
+
+/* view_rendering_loss (losses.hpp:37-38, losses.cpp:15-49). target_mask may be
+ * NULL. adjoint_out is W x H x 3. */
+int cdr_view_loss(cdr_ctx* ctx, int32_t width, int32_t height, const double* rendered,
+                  const double* target, const double* target_mask, double lambda_rend,
+                  double gamma, int32_t use_target_mask, double* value_out,
+                  double* adjoint_out);
+
+/* interior_pass (diff_render.hpp:48-50, diff_render.cpp:62-201); += into grad. */
+int cdr_interior_pass(cdr_ctx* ctx, int32_t view, const double* adjoint,
+                      const cdr_settings* settings, const int32_t* hit_cache,
+                      int64_t hit_cache_len, const cdr_layout* layout, double* grad_inout);
+
+/* extract_silhouettes (silhouette.hpp:36, silhouette.cpp:55-106). Writes at most
+ * `capacity` segments; *count receives the full count. */
+int cdr_extract_silhouettes(cdr_ctx* ctx, int32_t view, cdr_segment* segments_out,
+                            int32_t capacity, int32_t* count, double* total_length);
+
+/* boundary_pass (diff_render.hpp:56-59, diff_render.cpp:203-283); += into grad.
+ * segments may be NULL to use this context's own extract_silhouettes. */
+int cdr_boundary_pass(cdr_ctx* ctx, int32_t view, const double* adjoint,
+                      const cdr_segment* segments, int32_t n_segments, int32_t samples,
+                      uint64_t seed, int32_t probe, const cdr_layout* layout,
+                      double* grad_inout, int32_t* degenerate_skipped);
+
+/* Hot subset of total_loss (losses.hpp:94-96, losses.cpp:244-297): for each
+ * listed view slot render -> view_rendering_loss -> interior_pass ->
+ * extract_silhouettes -> boundary_pass, then the Laplacian term
+ * (laplacian.cpp:21-55, losses.cpp:66-78) with lambda_lap (0 disables it).
+ * loss_out[0] = rendering term, loss_out[1] = Laplacian term.
+ * grad_inout (nullable): += of the gradient in `layout` order; when NULL the
+ * gradient stays on the device (cdr_get_grad / cdr_grad_device_ptr).
+ * rendered_rgb / rendered_mask (nullable): n_views images, in call order.
+ * When a communicator is attached (cdr_comm_init), the device gradient and
+ * loss terms are summed across ranks before being returned. */
+int cdr_loss_grad(cdr_ctx* ctx, const int32_t* views, int32_t n_views,
+                  const cdr_settings* settings, double lambda_rend, double lambda_lap,
+                  int32_t laplacian_mode, int32_t use_target_mask, const cdr_layout* layout,
+                  double* loss_out, double* grad_inout, double* rendered_rgb,
+                  double* rendered_mask, cdr_stats* stats);
+int cdr_get_grad(cdr_ctx* ctx, double* grad_out, int64_t n);
+int cdr_grad_device_ptr(cdr_ctx* ctx, void** ptr, int64_t* n);
+
+/* cotangent_laplacian (laplacian.hpp:14-15) as CSC (Eigen's default storage):
+ * outer V+1, inner/values nnz = V + 2E. Any output pointer may be NULL. */
+int cdr_laplacian_matrix(cdr_ctx* ctx, int32_t mode, int32_t* outer, int32_t* inner,
+                         double* values, int64_t* nnz);
+/* laplacian_loss (losses.hpp:53-54, losses.cpp:66-78) on the matrix of `mode`;
+ * grad_positions_inout (V x 3, nullable) receives +=. */
+int cdr_laplacian_loss(cdr_ctx* ctx, int32_t mode, double lambda, double* value_out,
+                       double* grad_positions_inout);
+
+/* Multi-GPU view sharding: one context per GPU/rank, gradient all-reduce over
+ * NCCL (loaded at run time). id is an ncclUniqueId (128 bytes). */
+int cdr_nccl_unique_id(char id_out[128]);
+int cdr_comm_init(cdr_ctx* ctx, const char id[128], int32_t n_ranks, int32_t rank);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CDR_H */
