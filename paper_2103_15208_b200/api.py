@@ -1,0 +1,437 @@
+"""Python host mirror of the reference hot-path API over libcdr.so (ctypes).
+
+The reference is a C++ library; its drop-in is the C-ABI in include/cdr.h
+(see INTEGRATION.md for the C++ shim that defines the collodiff:: symbols on
+top of it). This module is the same boundary seen from Python, used by the
+tests, smoke() and bench.py. Names, argument meaning and error behaviour
+follow the reference:
+
+  Renderer.render             render           (render.hpp:67-68)
+  Renderer.radiance_at        radiance_at      (render.hpp:61-62)
+  Renderer.view_rendering_loss view_rendering_loss (losses.hpp:37-38)
+  Renderer.interior_pass      interior_pass    (diff_render.hpp:48-50)
+  Renderer.extract_silhouettes extract_silhouettes (silhouette.hpp:36)
+  Renderer.boundary_pass      boundary_pass    (diff_render.hpp:56-59)
+  Renderer.grad_image_loss    grad_image_loss  (diff_render.hpp:65-67)
+  Renderer.total_loss         total_loss, hot subset (losses.hpp:94-96)
+  Renderer.cotangent_laplacian / laplacian_loss (laplacian.hpp:14, losses.hpp:53)
+
+Errors raise SizeMismatch / NonFiniteGradient / CollodiffError (errors.hpp).
+There is no CPU fallback: without the built library or a CUDA device every
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .scenes import CAMERA_DTYPE, Scene, camera_struct_array
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libcdr.so")
+
+
+class CollodiffError(RuntimeError):
+    """collodiff::Error (errors.hpp:8-10)."""
+
+
+class SizeMismatch(CollodiffError):
+    """collodiff::SizeMismatch (errors.hpp:24-26)."""
+
+
+class NonFiniteGradient(CollodiffError):
+    """collodiff::NonFiniteGradient (errors.hpp:28-30)."""
+
+
+class NoDevice(CollodiffError):
+    pass
+
+
+_d = C.POINTER(C.c_double)
+_i = C.POINTER(C.c_int32)
+_vp = C.c_void_p
+
+
+class cdr_settings(C.Structure):
+    _fields_ = [("spp", C.c_int32), ("boundary_term", C.c_int32), ("boundary_samples", C.c_int32),
+                ("reserved", C.c_int32), ("seed", C.c_uint64), ("gamma", C.c_double)]
+
+
+class cdr_layout(C.Structure):
+    _fields_ = [("positions", C.c_int64), ("diffuse", C.c_int64), ("specular", C.c_int64),
+                ("roughness", C.c_int64), ("light", C.c_int64), ("total", C.c_int64)]
+
+
+class cdr_stats(C.Structure):
+    _fields_ = [("pixels", C.c_int64), ("samples", C.c_int64), ("hit_samples", C.c_int64),
+                ("adjoint_samples", C.c_int64), ("boundary_samples", C.c_int64),
+                ("boundary_active", C.c_int64), ("segments", C.c_int64),
+                ("degenerate_skipped", C.c_int32), ("nonfinite", C.c_int32),
+                ("ms_prepare", C.c_double), ("ms_render", C.c_double), ("ms_silhouette", C.c_double),
+                ("ms_boundary", C.c_double), ("ms_finalize", C.c_double), ("ms_total", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+SEGMENT_DTYPE = np.dtype([("v0", "<i4"), ("v1", "<i4"), ("p0", "<f8", 3), ("p1", "<f8", 3),
+                          ("t0", "<f8"), ("t1", "<f8"), ("q0", "<f8", 2), ("q1", "<f8", 2),
+                          ("z0", "<f8"), ("z1", "<f8"), ("length_px", "<f8")])
+
+_ERRORS = {1: SizeMismatch, 2: NonFiniteGradient, 3: CollodiffError, 4: CollodiffError,
+           5: CollodiffError, 6: NoDevice}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libcdr.so; raises if it was not built (no silent fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} missing: run `python -m paper_2103_15208_b200.build`")
+    L = C.CDLL(path)
+    L.cdr_last_error.restype = C.c_char_p
+    L.cdr_last_error.argtypes = [_vp]
+    L.cdr_create.argtypes = [C.c_int, C.POINTER(_vp)]
+    L.cdr_destroy.argtypes = [_vp]
+    L.cdr_destroy.restype = None
+    L.cdr_get_stream.argtypes = [_vp, C.POINTER(_vp)]
+    L.cdr_set_mesh.argtypes = [_vp, _d, C.c_int32, _i, C.c_int32, _d, _i, C.c_int32]
+    L.cdr_update_positions.argtypes = [_vp, _d]
+    L.cdr_get_edges.argtypes = [_vp, _i, _i]
+    L.cdr_set_textures.argtypes = [_vp, _d, _d, _d, C.c_int32, C.c_int32]
+    L.cdr_set_light.argtypes = [_vp, _d, _d]
+    L.cdr_set_views.argtypes = [_vp, _vp, _i, C.c_int32]
+    L.cdr_set_target.argtypes = [_vp, C.c_int32, _d, _d]
+    L.cdr_vertex_normals.argtypes = [_vp, _d]
+    L.cdr_render.argtypes = [_vp, C.c_int32, C.POINTER(cdr_settings), _d, _d, _i]
+    L.cdr_radiance_at.argtypes = [_vp, C.c_int32, C.c_int32, _d, _d, _i]
+    L.cdr_view_loss.argtypes = [_vp, C.c_int32, C.c_int32, _d, _d, _d, C.c_double, C.c_double, C.c_int32,
+                                _d, _d]
+    L.cdr_interior_pass.argtypes = [_vp, C.c_int32, _d, C.POINTER(cdr_settings), _i, C.c_int64,
+                                    C.POINTER(cdr_layout), _d]
+    L.cdr_extract_silhouettes.argtypes = [_vp, C.c_int32, _vp, C.c_int32, _i, _d]
+    L.cdr_boundary_pass.argtypes = [_vp, C.c_int32, _d, _vp, C.c_int32, C.c_int32, C.c_uint64, C.c_int32,
+                                    C.POINTER(cdr_layout), _d, _i]
+    L.cdr_loss_grad.argtypes = [_vp, _i, C.c_int32, C.POINTER(cdr_settings), C.c_double, C.c_double,
+                                C.c_int32, C.c_int32, C.POINTER(cdr_layout), _d, _d, _d, _d,
+                                C.POINTER(cdr_stats)]
+    L.cdr_get_grad.argtypes = [_vp, _d, C.c_int64]
+    L.cdr_grad_device_ptr.argtypes = [_vp, C.POINTER(_vp), C.POINTER(C.c_int64)]
+    L.cdr_laplacian_matrix.argtypes = [_vp, C.c_int32, _i, _i, _d, C.POINTER(C.c_int64)]
+    L.cdr_laplacian_loss.argtypes = [_vp, C.c_int32, C.c_double, _d, _d]
+    L.cdr_nccl_unique_id.argtypes = [C.c_char_p]
+    L.cdr_comm_init.argtypes = [_vp, C.c_char_p, C.c_int32, C.c_int32]
+    L.cdr_device_count.argtypes = [C.POINTER(C.c_int)]
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    """Names declared in include/cdr.h (for the load/export test)."""
+    import re
+    hdr = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "cdr.h")
+    src = open(hdr).read()
+    return sorted(set(re.findall(r"\b(cdr_[a-z_0-9]+)\s*\(", src)))
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(_d)
+
+
+def _ip(a):
+    return None if a is None else a.ctypes.data_as(_i)
+
+
+@dataclass
+class RenderSettings:
+    """RenderSettings (render.hpp:27-35)."""
+    spp: int = 4
+    seed: int = 0
+    gamma: float = 2.2
+    boundary_term: bool = True
+    boundary_samples: int = 0
+
+    def c(self):
+        return cdr_settings(int(self.spp), int(bool(self.boundary_term)), int(self.boundary_samples), 0,
+                            int(self.seed) & (2 ** 64 - 1), float(self.gamma))
+
+
+def param_layout(scene: Scene, optimize_light: bool = False) -> dict:
+    """ParamLayout::for_scene (params.cpp:30-43)."""
+    tw, th = scene.tex_res
+    n = tw * th
+    lay, off = {}, 0
+    for name, size in (("positions", 3 * scene.mesh.V), ("diffuse", 3 * n), ("specular", 3 * n),
+                       ("roughness", n)):
+        lay[name] = off
+        off += size
+    lay["light"] = off if optimize_light else -1
+    off += 3 if optimize_light else 0
+    lay["total"] = off
+    return lay
+
+
+def _clayout(lay):
+    return cdr_layout(lay["positions"], lay["diffuse"], lay["specular"], lay["roughness"], lay["light"],
+                      lay["total"])
+
+
+class Renderer:
+    """One GPU context (cdr_ctx) holding a scene: the GradContext equivalent."""
+
+    def __init__(self, device: int = 0, scene: Scene | None = None, view_ids=None):
+        self.L = load_library()
+        h = _vp()
+        rc = self.L.cdr_create(device, C.byref(h))
+        if rc != 0:
+            raise _ERRORS.get(rc, CollodiffError)(f"cdr_create failed with status {rc}")
+        self.h = h
+        self.scene = None
+        if scene is not None:
+            self.set_scene(scene, view_ids)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.cdr_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, rc):
+        if rc != 0:
+            msg = self.L.cdr_last_error(self.h).decode()
+            raise _ERRORS.get(rc, CollodiffError)(msg)
+
+    # ---------------------------------------------------------------- state
+    def set_scene(self, scene: Scene, view_ids=None):
+        self.scene = scene
+        self.set_mesh(scene.mesh)
+        self.set_textures(scene.diffuse, scene.specular, scene.roughness)
+        self.set_light(scene.light, scene.background)
+        self.set_views(scene.cameras, view_ids)
+
+    def set_mesh(self, mesh):
+        self._pos = np.ascontiguousarray(mesh.positions, dtype=np.float64)
+        tris = np.ascontiguousarray(mesh.triangles, dtype=np.int32)
+        uv = None if mesh.uvs is None else np.ascontiguousarray(mesh.uvs, dtype=np.float64)
+        edges = None if mesh.edges is None else np.ascontiguousarray(mesh.edges, dtype=np.int32)
+        self._chk(self.L.cdr_set_mesh(self.h, _dp(self._pos), len(self._pos), _ip(tris), len(tris), _dp(uv),
+                                      _ip(edges), 0 if edges is None else len(edges)))
+        self.V = len(self._pos)
+
+    def update_positions(self, pos):
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        self._chk(self.L.cdr_update_positions(self.h, _dp(pos)))
+
+    def edges(self):
+        n = C.c_int32()
+        self._chk(self.L.cdr_get_edges(self.h, None, C.byref(n)))
+        out = np.zeros((n.value, 4), np.int32)
+        self._chk(self.L.cdr_get_edges(self.h, _ip(out), C.byref(n)))
+        return out
+
+    def set_textures(self, diffuse, specular, roughness):
+        d = np.ascontiguousarray(diffuse, dtype=np.float64)
+        s = np.ascontiguousarray(specular, dtype=np.float64)
+        r = np.ascontiguousarray(roughness, dtype=np.float64)
+        h, w = r.shape[:2]
+        self._chk(self.L.cdr_set_textures(self.h, _dp(d), _dp(s), _dp(r), w, h))
+
+    def set_light(self, intensity, background=(0.0, 0.0, 0.0)):
+        a = np.asarray(intensity, dtype=np.float64)
+        b = np.asarray(background, dtype=np.float64)
+        self._chk(self.L.cdr_set_light(self.h, _dp(a), _dp(b)))
+
+    def set_views(self, cameras, view_ids=None):
+        self._cams = np.ascontiguousarray(camera_struct_array(cameras))
+        ids = None if view_ids is None else np.ascontiguousarray(view_ids, dtype=np.int32)
+        self._chk(self.L.cdr_set_views(self.h, self._cams.ctypes.data_as(_vp), _ip(ids), len(cameras)))
+        self.cameras = list(cameras)
+
+    def set_target(self, view, rgb, mask=None):
+        rgb = np.ascontiguousarray(rgb, dtype=np.float64)
+        mask = None if mask is None else np.ascontiguousarray(mask, dtype=np.float64)
+        self._chk(self.L.cdr_set_target(self.h, view, _dp(rgb), _dp(mask)))
+
+    def stream(self):
+        s = _vp()
+        self._chk(self.L.cdr_get_stream(self.h, C.byref(s)))
+        return s.value
+
+    # ---------------------------------------------------------------- reference API
+    def vertex_normals(self):
+        out = np.zeros((self.V, 3))
+        self._chk(self.L.cdr_vertex_normals(self.h, _dp(out)))
+        return out
+
+    def render(self, view, settings: RenderSettings, want_hits=True):
+        cam = self.cameras[view]
+        W, H = cam.width, cam.height
+        spp = max(1, settings.spp)
+        rgb = np.zeros((H, W, 3))
+        mask = np.zeros((H, W))
+        hit = np.zeros(W * H * spp, np.int32) if want_hits else None
+        st = settings.c()
+        self._chk(self.L.cdr_render(self.h, view, C.byref(st), _dp(rgb), _dp(mask), _ip(hit)))
+        return rgb, mask, hit
+
+    def radiance_at(self, view, xy):
+        xy = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
+        rgb = np.zeros((len(xy), 3))
+        tri = np.zeros(len(xy), np.int32)
+        self._chk(self.L.cdr_radiance_at(self.h, view, len(xy), _dp(xy), _dp(rgb), _ip(tri)))
+        return rgb, tri
+
+    def view_rendering_loss(self, rendered, target, lambda_rend=1.0, gamma=2.2, target_mask=None,
+                            use_target_mask=False):
+        rendered = np.ascontiguousarray(rendered, dtype=np.float64)
+        target = np.ascontiguousarray(target, dtype=np.float64)
+        if rendered.shape != target.shape:
+            raise SizeMismatch("rendered/target size mismatch")
+        H, W = rendered.shape[:2]
+        adj = np.zeros((H, W, 3))
+        v = C.c_double()
+        tm = None if target_mask is None else np.ascontiguousarray(target_mask, dtype=np.float64)
+        self._chk(self.L.cdr_view_loss(self.h, W, H, _dp(rendered), _dp(target), _dp(tm), lambda_rend, gamma,
+                                       int(use_target_mask), C.byref(v), _dp(adj)))
+        return v.value, adj
+
+    def interior_pass(self, view, adjoint, settings: RenderSettings, hit_cache, layout, grad=None):
+        g = np.zeros(layout["total"]) if grad is None else grad
+        adjoint = np.ascontiguousarray(adjoint, dtype=np.float64)
+        cam = self.cameras[view]
+        if adjoint.shape[:2] != (cam.height, cam.width):
+            raise SizeMismatch("adjoint size does not match view")
+        hc = np.ascontiguousarray(hit_cache, dtype=np.int32)
+        st = settings.c()
+        lay = _clayout(layout)
+        self._chk(self.L.cdr_interior_pass(self.h, view, _dp(adjoint), C.byref(st), _ip(hc), len(hc),
+                                           C.byref(lay), _dp(g)))
+        return g
+
+    def extract_silhouettes(self, view):
+        n = C.c_int32()
+        tot = C.c_double()
+        self._chk(self.L.cdr_extract_silhouettes(self.h, view, None, 0, C.byref(n), C.byref(tot)))
+        out = np.zeros(n.value, SEGMENT_DTYPE)
+        self._chk(self.L.cdr_extract_silhouettes(self.h, view, out.ctypes.data_as(_vp), n.value, C.byref(n),
+                                                 C.byref(tot)))
+        return out, tot.value
+
+    def boundary_pass(self, view, adjoint, samples, seed, layout, segments=None, probe=0, grad=None):
+        g = np.zeros(layout["total"]) if grad is None else grad
+        adjoint = np.ascontiguousarray(adjoint, dtype=np.float64)
+        cam = self.cameras[view]
+        if adjoint.shape[:2] != (cam.height, cam.width):
+            raise SizeMismatch("adjoint size does not match view")
+        lay = _clayout(layout)
+        deg = C.c_int32()
+        segp, nseg = None, 0
+        if segments is not None:
+            segments = np.ascontiguousarray(segments, dtype=SEGMENT_DTYPE)
+            segp, nseg = segments.ctypes.data_as(_vp), len(segments)
+        self._chk(self.L.cdr_boundary_pass(self.h, view, _dp(adjoint), segp, nseg, samples, seed & (2 ** 64 - 1),
+                                           probe, C.byref(lay), _dp(g), C.byref(deg)))
+        return g, deg.value
+
+    def loss_grad(self, views, settings: RenderSettings, layout, lambda_rend=1.0, lambda_lap=0.1,
+                  laplacian_mode=0, use_target_mask=False, grad=None, want_rendered=False, device_only=False):
+        """Hot subset of total_loss over `views` (slots). Returns (loss[2], grad, stats, rendered)."""
+        views = np.ascontiguousarray(views, dtype=np.int32)
+        st = settings.c()
+        lay = _clayout(layout)
+        loss = np.zeros(2)
+        g = None if device_only else (np.zeros(layout["total"]) if grad is None else grad)
+        rend = None
+        if want_rendered:
+            npx = sum(self.cameras[v].width * self.cameras[v].height for v in views)
+            rend = np.zeros(3 * npx)
+        stats = cdr_stats()
+        self._chk(self.L.cdr_loss_grad(self.h, _ip(views), len(views), C.byref(st), lambda_rend, lambda_lap,
+                                       laplacian_mode, int(use_target_mask), C.byref(lay), _dp(loss), _dp(g),
+                                       _dp(rend), None, C.byref(stats)))
+        return loss, g, stats, rend
+
+    def total_loss(self, targets, settings: RenderSettings, layout, lambda_rend=1.0, lambda_lap=0.1,
+                   laplacian_mode=0, use_target_masks=False, target_masks=None):
+        """total_loss (losses.cpp:244-297) with the out-of-scope regularisers at
+        weight zero: breakdown {rend, lap, total}, fresh gradient, rendered images."""
+        if len(targets) != len(self.cameras):
+            raise SizeMismatch("target count does not match views")
+        for k, t in enumerate(targets):
+            self.set_target(k, t, None if target_masks is None else target_masks[k])
+        loss, g, stats, rend = self.loss_grad(np.arange(len(self.cameras)), settings, layout, lambda_rend,
+                                              lambda_lap, laplacian_mode, use_target_masks, want_rendered=True)
+        rendered, off = [], 0
+        for cam in self.cameras:
+            n = cam.width * cam.height * 3
+            rendered.append(rend[off:off + n].reshape(cam.height, cam.width, 3))
+            off += n
+        bd = {"rend": loss[0], "lap": loss[1], "total": loss[0] + loss[1]}
+        return bd, g, rendered
+
+    def grad_image_loss(self, view, target, settings: RenderSettings, lambda_rend, use_target_mask, layout,
+                        grad=None, target_mask=None):
+        """grad_image_loss (diff_render.cpp:285-305): one view, no Laplacian."""
+        self.set_target(view, target, target_mask)
+        loss, g, _, _ = self.loss_grad([view], settings, layout, lambda_rend, 0.0, 0, use_target_mask, grad=grad)
+        return loss[0], g
+
+    def cotangent_laplacian(self, mode=0):
+        nnz = C.c_int64()
+        self._chk(self.L.cdr_laplacian_matrix(self.h, mode, None, None, None, C.byref(nnz)))
+        outer = np.zeros(self.V + 1, np.int32)
+        inner = np.zeros(nnz.value, np.int32)
+        vals = np.zeros(nnz.value)
+        self._chk(self.L.cdr_laplacian_matrix(self.h, mode, _ip(outer), _ip(inner), _dp(vals), C.byref(nnz)))
+        return outer, inner, vals
+
+    def laplacian_loss(self, mode=0, lam=0.1):
+        g = np.zeros((self.V, 3))
+        v = C.c_double()
+        self._chk(self.L.cdr_laplacian_loss(self.h, mode, lam, C.byref(v), _dp(g)))
+        return v.value, g
+
+    def grad_device(self):
+        p = _vp()
+        n = C.c_int64()
+        self._chk(self.L.cdr_grad_device_ptr(self.h, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def get_grad(self, n):
+        out = np.zeros(n)
+        self._chk(self.L.cdr_get_grad(self.h, _dp(out), n))
+        return out
+
+    # ---------------------------------------------------------------- multi-GPU
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        L = load_library()
+        buf = C.create_string_buffer(128)
+        rc = L.cdr_nccl_unique_id(buf)
+        if rc != 0:
+            raise CollodiffError("ncclGetUniqueId failed (NCCL not loadable?)")
+        return buf.raw
+
+    def comm_init(self, uid: bytes, n_ranks: int, rank: int):
+        self._chk(self.L.cdr_comm_init(self.h, C.c_char_p(uid), n_ranks, rank))
+
+
+def device_count() -> int:
+    L = load_library()
+    n = C.c_int()
+    L.cdr_device_count(C.byref(n))
+    return n.value
+
+
+__all__ = ["Renderer", "RenderSettings", "param_layout", "SizeMismatch", "NonFiniteGradient", "CollodiffError",
+           "load_library", "SEGMENT_DTYPE", "CAMERA_DTYPE", "device_count"]

@@ -1,0 +1,893 @@
+// api.cu — the C-ABI of include/cdr.h over the sm_100a kernels.
+//
+// Host-side work here is bookkeeping only (validation, topology tables built
+// once per set_mesh, uploads/downloads); every per-sample, per-edge and
+// per-vertex computation of the hot path runs in the kernels of prepare.cu,
+// render.cu, boundary.cu and finalize.cu. There is no CPU fallback: without a
+// CUDA device every call fails with CDR_ERR_NO_DEVICE / CDR_ERR_CUDA.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+using namespace cdr;
+
+namespace {
+
+struct SizeMismatchErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ApiErr : std::runtime_error {
+    int code;
+    ApiErr(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+int handle(cdr_ctx* c, const std::function<void()>& fn);
+
+#define API_BEGIN(ctx)                                            \
+    if (!(ctx)) return CDR_ERR_INVALID_ARG;                       \
+    return handle((ctx), [&]() {
+#define API_END \
+    });
+
+int handle(cdr_ctx* c, const std::function<void()>& fn) {
+    try {
+        if (cudaSetDevice(c->device) != cudaSuccess) throw ApiErr(CDR_ERR_NO_DEVICE, "cudaSetDevice failed");
+        fn();
+        c->err.clear();
+        return CDR_OK;
+    } catch (const SizeMismatchErr& e) {
+        c->err = e.what();
+        return CDR_ERR_SIZE_MISMATCH;
+    } catch (const ApiErr& e) {
+        c->err = e.what();
+        return e.code;
+    } catch (const CudaError& e) {
+        c->err = e.what();
+        return CDR_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        c->err = "out of device or host memory";
+        return CDR_ERR_CUDA;
+    } catch (const std::exception& e) {
+        c->err = e.what();
+        return CDR_ERR_ERROR;
+    }
+}
+
+template <typename T>
+void h2d(DBuf<T>& b, const T* src, size_t n, cudaStream_t s) {
+    b.ensure(std::max<size_t>(1, n));
+    if (n) CDR_CUDA_CHECK(cudaMemcpyAsync(b.p, src, sizeof(T) * n, cudaMemcpyHostToDevice, s));
+}
+
+void sync(cdr_ctx* c) { CDR_CUDA_CHECK(cudaStreamSynchronize(c->stream)); }
+
+double cam_abs_max(const cdr_ctx* c) {
+    double m = 0;
+    for (const auto& v : c->views)
+        for (int k = 0; k < 3; ++k) m = std::max(m, std::fabs(v.cam.o[k]));
+    return m;
+}
+
+void ensure_prepared(cdr_ctx* c, bool force = false) {
+    if (!force && !c->geometry_dirty) return;
+    launch_prepare(c, cam_abs_max(c));
+    c->geometry_dirty = false;
+}
+
+void check_view(const cdr_ctx* c, int view) {
+    if (view < 0 || view >= int(c->views.size()))
+        throw ApiErr(CDR_ERR_INVALID_ARG, "view slot " + std::to_string(view) + " out of range");
+}
+
+void check_ready(const cdr_ctx* c) {
+    if (c->T > 0 && c->tw <= 0) throw ApiErr(CDR_ERR_INVALID_ARG, "textures not set");
+}
+
+int spp_of(const cdr_settings* s) { return std::max(1, s->spp); }
+
+void check_spp(int spp) {
+    if (spp > 256)
+        throw ApiErr(CDR_ERR_INVALID_ARG, "spp > 256 is not supported by the fused kernel");
+}
+
+RenderArgs render_args(const cdr_ctx* c, const cdr_settings* s, const cdr_layout* lay) {
+    RenderArgs a{};
+    a.spp = spp_of(s);
+    a.k = int(std::lround(std::sqrt(double(a.spp))));  // render.cpp:15
+    a.seed = s->seed;
+    a.gamma = s->gamma;
+    a.write_hits = 1;
+    if (lay) {
+        a.lay_diffuse = lay->diffuse;
+        a.lay_specular = lay->specular;
+        a.lay_roughness = lay->roughness;
+        a.lay_light = lay->light;
+    } else {
+        a.lay_diffuse = a.lay_specular = a.lay_roughness = a.lay_light = -1;
+    }
+    (void)c;
+    return a;
+}
+
+void check_layout(const cdr_ctx* c, const cdr_layout* lay) {
+    if (!lay) throw ApiErr(CDR_ERR_INVALID_ARG, "layout is null");
+    int64_t n = int64_t(c->tw) * c->th;
+    auto seg = [&](int64_t off, int64_t size, const char* name) {
+        if (off < 0 || off + size > lay->total)
+            throw SizeMismatchErr(std::string("gradient layout segment ") + name + " out of range");
+    };
+    seg(lay->positions, 3 * int64_t(c->V), "positions");
+    seg(lay->diffuse, 3 * n, "diffuse");
+    seg(lay->specular, 3 * n, "specular");
+    seg(lay->roughness, n, "roughness");
+    if (lay->light >= 0) seg(lay->light, 3, "light");
+}
+
+void zero_grad(cdr_ctx* c, int64_t total) {
+    c->grad.ensure(std::max<int64_t>(1, total));
+    c->grad_n = total;
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->grad.p, 0, sizeof(double) * std::max<int64_t>(1, total), c->stream));
+    c->corner_acc.ensure(std::max<size_t>(1, size_t(c->T) * 18));
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->corner_acc.p, 0, sizeof(double) * std::max<size_t>(1, size_t(c->T) * 18),
+                                   c->stream));
+}
+
+void reset_flags(cdr_ctx* c) {
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->errinfo.p, 0, sizeof(ErrorInfo), c->stream));
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->counters.p, 0, sizeof(Counters), c->stream));
+}
+
+void raise_device_error(cdr_ctx* c) {
+    ErrorInfo e;
+    CDR_CUDA_CHECK(cudaMemcpy(&e, c->errinfo.p, sizeof(e), cudaMemcpyDeviceToHost));
+    if (e.flag == 1)
+        throw ApiErr(CDR_ERR_NONFINITE, "non-finite interior gradient at pixel (" + std::to_string(e.x) + "," +
+                                            std::to_string(e.y) + ")");
+    if (e.flag == 2)
+        throw ApiErr(CDR_ERR_NONFINITE, "non-finite boundary gradient at segment " + std::to_string(e.segment));
+}
+
+// D2H of a device gradient slice and += into the caller's host buffer.
+void add_grad_to_host(cdr_ctx* c, double* host, int64_t off, int64_t n) {
+    if (!host || n <= 0) return;
+    std::vector<double> tmp(n);
+    CDR_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), c->grad.p + off, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                   c->stream));
+    sync(c);
+    for (int64_t i = 0; i < n; ++i) host[off + i] += tmp[i];
+}
+
+void ensure_hit_arena(cdr_ctx* c, int spp) {
+    c->hit.ensure(std::max<size_t>(1, c->total_pixels * size_t(spp)));
+}
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+    void* h = nullptr;
+    int (*getUniqueId)(void*) = nullptr;
+    int (*commInitRank)(void**, int, const void* /* by value 128B */, int) = nullptr;
+    int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*commDestroy)(void*) = nullptr;
+    const char* (*getErrorString)(int) = nullptr;
+    bool ok = false;
+};
+
+struct NcclUid {
+    char internal[128];
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+        api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+        if (api.h) break;
+    }
+    if (!api.h) return api;
+    api.getUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclGetUniqueId"));
+    api.commInitRank = reinterpret_cast<int (*)(void**, int, const void*, int)>(dlsym(api.h, "ncclCommInitRank"));
+    api.allReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+        dlsym(api.h, "ncclAllReduce"));
+    api.commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclCommDestroy"));
+    api.getErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(api.h, "ncclGetErrorString"));
+    api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy;
+    return api;
+}
+
+using CommInitByValue = int (*)(void**, int, NcclUid, int);
+
+void nccl_check(int r, const char* what) {
+    if (r != 0) {
+        const char* m = nccl().getErrorString ? nccl().getErrorString(r) : "?";
+        throw ApiErr(CDR_ERR_ERROR, std::string(what) + ": " + m);
+    }
+}
+
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+
+}  // namespace
+
+extern "C" {
+
+int cdr_abi_version(void) { return CDR_ABI_VERSION; }
+
+int cdr_device_count(int* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (count) *count = e == cudaSuccess ? n : 0;
+    return e == cudaSuccess ? CDR_OK : CDR_ERR_NO_DEVICE;
+}
+
+int cdr_create(int device, cdr_ctx** out) {
+    if (!out) return CDR_ERR_INVALID_ARG;
+    *out = nullptr;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return CDR_ERR_NO_DEVICE;
+    if (device < 0 || device >= n) return CDR_ERR_INVALID_ARG;
+    auto c = std::make_unique<cdr_ctx>();
+    c->device = device;
+    try {
+        CDR_CUDA_CHECK(cudaSetDevice(device));
+        CDR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->errinfo.ensure(1);
+        c->counters.ensure(1);
+        c->info.ensure(1);
+        c->ev.resize(8);
+        for (auto& e : c->ev) CDR_CUDA_CHECK(cudaEventCreate(&e));
+    } catch (...) {
+        return CDR_ERR_CUDA;
+    }
+    *out = c.release();
+    return CDR_OK;
+}
+
+void cdr_destroy(cdr_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->nccl_comm && nccl().ok) nccl().commDestroy(c->nccl_comm);
+    cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev) cudaEventDestroy(e);
+    // DBufs are released with the process/context; free the big ones explicitly
+    c->pos.release(); c->uv.release(); c->normals.release(); c->accum.release(); c->fnormal.release();
+    c->tris.release(); c->edges.release(); c->vf_start.release(); c->vf_list.release();
+    c->lap_rowptr.release(); c->lap_col.release(); c->lap_edge_slot.release(); c->lap_diag_slot.release();
+    c->lap_val.release(); c->lap_lv.release(); c->lap_grad.release(); c->lap_partial.release();
+    c->info.release(); c->bbox_partial.release(); c->keys.release(); c->keys_alt.release();
+    c->sort_tmp.release(); c->parent_internal.release(); c->parent_leaf.release(); c->refit_flag.release();
+    c->node_box.release(); c->nodes.release(); c->recs.release(); c->tex.release(); c->d_cams.release();
+    c->target.release(); c->target_mask.release(); c->img.release(); c->mask.release(); c->adj.release();
+    c->hit.release(); c->sil_flag.release(); c->sil_block_count.release(); c->sil_block_off.release();
+    c->sil_count.release(); c->segs.release(); c->cdf.release(); c->total_len.release();
+    c->degenerate.release(); c->grad.release(); c->corner_acc.release(); c->qvec.release();
+    c->loss_acc.release(); c->errinfo.release(); c->counters.release();
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* cdr_last_error(const cdr_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int cdr_get_stream(cdr_ctx* c, void** stream) {
+    if (!c || !stream) return CDR_ERR_INVALID_ARG;
+    *stream = reinterpret_cast<void*>(c->stream);
+    return CDR_OK;
+}
+
+int cdr_set_mesh(cdr_ctx* c, const double* positions, int32_t nv, const int32_t* triangles, int32_t nt,
+                 const double* uvs, const int32_t* edges, int32_t ne) {
+    API_BEGIN(c)
+    if (nv < 0 || nt < 0 || (nv > 0 && !positions) || (nt > 0 && !triangles))
+        throw ApiErr(CDR_ERR_INVALID_ARG, "bad mesh arguments");
+    // build_adjacency validation (mesh.cpp:27-38)
+    for (int f = 0; f < nt; ++f) {
+        const int32_t* t = triangles + 3 * f;
+        for (int k = 0; k < 3; ++k)
+            if (t[k] < 0 || t[k] >= nv)
+                throw ApiErr(CDR_ERR_ERROR, "triangle " + std::to_string(f) + " references vertex " +
+                                                std::to_string(t[k]) + " out of range");
+        if (t[0] == t[1] || t[1] == t[2] || t[0] == t[2])
+            throw ApiErr(CDR_ERR_ERROR, "triangle " + std::to_string(f) + " repeats a vertex");
+    }
+    c->V = nv;
+    c->T = nt;
+    c->h_tris.assign(triangles, triangles + 3 * size_t(nt));
+    // edges: caller's (reference order) or rebuilt with build_adjacency's order
+    if (edges) {
+        if (ne < 0) throw ApiErr(CDR_ERR_INVALID_ARG, "negative edge count");
+        c->h_edges.assign(edges, edges + 4 * size_t(ne));
+    } else {
+        std::vector<std::pair<int64_t, int>> keys;
+        keys.reserve(3 * size_t(nt));
+        for (int f = 0; f < nt; ++f)
+            for (int k = 0; k < 3; ++k) {
+                int a = triangles[3 * f + k], b = triangles[3 * f + (k + 1) % 3];
+                keys.push_back({int64_t(std::min(a, b)) * nv + std::max(a, b), f});
+            }
+        std::sort(keys.begin(), keys.end());
+        c->h_edges.clear();
+        for (size_t i = 0; i < keys.size();) {
+            size_t j = i;
+            while (j < keys.size() && keys[j].first == keys[i].first) ++j;
+            int64_t key = keys[i].first;
+            if (j - i > 2)
+                throw ApiErr(CDR_ERR_ERROR, "non-manifold edge (" + std::to_string(key / nv) + "," +
+                                                std::to_string(key % nv) + ") with " + std::to_string(j - i) +
+                                                " incident faces");
+            c->h_edges.push_back(int32_t(key / nv));
+            c->h_edges.push_back(int32_t(key % nv));
+            c->h_edges.push_back(keys[i].second);
+            c->h_edges.push_back(j - i > 1 ? keys[i + 1].second : -1);
+            i = j;
+        }
+    }
+    c->E = int(c->h_edges.size() / 4);
+    cudaStream_t s = c->stream;
+    h2d(c->pos, positions, 3 * size_t(nv), s);
+    c->has_uv = uvs != nullptr;
+    if (uvs) h2d(c->uv, uvs, 2 * size_t(nv), s);
+    h2d(c->tris, triangles, 3 * size_t(nt), s);
+    h2d(c->edges, reinterpret_cast<const int4*>(c->h_edges.data()), size_t(c->E), s);
+    // vertex -> (face*3+corner), ascending face (the reference's face-loop order)
+    std::vector<int32_t> vstart(size_t(nv) + 1, 0), vlist(3 * size_t(nt));
+    for (int f = 0; f < nt; ++f)
+        for (int k = 0; k < 3; ++k) vstart[triangles[3 * f + k] + 1]++;
+    for (int v = 0; v < nv; ++v) vstart[v + 1] += vstart[v];
+    {
+        std::vector<int32_t> fill(vstart.begin(), vstart.end() - 1);
+        for (int f = 0; f < nt; ++f)
+            for (int k = 0; k < 3; ++k) vlist[fill[triangles[3 * f + k]]++] = 3 * f + k;
+    }
+    h2d(c->vf_start, vstart.data(), vstart.size(), s);
+    h2d(c->vf_list, vlist.data(), vlist.size(), s);
+    // Laplacian CSR pattern: row i = sorted {neighbours} ∪ {i}
+    std::vector<std::vector<int32_t>> nb(nv);
+    for (int e = 0; e < c->E; ++e) {
+        int a = c->h_edges[4 * e], b = c->h_edges[4 * e + 1];
+        if (a < 0 || a >= nv || b < 0 || b >= nv) throw ApiErr(CDR_ERR_INVALID_ARG, "edge vertex out of range");
+        nb[a].push_back(b);
+        nb[b].push_back(a);
+    }
+    std::vector<int32_t> rowptr(size_t(nv) + 1, 0), col, dslot(nv);
+    col.reserve(size_t(nv) + 2 * size_t(c->E));
+    for (int i = 0; i < nv; ++i) {
+        nb[i].push_back(i);
+        std::sort(nb[i].begin(), nb[i].end());
+        for (int32_t j : nb[i]) {
+            if (j == i) dslot[i] = int32_t(col.size());
+            col.push_back(j);
+        }
+        rowptr[i + 1] = int32_t(col.size());
+    }
+    std::vector<int2> eslot(c->E);
+    for (int e = 0; e < c->E; ++e) {
+        int a = c->h_edges[4 * e], b = c->h_edges[4 * e + 1];
+        auto find = [&](int row, int cc) {
+            auto it = std::lower_bound(col.begin() + rowptr[row], col.begin() + rowptr[row + 1], cc);
+            return int32_t(it - col.begin());
+        };
+        eslot[e] = make_int2(find(a, b), find(b, a));
+    }
+    h2d(c->lap_rowptr, rowptr.data(), rowptr.size(), s);
+    h2d(c->lap_col, col.data(), col.size(), s);
+    h2d(c->lap_diag_slot, dslot.data(), dslot.size(), s);
+    h2d(c->lap_edge_slot, eslot.data(), eslot.size(), s);
+    c->lap_val.ensure(std::max<size_t>(1, col.size()));
+    c->normals.ensure(3 * size_t(std::max(1, nv)));
+    c->accum.ensure(3 * size_t(std::max(1, nv)));
+    c->fnormal.ensure(3 * size_t(std::max(1, nt)));
+    c->geometry_dirty = true;
+    sync(c);
+    API_END
+}
+
+int cdr_update_positions(cdr_ctx* c, const double* positions) {
+    API_BEGIN(c)
+    if (!positions && c->V > 0) throw ApiErr(CDR_ERR_INVALID_ARG, "positions is null");
+    if (c->V > 0)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(c->pos.p, positions, sizeof(double) * 3 * size_t(c->V),
+                                       cudaMemcpyHostToDevice, c->stream));
+    c->geometry_dirty = true;
+    API_END
+}
+
+int cdr_get_edges(cdr_ctx* c, int32_t* out, int32_t* n) {
+    API_BEGIN(c)
+    if (n) *n = c->E;
+    if (out) std::memcpy(out, c->h_edges.data(), sizeof(int32_t) * c->h_edges.size());
+    API_END
+}
+
+int cdr_set_textures(cdr_ctx* c, const double* diffuse, const double* specular, const double* roughness,
+                     int32_t w, int32_t h) {
+    API_BEGIN(c)
+    if (w <= 0 || h <= 0 || !diffuse || !specular || !roughness)
+        throw ApiErr(CDR_ERR_INVALID_ARG, "bad texture arguments");
+    size_t n = size_t(w) * h;
+    c->tw = w;
+    c->th = h;
+    c->tex.ensure(n);
+    // fp64 inputs are staged on the device and packed into fp32 texel records
+    static thread_local DBuf<double> sd, ss, sr;
+    h2d(sd, diffuse, 3 * n, c->stream);
+    h2d(ss, specular, 3 * n, c->stream);
+    h2d(sr, roughness, n, c->stream);
+    launch_pack_textures(c, sd.p, ss.p, sr.p, int(n));
+    sync(c);
+    API_END
+}
+
+int cdr_set_light(cdr_ctx* c, const double intensity[3], const double background[3]) {
+    API_BEGIN(c)
+    for (int i = 0; i < 3; ++i) {
+        if (intensity) c->light[i] = intensity[i];
+        if (background) c->background[i] = background[i];
+    }
+    API_END
+}
+
+int cdr_set_views(cdr_ctx* c, const cdr_camera* cams, const int32_t* gids, int32_t n) {
+    API_BEGIN(c)
+    if (n < 0 || (n > 0 && !cams)) throw ApiErr(CDR_ERR_INVALID_ARG, "bad views");
+    c->views.assign(n, ViewData{});
+    size_t off = 0;
+    std::vector<DevCamera> dc(n);
+    for (int i = 0; i < n; ++i) {
+        const cdr_camera& k = cams[i];
+        if (k.width <= 0 || k.height <= 0) throw ApiErr(CDR_ERR_INVALID_ARG, "bad view size");
+        DevCamera& d = dc[i];
+        std::memset(&d, 0, sizeof(d));
+        for (int j = 0; j < 3; ++j) {
+            d.o[j] = k.origin[j];
+            d.r[j] = k.right[j];
+            d.u[j] = k.up[j];
+            d.f[j] = k.forward[j];
+        }
+        d.th = std::tan(k.fov_deg * 3.14159265358979323846 / 360.0);  // camera.cpp:25-27
+        d.aspect = double(k.width) / double(k.height);                 // camera.hpp:22
+        d.W = k.width;
+        d.H = k.height;
+        d.gid = gids ? gids[i] : i;
+        c->views[i].cam = d;
+        c->views[i].pix_off = off;
+        off += size_t(k.width) * k.height;
+    }
+    c->total_pixels = off;
+    h2d(c->d_cams, dc.data(), dc.size(), c->stream);
+    size_t np = std::max<size_t>(1, off);
+    c->img.ensure(3 * np);
+    c->mask.ensure(np);
+    c->adj.ensure(3 * np);
+    c->target.ensure(3 * np);
+    c->target_mask.ensure(np);
+    c->loss_acc.ensure(std::max(1, n));
+    sync(c);
+    API_END
+}
+
+int cdr_set_target(cdr_ctx* c, int32_t view, const double* rgb, const double* mask) {
+    API_BEGIN(c)
+    check_view(c, view);
+    if (!rgb) throw ApiErr(CDR_ERR_INVALID_ARG, "target rgb is null");
+    ViewData& v = c->views[view];
+    size_t np = size_t(v.cam.W) * v.cam.H;
+    CDR_CUDA_CHECK(cudaMemcpyAsync(c->target.p + 3 * v.pix_off, rgb, sizeof(double) * 3 * np,
+                                   cudaMemcpyHostToDevice, c->stream));
+    v.has_target = true;
+    v.has_target_mask = mask != nullptr;
+    v.target_mask_sum = 0;
+    if (mask) {
+        for (size_t i = 0; i < np; ++i) v.target_mask_sum += mask[i];  // losses.cpp:26 order
+        CDR_CUDA_CHECK(cudaMemcpyAsync(c->target_mask.p + v.pix_off, mask, sizeof(double) * np,
+                                       cudaMemcpyHostToDevice, c->stream));
+    }
+    sync(c);
+    API_END
+}
+
+int cdr_vertex_normals(cdr_ctx* c, double* out) {
+    API_BEGIN(c)
+    ensure_prepared(c);
+    if (c->V > 0 && out)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(out, c->normals.p, sizeof(double) * 3 * c->V, cudaMemcpyDeviceToHost,
+                                       c->stream));
+    sync(c);
+    API_END
+}
+
+int cdr_render(cdr_ctx* c, int32_t view, const cdr_settings* st, double* rgb, double* mask, int32_t* hit) {
+    API_BEGIN(c)
+    check_view(c, view);
+    check_ready(c);
+    if (!st) throw ApiErr(CDR_ERR_INVALID_ARG, "settings is null");
+    int spp = spp_of(st);
+    check_spp(spp);
+    ensure_prepared(c);
+    ensure_hit_arena(c, spp);
+    reset_flags(c);
+    RenderArgs a = render_args(c, st, nullptr);
+    a.write_hits = hit != nullptr;
+    int slot = view;
+    launch_render(c, &slot, 1, a, true, false, false, nullptr);
+    const ViewData& v = c->views[view];
+    size_t np = size_t(v.cam.W) * v.cam.H;
+    if (rgb)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(rgb, c->img.p + 3 * v.pix_off, sizeof(double) * 3 * np,
+                                       cudaMemcpyDeviceToHost, c->stream));
+    if (mask)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(mask, c->mask.p + v.pix_off, sizeof(double) * np, cudaMemcpyDeviceToHost,
+                                       c->stream));
+    if (hit)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(hit, c->hit.p + v.pix_off * spp, sizeof(int32_t) * np * spp,
+                                       cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+int cdr_radiance_at(cdr_ctx* c, int32_t view, int32_t n, const double* xy, double* rgb, int32_t* tri) {
+    API_BEGIN(c)
+    check_view(c, view);
+    check_ready(c);
+    if (n <= 0) return;
+    ensure_prepared(c);
+    static thread_local DBuf<double> dxy, drgb;
+    static thread_local DBuf<int32_t> dtri;
+    h2d(dxy, xy, 2 * size_t(n), c->stream);
+    drgb.ensure(3 * size_t(n));
+    dtri.ensure(n);
+    launch_radiance_points(c, view, n, dxy.p, drgb.p, dtri.p);
+    CDR_CUDA_CHECK(cudaMemcpyAsync(rgb, drgb.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (tri) CDR_CUDA_CHECK(cudaMemcpyAsync(tri, dtri.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+int cdr_view_loss(cdr_ctx* c, int32_t w, int32_t h, const double* rendered, const double* target,
+                  const double* tmask, double lambda, double gamma, int32_t use_mask, double* value,
+                  double* adjoint) {
+    API_BEGIN(c)
+    if (w <= 0 || h <= 0 || !rendered || !target || !adjoint)
+        throw ApiErr(CDR_ERR_INVALID_ARG, "bad view_loss arguments");
+    size_t np = size_t(w) * h;
+    if (value) *value = 0;
+    std::memset(adjoint, 0, sizeof(double) * 3 * np);
+    if (lambda == 0) return;  // losses.cpp:21
+    const bool masked = use_mask && tmask;
+    double n_valid = 0;
+    if (masked) {
+        for (size_t i = 0; i < np; ++i) n_valid += tmask[i];
+        if (n_valid <= 0) return;
+    } else {
+        n_valid = double(w) * h;
+    }
+    const double scale = lambda / n_valid;
+    static thread_local DBuf<double> dr, dt, dm, da, ds;
+    h2d(dr, rendered, 3 * np, c->stream);
+    h2d(dt, target, 3 * np, c->stream);
+    if (masked) h2d(dm, tmask, np, c->stream);
+    da.ensure(3 * np);
+    ds.ensure(1);
+    CDR_CUDA_CHECK(cudaMemsetAsync(ds.p, 0, sizeof(double), c->stream));
+    launch_view_loss(c, w, h, dr.p, dt.p, masked ? dm.p : nullptr, scale, gamma, masked ? 1 : 0, da.p, ds.p);
+    double sum = 0;
+    CDR_CUDA_CHECK(cudaMemcpyAsync(adjoint, da.p, sizeof(double) * 3 * np, cudaMemcpyDeviceToHost, c->stream));
+    CDR_CUDA_CHECK(cudaMemcpyAsync(&sum, ds.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (value) *value = scale * sum;
+    API_END
+}
+
+int cdr_interior_pass(cdr_ctx* c, int32_t view, const double* adjoint, const cdr_settings* st,
+                      const int32_t* hit_cache, int64_t hit_len, const cdr_layout* lay, double* grad) {
+    API_BEGIN(c)
+    check_view(c, view);
+    check_ready(c);
+    check_layout(c, lay);
+    if (!st || !adjoint || !grad) throw ApiErr(CDR_ERR_INVALID_ARG, "null argument");
+    const ViewData& v = c->views[view];
+    const int spp = spp_of(st);
+    check_spp(spp);
+    size_t np = size_t(v.cam.W) * v.cam.H;
+    if (!hit_cache || hit_len != int64_t(np) * spp)  // diff_render.cpp:69-70
+        throw SizeMismatchErr("hit cache does not match view and spp");
+    ensure_prepared(c);
+    ensure_hit_arena(c, spp);
+    CDR_CUDA_CHECK(cudaMemcpyAsync(c->adj.p + 3 * v.pix_off, adjoint, sizeof(double) * 3 * np,
+                                   cudaMemcpyHostToDevice, c->stream));
+    CDR_CUDA_CHECK(cudaMemcpyAsync(c->hit.p + v.pix_off * spp, hit_cache, sizeof(int32_t) * np * spp,
+                                   cudaMemcpyHostToDevice, c->stream));
+    zero_grad(c, lay->total);
+    reset_flags(c);
+    RenderArgs a = render_args(c, st, lay);
+    int slot = view;
+    launch_render(c, &slot, 1, a, false, false, true, nullptr);
+    launch_finalize_positions(c, lay->positions);
+    sync(c);
+    raise_device_error(c);
+    add_grad_to_host(c, grad, 0, lay->total);
+    API_END
+}
+
+int cdr_extract_silhouettes(cdr_ctx* c, int32_t view, cdr_segment* out, int32_t cap, int32_t* count,
+                            double* total) {
+    API_BEGIN(c)
+    check_view(c, view);
+    ensure_prepared(c);
+    int slot = view;
+    set_view_calls(c, &slot, nullptr, 1);
+    launch_silhouettes(c, 1);
+    launch_cdf(c, 1);
+    int32_t n = 0;
+    double tot[3] = {0, 0, 0};
+    CDR_CUDA_CHECK(cudaMemcpyAsync(&n, c->sil_count.p, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+    CDR_CUDA_CHECK(cudaMemcpyAsync(tot, c->total_len.p, sizeof(tot), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (count) *count = n;
+    if (total) *total = tot[2];
+    if (out && cap > 0 && n > 0)
+        CDR_CUDA_CHECK(cudaMemcpy(out, c->segs.p, sizeof(cdr_segment) * std::min(cap, n), cudaMemcpyDeviceToHost));
+    API_END
+}
+
+int cdr_boundary_pass(cdr_ctx* c, int32_t view, const double* adjoint, const cdr_segment* segments,
+                      int32_t nseg, int32_t samples, uint64_t seed, int32_t probe, const cdr_layout* lay,
+                      double* grad, int32_t* degenerate) {
+    API_BEGIN(c)
+    check_view(c, view);
+    check_ready(c);
+    check_layout(c, lay);
+    if (!adjoint || !grad) throw ApiErr(CDR_ERR_INVALID_ARG, "null argument");
+    if (degenerate) *degenerate = 0;
+    if (samples <= 0) return;  // diff_render.cpp:210-211
+    const ViewData& v = c->views[view];
+    size_t np = size_t(v.cam.W) * v.cam.H;
+    ensure_prepared(c);
+    CDR_CUDA_CHECK(cudaMemcpyAsync(c->adj.p + 3 * v.pix_off, adjoint, sizeof(double) * 3 * np,
+                                   cudaMemcpyHostToDevice, c->stream));
+    int slot = view;
+    int m = samples;
+    if (segments) {
+        if (nseg > std::max(1, c->E)) {
+            // caller-provided sets may exceed the per-view capacity of E
+            c->segs.ensure(size_t(nseg));
+            c->cdf.ensure(size_t(nseg));
+        }
+        set_view_calls(c, &slot, &m, 1);
+        if (nseg > 0)
+            CDR_CUDA_CHECK(cudaMemcpyAsync(c->segs.p, segments, sizeof(cdr_segment) * nseg, cudaMemcpyHostToDevice,
+                                           c->stream));
+        CDR_CUDA_CHECK(cudaMemcpyAsync(c->sil_count.p, &nseg, sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+        sync(c);
+    } else {
+        set_view_calls(c, &slot, &m, 1);
+        launch_silhouettes(c, 1);
+    }
+    launch_cdf(c, 1);
+    zero_grad(c, lay->total);
+    reset_flags(c);
+    launch_boundary(c, 1, m, seed, probe, lay->positions);
+    sync(c);
+    raise_device_error(c);
+    if (degenerate)
+        CDR_CUDA_CHECK(cudaMemcpy(degenerate, c->degenerate.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    add_grad_to_host(c, grad, lay->positions, 3 * int64_t(c->V));
+    API_END
+}
+
+int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_settings* st, double lambda_rend,
+                  double lambda_lap, int32_t lap_mode, int32_t use_mask, const cdr_layout* lay, double* loss_out,
+                  double* grad, double* rendered_rgb, double* rendered_mask, cdr_stats* stats) {
+    API_BEGIN(c)
+    if (!st || n < 0 || (n > 0 && !views)) throw ApiErr(CDR_ERR_INVALID_ARG, "bad arguments");
+    check_layout(c, lay);
+    check_ready(c);
+    const int spp = spp_of(st);
+    check_spp(spp);
+    std::vector<int> slots(views, views + n);
+    std::vector<double> scales(n);
+    std::vector<int> samples(n);
+    int max_samples = 0;
+    for (int i = 0; i < n; ++i) {
+        check_view(c, slots[i]);
+        const ViewData& v = c->views[slots[i]];
+        if (!v.has_target) throw SizeMismatchErr("target count does not match views");  // losses.cpp:247
+        const bool masked = use_mask && v.has_target_mask;
+        double n_valid = masked ? v.target_mask_sum : double(v.cam.W) * v.cam.H;
+        scales[i] = (lambda_rend == 0 || n_valid <= 0) ? 0.0 : lambda_rend / n_valid;
+        samples[i] = st->boundary_samples > 0 ? st->boundary_samples : v.cam.W * v.cam.H;
+        max_samples = std::max(max_samples, samples[i]);
+    }
+    cudaStream_t s = c->stream;
+    auto& ev = c->ev;
+    CDR_CUDA_CHECK(cudaEventRecord(ev[0], s));
+    ensure_prepared(c, /*force=*/true);  // GradContext is rebuilt per total_loss (losses.cpp:251)
+    CDR_CUDA_CHECK(cudaEventRecord(ev[1], s));
+    zero_grad(c, lay->total);
+    reset_flags(c);
+    ensure_hit_arena(c, spp);
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->loss_acc.p, 0, sizeof(double) * c->views.size(), s));
+    RenderArgs a = render_args(c, st, lay);
+    a.use_mask = use_mask;
+    launch_render(c, slots.data(), n, a, true, true, true, scales.data());
+    CDR_CUDA_CHECK(cudaEventRecord(ev[2], s));
+    if (st->boundary_term) {
+        set_view_calls(c, slots.data(), samples.data(), n);
+        launch_silhouettes(c, n);
+        launch_cdf(c, n);
+    }
+    CDR_CUDA_CHECK(cudaEventRecord(ev[3], s));
+    if (st->boundary_term) launch_boundary(c, n, max_samples, st->seed, CDR_PROBE_RADIANCE, lay->positions);
+    CDR_CUDA_CHECK(cudaEventRecord(ev[4], s));
+    launch_finalize_positions(c, lay->positions);
+    const bool lap_here = c->rank == 0;  // computed once across ranks
+    if (lap_here) launch_laplacian(c, lap_mode, lambda_lap, c->grad.p + lay->positions);
+    CDR_CUDA_CHECK(cudaEventRecord(ev[5], s));
+    if (c->nccl_comm)
+        nccl_check(nccl().allReduce(c->grad.p, c->grad.p, size_t(lay->total), kNcclFloat64, kNcclSum, c->nccl_comm, s),
+                   "ncclAllReduce(grad)");
+    CDR_CUDA_CHECK(cudaEventRecord(ev[6], s));
+    std::vector<double> lacc(c->views.size());
+    double lap_sq = 0;
+    CDR_CUDA_CHECK(cudaMemcpyAsync(lacc.data(), c->loss_acc.p, sizeof(double) * lacc.size(), cudaMemcpyDeviceToHost, s));
+    CDR_CUDA_CHECK(cudaMemcpyAsync(&lap_sq, c->lap_partial.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (grad) {
+        static thread_local std::vector<double> tmp;
+        tmp.resize(size_t(lay->total));
+        CDR_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), c->grad.p, sizeof(double) * lay->total, cudaMemcpyDeviceToHost, s));
+        sync(c);
+        for (int64_t i = 0; i < lay->total; ++i) grad[i] += tmp[i];
+    }
+    size_t ro = 0, mo = 0;
+    for (int i = 0; i < n; ++i) {
+        const ViewData& v = c->views[slots[i]];
+        size_t np = size_t(v.cam.W) * v.cam.H;
+        if (rendered_rgb)
+            CDR_CUDA_CHECK(cudaMemcpyAsync(rendered_rgb + ro, c->img.p + 3 * v.pix_off, sizeof(double) * 3 * np,
+                                           cudaMemcpyDeviceToHost, s));
+        if (rendered_mask)
+            CDR_CUDA_CHECK(cudaMemcpyAsync(rendered_mask + mo, c->mask.p + v.pix_off, sizeof(double) * np,
+                                           cudaMemcpyDeviceToHost, s));
+        ro += 3 * np;
+        mo += np;
+    }
+    sync(c);
+    raise_device_error(c);
+    // rendering term in view order, each view scale * Σ m|d| (losses.cpp:44-47, :257)
+    double terms[2] = {0.0, lap_here ? lambda_lap * lap_sq : 0.0};
+    for (int i = 0; i < n; ++i) terms[0] += scales[i] * lacc[slots[i]];
+    if (c->nccl_comm) {  // sum the loss terms of all view shards
+        c->lap_lv.ensure(2);
+        static thread_local DBuf<double> dterm;
+        dterm.ensure(2);
+        CDR_CUDA_CHECK(cudaMemcpyAsync(dterm.p, terms, sizeof(terms), cudaMemcpyHostToDevice, s));
+        nccl_check(nccl().allReduce(dterm.p, dterm.p, 2, kNcclFloat64, kNcclSum, c->nccl_comm, s),
+                   "ncclAllReduce(loss)");
+        CDR_CUDA_CHECK(cudaMemcpyAsync(terms, dterm.p, sizeof(terms), cudaMemcpyDeviceToHost, s));
+        sync(c);
+    }
+    if (loss_out) {
+        loss_out[0] = terms[0];
+        loss_out[1] = terms[1];
+    }
+    if (stats) {
+        Counters k;
+        CDR_CUDA_CHECK(cudaMemcpy(&k, c->counters.p, sizeof(k), cudaMemcpyDeviceToHost));
+        std::memset(stats, 0, sizeof(*stats));
+        for (int i = 0; i < n; ++i) {
+            const ViewData& v = c->views[slots[i]];
+            stats->pixels += int64_t(v.cam.W) * v.cam.H;
+            stats->samples += int64_t(v.cam.W) * v.cam.H * spp;
+            if (st->boundary_term) stats->boundary_samples += samples[i];
+        }
+        stats->hit_samples = int64_t(k.hit_samples);
+        stats->adjoint_samples = int64_t(k.adjoint_samples);
+        stats->boundary_active = int64_t(k.boundary_active);
+        if (st->boundary_term) {
+            std::vector<int32_t> cnt(n), deg(n);
+            CDR_CUDA_CHECK(cudaMemcpy(cnt.data(), c->sil_count.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+            CDR_CUDA_CHECK(cudaMemcpy(deg.data(), c->degenerate.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+            for (int i = 0; i < n; ++i) {
+                stats->segments += cnt[i];
+                stats->degenerate_skipped += deg[i];
+            }
+        }
+        float ms[7];
+        for (int i = 0; i < 6; ++i) CDR_CUDA_CHECK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+        stats->ms_prepare = ms[0];
+        stats->ms_render = ms[1];
+        stats->ms_silhouette = ms[2];
+        stats->ms_boundary = ms[3];
+        stats->ms_finalize = ms[4];
+        float tot;
+        CDR_CUDA_CHECK(cudaEventElapsedTime(&tot, ev[0], ev[6]));
+        stats->ms_total = tot;
+    }
+    API_END
+}
+
+int cdr_get_grad(cdr_ctx* c, double* out, int64_t n) {
+    API_BEGIN(c)
+    if (n > c->grad_n) throw SizeMismatchErr("gradient buffer smaller than requested");
+    if (n > 0) CDR_CUDA_CHECK(cudaMemcpyAsync(out, c->grad.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
+int cdr_grad_device_ptr(cdr_ctx* c, void** ptr, int64_t* n) {
+    if (!c || !ptr) return CDR_ERR_INVALID_ARG;
+    *ptr = c->grad.p;
+    if (n) *n = c->grad_n;
+    return CDR_OK;
+}
+
+int cdr_laplacian_matrix(cdr_ctx* c, int32_t mode, int32_t* outer, int32_t* inner, double* values, int64_t* nnz) {
+    API_BEGIN(c)
+    int64_t z = int64_t(c->V) + 2 * int64_t(c->E);
+    if (nnz) *nnz = z;
+    if (!outer && !inner && !values) return;
+    launch_laplacian(c, mode, 0.0, nullptr);
+    // L is symmetric, so its CSR (row-sorted) equals Eigen's CSC layout
+    if (outer) CDR_CUDA_CHECK(cudaMemcpyAsync(outer, c->lap_rowptr.p, sizeof(int32_t) * (size_t(c->V) + 1),
+                                              cudaMemcpyDeviceToHost, c->stream));
+    if (inner && z) CDR_CUDA_CHECK(cudaMemcpyAsync(inner, c->lap_col.p, sizeof(int32_t) * z, cudaMemcpyDeviceToHost,
+                                                   c->stream));
+    if (values && z) CDR_CUDA_CHECK(cudaMemcpyAsync(values, c->lap_val.p, sizeof(double) * z, cudaMemcpyDeviceToHost,
+                                                    c->stream));
+    sync(c);
+    API_END
+}
+
+int cdr_laplacian_loss(cdr_ctx* c, int32_t mode, double lambda, double* value, double* grad) {
+    API_BEGIN(c)
+    if (value) *value = 0;
+    if (lambda == 0 || c->V == 0) return;  // losses.cpp:69
+    c->lap_grad.ensure(size_t(3) * c->V);
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->lap_grad.p, 0, sizeof(double) * 3 * c->V, c->stream));
+    launch_laplacian(c, mode, lambda, c->lap_grad.p);
+    double sq = 0;
+    CDR_CUDA_CHECK(cudaMemcpyAsync(&sq, c->lap_partial.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    std::vector<double> g(size_t(3) * c->V);
+    CDR_CUDA_CHECK(cudaMemcpyAsync(g.data(), c->lap_grad.p, sizeof(double) * g.size(), cudaMemcpyDeviceToHost,
+                                   c->stream));
+    sync(c);
+    if (value) *value = lambda * sq;
+    if (grad)
+        for (size_t i = 0; i < g.size(); ++i) grad[i] += g[i];
+    API_END
+}
+
+int cdr_nccl_unique_id(char id_out[128]) {
+    NcclApi& api = nccl();
+    if (!api.ok) return CDR_ERR_ERROR;
+    return api.getUniqueId(id_out) == 0 ? CDR_OK : CDR_ERR_ERROR;
+}
+
+int cdr_comm_init(cdr_ctx* c, const char id[128], int32_t n_ranks, int32_t rank) {
+    API_BEGIN(c)
+    NcclApi& api = nccl();
+    if (!api.ok) throw ApiErr(CDR_ERR_ERROR, "NCCL (libnccl.so.2) not loadable");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) throw ApiErr(CDR_ERR_INVALID_ARG, "bad rank");
+    NcclUid uid;
+    std::memcpy(uid.internal, id, 128);
+    void* comm = nullptr;
+    auto init = reinterpret_cast<CommInitByValue>(api.commInitRank);
+    nccl_check(init(&comm, n_ranks, uid, rank), "ncclCommInitRank");
+    c->nccl_comm = comm;
+    c->n_ranks = n_ranks;
+    c->rank = rank;
+    API_END
+}
+
+}  // extern "C"

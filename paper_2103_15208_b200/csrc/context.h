@@ -1,0 +1,135 @@
+// context.h — host-side state of one cdr_ctx (one GPU).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/cdr.h"
+#include "bvh.cuh"
+#include "common.cuh"
+
+namespace cdr {
+
+struct SceneInfo {        // device-resident, rewritten by prepare()
+    double lo[3], hi[3];  // vertex bounding box (Mesh::bbox_min/max, mesh.cpp:15-25)
+    double t_min;         // Bvh::default_t_min_ (bvh.cpp:92)
+    double pad;           // absolute box padding for the fp32 traversal
+};
+
+// Device buffer with grow-only capacity.
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void ensure(size_t count) {
+        if (count <= n) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        if (cudaMalloc(&p, sizeof(T) * (count ? count : 1)) != cudaSuccess) throw std::bad_alloc();
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct ViewData {
+    DevCamera cam;
+    bool has_target = false;
+    bool has_target_mask = false;
+    double target_mask_sum = 0;  // Σ target mask in pixel order (losses.cpp:26)
+    size_t pix_off = 0;          // offset (pixels) of this view in the image arena
+};
+
+struct ErrorInfo {  // device-side NonFiniteGradient report
+    int flag;
+    int x, y;
+    int segment;
+};
+
+struct Counters {  // device-side work counters (cdr_stats)
+    unsigned long long hit_samples;
+    unsigned long long adjoint_samples;
+    unsigned long long boundary_active;
+    double loss_sum[1];
+};
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+};
+
+}  // namespace cdr
+
+struct cdr_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::string err;
+
+    // mesh (topology fixed between set_mesh calls)
+    int V = 0, T = 0, E = 0;
+    bool has_uv = false;
+    std::vector<int32_t> h_tris, h_edges;
+    cdr::DBuf<double> pos, uv, normals, accum, fnormal;
+    cdr::DBuf<int32_t> tris;
+    cdr::DBuf<int4> edges;
+    cdr::DBuf<int32_t> vf_start, vf_list;   // vertex -> (face*3+corner), ascending face
+    cdr::DBuf<int32_t> lap_rowptr, lap_col;  // CSR pattern of the Laplacian (symmetric)
+    cdr::DBuf<int2> lap_edge_slot;           // per edge: slot of (v0,v1) and (v1,v0)
+    cdr::DBuf<int32_t> lap_diag_slot;
+    cdr::DBuf<double> lap_val, lap_lv, lap_grad, lap_partial;
+    bool geometry_dirty = true;
+
+    // per-iteration acceleration data
+    cdr::DBuf<cdr::SceneInfo> info;
+    cdr::DBuf<double> bbox_partial;
+    cdr::DBuf<unsigned long long> keys, keys_alt;
+    cdr::DBuf<unsigned char> sort_tmp;
+    cdr::DBuf<int32_t> parent_internal, parent_leaf, refit_flag;
+    cdr::DBuf<float> node_box;  // internal node boxes (6 floats) for the refit
+    cdr::DBuf<cdr::BNode> nodes;
+    cdr::DBuf<cdr::TriRec> recs;
+    double t_min_host = 1e-8;
+
+    // materials, light
+    int tw = 0, th = 0;
+    cdr::DBuf<cdr::Texel> tex;
+    double light[3] = {1, 1, 1};
+    double background[3] = {0, 0, 0};
+
+    // views and per-view device images (arena indexed by ViewData::pix_off)
+    std::vector<cdr::ViewData> views;
+    cdr::DBuf<cdr::DevCamera> d_cams;
+    size_t total_pixels = 0;
+    cdr::DBuf<double> target, target_mask, img, mask, adj;
+    cdr::DBuf<int32_t> hit;  // hit caches (per view W*H*spp), arena sized on demand
+    size_t hit_stride_spp = 0;
+
+    // silhouettes (per view slot capacity E)
+    cdr::DBuf<unsigned char> sil_flag;
+    cdr::DBuf<int32_t> sil_block_count, sil_block_off, sil_count;
+    cdr::DBuf<cdr_segment> segs;
+    cdr::DBuf<double> cdf, total_len;
+    cdr::DBuf<int32_t> degenerate;
+
+    // gradient + accumulators
+    int64_t grad_n = 0;
+    cdr::DBuf<double> grad;
+    cdr::DBuf<double> corner_acc;  // T x 3 corners x (g[3], h[3])
+    cdr::DBuf<double> qvec;        // V x 3: Jn_v * H_v
+    cdr::DBuf<double> loss_acc;    // per view: Σ m |d|
+    cdr::DBuf<cdr::ErrorInfo> errinfo;
+    cdr::DBuf<cdr::Counters> counters;
+
+    // timing
+    std::vector<cudaEvent_t> ev;
+
+    // multi-GPU
+    void* nccl_comm = nullptr;
+    int n_ranks = 1, rank = 0;
+};

@@ -1,0 +1,92 @@
+// kernels.h — host launch wrappers of the sm_100a kernels (one per stage).
+#pragma once
+
+#include <stdexcept>
+#include <string>
+
+#include "context.h"
+#include "shade.cuh"
+
+namespace cdr {
+
+inline ShadeScene shade_scene(const cdr_ctx* c) {
+    ShadeScene sc{};
+    sc.nodes = c->nodes.p;
+    sc.recs = c->recs.p;
+    sc.n_tris = c->T;
+    sc.pos = c->pos.p;
+    sc.tris = c->tris.p;
+    sc.uv = c->has_uv ? c->uv.p : nullptr;
+    sc.normals = c->normals.p;
+    sc.fnormal = c->fnormal.p;
+    sc.tex = c->tex.p;
+    sc.tw = c->tw;
+    sc.th = c->th;
+    for (int i = 0; i < 3; ++i) {
+        sc.L[i] = c->light[i];
+        sc.bg[i] = c->background[i];
+    }
+    return sc;
+}
+
+// prepare.cu — per-iteration geometry: face normals, vertex normals
+// (mesh.cpp:65-95), bbox + t_min (bvh.cpp:92), LBVH (Morton -> radix sort ->
+// Karras hierarchy -> bottom-up fp32 refit).
+void launch_prepare(cdr_ctx* c, double cam_abs_max);
+
+// render.cu — fused per-sample kernel. Modes:
+//   kTrace     primary-ray generation + LBVH traversal + shading (render.cpp:35-64)
+//   kLoss      per-pixel tone-mapped L1 + adjoint (losses.cpp:15-49)
+//   kInterior  interior adjoint scatter (diff_render.cpp:62-201)
+struct RenderArgs {
+    int spp;
+    int k;  // lround(sqrt(spp))
+    uint64_t seed;
+    double gamma;
+    double loss_scale;  // lambda / n_valid (per call, all views share W*H here)
+    int use_mask;
+    int write_hits;
+    int64_t lay_diffuse, lay_specular, lay_roughness, lay_light;  // -1 = absent
+};
+void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a,
+                   bool trace, bool loss, bool interior, const double* loss_scales);
+
+// boundary.cu — extract_silhouettes (silhouette.cpp:55-106), the CDF of
+// boundary_pass (diff_render.cpp:213-228) and its edge samples (:230-278).
+// view list of the next silhouette/CDF/boundary launches; samples[i] = M per view
+void set_view_calls(cdr_ctx* c, const int* view_slots, const int* samples, int n_views);
+void launch_silhouettes(cdr_ctx* c, int n_views);
+void launch_cdf(cdr_ctx* c, int n_views);
+void launch_boundary(cdr_ctx* c, int n_views, int max_samples, uint64_t seed, int probe,
+                     int64_t lay_pos);
+
+// finalize.cu — position gradient assembly: per-corner interior sums, the
+// one-ring normal chain (diff_render.cpp:174-184) restated as q_v x d_{f,w},
+// and the Laplacian (laplacian.cpp:21-55, losses.cpp:66-78) as CSR SpMVs.
+void launch_finalize_positions(cdr_ctx* c, int64_t lay_pos);
+void launch_laplacian(cdr_ctx* c, int mode, double lambda, double* grad_pos /* nullable */);
+
+// generic loss kernel over device images (cdr_view_loss)
+// radiance_at for n pixel positions of one view (device buffers)
+void launch_radiance_points(cdr_ctx* c, int slot, int n, const double* xy, double* rgb, int32_t* tri);
+// pack diffuse/specular/roughness (fp64, device) into 32-byte fp32 texel records
+void launch_pack_textures(cdr_ctx* c, const double* d, const double* s, const double* r, int n);
+
+void launch_view_loss(cdr_ctx* c, int W, int H, const double* rendered, const double* target,
+                      const double* tmask, double scale, double gamma, int masked, double* adj,
+                      double* sum);
+
+}  // namespace cdr
+
+#define CDR_CUDA_CHECK(x)                                                              \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess)                                                         \
+            throw cdr::CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));     \
+    } while (0)
+
+namespace cdr {
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+}  // namespace cdr

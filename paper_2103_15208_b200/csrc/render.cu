@@ -1,0 +1,531 @@
+// render.cu — the fused per-sample kernel of the hot path.
+//
+// One CTA of 256 threads owns a TW x TH pixel tile of one view; thread =
+// (pixel, sample), so the spp samples of a pixel are adjacent lanes (coherent
+// rays, shared texels). Three phases separated by CTA barriers:
+//   1. trace + shade every sample            render.cpp:35-64 / radiance_at :24-33
+//   2. per-pixel mean, mask, tone-mapped L1 loss partial and adjoint
+//                                            losses.cpp:15-49 (sum in sample order)
+//   3. interior adjoint of every hit sample  diff_render.cpp:62-201
+// so the reference's hit-cache round trip between render and interior_pass
+// disappears (the cache is still written: it is the bit-exact output).
+//
+// Phase-3 scatter is warp-aggregated: lanes are grouped with __match_any_sync by
+// texel (28 texel-gradient values) and by triangle (18 per-corner values), each
+// group is summed with log-depth shuffles, and one lane issues the atomics.
+// The one-ring normal chain is deferred: per-corner sums of coeff_mu*b_j*h feed
+// the finalize kernels (finalize.cu), which apply it once per iteration.
+#include "kernels.h"
+#include "shade.cuh"
+
+namespace cdr {
+namespace {
+
+struct ViewCall {
+    int slot;
+    int pad;
+    double scale;  // lambda / n_valid
+};
+
+struct Params {
+    ShadeScene sc;
+    const SceneInfo* info;
+    const DevCamera* cams;
+    const ViewCall* calls;
+    size_t* pix_off;  // per slot
+    int spp, k, TW, TH;
+    uint64_t seed;
+    double gamma;
+    int use_mask, write_hits;
+    double* img;
+    double* mask;
+    double* adj;
+    int32_t* hit;
+    const double* target;
+    const double* target_mask;
+    const unsigned char* has_mask;  // per slot
+    double* grad;
+    int64_t lay_d, lay_s, lay_r, lay_l;
+    double* corner;
+    double* loss_acc;
+    ErrorInfo* err;
+    Counters* counters;
+};
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void raise_nonfinite(ErrorInfo* e, int x, int y) {
+    if (atomicCAS(&e->flag, 0, 1) == 0) {
+        e->x = x;
+        e->y = y;
+        e->segment = -1;
+    }
+}
+
+template <bool kTrace, bool kLoss, bool kInterior>
+__global__ void __launch_bounds__(kThreads) k_render(Params p) {
+    __shared__ double s_rad[kThreads][3];
+    __shared__ double s_adj[kThreads][3];  // per pixel (index = pixel in tile)
+    __shared__ unsigned char s_hit[kThreads];
+
+    const ViewCall vc = p.calls[blockIdx.y];
+    const DevCamera& cam = p.cams[vc.slot];
+    const int W = cam.W, H = cam.H;
+    const int tiles_x = (W + p.TW - 1) / p.TW;
+    const int tiles_y = (H + p.TH - 1) / p.TH;
+    if (int(blockIdx.x) >= tiles_x * tiles_y) return;  // uniform per CTA
+    const int tid = threadIdx.x;
+    const int spp = p.spp;
+    const int P = kThreads / spp;
+    const int pix = tid / spp, s = tid - (tid / spp) * spp;
+    const int x = (blockIdx.x % tiles_x) * p.TW + pix % p.TW;
+    const int y = (blockIdx.x / tiles_x) * p.TH + pix / p.TW;
+    const bool valid = pix < P && x < W && y < H;
+    const size_t pbase = p.pix_off[vc.slot];
+    const size_t pidx = pbase + size_t(y) * W + x;  // arena pixel index
+    const double t_min = p.info->t_min;
+    const D3 org{cam.o[0], cam.o[1], cam.o[2]};
+
+    // ---------------- phase 1: sample -> (tri, t, b1, b2), radiance
+    int tri = -1;
+    double t = 0, b1 = 0, b2 = 0;
+    D3 dir{0, 0, 1};
+    if (valid) {
+        D2 ps = pixel_sample_position(p.seed, cam.gid, x, y, W, s, spp, p.k);
+        dir = primary_dir(cam, ps);
+        if (kTrace) {
+            Hit h = trace(p.sc.nodes, p.sc.recs, p.sc.n_tris, org, dir, t_min);
+            tri = h.tri;
+            t = h.t;
+            b1 = h.b1;
+            b2 = h.b2;
+            if (p.write_hits) p.hit[pidx * spp + s] = tri;
+        } else {
+            // interior_pass replay: re-intersect the cached triangle (diff_render.cpp:84-93)
+            tri = p.hit[pidx * spp + s];
+            if (tri >= 0) {
+                int a = p.sc.tris[3 * tri], b = p.sc.tris[3 * tri + 1], c = p.sc.tris[3 * tri + 2];
+                if (!ray_triangle(org, dir, ld3(p.sc.pos + 3 * a), ld3(p.sc.pos + 3 * b), ld3(p.sc.pos + 3 * c), t, b1, b2))
+                    tri = -1;
+            }
+        }
+    }
+    if (kTrace) {
+        D3 rad{p.sc.bg[0], p.sc.bg[1], p.sc.bg[2]};
+        if (tri >= 0) rad = shade_hit(p.sc, Hit{tri, t, b1, b2}, dir);
+        s_rad[tid][0] = rad.x;
+        s_rad[tid][1] = rad.y;
+        s_rad[tid][2] = rad.z;
+        s_hit[tid] = tri >= 0;
+    }
+    __syncthreads();
+
+    // ---------------- phase 2: pixel mean / mask / loss / adjoint
+    double loss_part = 0;
+    if (tid < P) {
+        const int px = (blockIdx.x % tiles_x) * p.TW + tid % p.TW;
+        const int py = (blockIdx.x / tiles_x) * p.TH + tid / p.TW;
+        if (px < W && py < H) {
+            const size_t q = pbase + size_t(py) * W + px;
+            D3 mean;
+            if (kTrace) {
+                D3 sum{0, 0, 0};
+                int hits = 0;
+                for (int j = 0; j < spp; ++j) {
+                    int o = tid * spp + j;
+                    sum = sum + D3{s_rad[o][0], s_rad[o][1], s_rad[o][2]};
+                    hits += s_hit[o];
+                }
+                mean = sum / double(spp);
+                p.img[3 * q] = mean.x;
+                p.img[3 * q + 1] = mean.y;
+                p.img[3 * q + 2] = mean.z;
+                p.mask[q] = double(hits) / double(spp);
+            }
+            if (kLoss) {
+                double m = (p.use_mask && p.has_mask[vc.slot]) ? p.target_mask[q] : 1.0;
+                D3 adj{0, 0, 0};
+                if (m != 0) {
+                    double r[3] = {mean.x, mean.y, mean.z}, a[3];
+                    for (int c = 0; c < 3; ++c) {
+                        double d = tone_map(r[c], p.gamma) - tone_map(p.target[3 * q + c], p.gamma);
+                        loss_part += m * fabs(d);
+                        double sg = double((d > 0) - (d < 0));
+                        a[c] = vc.scale * m * sg * tone_map_derivative(r[c], p.gamma);
+                    }
+                    adj = D3{a[0], a[1], a[2]};
+                }
+                p.adj[3 * q] = adj.x;
+                p.adj[3 * q + 1] = adj.y;
+                p.adj[3 * q + 2] = adj.z;
+                s_adj[tid][0] = adj.x;
+                s_adj[tid][1] = adj.y;
+                s_adj[tid][2] = adj.z;
+            }
+        }
+    }
+    if (kLoss) {
+        // CTA reduction of the loss partial (one fp64 atomic per CTA)
+        for (int o = 16; o > 0; o >>= 1) loss_part += __shfl_xor_sync(0xffffffffu, loss_part, o);
+        __shared__ double s_red[kThreads / 32];
+        if ((tid & 31) == 0) s_red[tid >> 5] = loss_part;
+        __syncthreads();
+        if (tid == 0) {
+            double tot = 0;
+            for (int w = 0; w < kThreads / 32; ++w) tot += s_red[w];
+            if (tot != 0) atomicAdd(&p.loss_acc[vc.slot], tot);
+        }
+    }
+    if (!kInterior) {
+        if (kTrace) {
+            int nh = __syncthreads_count(valid && tri >= 0);
+            if (tid == 0 && nh) atomicAdd(&p.counters->hit_samples, (unsigned long long)nh);
+        }
+        return;
+    }
+
+    // ---------------- phase 3: interior adjoint scatter
+    D3 a{0, 0, 0};
+    if (valid && tri >= 0) {
+        if (kLoss) {
+            a = D3{s_adj[pix][0], s_adj[pix][1], s_adj[pix][2]};
+        } else {
+            a = ld3(p.adj + 3 * pidx);
+        }
+    }
+    bool act = valid && tri >= 0 && !(a.x == 0 && a.y == 0 && a.z == 0);
+    {
+        int nh = __syncthreads_count(valid && tri >= 0);
+        int na = __syncthreads_count(act);
+        if (tid == 0) {
+            if (nh) atomicAdd(&p.counters->hit_samples, (unsigned long long)nh);
+            if (na) atomicAdd(&p.counters->adjoint_samples, (unsigned long long)na);
+        }
+    }
+    a = a / double(spp);  // diff_render.cpp:82
+    const double Lc[3] = {p.sc.L[0], p.sc.L[1], p.sc.L[2]};
+    const double ac[3] = {a.x, a.y, a.z};
+
+    int va = 0, vb = 0, vcx = 0;
+    double b0 = 0;
+    D3 p0{0, 0, 0}, p1{0, 0, 0}, p2{0, 0, 0};
+    D2 uv0{0, 0}, uv1{0, 0}, uv2{0, 0};
+    D3 N0{0, 0, 0}, N1{0, 0, 0}, N2{0, 0, 0}, nt{0, 0, 0};
+    double mu = 0;
+    TexSample3 ts;
+    Brdf br;
+    double inv_r2 = 0;
+    if (act) {
+        b0 = 1.0 - b1 - b2;
+        va = p.sc.tris[3 * tri];
+        vb = p.sc.tris[3 * tri + 1];
+        vcx = p.sc.tris[3 * tri + 2];
+        p0 = ld3(p.sc.pos + 3 * va);
+        p1 = ld3(p.sc.pos + 3 * vb);
+        p2 = ld3(p.sc.pos + 3 * vcx);
+        if (p.sc.uv) {
+            uv0 = D2{p.sc.uv[2 * va], p.sc.uv[2 * va + 1]};
+            uv1 = D2{p.sc.uv[2 * vb], p.sc.uv[2 * vb + 1]};
+            uv2 = D2{p.sc.uv[2 * vcx], p.sc.uv[2 * vcx + 1]};
+        }
+        D2 uv{uv0.x * b0 + uv1.x * b1 + uv2.x * b2, uv0.y * b0 + uv1.y * b1 + uv2.y * b2};
+        N0 = ld3(p.sc.normals + 3 * va);
+        N1 = ld3(p.sc.normals + 3 * vb);
+        N2 = ld3(p.sc.normals + 3 * vcx);
+        nt = N0 * b0 + N1 * b1 + N2 * b2;
+        double n_len = length(nt);
+        if (n_len < 1e-14) {
+            act = false;  // diff_render.cpp:101
+        } else {
+            D3 n_hat = nt / n_len;
+            mu = dot(n_hat, -dir);
+            ts = sample_maps(p.sc.tex, p.sc.tw, p.sc.th, uv, true);
+            br = eval_brdf(ts.dv, ts.sv, ts.rv, mu, true);
+            inv_r2 = 1.0 / (t * t);
+        }
+    }
+
+    // texel scatter through the bilinear weights (diff_render.cpp:110-128):
+    // group by the texel quad (texel[0] determines all four)
+    {
+        const int key = act ? ts.texel[0] : -1 - (tid & 31);
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const bool leader = act && (__ffs(peers) - 1) == (tid & 31);
+#pragma unroll 1
+        for (int kq = 0; kq < 4; ++kq) {
+            double v[7];
+            if (act) {
+                double wd = ts.w[kq] * br.d_diffuse * inv_r2;
+                double ws = ts.w[kq] * br.d_specular * inv_r2;
+                double wr = 0;
+                for (int c = 0; c < 3; ++c) {
+                    v[c] = ac[c] * Lc[c] * wd;
+                    v[3 + c] = ac[c] * Lc[c] * ws;
+                    wr += ac[c] * Lc[c] * comp(br.d_rough, c) * inv_r2;
+                }
+                v[6] = wr * ts.w[kq];
+            } else {
+                for (int i = 0; i < 7; ++i) v[i] = 0;
+            }
+            reduce_peers<7>(0xffffffffu, peers, v);
+            if (leader) {
+                int64_t tx = ts.texel[kq];
+                for (int c = 0; c < 3; ++c) {
+                    if (v[c] != 0) atomicAdd(p.grad + p.lay_d + 3 * tx + c, v[c]);
+                    if (v[3 + c] != 0) atomicAdd(p.grad + p.lay_s + 3 * tx + c, v[3 + c]);
+                }
+                if (v[6] != 0) atomicAdd(p.grad + p.lay_r + tx, v[6]);
+            }
+        }
+    }
+    if (p.lay_l >= 0) {  // light intensity (diff_render.cpp:129-131)
+        double v[3];
+        for (int c = 0; c < 3; ++c) v[c] = act ? ac[c] * comp(br.value, c) * inv_r2 : 0.0;
+        for (int o = 16; o > 0; o >>= 1)
+            for (int c = 0; c < 3; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+        if ((tid & 31) == 0)
+            for (int c = 0; c < 3; ++c)
+                if (v[c] != 0) atomicAdd(p.grad + p.lay_l + c, v[c]);
+    }
+
+    // intersection response + normal chain (diff_render.cpp:133-184)
+    bool pact = act && mu > 0;
+    D3 gc{0, 0, 0}, hv{0, 0, 0};
+    double cm = 0;
+    if (pact) {
+        // M = [d, p0-p1, p0-p2] (Mat3::from_columns), inverse rows r0..r2
+        double m[9] = {dir.x, p0.x - p1.x, p0.x - p2.x, dir.y, p0.y - p1.y, p0.y - p2.y,
+                       dir.z, p0.z - p1.z, p0.z - p2.z};
+        double det = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                     m[2] * (m[3] * m[7] - m[4] * m[6]);
+        if (fabs(det) < 1e-18) {
+            pact = false;
+        } else {
+            double inv = 1.0 / det;
+            D3 r0{(m[4] * m[8] - m[5] * m[7]) * inv, (m[2] * m[7] - m[1] * m[8]) * inv,
+                  (m[1] * m[5] - m[2] * m[4]) * inv};
+            D3 r1{(m[5] * m[6] - m[3] * m[8]) * inv, (m[0] * m[8] - m[2] * m[6]) * inv,
+                  (m[2] * m[3] - m[0] * m[5]) * inv};
+            D3 r2{(m[3] * m[7] - m[4] * m[6]) * inv, (m[1] * m[6] - m[0] * m[7]) * inv,
+                  (m[0] * m[4] - m[1] * m[3]) * inv};
+            double cs = 0, cu = 0, cv = 0;
+            for (int c = 0; c < 3; ++c) {
+                double w = ac[c] * Lc[c] * inv_r2;
+                cs += ac[c] * Lc[c] * (-2.0 * comp(br.value, c) / (t * t * t));
+                double gu = br.d_diffuse * comp(ts.ddu, c) + br.d_specular * comp(ts.sdu, c) +
+                            comp(br.d_rough, c) * ts.rdu;
+                double gv = br.d_diffuse * comp(ts.ddv, c) + br.d_specular * comp(ts.sdv, c) +
+                            comp(br.d_rough, c) * ts.rdv;
+                cu += w * gu;
+                cv += w * gv;
+                cm += w * comp(br.d_mu, c);
+            }
+            if (!isfinite(cs + cu + cv + cm)) {
+                raise_nonfinite(p.err, x, y);
+                pact = false;
+            } else {
+                // h = normalize_jacobian(n_tilde) * v_hat (vec.hpp:179-183)
+                double len = length(nt);
+                D3 n = nt / len;
+                D3 v = -dir;
+                double sc = 1.0 / len;
+                double J[9] = {(1 - n.x * n.x) * sc, (0 - n.x * n.y) * sc, (0 - n.x * n.z) * sc,
+                               (0 - n.y * n.x) * sc, (1 - n.y * n.y) * sc, (0 - n.y * n.z) * sc,
+                               (0 - n.z * n.x) * sc, (0 - n.z * n.y) * sc, (1 - n.z * n.z) * sc};
+                hv = D3{J[0] * v.x + J[1] * v.y + J[2] * v.z, J[3] * v.x + J[4] * v.y + J[5] * v.z,
+                        J[6] * v.x + J[7] * v.y + J[8] * v.z};
+                double k1 = cu * (uv1.x - uv0.x) + cv * (uv1.y - uv0.y) + cm * (dot(hv, N1) - dot(hv, N0));
+                double k2 = cu * (uv2.x - uv0.x) + cv * (uv2.y - uv0.y) + cm * (dot(hv, N2) - dot(hv, N0));
+                gc = r0 * cs + r1 * k1 + r2 * k2;
+            }
+        }
+    }
+    {
+        const int key = pact ? tri : -1 - (tid & 31);
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const bool leader = pact && (__ffs(peers) - 1) == (tid & 31);
+        const double bc[3] = {b0, b1, b2};
+#pragma unroll 1
+        for (int j = 0; j < 3; ++j) {
+            double v[6];
+            if (pact) {
+                D3 g = gc * bc[j];
+                D3 h = hv * (cm * bc[j]);
+                v[0] = g.x; v[1] = g.y; v[2] = g.z;
+                v[3] = h.x; v[4] = h.y; v[5] = h.z;
+            } else {
+                for (int i = 0; i < 6; ++i) v[i] = 0;
+            }
+            reduce_peers<6>(0xffffffffu, peers, v);
+            if (leader) {
+                double* dst = p.corner + (size_t(tri) * 3 + j) * 6;
+                for (int i = 0; i < 6; ++i)
+                    if (v[i] != 0) atomicAdd(dst + i, v[i]);
+            }
+        }
+    }
+}
+
+__global__ void k_view_loss(int n, const double* __restrict__ r, const double* __restrict__ tg,
+                            const double* __restrict__ tm, double scale, double gamma, int masked,
+                            double* __restrict__ adj, double* __restrict__ sum) {
+    double part = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double m = masked ? tm[i] : 1.0;
+        double a[3] = {0, 0, 0};
+        if (m != 0)
+            for (int c = 0; c < 3; ++c) {
+                double d = tone_map(r[3 * i + c], gamma) - tone_map(tg[3 * i + c], gamma);
+                part += m * fabs(d);
+                a[c] = scale * m * double((d > 0) - (d < 0)) * tone_map_derivative(r[3 * i + c], gamma);
+            }
+        for (int c = 0; c < 3; ++c) adj[3 * i + c] = a[c];
+    }
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0 && part != 0) atomicAdd(sum, part);
+}
+
+__global__ void k_radiance_points(ShadeScene sc, const SceneInfo* __restrict__ info,
+                                  const DevCamera* __restrict__ cams, int slot, int n,
+                                  const double* __restrict__ xy, double* __restrict__ rgb,
+                                  int32_t* __restrict__ tri) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int t = -1;
+    D3 r = radiance_at(sc, cams[slot], D2{xy[2 * i], xy[2 * i + 1]}, info->t_min, &t);
+    rgb[3 * i] = r.x;
+    rgb[3 * i + 1] = r.y;
+    rgb[3 * i + 2] = r.z;
+    if (tri) tri[i] = t;
+}
+
+__global__ void k_pack_textures(const double* __restrict__ d, const double* __restrict__ s,
+                                const double* __restrict__ r, int n, Texel* __restrict__ out) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Texel t;
+    t.a = make_float4(float(d[3 * i]), float(d[3 * i + 1]), float(d[3 * i + 2]), float(s[3 * i]));
+    t.b = make_float4(float(s[3 * i + 1]), float(s[3 * i + 2]), float(r[i]), 0.0f);
+    out[i] = t;
+}
+
+}  // namespace
+
+void launch_radiance_points(cdr_ctx* c, int slot, int n, const double* xy, double* rgb, int32_t* tri) {
+    if (n <= 0) return;
+    k_radiance_points<<<(n + 255) / 256, 256, 0, c->stream>>>(shade_scene(c), c->info.p, c->d_cams.p, slot, n,
+                                                              xy, rgb, tri);
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_pack_textures(cdr_ctx* c, const double* d, const double* s, const double* r, int n) {
+    if (n <= 0) return;
+    k_pack_textures<<<(n + 255) / 256, 256, 0, c->stream>>>(d, s, r, n, c->tex.p);
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_view_loss(cdr_ctx* c, int W, int H, const double* rendered, const double* target,
+                      const double* tmask, double scale, double gamma, int masked, double* adj,
+                      double* sum) {
+    int n = W * H;
+    int nb = std::max(1, std::min((n + 255) / 256, 148 * 8));
+    k_view_loss<<<nb, 256, 0, c->stream>>>(n, rendered, target, tmask, scale, gamma, masked, adj, sum);
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+// Host side of the fused kernel (declared in kernels.h).
+struct RenderStatics {
+    DBuf<ViewCall> calls;
+    DBuf<size_t> pix_off;
+    DBuf<unsigned char> has_mask;
+};
+
+static RenderStatics& statics(cdr_ctx* c) {
+    // one per context: keyed by address in a small registry
+    static thread_local std::vector<std::pair<cdr_ctx*, RenderStatics*>> reg;
+    for (auto& e : reg)
+        if (e.first == c) return *e.second;
+    reg.push_back({c, new RenderStatics()});
+    return *reg.back().second;
+}
+
+void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a, bool trace,
+                   bool loss, bool interior, const double* loss_scales) {
+    if (n_views <= 0) return;
+    RenderStatics& st = statics(c);
+    std::vector<ViewCall> calls(n_views);
+    int maxW = 0, maxH = 0;
+    for (int i = 0; i < n_views; ++i) {
+        calls[i].slot = view_slots[i];
+        calls[i].pad = 0;
+        calls[i].scale = loss_scales ? loss_scales[i] : 0.0;
+        maxW = std::max(maxW, c->views[view_slots[i]].cam.W);
+        maxH = std::max(maxH, c->views[view_slots[i]].cam.H);
+    }
+    size_t nslots = c->views.size();
+    std::vector<size_t> offs(nslots);
+    std::vector<unsigned char> hm(nslots);
+    for (size_t i = 0; i < nslots; ++i) {
+        offs[i] = c->views[i].pix_off;
+        hm[i] = c->views[i].has_target_mask;
+    }
+    st.calls.ensure(n_views);
+    st.pix_off.ensure(nslots);
+    st.has_mask.ensure(nslots);
+    CDR_CUDA_CHECK(cudaMemcpyAsync(st.calls.p, calls.data(), sizeof(ViewCall) * n_views,
+                                   cudaMemcpyHostToDevice, c->stream));
+    CDR_CUDA_CHECK(cudaMemcpyAsync(st.pix_off.p, offs.data(), sizeof(size_t) * nslots,
+                                   cudaMemcpyHostToDevice, c->stream));
+    CDR_CUDA_CHECK(cudaMemcpyAsync(st.has_mask.p, hm.data(), nslots, cudaMemcpyHostToDevice, c->stream));
+
+    Params p{};
+    p.sc = shade_scene(c);
+    p.info = c->info.p;
+    p.cams = c->d_cams.p;
+    p.calls = st.calls.p;
+    p.pix_off = st.pix_off.p;
+    p.spp = a.spp;
+    p.k = a.k;
+    int P = kThreads / a.spp;
+    int TW = 1;
+    while (TW * TW * 4 <= P) TW *= 2;  // near-square power-of-two width
+    p.TW = TW;
+    p.TH = (P + TW - 1) / TW;
+    while (TW * p.TH > P) --p.TH;
+    p.seed = a.seed;
+    p.gamma = a.gamma;
+    p.use_mask = a.use_mask;
+    p.write_hits = a.write_hits;
+    p.img = c->img.p;
+    p.mask = c->mask.p;
+    p.adj = c->adj.p;
+    p.hit = c->hit.p;
+    p.target = c->target.p;
+    p.target_mask = c->target_mask.p;
+    p.has_mask = st.has_mask.p;
+    p.grad = c->grad.p;
+    p.lay_d = a.lay_diffuse;
+    p.lay_s = a.lay_specular;
+    p.lay_r = a.lay_roughness;
+    p.lay_l = a.lay_light;
+    p.corner = c->corner_acc.p;
+    p.loss_acc = c->loss_acc.p;
+    p.err = c->errinfo.p;
+    p.counters = c->counters.p;
+
+    int tiles = ((maxW + p.TW - 1) / p.TW) * ((maxH + p.TH - 1) / p.TH);
+    dim3 grid(tiles, n_views);
+    if (trace && loss && interior)
+        k_render<true, true, true><<<grid, kThreads, 0, c->stream>>>(p);
+    else if (trace && !loss && !interior)
+        k_render<true, false, false><<<grid, kThreads, 0, c->stream>>>(p);
+    else if (!trace && !loss && interior)
+        k_render<false, false, true><<<grid, kThreads, 0, c->stream>>>(p);
+    else if (trace && loss && !interior)
+        k_render<true, true, false><<<grid, kThreads, 0, c->stream>>>(p);
+    else
+        throw std::runtime_error("unsupported render mode");
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace cdr

@@ -1,0 +1,236 @@
+"""GPU parity: libcdr.so (through the C-ABI) against the CPU oracle on identical
+inputs and the shared counter-RNG stream.
+
+Bars (BASELINE.json north_star): triangle-ID and visibility buffers bit-exact;
+images within 1e-5 relative L2; vertex and texel gradients within 1e-4
+relative L2. Silhouette segment sets are required bit-exact too (the boundary
+pass's importance sampling depends on them).
+"""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import Oracle, RefLib, SEGMENT_DTYPE as ORC_SEG
+from paper_2103_15208_b200 import scenes as S
+from paper_2103_15208_b200.api import (NonFiniteGradient, RenderSettings, Renderer, SizeMismatch,
+                                       param_layout)
+from tests.scenes_util import blob_scene, rel_l2, small_scene, targets_for
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-5
+GRAD_TOL = 1e-4
+
+
+def _pair(scene):
+    return Renderer(0, scene), Oracle(scene)
+
+
+def _seg_equal(a, b):
+    assert len(a) == len(b)
+    for k in ORC_SEG.names:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+@pytest.fixture(scope="module")
+def sphere():
+    return small_scene(freq=5, tex=16, views=3, image=40)
+
+
+def test_normals_and_tmin_bit_exact(sphere):
+    r, o = _pair(sphere)
+    np.testing.assert_array_equal(r.vertex_normals(), o.vertex_normals())
+
+
+@pytest.mark.parametrize("spp", [1, 4, 9, 16])
+def test_render_bit_exact(sphere, spp):
+    r, o = _pair(sphere)
+    st = RenderSettings(spp=spp, seed=3)
+    for v in range(len(sphere.cameras)):
+        rg, mg, hg = r.render(v, st)
+        ro, mo, ho = o.render(v, spp, 3)
+        np.testing.assert_array_equal(hg, ho)      # triangle IDs: bit-exact
+        np.testing.assert_array_equal(mg, mo)      # visibility mask: bit-exact
+        assert rel_l2(rg, ro) <= IMG_TOL
+        # fp32-representable textures + unfused fp64: the image is bit-exact too
+        np.testing.assert_array_equal(rg, ro)
+
+
+def test_radiance_at_matches(sphere):
+    r, o = _pair(sphere)
+    rng = np.random.default_rng(0)
+    xy = rng.uniform(0, 40, size=(500, 2))
+    a, ta = r.radiance_at(1, xy)
+    b, tb = o.radiance_at(1, xy)
+    np.testing.assert_array_equal(ta, tb)
+    assert rel_l2(a, b) <= IMG_TOL
+
+
+def test_view_loss(sphere):
+    r, o = _pair(sphere)
+    rng = np.random.default_rng(1)
+    a = rng.uniform(-0.1, 1.2, size=(40, 40, 3))
+    t = rng.uniform(0, 1, size=(40, 40, 3))
+    m = (rng.uniform(size=(40, 40)) > 0.3).astype(np.float64)
+    for mask, use in ((None, False), (m, True)):
+        vg, ag = r.view_rendering_loss(a, t, 0.7, 2.2, mask, use)
+        vo, ao = o.view_loss(a, t, mask, 0.7, 2.2, use)
+        assert abs(vg - vo) <= 1e-12 * abs(vo)
+        assert rel_l2(ag, ao) <= 1e-12
+    v0, a0 = r.view_rendering_loss(a, t, 0.0)
+    assert v0 == 0 and not a0.any()
+    with pytest.raises(SizeMismatch):
+        r.view_rendering_loss(a, t[:20])
+
+
+@pytest.mark.parametrize("light", [False, True])
+def test_interior_pass(sphere, light):
+    r, o = _pair(sphere)
+    spp, seed = 4, 5
+    tg = targets_for(sphere, spp, seed, Oracle)
+    lay = param_layout(sphere, optimize_light=light)
+    for v in range(len(sphere.cameras)):
+        img, _, hit = o.render(v, spp, seed)
+        _, adj = o.view_loss(img, tg[v])
+        go = o.interior(v, adj, spp, seed, hit, lay)
+        gg = r.interior_pass(v, adj, RenderSettings(spp=spp, seed=seed), hit, lay)
+        ntex = sphere.tex_res[0] * sphere.tex_res[1]
+        sizes = {"positions": 3 * sphere.mesh.V, "diffuse": 3 * ntex, "specular": 3 * ntex, "roughness": ntex}
+        for name, n in sizes.items():
+            a0 = lay[name]
+            assert rel_l2(gg[a0:a0 + n], go[a0:a0 + n]) <= GRAD_TOL, name
+        if light:
+            assert rel_l2(gg[-3:], go[-3:]) <= GRAD_TOL
+    with pytest.raises(SizeMismatch):
+        r.interior_pass(0, adj, RenderSettings(spp=spp, seed=seed), hit[:-1], lay)
+
+
+def test_silhouettes_bit_exact(sphere):
+    r, o = _pair(sphere)
+    for v in range(len(sphere.cameras)):
+        sg, tg = r.extract_silhouettes(v)
+        so, to = o.silhouettes(v)
+        _seg_equal(sg, so)
+        assert tg == to
+
+
+@pytest.mark.parametrize("probe", [0, 1])
+def test_boundary_pass(sphere, probe):
+    r, o = _pair(sphere)
+    spp, seed = 4, 9
+    tg = targets_for(sphere, spp, seed, Oracle)
+    lay = param_layout(sphere)
+    for v in range(len(sphere.cameras)):
+        img, _, _ = o.render(v, spp, seed)
+        _, adj = o.view_loss(img, tg[v])
+        go, do = o.boundary(v, adj, 40 * 40, seed, lay, probe=probe)
+        gg, dg = r.boundary_pass(v, adj, 40 * 40, seed, lay, probe=probe)
+        assert dg == do
+        assert np.linalg.norm(go) > 0
+        assert rel_l2(gg, go) <= GRAD_TOL
+
+
+def _loss_grad_check(scene, spp, seed, lay, use_mask=False, masks=None, lam_lap=0.1, bterm=True, bsamples=0):
+    r, o = _pair(scene)
+    tg = targets_for(scene, spp, seed, Oracle)
+    st = RenderSettings(spp=spp, seed=seed, boundary_term=bterm, boundary_samples=bsamples)
+    from oracle.pyoracle import settings as osettings
+    lo, go, ro = o.loss_grad(tg, osettings(spp, seed, boundary_term=int(bterm), boundary_samples=bsamples), lay,
+                             lam_lap=lam_lap, targets_mask=masks, use_mask=use_mask, want_rendered=True)
+    for k in range(len(scene.cameras)):
+        r.set_target(k, tg[k], None if masks is None else masks[k])
+    lg, gg, stats, rg = r.loss_grad(np.arange(len(scene.cameras)), st, lay, 1.0, lam_lap, 0, use_mask,
+                                    want_rendered=True)
+    np.testing.assert_array_equal(rg, ro.ravel())
+    assert abs(lg[0] - lo[0]) <= 1e-10 * max(1e-300, abs(lo[0]))
+    assert abs(lg[1] - lo[1]) <= 1e-10 * max(1e-300, abs(lo[1]))
+    pos = slice(lay["positions"], lay["positions"] + 3 * scene.mesh.V)
+    tex = slice(lay["diffuse"], lay["total"])
+    assert rel_l2(gg[pos], go[pos]) <= GRAD_TOL
+    assert rel_l2(gg[tex], go[tex]) <= GRAD_TOL
+    assert stats.samples == sum(c.width * c.height for c in scene.cameras) * spp
+    return stats
+
+
+def test_loss_grad_matches_oracle(sphere):
+    st = _loss_grad_check(sphere, 4, 1, param_layout(sphere))
+    assert st.hit_samples > 0 and st.adjoint_samples > 0 and st.boundary_active > 0
+
+
+def test_loss_grad_blob_selfoccluding():
+    sc = blob_scene(freq=8, tex=32, views=2, image=48)
+    _loss_grad_check(sc, 4, 2, param_layout(sc, optimize_light=True))
+
+
+def test_loss_grad_masks_and_options(sphere):
+    rng = np.random.default_rng(3)
+    masks = (rng.uniform(size=(3, 40, 40)) > 0.2).astype(np.float64)
+    _loss_grad_check(sphere, 4, 1, param_layout(sphere), use_mask=True, masks=masks)
+    _loss_grad_check(sphere, 1, 4, param_layout(sphere), lam_lap=0.0, bterm=False)
+    _loss_grad_check(sphere, 9, 4, param_layout(sphere), bsamples=333)
+
+
+def test_laplacian(sphere):
+    r, o = _pair(sphere)
+    for mode in (0, 1):
+        vo, go, (oo, io, xo) = o.laplacian(mode, 0.3)
+        og, ig, xg = r.cotangent_laplacian(mode)
+        np.testing.assert_array_equal(og, oo)
+        np.testing.assert_array_equal(ig, io)
+        np.testing.assert_array_equal(xg, xo)
+        vg, gg = r.laplacian_loss(mode, 0.3)
+        assert abs(vg - vo) <= 1e-12 * abs(vo)
+        np.testing.assert_array_equal(gg, go)
+
+
+def test_empty_scene_renders_background():
+    # render.cpp / test_render.cpp:67-76: no triangles -> zero image and mask
+    m = S.Mesh(np.zeros((0, 3)), np.zeros((0, 3), np.int32), np.zeros((0, 2)))
+    d, s, rr = S.constant_maps(4, (1, 1, 1), (0, 0, 0), 0.5)
+    sc = S.Scene(m, d, s, rr, S.sample_views_on_sphere(1, 2.5, 11, 40, 16, 16))
+    r = Renderer(0, sc)
+    img, mask, hit = r.render(0, RenderSettings(spp=4))
+    assert not img.any() and not mask.any() and (hit == -1).all()
+
+
+def test_mixed_view_sizes_and_global_ids():
+    sc = small_scene(freq=4, tex=8, views=2, image=24)
+    sc.cameras[1] = S.look_at(sc.cameras[1].origin, [0, 0, 0], [0, 0, 1], 35.0, 31, 17)
+    ids = [5, 2]
+    r = Renderer(0, sc, view_ids=ids)
+    o = Oracle(sc, view_ids=ids)
+    for v in range(2):
+        a = r.render(v, RenderSettings(spp=4, seed=8))
+        b = o.render(v, 4, 8)
+        np.testing.assert_array_equal(a[2], b[2])
+        np.testing.assert_array_equal(a[0], b[0])
+
+
+def test_nonfinite_gradient_is_reported():
+    sc = small_scene(freq=3, tex=8, views=1, image=16)
+    sc.light = np.array([np.inf, 1.0, 1.0])
+    r = Renderer(0, sc)
+    o = Oracle(sc)
+    img, _, hit = o.render(0, 4, 1)
+    adj = np.full((16, 16, 3), 1e-3)
+    with pytest.raises(NonFiniteGradient):
+        r.interior_pass(0, adj, RenderSettings(spp=4, seed=1), hit, param_layout(sc))
+
+
+@pytest.mark.ref
+def test_gpu_matches_reference_directly(sphere):
+    """Straight against the reference compiled from its own sources."""
+    ref = RefLib(sphere)
+    r = Renderer(0, sphere)
+    spp, seed = 4, 1
+    lay = param_layout(sphere)
+    tg = targets_for(sphere, spp, seed, Oracle)
+    bd, gr, rr = ref.total_loss(tg, spp, seed, lay, want_rendered=True)
+    bd_g, gg, rend = r.total_loss(list(tg), RenderSettings(spp=spp, seed=seed), lay)
+    assert abs(bd_g["rend"] - bd[1]) <= 1e-10 * bd[1]
+    assert abs(bd_g["lap"] - bd[2]) <= 1e-10 * bd[2]
+    pos = slice(0, 3 * sphere.mesh.V)
+    assert rel_l2(gg[pos], gr[pos]) <= GRAD_TOL
+    assert rel_l2(gg[pos.stop:], gr[pos.stop:]) <= GRAD_TOL
+    for v in range(len(sphere.cameras)):
+        np.testing.assert_array_equal(r.render(v, RenderSettings(spp=spp, seed=seed))[2],
+                                      ref.render(v, spp, seed)[2])
