@@ -113,11 +113,13 @@ typedef struct cdr_stats {
     int32_t degenerate_skipped;
     int32_t nonfinite;         /* 1 if a NonFiniteGradient was raised */
     double ms_prepare;         /* normals + LBVH + t_min */
-    double ms_render;          /* fused trace/shade/loss/interior kernel */
+    double ms_render;          /* trace + fused shade/loss/interior kernels */
     double ms_silhouette;
     double ms_boundary;
     double ms_finalize;        /* normal chain + position gather + Laplacian */
     double ms_total;
+    int64_t kernel_launches;   /* kernels this library launched in the call */
+    double ms_trace;           /* primary-visibility kernel (part of ms_render) */
 } cdr_stats;
 
 int cdr_abi_version(void);

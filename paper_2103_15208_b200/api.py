@@ -70,7 +70,8 @@ class cdr_stats(C.Structure):
                 ("boundary_active", C.c_int64), ("segments", C.c_int64),
                 ("degenerate_skipped", C.c_int32), ("nonfinite", C.c_int32),
                 ("ms_prepare", C.c_double), ("ms_render", C.c_double), ("ms_silhouette", C.c_double),
-                ("ms_boundary", C.c_double), ("ms_finalize", C.c_double), ("ms_total", C.c_double)]
+                ("ms_boundary", C.c_double), ("ms_finalize", C.c_double), ("ms_total", C.c_double),
+                ("kernel_launches", C.c_int64), ("ms_trace", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

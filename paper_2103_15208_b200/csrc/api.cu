@@ -711,16 +711,17 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
     }
     cudaStream_t s = c->stream;
     auto& ev = c->ev;
+    c->launches = 0;
     CDR_CUDA_CHECK(cudaEventRecord(ev[0], s));
-    ensure_prepared(c, /*force=*/true);  // GradContext is rebuilt per total_loss (losses.cpp:251)
-    CDR_CUDA_CHECK(cudaEventRecord(ev[1], s));
-    zero_grad(c, lay->total);
+    zero_grad(c, lay->total);  // fresh GradVector (losses.cpp:250)
     reset_flags(c);
     ensure_hit_arena(c, spp);
     CDR_CUDA_CHECK(cudaMemsetAsync(c->loss_acc.p, 0, sizeof(double) * c->views.size(), s));
+    ensure_prepared(c, /*force=*/true);  // GradContext is rebuilt per total_loss (losses.cpp:251)
+    CDR_CUDA_CHECK(cudaEventRecord(ev[1], s));
     RenderArgs a = render_args(c, st, lay);
     a.use_mask = use_mask;
-    launch_render(c, slots.data(), n, a, true, true, true, scales.data());
+    launch_render(c, slots.data(), n, a, true, true, true, scales.data(), ev[7]);
     CDR_CUDA_CHECK(cudaEventRecord(ev[2], s));
     if (st->boundary_term) {
         set_view_calls(c, slots.data(), samples.data(), n);
@@ -807,12 +808,16 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
         for (int i = 0; i < 6; ++i) CDR_CUDA_CHECK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
         stats->ms_prepare = ms[0];
         stats->ms_render = ms[1];
+        float mt;
+        CDR_CUDA_CHECK(cudaEventElapsedTime(&mt, ev[1], ev[7]));
+        stats->ms_trace = mt;
         stats->ms_silhouette = ms[2];
         stats->ms_boundary = ms[3];
         stats->ms_finalize = ms[4];
         float tot;
         CDR_CUDA_CHECK(cudaEventElapsedTime(&tot, ev[0], ev[6]));
         stats->ms_total = tot;
+        stats->kernel_launches = c->launches;
     }
     API_END
 }

@@ -202,6 +202,7 @@ struct BParams {
     const double* totals;
     const int32_t* count;
     int E;
+    int m_stride;  // per-view stride of the sample arrays (max M)
     uint64_t seed;
     int probe;
     const double* adj;
@@ -209,51 +210,131 @@ struct BParams {
     int64_t lay_pos;
     ErrorInfo* err;
     Counters* counters;
+    int32_t* seg_count;  // n_views x E : active samples per segment
+    int32_t* seg_off;    // n_views x E : exclusive scan of seg_count
+    int32_t* n_active;   // n_views
+    int32_t* key;        // n_views x m_stride : segment of sample i (-1 inactive)
+    int32_t* slot;       // n_views x m_stride : rank inside its segment
+    int32_t* order;      // n_views x m_stride : sample indices grouped by segment
 };
 
+// Steps of diff_render.cpp:232-244 for sample i: RNG pick, lower_bound,
+// position on the segment, pixel adjoint; false when the sample is skipped.
+struct BSample {
+    int si;
+    double s;
+    D2 xq;
+    D3 adj;
+    const cdr_segment* sg;
+};
+
+__device__ __forceinline__ bool boundary_setup(const BParams& p, int vi, int64_t i, BSample& b) {
+    const DevCamera& cam = p.cams[p.calls[vi].slot];
+    const int nseg = p.count[vi];
+    if (p.totals[3 * vi + 1] == 0.0 || i >= p.calls[vi].samples) return false;
+    const double total_len = p.totals[3 * vi];
+    Rng rng = rng2(p.seed, uint64_t(cam.gid) + 0xb0d1, uint64_t(i));
+    double pick = rng.next_double() * total_len;
+    const double* cdf = p.cdf + size_t(vi) * p.E;
+    int lo = 0, hi = nseg;  // std::lower_bound
+    while (lo < hi) {
+        int mid = lo + ((hi - lo) >> 1);
+        if (cdf[mid] < pick) lo = mid + 1;
+        else hi = mid;
+    }
+    b.si = lo < nseg - 1 ? lo : nseg - 1;
+    b.sg = p.segs + size_t(vi) * p.E + b.si;
+    if (b.sg->length_px < 1e-12) return false;
+    b.s = rng.next_double();
+    const cdr_segment* sg = b.sg;
+    b.xq = D2{sg->q0[0] + (sg->q1[0] - sg->q0[0]) * b.s, sg->q0[1] + (sg->q1[1] - sg->q0[1]) * b.s};
+    int px = int(floor(b.xq.x)), py = int(floor(b.xq.y));
+    px = px < 0 ? 0 : (px > cam.W - 1 ? cam.W - 1 : px);
+    py = py < 0 ? 0 : (py > cam.H - 1 ? cam.H - 1 : py);
+    b.adj = ld3(p.adj + 3 * (p.pix_off[p.calls[vi].slot] + size_t(py) * cam.W + px));
+    return !(b.adj.x == 0 && b.adj.y == 0 && b.adj.z == 0);
+}
+
+// pass 1: classify every sample, count active samples per segment
+__global__ void __launch_bounds__(kBlock) k_bsample(BParams p) {
+    const int vi = blockIdx.y;
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    BSample b;
+    bool act = i < p.m_stride && boundary_setup(p, vi, i, b);
+    const int key = act ? b.si : -1 - int(threadIdx.x & 31);
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (act && lane == leader) base = atomicAdd(&p.seg_count[size_t(vi) * p.E + b.si], __popc(peers));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (i < p.m_stride) {
+        size_t o = size_t(vi) * p.m_stride + i;
+        p.key[o] = act ? b.si : -1;
+        p.slot[o] = base + __popc(peers & ((1u << lane) - 1u));
+    }
+}
+
+// pass 2 (one CTA per view): exclusive scan of the per-segment counts
+__global__ void k_bscan(const int32_t* __restrict__ count, const int32_t* __restrict__ nseg, int E,
+                        int32_t* __restrict__ off, int32_t* __restrict__ n_active) {
+    const int vi = blockIdx.x;
+    const int n = nseg[vi];
+    __shared__ int32_t sh[1024];
+    __shared__ int32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int base = 0; base < n; base += 1024) {
+        int i = base + threadIdx.x;
+        int v = i < n ? count[size_t(vi) * E + i] : 0;
+        sh[threadIdx.x] = v;
+        __syncthreads();
+        for (int o = 1; o < 1024; o <<= 1) {
+            int t = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+            __syncthreads();
+            sh[threadIdx.x] += t;
+            __syncthreads();
+        }
+        if (i < n) off[size_t(vi) * E + i] = carry + sh[threadIdx.x] - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += sh[1023];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) n_active[vi] = carry;
+}
+
+// pass 3: sample indices grouped by segment
+__global__ void k_bscatter(BParams p) {
+    const int vi = blockIdx.y;
+    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= p.m_stride) return;
+    size_t o = size_t(vi) * p.m_stride + i;
+    int k = p.key[o];
+    if (k < 0) return;
+    p.order[size_t(vi) * p.m_stride + p.seg_off[size_t(vi) * p.E + k] + p.slot[o]] = int32_t(i);
+}
+
+// pass 4: the two radiance probes and the vertex deposit, in segment order so a
+// warp traces neighbouring rays along one silhouette edge (diff_render.cpp:246-277)
 __global__ void __launch_bounds__(kBlock) k_boundary(BParams p) {
     const int vi = blockIdx.y;
     const int lane = threadIdx.x & 31;
     const DevCamera& cam = p.cams[p.calls[vi].slot];
-    const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int nseg = p.count[vi];
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int n_act = p.n_active[vi];
+    if (int64_t(blockIdx.x) * blockDim.x >= n_act) return;  // whole CTA idle (uniform)
+    BSample b;
+    bool act = false;
+    if (j < n_act) act = boundary_setup(p, vi, p.order[size_t(vi) * p.m_stride + j], b);
     const int samples = p.calls[vi].samples;
-    const bool enabled = p.totals[3 * vi + 1] != 0.0;
     const double total_len = p.totals[3 * vi];
-    bool act = enabled && i < samples;
-    int si = 0;
-    double s = 0;
-    D2 xq{0, 0}, n2{0, 0};
-    D3 adj{0, 0, 0};
-    const cdr_segment* sg = nullptr;
-    if (act) {
-        Rng rng = rng2(p.seed, uint64_t(cam.gid) + 0xb0d1, uint64_t(i));
-        double pick = rng.next_double() * total_len;
-        const double* cdf = p.cdf + size_t(vi) * p.E;
-        int lo = 0, hi = nseg;  // std::lower_bound
-        while (lo < hi) {
-            int mid = lo + ((hi - lo) >> 1);
-            if (cdf[mid] < pick) lo = mid + 1;
-            else hi = mid;
-        }
-        si = lo < nseg - 1 ? lo : nseg - 1;
-        sg = p.segs + size_t(vi) * p.E + si;
-        if (sg->length_px < 1e-12) act = false;
-        if (act) {
-            s = rng.next_double();
-            xq = D2{sg->q0[0] + (sg->q1[0] - sg->q0[0]) * s, sg->q0[1] + (sg->q1[1] - sg->q0[1]) * s};
-            int px = int(floor(xq.x)), py = int(floor(xq.y));
-            px = px < 0 ? 0 : (px > cam.W - 1 ? cam.W - 1 : px);
-            py = py < 0 ? 0 : (py > cam.H - 1 ? cam.H - 1 : py);
-            adj = ld3(p.adj + 3 * (p.pix_off[p.calls[vi].slot] + size_t(py) * cam.W + px));
-            if (adj.x == 0 && adj.y == 0 && adj.z == 0) act = false;
-        }
-    }
     double weighted = 0;
+    D2 n2{0, 0};
     if (act) {
+        const cdr_segment* sg = b.sg;
         D2 tg{(sg->q1[0] - sg->q0[0]) / sg->length_px, (sg->q1[1] - sg->q0[1]) / sg->length_px};
         n2 = D2{-tg.y, tg.x};
-        D2 xm{xq.x - n2.x * 0.5, xq.y - n2.y * 0.5}, xp{xq.x + n2.x * 0.5, xq.y + n2.y * 0.5};
+        D2 xm{b.xq.x - n2.x * 0.5, b.xq.y - n2.y * 0.5}, xp{b.xq.x + n2.x * 0.5, b.xq.y + n2.y * 0.5};
         const double t_min = p.info->t_min;
         D3 delta;
         if (p.probe == CDR_PROBE_RADIANCE) {
@@ -266,10 +347,10 @@ __global__ void __launch_bounds__(kBlock) k_boundary(BParams p) {
             double cp = trace(p.sc.nodes, p.sc.recs, p.sc.n_tris, org, primary_dir(cam, xp), t_min).tri >= 0 ? 1.0 : 0.0;
             delta = D3{cm - cp, cm - cp, cm - cp};
         }
-        weighted = dot(adj, delta);
+        weighted = dot(b.adj, delta);
         if (weighted == 0) act = false;
         else if (!isfinite(weighted)) {
-            if (atomicCAS(&p.err->flag, 0, 2) == 0) p.err->segment = si;
+            if (atomicCAS(&p.err->flag, 0, 2) == 0) p.err->segment = b.si;
             act = false;
         }
     }
@@ -279,7 +360,8 @@ __global__ void __launch_bounds__(kBlock) k_boundary(BParams p) {
     }
     double v[6] = {0, 0, 0, 0, 0, 0};
     if (act) {
-        double w0 = (1.0 - s) / sg->z0, w1 = s / sg->z1;
+        const cdr_segment* sg = b.sg;
+        double w0 = (1.0 - b.s) / sg->z0, w1 = b.s / sg->z1;
         double t3 = (w0 * sg->t0 + w1 * sg->t1) / (w0 + w1);  // segment_param_2d_to_3d
         D3 p0{sg->p0[0], sg->p0[1], sg->p0[2]}, p1{sg->p1[0], sg->p1[1], sg->p1[2]};
         D3 point = p0 + (p1 - p0) * t3;
@@ -291,14 +373,14 @@ __global__ void __launch_bounds__(kBlock) k_boundary(BParams p) {
         v[0] = g0.x; v[1] = g0.y; v[2] = g0.z;
         v[3] = g1.x; v[4] = g1.y; v[5] = g1.z;
     }
-    const int key = act ? si : -1 - lane;
+    const int key = act ? b.si : -1 - lane;
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     reduce_peers<6>(0xffffffffu, peers, v);
     if (act && (__ffs(peers) - 1) == lane) {
         double* g = p.grad + p.lay_pos;
         for (int c = 0; c < 3; ++c) {
-            if (v[c] != 0) atomicAdd(g + 3 * int64_t(sg->v0) + c, v[c]);
-            if (v[3 + c] != 0) atomicAdd(g + 3 * int64_t(sg->v1) + c, v[3 + c]);
+            if (v[c] != 0) atomicAdd(g + 3 * int64_t(b.sg->v0) + c, v[c]);
+            if (v[3 + c] != 0) atomicAdd(g + 3 * int64_t(b.sg->v1) + c, v[3 + c]);
         }
     }
 }
@@ -348,20 +430,20 @@ void launch_silhouettes(cdr_ctx* c, int n_views) {
         return;
     }
     dim3 grid(nb, n_views);
-    k_sil_flag<<<grid, kBlock, 0, c->stream>>>(c->pos.p, c->fnormal.p, c->edges.p, c->E, c->d_cams.p,
-                                               st.calls.p, c->sil_flag.p, c->sil_block_count.p, nb);
-    k_sil_scan<<<n_views, 1024, 0, c->stream>>>(c->sil_block_count.p, nb, c->sil_block_off.p,
-                                                c->sil_count.p);
-    k_sil_write<<<grid, kBlock, 0, c->stream>>>(c->pos.p, c->fnormal.p, c->edges.p, c->E, c->d_cams.p,
+    { ++c->launches; k_sil_flag<<<grid, kBlock, 0, c->stream>>>(c->pos.p, c->fnormal.p, c->edges.p, c->E, c->d_cams.p,
+                                               st.calls.p, c->sil_flag.p, c->sil_block_count.p, nb); }
+    { ++c->launches; k_sil_scan<<<n_views, 1024, 0, c->stream>>>(c->sil_block_count.p, nb, c->sil_block_off.p,
+                                                c->sil_count.p); }
+    { ++c->launches; k_sil_write<<<grid, kBlock, 0, c->stream>>>(c->pos.p, c->fnormal.p, c->edges.p, c->E, c->d_cams.p,
                                                 st.calls.p, c->sil_flag.p, c->sil_block_off.p, nb,
-                                                c->segs.p);
+                                                c->segs.p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_cdf(cdr_ctx* c, int n_views) {
     if (n_views <= 0) return;
-    k_cdf<<<(n_views + 31) / 32, 32, 0, c->stream>>>(c->segs.p, c->sil_count.p, std::max(1, c->E),
-                                                     n_views, c->cdf.p, c->total_len.p, c->degenerate.p);
+    { ++c->launches; k_cdf<<<(n_views + 31) / 32, 32, 0, c->stream>>>(c->segs.p, c->sil_count.p, std::max(1, c->E),
+                                                     n_views, c->cdf.p, c->total_len.p, c->degenerate.p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -375,6 +457,15 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     st.pix_off.ensure(nslots);
     CDR_CUDA_CHECK(cudaMemcpyAsync(st.pix_off.p, offs.data(), sizeof(size_t) * nslots,
                                    cudaMemcpyHostToDevice, c->stream));
+    const int E = std::max(1, c->E);
+    const size_t nm = size_t(n_views) * samples;
+    c->b_seg_count.ensure(size_t(n_views) * E);
+    c->b_seg_off.ensure(size_t(n_views) * E);
+    c->b_n_active.ensure(n_views);
+    c->b_key.ensure(nm);
+    c->b_slot.ensure(nm);
+    c->b_order.ensure(nm);
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->b_seg_count.p, 0, sizeof(int32_t) * size_t(n_views) * E, c->stream));
     BParams p{};
     p.sc = shade_scene(c);
     p.info = c->info.p;
@@ -385,7 +476,8 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     p.cdf = c->cdf.p;
     p.totals = c->total_len.p;
     p.count = c->sil_count.p;
-    p.E = std::max(1, c->E);
+    p.E = E;
+    p.m_stride = samples;
     p.seed = seed;
     p.probe = probe;
     p.adj = c->adj.p;
@@ -393,8 +485,17 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     p.lay_pos = lay_pos;
     p.err = c->errinfo.p;
     p.counters = c->counters.p;
+    p.seg_count = c->b_seg_count.p;
+    p.seg_off = c->b_seg_off.p;
+    p.n_active = c->b_n_active.p;
+    p.key = c->b_key.p;
+    p.slot = c->b_slot.p;
+    p.order = c->b_order.p;
     dim3 grid((samples + kBlock - 1) / kBlock, n_views);
-    k_boundary<<<grid, kBlock, 0, c->stream>>>(p);
+    { ++c->launches; k_bsample<<<grid, kBlock, 0, c->stream>>>(p); }
+    { ++c->launches; k_bscan<<<n_views, 1024, 0, c->stream>>>(p.seg_count, p.count, E, p.seg_off, p.n_active); }
+    { ++c->launches; k_bscatter<<<grid, kBlock, 0, c->stream>>>(p); }
+    { ++c->launches; k_boundary<<<grid, kBlock, 0, c->stream>>>(p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -116,6 +116,8 @@ struct cdr_ctx {
     cdr::DBuf<cdr_segment> segs;
     cdr::DBuf<double> cdf, total_len;
     cdr::DBuf<int32_t> degenerate;
+    // boundary samples binned by segment
+    cdr::DBuf<int32_t> b_seg_count, b_seg_off, b_n_active, b_key, b_slot, b_order;
 
     // gradient + accumulators
     int64_t grad_n = 0;
@@ -126,8 +128,9 @@ struct cdr_ctx {
     cdr::DBuf<cdr::ErrorInfo> errinfo;
     cdr::DBuf<cdr::Counters> counters;
 
-    // timing
+    // timing and launch accounting (cdr_stats::kernel_launches)
     std::vector<cudaEvent_t> ev;
+    int64_t launches = 0;
 
     // multi-GPU
     void* nccl_comm = nullptr;

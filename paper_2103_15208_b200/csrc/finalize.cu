@@ -156,10 +156,10 @@ void launch_finalize_positions(cdr_ctx* c, int64_t lay_pos) {
     if (c->V == 0) return;
     c->qvec.ensure(size_t(3) * c->V);
     double* gp = c->grad.p + lay_pos;
-    k_corner_gather<<<blocks(c->V), kBlock, 0, c->stream>>>(c->corner_acc.p, c->vf_start.p, c->vf_list.p,
-                                                            c->accum.p, c->V, gp, c->qvec.p);
-    k_normal_chain<<<blocks(c->V), kBlock, 0, c->stream>>>(c->pos.p, c->tris.p, c->vf_start.p,
-                                                           c->vf_list.p, c->qvec.p, c->V, gp);
+    { ++c->launches; k_corner_gather<<<blocks(c->V), kBlock, 0, c->stream>>>(c->corner_acc.p, c->vf_start.p, c->vf_list.p,
+                                                            c->accum.p, c->V, gp, c->qvec.p); }
+    { ++c->launches; k_normal_chain<<<blocks(c->V), kBlock, 0, c->stream>>>(c->pos.p, c->tris.p, c->vf_start.p,
+                                                           c->vf_list.p, c->qvec.p, c->V, gp); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -171,17 +171,17 @@ void launch_laplacian(cdr_ctx* c, int mode, double lambda, double* grad_pos) {
     CDR_CUDA_CHECK(cudaMemsetAsync(c->lap_partial.p, 0, sizeof(double), c->stream));
     if (V == 0) return;
     if (c->E > 0)
-        k_lap_weights<<<blocks(c->E), kBlock, 0, c->stream>>>(c->pos.p, c->tris.p, c->edges.p,
-                                                              c->lap_edge_slot.p, c->E, mode, c->lap_val.p);
-    k_lap_diag<<<blocks(V), kBlock, 0, c->stream>>>(c->lap_rowptr.p, c->lap_col.p, c->lap_diag_slot.p, V,
-                                                    c->lap_val.p);
+        { ++c->launches; k_lap_weights<<<blocks(c->E), kBlock, 0, c->stream>>>(c->pos.p, c->tris.p, c->edges.p,
+                                                              c->lap_edge_slot.p, c->E, mode, c->lap_val.p); }
+    { ++c->launches; k_lap_diag<<<blocks(V), kBlock, 0, c->stream>>>(c->lap_rowptr.p, c->lap_col.p, c->lap_diag_slot.p, V,
+                                                    c->lap_val.p); }
     if (lambda != 0) {
         c->lap_lv.ensure(size_t(3) * V);
-        k_lap_lv<<<blocks(V), kBlock, 0, c->stream>>>(c->lap_rowptr.p, c->lap_col.p, c->lap_val.p, c->pos.p,
-                                                      V, c->lap_lv.p, c->lap_partial.p);
+        { ++c->launches; k_lap_lv<<<blocks(V), kBlock, 0, c->stream>>>(c->lap_rowptr.p, c->lap_col.p, c->lap_val.p, c->pos.p,
+                                                      V, c->lap_lv.p, c->lap_partial.p); }
         if (grad_pos)
-            k_lap_grad<<<blocks(V), kBlock, 0, c->stream>>>(c->lap_rowptr.p, c->lap_col.p, c->lap_val.p,
-                                                            c->lap_lv.p, V, 2.0 * lambda, grad_pos);
+            { ++c->launches; k_lap_grad<<<blocks(V), kBlock, 0, c->stream>>>(c->lap_rowptr.p, c->lap_col.p, c->lap_val.p,
+                                                            c->lap_lv.p, V, 2.0 * lambda, grad_pos); }
     }
     CDR_CUDA_CHECK(cudaGetLastError());
 }

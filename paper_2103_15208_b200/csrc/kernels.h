@@ -49,7 +49,8 @@ struct RenderArgs {
     int64_t lay_diffuse, lay_specular, lay_roughness, lay_light;  // -1 = absent
 };
 void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a,
-                   bool trace, bool loss, bool interior, const double* loss_scales);
+                   bool trace, bool loss, bool interior, const double* loss_scales,
+                   cudaEvent_t after_trace = nullptr);
 
 // boundary.cu — extract_silhouettes (silhouette.cpp:55-106), the CDF of
 // boundary_pass (diff_render.cpp:213-228) and its edge samples (:230-278).

@@ -243,14 +243,14 @@ void launch_prepare(cdr_ctx* c, double cam_abs_max) {
     cudaStream_t s = c->stream;
     const int V = c->V, T = c->T;
     c->info.ensure(1);
-    if (T > 0) k_face_normals<<<blocks(T), kBlock, 0, s>>>(c->pos.p, c->tris.p, T, c->fnormal.p);
+    if (T > 0) { ++c->launches; k_face_normals<<<blocks(T), kBlock, 0, s>>>(c->pos.p, c->tris.p, T, c->fnormal.p); }
     if (V > 0)
-        k_vertex_normals<<<blocks(V), kBlock, 0, s>>>(c->fnormal.p, c->vf_start.p, c->vf_list.p, V,
-                                                      c->normals.p, c->accum.p);
+        { ++c->launches; k_vertex_normals<<<blocks(V), kBlock, 0, s>>>(c->fnormal.p, c->vf_start.p, c->vf_list.p, V,
+                                                      c->normals.p, c->accum.p); }
     int nb = std::max(1, std::min(blocks(V), 1184));
     c->bbox_partial.ensure(size_t(nb) * 6);
-    k_bbox_partial<<<nb, kBlock, 0, s>>>(c->pos.p, V, c->bbox_partial.p);
-    k_bbox_final<<<1, 32, 0, s>>>(c->bbox_partial.p, nb, T, cam_abs_max, c->info.p);
+    { ++c->launches; k_bbox_partial<<<nb, kBlock, 0, s>>>(c->pos.p, V, c->bbox_partial.p); }
+    { ++c->launches; k_bbox_final<<<1, 32, 0, s>>>(c->bbox_partial.p, nb, T, cam_abs_max, c->info.p); }
     if (T == 0) return;
 
     c->keys.ensure(T);
@@ -260,20 +260,21 @@ void launch_prepare(cdr_ctx* c, double cam_abs_max) {
     c->parent_internal.ensure(std::max(1, T - 1));
     c->parent_leaf.ensure(T);
     c->refit_flag.ensure(std::max(1, T - 1));
-    k_morton<<<blocks(T), kBlock, 0, s>>>(c->pos.p, c->tris.p, T, c->info.p, c->keys.p);
+    { ++c->launches; k_morton<<<blocks(T), kBlock, 0, s>>>(c->pos.p, c->tris.p, T, c->info.p, c->keys.p); }
     size_t tmp = 0;
     int end_bit = 32 + 30;
     cub::DeviceRadixSort::SortKeys(nullptr, tmp, c->keys.p, c->keys_alt.p, T, 0, end_bit, s);
     c->sort_tmp.ensure(tmp);
     cub::DeviceRadixSort::SortKeys(c->sort_tmp.p, tmp, c->keys.p, c->keys_alt.p, T, 0, end_bit, s);
+    c->launches += 1;  // counted as one (CUB onesweep passes)
     if (T > 1) {
-        k_hierarchy<<<blocks(T - 1), kBlock, 0, s>>>(c->keys_alt.p, T, c->nodes.p,
-                                                     c->parent_internal.p, c->parent_leaf.p);
+        { ++c->launches; k_hierarchy<<<blocks(T - 1), kBlock, 0, s>>>(c->keys_alt.p, T, c->nodes.p,
+                                                     c->parent_internal.p, c->parent_leaf.p); }
         CDR_CUDA_CHECK(cudaMemsetAsync(c->refit_flag.p, 0, sizeof(int32_t) * (T - 1), s));
     }
-    k_refit<<<blocks(T), kBlock, 0, s>>>(c->keys_alt.p, c->pos.p, c->tris.p, T, c->info.p,
+    { ++c->launches; k_refit<<<blocks(T), kBlock, 0, s>>>(c->keys_alt.p, c->pos.p, c->tris.p, T, c->info.p,
                                          c->parent_internal.p, c->parent_leaf.p, c->refit_flag.p,
-                                         c->nodes.p, c->recs.p);
+                                         c->nodes.p, c->recs.p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -62,7 +62,34 @@ __device__ __forceinline__ void raise_nonfinite(ErrorInfo* e, int x, int y) {
     }
 }
 
-template <bool kTrace, bool kLoss, bool kInterior>
+// Primary visibility: one thread per sample, tile order as k_render, writes the
+// hit cache (the bit-exact output). Kept slim so it runs at high occupancy —
+// traversal is latency-bound, not bandwidth-bound.
+__global__ void __launch_bounds__(kThreads, 3) k_trace(Params p) {
+    const ViewCall vc = p.calls[blockIdx.y];
+    const DevCamera& cam = p.cams[vc.slot];
+    const int W = cam.W, H = cam.H;
+    const int tiles_x = (W + p.TW - 1) / p.TW;
+    const int tiles_y = (H + p.TH - 1) / p.TH;
+    if (int(blockIdx.x) >= tiles_x * tiles_y) return;
+    const int tid = threadIdx.x;
+    const int spp = p.spp;
+    const int P = kThreads / spp;
+    const int pix = tid / spp, s = tid - (tid / spp) * spp;
+    const int x = (blockIdx.x % tiles_x) * p.TW + pix % p.TW;
+    const int y = (blockIdx.x / tiles_x) * p.TH + pix / p.TW;
+    if (!(pix < P && x < W && y < H)) return;
+    const size_t pidx = p.pix_off[vc.slot] + size_t(y) * W + x;
+    D2 ps = pixel_sample_position(p.seed, cam.gid, x, y, W, s, spp, p.k);
+    D3 dir = primary_dir(cam, ps);
+    Hit h = trace(p.sc.nodes, p.sc.recs, p.sc.n_tris, D3{cam.o[0], cam.o[1], cam.o[2]}, dir, p.info->t_min);
+    p.hit[pidx * spp + s] = h.tri;
+}
+
+// kShade: radiance + pixel mean/mask; kLoss: loss + adjoint; kInterior: scatter.
+// The hit triangle comes from the hit cache and is re-intersected with
+// ray_triangle, exactly as interior_pass replays it (diff_render.cpp:84-93).
+template <bool kShade, bool kLoss, bool kInterior>
 __global__ void __launch_bounds__(kThreads) k_render(Params p) {
     __shared__ double s_rad[kThreads][3];
     __shared__ double s_adj[kThreads][3];  // per pixel (index = pixel in tile)
@@ -83,34 +110,23 @@ __global__ void __launch_bounds__(kThreads) k_render(Params p) {
     const bool valid = pix < P && x < W && y < H;
     const size_t pbase = p.pix_off[vc.slot];
     const size_t pidx = pbase + size_t(y) * W + x;  // arena pixel index
-    const double t_min = p.info->t_min;
     const D3 org{cam.o[0], cam.o[1], cam.o[2]};
 
-    // ---------------- phase 1: sample -> (tri, t, b1, b2), radiance
+    // ---------------- phase 1: cached triangle -> (t, b1, b2), radiance
     int tri = -1;
     double t = 0, b1 = 0, b2 = 0;
     D3 dir{0, 0, 1};
     if (valid) {
         D2 ps = pixel_sample_position(p.seed, cam.gid, x, y, W, s, spp, p.k);
         dir = primary_dir(cam, ps);
-        if (kTrace) {
-            Hit h = trace(p.sc.nodes, p.sc.recs, p.sc.n_tris, org, dir, t_min);
-            tri = h.tri;
-            t = h.t;
-            b1 = h.b1;
-            b2 = h.b2;
-            if (p.write_hits) p.hit[pidx * spp + s] = tri;
-        } else {
-            // interior_pass replay: re-intersect the cached triangle (diff_render.cpp:84-93)
-            tri = p.hit[pidx * spp + s];
-            if (tri >= 0) {
-                int a = p.sc.tris[3 * tri], b = p.sc.tris[3 * tri + 1], c = p.sc.tris[3 * tri + 2];
-                if (!ray_triangle(org, dir, ld3(p.sc.pos + 3 * a), ld3(p.sc.pos + 3 * b), ld3(p.sc.pos + 3 * c), t, b1, b2))
-                    tri = -1;
-            }
+        tri = p.hit[pidx * spp + s];
+        if (tri >= 0) {
+            int a = p.sc.tris[3 * tri], b = p.sc.tris[3 * tri + 1], c = p.sc.tris[3 * tri + 2];
+            if (!ray_triangle(org, dir, ld3(p.sc.pos + 3 * a), ld3(p.sc.pos + 3 * b), ld3(p.sc.pos + 3 * c), t, b1, b2))
+                tri = -1;
         }
     }
-    if (kTrace) {
+    if (kShade) {
         D3 rad{p.sc.bg[0], p.sc.bg[1], p.sc.bg[2]};
         if (tri >= 0) rad = shade_hit(p.sc, Hit{tri, t, b1, b2}, dir);
         s_rad[tid][0] = rad.x;
@@ -127,8 +143,8 @@ __global__ void __launch_bounds__(kThreads) k_render(Params p) {
         const int py = (blockIdx.x / tiles_x) * p.TH + tid / p.TW;
         if (px < W && py < H) {
             const size_t q = pbase + size_t(py) * W + px;
-            D3 mean;
-            if (kTrace) {
+            D3 mean{0, 0, 0};
+            if (kShade) {
                 D3 sum{0, 0, 0};
                 int hits = 0;
                 for (int j = 0; j < spp; ++j) {
@@ -177,7 +193,7 @@ __global__ void __launch_bounds__(kThreads) k_render(Params p) {
         }
     }
     if (!kInterior) {
-        if (kTrace) {
+        if (kShade) {
             int nh = __syncthreads_count(valid && tri >= 0);
             if (tid == 0 && nh) atomicAdd(&p.counters->hit_samples, (unsigned long long)nh);
         }
@@ -413,14 +429,14 @@ __global__ void k_pack_textures(const double* __restrict__ d, const double* __re
 
 void launch_radiance_points(cdr_ctx* c, int slot, int n, const double* xy, double* rgb, int32_t* tri) {
     if (n <= 0) return;
-    k_radiance_points<<<(n + 255) / 256, 256, 0, c->stream>>>(shade_scene(c), c->info.p, c->d_cams.p, slot, n,
-                                                              xy, rgb, tri);
+    { ++c->launches; k_radiance_points<<<(n + 255) / 256, 256, 0, c->stream>>>(shade_scene(c), c->info.p, c->d_cams.p, slot, n,
+                                                              xy, rgb, tri); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_pack_textures(cdr_ctx* c, const double* d, const double* s, const double* r, int n) {
     if (n <= 0) return;
-    k_pack_textures<<<(n + 255) / 256, 256, 0, c->stream>>>(d, s, r, n, c->tex.p);
+    { ++c->launches; k_pack_textures<<<(n + 255) / 256, 256, 0, c->stream>>>(d, s, r, n, c->tex.p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -429,7 +445,7 @@ void launch_view_loss(cdr_ctx* c, int W, int H, const double* rendered, const do
                       double* sum) {
     int n = W * H;
     int nb = std::max(1, std::min((n + 255) / 256, 148 * 8));
-    k_view_loss<<<nb, 256, 0, c->stream>>>(n, rendered, target, tmask, scale, gamma, masked, adj, sum);
+    { ++c->launches; k_view_loss<<<nb, 256, 0, c->stream>>>(n, rendered, target, tmask, scale, gamma, masked, adj, sum); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -450,7 +466,7 @@ static RenderStatics& statics(cdr_ctx* c) {
 }
 
 void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a, bool trace,
-                   bool loss, bool interior, const double* loss_scales) {
+                   bool loss, bool interior, const double* loss_scales, cudaEvent_t after_trace) {
     if (n_views <= 0) return;
     RenderStatics& st = statics(c);
     std::vector<ViewCall> calls(n_views);
@@ -515,14 +531,16 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
 
     int tiles = ((maxW + p.TW - 1) / p.TW) * ((maxH + p.TH - 1) / p.TH);
     dim3 grid(tiles, n_views);
+    if (trace) { ++c->launches; k_trace<<<grid, kThreads, 0, c->stream>>>(p); }
+    if (after_trace) CDR_CUDA_CHECK(cudaEventRecord(after_trace, c->stream));
     if (trace && loss && interior)
-        k_render<true, true, true><<<grid, kThreads, 0, c->stream>>>(p);
+        { ++c->launches; k_render<true, true, true><<<grid, kThreads, 0, c->stream>>>(p); }
     else if (trace && !loss && !interior)
-        k_render<true, false, false><<<grid, kThreads, 0, c->stream>>>(p);
+        { ++c->launches; k_render<true, false, false><<<grid, kThreads, 0, c->stream>>>(p); }
     else if (!trace && !loss && interior)
-        k_render<false, false, true><<<grid, kThreads, 0, c->stream>>>(p);
+        { ++c->launches; k_render<false, false, true><<<grid, kThreads, 0, c->stream>>>(p); }
     else if (trace && loss && !interior)
-        k_render<true, true, false><<<grid, kThreads, 0, c->stream>>>(p);
+        { ++c->launches; k_render<true, true, false><<<grid, kThreads, 0, c->stream>>>(p); }
     else
         throw std::runtime_error("unsupported render mode");
     CDR_CUDA_CHECK(cudaGetLastError());
