@@ -30,7 +30,7 @@ import numpy as np
 
 from .scenes import CAMERA_DTYPE, Scene, camera_struct_array
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libcdr.so")
+LIB_PATH = os.environ.get("CDR_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libcdr.so")
 
 
 class CollodiffError(RuntimeError):

@@ -44,9 +44,9 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, verbose):
-    obj = os.path.join(OBJ_DIR, os.path.basename(src)[:-3] + ".o")
-    cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+def _compile(src, verbose, obj_dir=None, extra=()):
+    obj = os.path.join(obj_dir or OBJ_DIR, os.path.basename(src)[:-3] + ".o")
+    cmd = [NVCC, *FLAGS, *extra, "-c", src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -55,25 +55,29 @@ def _compile(src, verbose):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ_DIR, exist_ok=True)
-    if not force and not _stale(LIB, _deps()):
-        return LIB
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile + link; `out`/`defines` build an experimental variant elsewhere."""
+    lib = out or LIB
+    obj_dir = OBJ_DIR if out is None else os.path.join(os.path.dirname(out), "obj_" + os.path.basename(out))
+    os.makedirs(obj_dir, exist_ok=True)
+    if not force and not _stale(lib, _deps()):
+        return lib
+    extra = [f"-D{d}" for d in defines]
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-        results = list(ex.map(lambda s: _compile(s, verbose), _sources()))
+        results = list(ex.map(lambda s: _compile(s, verbose, obj_dir, extra), _sources()))
     objs = [o for o, _ in results]
     if verbose:
         for _, log in results:
             sys.stderr.write(log)
     # export exactly the C-ABI (cdr_*); everything else stays local
-    vs = os.path.join(OBJ_DIR, "exports.map")
+    vs = os.path.join(obj_dir, "exports.map")
     with open(vs, "w") as f:
         f.write("{ global: cdr_*; local: *; };\n")
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-Xlinker", f"--version-script={vs}", "-ldl"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-Xlinker", f"--version-script={vs}", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -65,7 +65,10 @@ __device__ __forceinline__ void raise_nonfinite(ErrorInfo* e, int x, int y) {
 // Primary visibility: one thread per sample, tile order as k_render, writes the
 // hit cache (the bit-exact output). Kept slim so it runs at high occupancy —
 // traversal is latency-bound, not bandwidth-bound.
-__global__ void __launch_bounds__(kThreads, 3) k_trace(Params p) {
+#ifndef CDR_TRACE_MIN_BLOCKS
+#define CDR_TRACE_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
     const ViewCall vc = p.calls[blockIdx.y];
     const DevCamera& cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
@@ -89,8 +92,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_trace(Params p) {
 // kShade: radiance + pixel mean/mask; kLoss: loss + adjoint; kInterior: scatter.
 // The hit triangle comes from the hit cache and is re-intersected with
 // ray_triangle, exactly as interior_pass replays it (diff_render.cpp:84-93).
+#ifndef CDR_RENDER_MIN_BLOCKS
+#define CDR_RENDER_MIN_BLOCKS 4
+#endif
 template <bool kShade, bool kLoss, bool kInterior>
-__global__ void __launch_bounds__(kThreads) k_render(Params p) {
+__global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
     __shared__ double s_rad[kThreads][3];
     __shared__ double s_adj[kThreads][3];  // per pixel (index = pixel in tile)
     __shared__ unsigned char s_hit[kThreads];
