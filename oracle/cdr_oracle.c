@@ -1129,3 +1129,23 @@ int orc_adjacency(int32_t nv, int32_t nt, const int32_t* tris, int32_t* edges_ou
     free(ks);
     return 0;
 }
+
+/* ---- exported primitives for the known-answer tests ------------------------ */
+double orc_tone_map(double v, double gamma) { return tone(v, gamma); }
+double orc_tone_map_derivative(double v, double gamma) { return tone_d(v, gamma); }
+int orc_project(const cdr_camera* cam, const double* p, double* q, double* depth) {
+    d2 r;
+    int ok = project(cam, ld3(p), &r, depth);
+    if (ok) { q[0] = r.x; q[1] = r.y; }
+    return ok;
+}
+void orc_projection_jacobian(const cdr_camera* cam, const double* p, double* out) {
+    d3 a, b;
+    projection_jacobian(cam, ld3(p), &a, &b);
+    out[0] = a.x; out[1] = a.y; out[2] = a.z;
+    out[3] = b.x; out[4] = b.y; out[5] = b.z;
+}
+int orc_ray_triangle(const double* o, const double* d, const double* p0, const double* p1,
+                     const double* p2, double* tbb) {
+    return ray_triangle(ld3(o), ld3(d), ld3(p0), ld3(p1), ld3(p2), &tbb[0], &tbb[1], &tbb[2]);
+}

@@ -74,6 +74,12 @@ int orc_boundary(const orc_ctx* c, int32_t view, const double* adjoint, int32_t 
                  int32_t* degenerate);
 int orc_laplacian(const orc_scene* s, int32_t mode, double lambda, double* value, double* grad,
                   int32_t* outer, int32_t* inner, double* vals);
+double orc_tone_map(double v, double gamma);
+double orc_tone_map_derivative(double v, double gamma);
+int orc_project(const cdr_camera* cam, const double* p, double* q, double* depth);
+void orc_projection_jacobian(const cdr_camera* cam, const double* p, double* out);
+int orc_ray_triangle(const double* o, const double* d, const double* p0, const double* p1,
+                     const double* p2, double* tbb);
 int orc_loss_grad(const orc_ctx* c, const double* targets_rgb, const double* targets_mask,
                   const cdr_settings* st, double lambda_rend, double lambda_lap,
                   int32_t lap_mode, int32_t use_mask, const cdr_layout* layout,

@@ -210,6 +210,32 @@ def geodesic_sphere(freq: int, radius: float = 0.5) -> Mesh:
     return Mesh(pos, tris.astype(np.int32), spherical_uvs(pos))
 
 
+def icosphere(subdivisions: int, radius: float = 0.5) -> Mesh:
+    """make_icosphere (mesh.cpp:270-298): 4^s midpoint subdivision, vertices in
+    creation order — the mesh the reference's own tests render."""
+    base, faces = _icosahedron()
+    pos = [base[i] for i in range(12)]
+    tris = [tuple(int(x) for x in f) for f in faces]
+    for _ in range(subdivisions):
+        mids = {}
+
+        def mid(a, b):
+            key = (min(a, b), max(a, b))
+            i = mids.get(key)
+            if i is None:
+                p = pos[a] + pos[b]
+                pos.append(p / math.sqrt(float(p[0] * p[0] + p[1] * p[1] + p[2] * p[2])))
+                i = mids[key] = len(pos) - 1
+            return i
+        nxt = []
+        for a, b, c in tris:
+            ab, bc, ca = mid(a, b), mid(b, c), mid(c, a)
+            nxt += [(a, ab, ca), (b, bc, ab), (c, ca, bc), (ab, bc, ca)]
+        tris = nxt
+    P = np.array(pos) * radius
+    return Mesh(P, np.array(tris, np.int32), spherical_uvs(P))
+
+
 def spherical_uvs(pos):
     """assign_spherical_uvs (mesh.cpp:352-369)."""
     c = pos.sum(axis=0) / max(1, len(pos))

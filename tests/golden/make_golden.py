@@ -1,0 +1,60 @@
+"""Generate tests/golden/*.npz from the REFERENCE library compiled from its own
+sources (oracle/_ref). Run where /root/reference exists:
+
+    python tests/golden/make_golden.py
+
+Each fixture stores the inputs (so it is self-contained) and the reference's
+outputs: hit caches, images, masks, per-view loss + adjoint, interior and
+boundary gradients, silhouette segments, the Laplacian (CSC, value, gradient)
+and the hot subset of total_loss (loss terms + gradient).
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle.pyoracle import RefLib, layout_for  # noqa: E402
+from paper_2103_15208_b200 import scenes as S  # noqa: E402
+
+CASES = {
+    "sphere_f4": dict(mesh=lambda: S.geodesic_sphere(4), tex=8, views=2, image=24, spp=4, seed=3, light=True),
+    "blob_f5": dict(mesh=lambda: S.blob(5), tex=16, views=2, image=32, spp=9, seed=1, light=False),
+}
+
+
+def make(name, c):
+    sc = S.make_scene(c["mesh"](), c["tex"], c["views"], c["image"])
+    ts = S.perturbed_target_scene(sc)
+    ref, tref = RefLib(sc), RefLib(ts)
+    spp, seed = c["spp"], c["seed"]
+    lay = layout_for(sc, optimize_light=c["light"])
+    out = dict(positions=sc.mesh.positions, triangles=sc.mesh.triangles, uvs=sc.mesh.uvs, edges=sc.mesh.edges,
+               diffuse=sc.diffuse, specular=sc.specular, roughness=sc.roughness, light=sc.light,
+               background=sc.background, cameras=S.camera_struct_array(sc.cameras), spp=spp, seed=seed,
+               optimize_light=int(c["light"]))
+    targets = np.stack([tref.render(v, spp, seed + 0x7A9)[0] for v in range(c["views"])])
+    out["targets"] = targets
+    for v in range(c["views"]):
+        rgb, mask, hit = ref.render(v, spp, seed)
+        val, adj = ref.view_loss(rgb, targets[v])
+        out[f"v{v}_rgb"], out[f"v{v}_mask"], out[f"v{v}_hit"] = rgb, mask, hit
+        out[f"v{v}_loss"], out[f"v{v}_adj"] = np.array(val), adj
+        out[f"v{v}_interior"] = ref.interior(v, adj, spp, seed, hit, lay)
+        segs, tot = ref.silhouettes(v)
+        out[f"v{v}_segments"], out[f"v{v}_seglen"] = segs, np.array(tot)
+        g, deg = ref.boundary(v, adj, c["image"] ** 2, seed, lay)
+        out[f"v{v}_boundary"], out[f"v{v}_degenerate"] = g, np.array(deg)
+    val, grad, (o_, i_, x_) = ref.laplacian(0, 0.1)
+    out.update(lap_value=np.array(val), lap_grad=grad, lap_outer=o_, lap_inner=i_, lap_vals=x_)
+    bd, g, _ = ref.total_loss(targets, spp, seed, lay)
+    out["total_breakdown"], out["total_grad"] = bd, g
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
+    print(name, os.path.getsize(os.path.join(HERE, name + ".npz")), "bytes")
+
+
+if __name__ == "__main__":
+    for n, c in CASES.items():
+        make(n, c)
