@@ -263,21 +263,24 @@ def main():
 
     # ---- roofline of the dominant kernel (fused trace/shade/loss/interior)
     s0 = stats[-1]
-    ms_render = statistics.mean(x["ms_render"] for x in stats)
+    ms_shade = statistics.mean(x["ms_render"] - x["ms_trace"] for x in stats)
     n_px, n_samp = s0["pixels"], s0["samples"]
     n_hit, n_adj = s0["hit_samples"], s0["adjoint_samples"]
     algo_bytes = 80 * n_px + 4 * n_samp + 332 * n_hit + 736 * n_adj
     pk, pk_kind = peaks()
-    achieved = algo_bytes / (ms_render / 1e3) / 1e9
-    roof = {"kernel": "k_render<trace,loss,interior> (fused)", "bound": "hbm", "achieved": achieved,
+    achieved = algo_bytes / (ms_shade / 1e3) / 1e9
+    roof = {"kernel": "k_render<shade,loss,interior> (fused shading + loss + interior scatter)",
+            "bound": "hbm", "achieved": achieved,
             "peak": pk["hbm_gbs"], "peak_source": pk_kind, "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
             "traffic": None, "algorithmic_bytes_per_launch": algo_bytes,
             "byte_model": "80*N_px + 4*N_samp + 332*N_hit + 736*N_adj (DESIGN.md §4)",
-            "ms_per_launch": ms_render, "share_of_step": ms_render / statistics.mean(ms_steps)}
+            "ms_per_launch": ms_shade, "share_of_step": ms_shade / statistics.mean(ms_steps)}
     traffic_file = os.path.join(ROOT, "profiles", "render_traffic.json")
     if os.path.exists(traffic_file):
-        try:
-            roof["traffic"] = json.load(open(traffic_file)).get("dram_bytes_per_launch")
+        try:  # ncu dram bytes per sample of this kernel, scaled to this launch
+            tr = json.load(open(traffic_file))
+            roof["traffic"] = tr["dram_bytes_per_sample"] * n_samp
+            roof["traffic_source"] = tr.get("source")
         except Exception:
             pass
 

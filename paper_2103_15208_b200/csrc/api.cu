@@ -465,6 +465,7 @@ int cdr_set_views(cdr_ctx* c, const cdr_camera* cams, const int32_t* gids, int32
         off += size_t(k.width) * k.height;
     }
     c->total_pixels = off;
+    c->target_tone_gamma = -1;
     h2d(c->d_cams, dc.data(), dc.size(), c->stream);
     size_t np = std::max<size_t>(1, off);
     c->img.ensure(3 * np);
@@ -486,6 +487,7 @@ int cdr_set_target(cdr_ctx* c, int32_t view, const double* rgb, const double* ma
     CDR_CUDA_CHECK(cudaMemcpyAsync(c->target.p + 3 * v.pix_off, rgb, sizeof(double) * 3 * np,
                                    cudaMemcpyHostToDevice, c->stream));
     v.has_target = true;
+    c->target_tone_gamma = -1;  // Φ(target) must be recomputed
     v.has_target_mask = mask != nullptr;
     v.target_mask_sum = 0;
     if (mask) {
@@ -718,6 +720,10 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
     ensure_hit_arena(c, spp);
     CDR_CUDA_CHECK(cudaMemsetAsync(c->loss_acc.p, 0, sizeof(double) * c->views.size(), s));
     ensure_prepared(c, /*force=*/true);  // GradContext is rebuilt per total_loss (losses.cpp:251)
+    if (c->target_tone_gamma != st->gamma) {
+        launch_tone_targets(c, st->gamma);
+        c->target_tone_gamma = st->gamma;
+    }
     CDR_CUDA_CHECK(cudaEventRecord(ev[1], s));
     RenderArgs a = render_args(c, st, lay);
     a.use_mask = use_mask;

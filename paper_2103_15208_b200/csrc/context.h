@@ -107,6 +107,8 @@ struct cdr_ctx {
     cdr::DBuf<cdr::DevCamera> d_cams;
     size_t total_pixels = 0;
     cdr::DBuf<double> target, target_mask, img, mask, adj;
+    cdr::DBuf<double> target_tone;   // Φ(target) for target_tone_gamma
+    double target_tone_gamma = -1;   // < 0: stale
     cdr::DBuf<int32_t> hit;  // hit caches (per view W*H*spp), arena sized on demand
     size_t hit_stride_spp = 0;
 

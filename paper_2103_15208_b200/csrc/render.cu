@@ -42,6 +42,7 @@ struct Params {
     double* adj;
     int32_t* hit;
     const double* target;
+    const double* target_tone;  // Φ(target), precomputed per (target, gamma)
     const double* target_mask;
     const unsigned char* has_mask;  // per slot
     double* grad;
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params
 // The hit triangle comes from the hit cache and is re-intersected with
 // ray_triangle, exactly as interior_pass replays it (diff_render.cpp:84-93).
 #ifndef CDR_RENDER_MIN_BLOCKS
-#define CDR_RENDER_MIN_BLOCKS 4
+#define CDR_RENDER_MIN_BLOCKS 3
 #endif
 template <bool kShade, bool kLoss, bool kInterior>
 __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
@@ -143,46 +144,42 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     __syncthreads();
 
     // ---------------- phase 2: pixel mean / mask / loss / adjoint
+    // One thread per (pixel, channel): channels are independent, each sums its
+    // pixel's samples in sample order (render.cpp:48-57), so the mean is the
+    // reference's bit for bit; the tone map of the target is precomputed.
     double loss_part = 0;
-    if (tid < P) {
-        const int px = (blockIdx.x % tiles_x) * p.TW + tid % p.TW;
-        const int py = (blockIdx.x / tiles_x) * p.TH + tid / p.TW;
+    for (int item = tid; item < 3 * P; item += kThreads) {
+        const int q = item % P, c = item / P;
+        const int px = (blockIdx.x % tiles_x) * p.TW + q % p.TW;
+        const int py = (blockIdx.x / tiles_x) * p.TH + q / p.TW;
         if (px < W && py < H) {
-            const size_t q = pbase + size_t(py) * W + px;
-            D3 mean{0, 0, 0};
+            const size_t qi = pbase + size_t(py) * W + px;
+            double mean = 0;
             if (kShade) {
-                D3 sum{0, 0, 0};
+                double sum = 0;
                 int hits = 0;
                 for (int j = 0; j < spp; ++j) {
-                    int o = tid * spp + j;
-                    sum = sum + D3{s_rad[o][0], s_rad[o][1], s_rad[o][2]};
-                    hits += s_hit[o];
+                    sum = sum + s_rad[q * spp + j][c];
+                    hits += s_hit[q * spp + j];
                 }
                 mean = sum / double(spp);
-                p.img[3 * q] = mean.x;
-                p.img[3 * q + 1] = mean.y;
-                p.img[3 * q + 2] = mean.z;
-                p.mask[q] = double(hits) / double(spp);
+                p.img[3 * qi + c] = mean;
+                if (c == 0) p.mask[qi] = double(hits) / double(spp);
             }
             if (kLoss) {
-                double m = (p.use_mask && p.has_mask[vc.slot]) ? p.target_mask[q] : 1.0;
-                D3 adj{0, 0, 0};
+                double m = (p.use_mask && p.has_mask[vc.slot]) ? p.target_mask[qi] : 1.0;
+                double a = 0;
                 if (m != 0) {
-                    double r[3] = {mean.x, mean.y, mean.z}, a[3];
-                    for (int c = 0; c < 3; ++c) {
-                        double d = tone_map(r[c], p.gamma) - tone_map(p.target[3 * q + c], p.gamma);
-                        loss_part += m * fabs(d);
-                        double sg = double((d > 0) - (d < 0));
-                        a[c] = vc.scale * m * sg * tone_map_derivative(r[c], p.gamma);
-                    }
-                    adj = D3{a[0], a[1], a[2]};
+                    // losses.cpp:37-44; Φ'(r) = Φ(r) / (γ r) for r in (0, 1)
+                    double tr = tone_map(mean, p.gamma);
+                    double d = tr - p.target_tone[3 * qi + c];
+                    loss_part += m * fabs(d);
+                    double sg = double((d > 0) - (d < 0));
+                    double der = (mean <= 0.0 || mean >= 1.0) ? 0.0 : tr / (p.gamma * mean);
+                    a = vc.scale * m * sg * der;
                 }
-                p.adj[3 * q] = adj.x;
-                p.adj[3 * q + 1] = adj.y;
-                p.adj[3 * q + 2] = adj.z;
-                s_adj[tid][0] = adj.x;
-                s_adj[tid][1] = adj.y;
-                s_adj[tid][2] = adj.z;
+                p.adj[3 * qi + c] = a;
+                s_adj[q][c] = a;
             }
         }
     }
@@ -225,73 +222,123 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
         }
     }
     a = a / double(spp);  // diff_render.cpp:82
-    const double Lc[3] = {p.sc.L[0], p.sc.L[1], p.sc.L[2]};
-    const double ac[3] = {a.x, a.y, a.z};
 
-    int va = 0, vb = 0, vcx = 0;
+    // Compute everything the scatter needs first, so the large temporaries
+    // (texture sample, BRDF partials, vertex data) are dead before the
+    // warp-aggregation loops; only a compact state crosses them.
+    int tex0 = 0;           // texel quad key (texel[0] determines all four)
+    double wq[4] = {0, 0, 0, 0};
+    double wd0 = 0, ws0 = 0, wr0 = 0;  // d_diffuse/r^2, d_specular/r^2, Σ a L d_rough / r^2
+    double aL[3] = {0, 0, 0};
+    double lv[3] = {0, 0, 0};          // light gradient (diff_render.cpp:129-131)
+    bool pact = false;                 // position terms present (mu > 0, det != 0, finite)
+    D3 gc{0, 0, 0}, hm{0, 0, 0};       // g_common and coeff_mu * h
     double b0 = 0;
-    D3 p0{0, 0, 0}, p1{0, 0, 0}, p2{0, 0, 0};
-    D2 uv0{0, 0}, uv1{0, 0}, uv2{0, 0};
-    D3 N0{0, 0, 0}, N1{0, 0, 0}, N2{0, 0, 0}, nt{0, 0, 0};
-    double mu = 0;
-    TexSample3 ts;
-    Brdf br;
-    double inv_r2 = 0;
+    int va = 0, vb = 0, vcx = 0;
     if (act) {
         b0 = 1.0 - b1 - b2;
         va = p.sc.tris[3 * tri];
         vb = p.sc.tris[3 * tri + 1];
         vcx = p.sc.tris[3 * tri + 2];
-        p0 = ld3(p.sc.pos + 3 * va);
-        p1 = ld3(p.sc.pos + 3 * vb);
-        p2 = ld3(p.sc.pos + 3 * vcx);
+        D2 uv0{0, 0}, uv1{0, 0}, uv2{0, 0};
         if (p.sc.uv) {
             uv0 = D2{p.sc.uv[2 * va], p.sc.uv[2 * va + 1]};
             uv1 = D2{p.sc.uv[2 * vb], p.sc.uv[2 * vb + 1]};
             uv2 = D2{p.sc.uv[2 * vcx], p.sc.uv[2 * vcx + 1]};
         }
         D2 uv{uv0.x * b0 + uv1.x * b1 + uv2.x * b2, uv0.y * b0 + uv1.y * b1 + uv2.y * b2};
-        N0 = ld3(p.sc.normals + 3 * va);
-        N1 = ld3(p.sc.normals + 3 * vb);
-        N2 = ld3(p.sc.normals + 3 * vcx);
-        nt = N0 * b0 + N1 * b1 + N2 * b2;
+        D3 N0 = ld3(p.sc.normals + 3 * va), N1 = ld3(p.sc.normals + 3 * vb), N2 = ld3(p.sc.normals + 3 * vcx);
+        D3 nt = N0 * b0 + N1 * b1 + N2 * b2;
         double n_len = length(nt);
         if (n_len < 1e-14) {
             act = false;  // diff_render.cpp:101
         } else {
             D3 n_hat = nt / n_len;
-            mu = dot(n_hat, -dir);
-            ts = sample_maps(p.sc.tex, p.sc.tw, p.sc.th, uv, true);
-            br = eval_brdf(ts.dv, ts.sv, ts.rv, mu, true);
-            inv_r2 = 1.0 / (t * t);
+            double mu = dot(n_hat, -dir);
+            TexSample3 ts = sample_maps(p.sc.tex, p.sc.tw, p.sc.th, uv, true);
+            Brdf br = eval_brdf(ts.dv, ts.sv, ts.rv, mu, true);
+            const double inv_r2 = 1.0 / (t * t);
+            const double Lc[3] = {p.sc.L[0], p.sc.L[1], p.sc.L[2]};
+            const double ac[3] = {a.x, a.y, a.z};
+            tex0 = ts.texel[0];
+            for (int k = 0; k < 4; ++k) wq[k] = ts.w[k];
+            wd0 = br.d_diffuse * inv_r2;
+            ws0 = br.d_specular * inv_r2;
+            for (int c = 0; c < 3; ++c) {
+                aL[c] = ac[c] * Lc[c];
+                wr0 += ac[c] * Lc[c] * comp(br.d_rough, c) * inv_r2;
+                lv[c] = ac[c] * comp(br.value, c) * inv_r2;
+            }
+            if (mu > 0) {  // diff_render.cpp:133
+                D3 p0 = ld3(p.sc.pos + 3 * va), p1 = ld3(p.sc.pos + 3 * vb), p2 = ld3(p.sc.pos + 3 * vcx);
+                // M = [d, p0-p1, p0-p2] (Mat3::from_columns), inverse rows r0..r2
+                double m[9] = {dir.x, p0.x - p1.x, p0.x - p2.x, dir.y, p0.y - p1.y, p0.y - p2.y,
+                               dir.z, p0.z - p1.z, p0.z - p2.z};
+                double det = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
+                             m[2] * (m[3] * m[7] - m[4] * m[6]);
+                if (fabs(det) >= 1e-18) {
+                    double cs = 0, cu = 0, cv = 0, cm = 0;
+                    for (int c = 0; c < 3; ++c) {
+                        double w = ac[c] * Lc[c] * inv_r2;
+                        cs += ac[c] * Lc[c] * (-2.0 * comp(br.value, c) / (t * t * t));
+                        double gu = br.d_diffuse * comp(ts.ddu, c) + br.d_specular * comp(ts.sdu, c) +
+                                    comp(br.d_rough, c) * ts.rdu;
+                        double gv = br.d_diffuse * comp(ts.ddv, c) + br.d_specular * comp(ts.sdv, c) +
+                                    comp(br.d_rough, c) * ts.rdv;
+                        cu += w * gu;
+                        cv += w * gv;
+                        cm += w * comp(br.d_mu, c);
+                    }
+                    if (!isfinite(cs + cu + cv + cm)) {
+                        raise_nonfinite(p.err, x, y);
+                    } else {
+                        double inv = 1.0 / det;
+                        D3 r0{(m[4] * m[8] - m[5] * m[7]) * inv, (m[2] * m[7] - m[1] * m[8]) * inv,
+                              (m[1] * m[5] - m[2] * m[4]) * inv};
+                        D3 r1{(m[5] * m[6] - m[3] * m[8]) * inv, (m[0] * m[8] - m[2] * m[6]) * inv,
+                              (m[2] * m[3] - m[0] * m[5]) * inv};
+                        D3 r2{(m[3] * m[7] - m[4] * m[6]) * inv, (m[1] * m[6] - m[0] * m[7]) * inv,
+                              (m[0] * m[4] - m[1] * m[3]) * inv};
+                        // h = normalize_jacobian(n_tilde) * v_hat (vec.hpp:179-183)
+                        D3 n = nt / n_len;
+                        D3 v = -dir;
+                        double sc = 1.0 / n_len;
+                        double J[9] = {(1 - n.x * n.x) * sc, (0 - n.x * n.y) * sc, (0 - n.x * n.z) * sc,
+                                       (0 - n.y * n.x) * sc, (1 - n.y * n.y) * sc, (0 - n.y * n.z) * sc,
+                                       (0 - n.z * n.x) * sc, (0 - n.z * n.y) * sc, (1 - n.z * n.z) * sc};
+                        D3 hv{J[0] * v.x + J[1] * v.y + J[2] * v.z, J[3] * v.x + J[4] * v.y + J[5] * v.z,
+                              J[6] * v.x + J[7] * v.y + J[8] * v.z};
+                        double k1 = cu * (uv1.x - uv0.x) + cv * (uv1.y - uv0.y) + cm * (dot(hv, N1) - dot(hv, N0));
+                        double k2 = cu * (uv2.x - uv0.x) + cv * (uv2.y - uv0.y) + cm * (dot(hv, N2) - dot(hv, N0));
+                        gc = r0 * cs + r1 * k1 + r2 * k2;
+                        hm = hv * cm;
+                        pact = true;
+                    }
+                }
+            }
         }
     }
 
-    // texel scatter through the bilinear weights (diff_render.cpp:110-128):
-    // group by the texel quad (texel[0] determines all four)
+    // texel scatter through the bilinear weights (diff_render.cpp:110-128)
     {
-        const int key = act ? ts.texel[0] : -1 - (tid & 31);
+        const int key = act ? tex0 : -1 - (tid & 31);
         const unsigned peers = __match_any_sync(0xffffffffu, key);
         const bool leader = act && (__ffs(peers) - 1) == (tid & 31);
+        const int tw = p.sc.tw, th = p.sc.th;
+        const int x0 = tex0 % tw, y0 = tex0 / tw;
+        const int x1 = x0 + 1 == tw ? 0 : x0 + 1, y1 = y0 + 1 == th ? 0 : y0 + 1;
 #pragma unroll 1
         for (int kq = 0; kq < 4; ++kq) {
             double v[7];
-            if (act) {
-                double wd = ts.w[kq] * br.d_diffuse * inv_r2;
-                double ws = ts.w[kq] * br.d_specular * inv_r2;
-                double wr = 0;
-                for (int c = 0; c < 3; ++c) {
-                    v[c] = ac[c] * Lc[c] * wd;
-                    v[3 + c] = ac[c] * Lc[c] * ws;
-                    wr += ac[c] * Lc[c] * comp(br.d_rough, c) * inv_r2;
-                }
-                v[6] = wr * ts.w[kq];
-            } else {
-                for (int i = 0; i < 7; ++i) v[i] = 0;
+            const double w = wq[kq];
+            for (int c = 0; c < 3; ++c) {
+                v[c] = aL[c] * (w * wd0);
+                v[3 + c] = aL[c] * (w * ws0);
             }
+            v[6] = wr0 * w;
             reduce_peers<7>(0xffffffffu, peers, v);
             if (leader) {
-                int64_t tx = ts.texel[kq];
+                const int64_t tx = int64_t((kq < 2 ? y0 : y1)) * tw + ((kq & 1) ? x1 : x0);
                 for (int c = 0; c < 3; ++c) {
                     if (v[c] != 0) atomicAdd(p.grad + p.lay_d + 3 * tx + c, v[c]);
                     if (v[3 + c] != 0) atomicAdd(p.grad + p.lay_s + 3 * tx + c, v[3 + c]);
@@ -301,83 +348,24 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
         }
     }
     if (p.lay_l >= 0) {  // light intensity (diff_render.cpp:129-131)
-        double v[3];
-        for (int c = 0; c < 3; ++c) v[c] = act ? ac[c] * comp(br.value, c) * inv_r2 : 0.0;
         for (int o = 16; o > 0; o >>= 1)
-            for (int c = 0; c < 3; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+            for (int c = 0; c < 3; ++c) lv[c] += __shfl_xor_sync(0xffffffffu, lv[c], o);
         if ((tid & 31) == 0)
             for (int c = 0; c < 3; ++c)
-                if (v[c] != 0) atomicAdd(p.grad + p.lay_l + c, v[c]);
+                if (lv[c] != 0) atomicAdd(p.grad + p.lay_l + c, lv[c]);
     }
-
-    // intersection response + normal chain (diff_render.cpp:133-184)
-    bool pact = act && mu > 0;
-    D3 gc{0, 0, 0}, hv{0, 0, 0};
-    double cm = 0;
-    if (pact) {
-        // M = [d, p0-p1, p0-p2] (Mat3::from_columns), inverse rows r0..r2
-        double m[9] = {dir.x, p0.x - p1.x, p0.x - p2.x, dir.y, p0.y - p1.y, p0.y - p2.y,
-                       dir.z, p0.z - p1.z, p0.z - p2.z};
-        double det = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
-                     m[2] * (m[3] * m[7] - m[4] * m[6]);
-        if (fabs(det) < 1e-18) {
-            pact = false;
-        } else {
-            double inv = 1.0 / det;
-            D3 r0{(m[4] * m[8] - m[5] * m[7]) * inv, (m[2] * m[7] - m[1] * m[8]) * inv,
-                  (m[1] * m[5] - m[2] * m[4]) * inv};
-            D3 r1{(m[5] * m[6] - m[3] * m[8]) * inv, (m[0] * m[8] - m[2] * m[6]) * inv,
-                  (m[2] * m[3] - m[0] * m[5]) * inv};
-            D3 r2{(m[3] * m[7] - m[4] * m[6]) * inv, (m[1] * m[6] - m[0] * m[7]) * inv,
-                  (m[0] * m[4] - m[1] * m[3]) * inv};
-            double cs = 0, cu = 0, cv = 0;
-            for (int c = 0; c < 3; ++c) {
-                double w = ac[c] * Lc[c] * inv_r2;
-                cs += ac[c] * Lc[c] * (-2.0 * comp(br.value, c) / (t * t * t));
-                double gu = br.d_diffuse * comp(ts.ddu, c) + br.d_specular * comp(ts.sdu, c) +
-                            comp(br.d_rough, c) * ts.rdu;
-                double gv = br.d_diffuse * comp(ts.ddv, c) + br.d_specular * comp(ts.sdv, c) +
-                            comp(br.d_rough, c) * ts.rdv;
-                cu += w * gu;
-                cv += w * gv;
-                cm += w * comp(br.d_mu, c);
-            }
-            if (!isfinite(cs + cu + cv + cm)) {
-                raise_nonfinite(p.err, x, y);
-                pact = false;
-            } else {
-                // h = normalize_jacobian(n_tilde) * v_hat (vec.hpp:179-183)
-                double len = length(nt);
-                D3 n = nt / len;
-                D3 v = -dir;
-                double sc = 1.0 / len;
-                double J[9] = {(1 - n.x * n.x) * sc, (0 - n.x * n.y) * sc, (0 - n.x * n.z) * sc,
-                               (0 - n.y * n.x) * sc, (1 - n.y * n.y) * sc, (0 - n.y * n.z) * sc,
-                               (0 - n.z * n.x) * sc, (0 - n.z * n.y) * sc, (1 - n.z * n.z) * sc};
-                hv = D3{J[0] * v.x + J[1] * v.y + J[2] * v.z, J[3] * v.x + J[4] * v.y + J[5] * v.z,
-                        J[6] * v.x + J[7] * v.y + J[8] * v.z};
-                double k1 = cu * (uv1.x - uv0.x) + cv * (uv1.y - uv0.y) + cm * (dot(hv, N1) - dot(hv, N0));
-                double k2 = cu * (uv2.x - uv0.x) + cv * (uv2.y - uv0.y) + cm * (dot(hv, N2) - dot(hv, N0));
-                gc = r0 * cs + r1 * k1 + r2 * k2;
-            }
-        }
-    }
+    // intersection response + normal-chain input, per triangle corner
+    // (diff_render.cpp:170-184; the chain itself is applied in finalize.cu)
     {
         const int key = pact ? tri : -1 - (tid & 31);
         const unsigned peers = __match_any_sync(0xffffffffu, key);
         const bool leader = pact && (__ffs(peers) - 1) == (tid & 31);
-        const double bc[3] = {b0, b1, b2};
 #pragma unroll 1
         for (int j = 0; j < 3; ++j) {
-            double v[6];
-            if (pact) {
-                D3 g = gc * bc[j];
-                D3 h = hv * (cm * bc[j]);
-                v[0] = g.x; v[1] = g.y; v[2] = g.z;
-                v[3] = h.x; v[4] = h.y; v[5] = h.z;
-            } else {
+            const double bj = j == 0 ? b0 : (j == 1 ? b1 : b2);
+            double v[6] = {gc.x * bj, gc.y * bj, gc.z * bj, hm.x * bj, hm.y * bj, hm.z * bj};
+            if (!pact)
                 for (int i = 0; i < 6; ++i) v[i] = 0;
-            }
             reduce_peers<6>(0xffffffffu, peers, v);
             if (leader) {
                 double* dst = p.corner + (size_t(tri) * 3 + j) * 6;
@@ -386,6 +374,11 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
             }
         }
     }
+}
+
+__global__ void k_tone(const double* __restrict__ in, size_t n, double gamma, double* __restrict__ out) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        out[i] = tone_map(in[i], gamma);
 }
 
 __global__ void k_view_loss(int n, const double* __restrict__ r, const double* __restrict__ tg,
@@ -443,6 +436,15 @@ void launch_radiance_points(cdr_ctx* c, int slot, int n, const double* xy, doubl
 void launch_pack_textures(cdr_ctx* c, const double* d, const double* s, const double* r, int n) {
     if (n <= 0) return;
     { ++c->launches; k_pack_textures<<<(n + 255) / 256, 256, 0, c->stream>>>(d, s, r, n, c->tex.p); }
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_tone_targets(cdr_ctx* c, double gamma) {
+    size_t n = 3 * c->total_pixels;
+    c->target_tone.ensure(std::max<size_t>(1, n));
+    if (n == 0) return;
+    int nb = int(std::min<size_t>((n + 255) / 256, 148 * 16));
+    { ++c->launches; k_tone<<<nb, 256, 0, c->stream>>>(c->target.p, n, gamma, c->target_tone.p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -523,6 +525,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     p.adj = c->adj.p;
     p.hit = c->hit.p;
     p.target = c->target.p;
+    p.target_tone = c->target_tone.p;
     p.target_mask = c->target_mask.p;
     p.has_mask = st.has_mask.p;
     p.grad = c->grad.p;
