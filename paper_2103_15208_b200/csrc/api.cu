@@ -457,6 +457,8 @@ int cdr_set_views(cdr_ctx* c, const cdr_camera* cams, const int32_t* gids, int32
         }
         d.th = std::tan(k.fov_deg * 3.14159265358979323846 / 360.0);  // camera.cpp:25-27
         d.aspect = double(k.width) / double(k.height);                 // camera.hpp:22
+        d.inv_w = (k.width & (k.width - 1)) == 0 ? 1.0 / k.width : 0.0;  // exact powers of two
+        d.inv_h = (k.height & (k.height - 1)) == 0 ? 1.0 / k.height : 0.0;
         d.W = k.width;
         d.H = k.height;
         d.gid = gids ? gids[i] : i;

@@ -216,6 +216,9 @@ struct BParams {
     int32_t* key;        // n_views x m_stride : segment of sample i (-1 inactive)
     int32_t* slot;       // n_views x m_stride : rank inside its segment
     int32_t* order;      // n_views x m_stride : sample indices grouped by segment
+    double* s_param;     // n_views x m_stride : s of sample i (pass 1)
+    int32_t* sorted_si;  // n_views x m_stride : segment of the j-th grouped sample
+    double* sorted_s;    // n_views x m_stride : its s
 };
 
 // Steps of diff_render.cpp:232-244 for sample i: RNG pick, lower_bound,
@@ -272,6 +275,7 @@ __global__ void __launch_bounds__(kBlock) k_bsample(BParams p) {
         size_t o = size_t(vi) * p.m_stride + i;
         p.key[o] = act ? b.si : -1;
         p.slot[o] = base + __popc(peers & ((1u << lane) - 1u));
+        if (act) p.s_param[o] = b.s;
     }
 }
 
@@ -311,7 +315,10 @@ __global__ void k_bscatter(BParams p) {
     size_t o = size_t(vi) * p.m_stride + i;
     int k = p.key[o];
     if (k < 0) return;
-    p.order[size_t(vi) * p.m_stride + p.seg_off[size_t(vi) * p.E + k] + p.slot[o]] = int32_t(i);
+    size_t d = size_t(vi) * p.m_stride + p.seg_off[size_t(vi) * p.E + k] + p.slot[o];
+    p.order[d] = int32_t(i);
+    p.sorted_si[d] = k;
+    p.sorted_s[d] = p.s_param[o];
 }
 
 // pass 4: the two radiance probes and the vertex deposit, in segment order so a
@@ -322,13 +329,25 @@ __global__ void k_bscatter(BParams p) {
 __global__ void __launch_bounds__(kBlock, CDR_BOUNDARY_MIN_BLOCKS) k_boundary(BParams p) {
     const int vi = blockIdx.y;
     const int lane = threadIdx.x & 31;
-    const DevCamera& cam = p.cams[p.calls[vi].slot];
+    const DevCamera cam = p.cams[p.calls[vi].slot];
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int n_act = p.n_active[vi];
     if (int64_t(blockIdx.x) * blockDim.x >= n_act) return;  // whole CTA idle (uniform)
+    // the RNG pick and lower_bound were done in pass 1: read the grouped result
     BSample b;
-    bool act = false;
-    if (j < n_act) act = boundary_setup(p, vi, p.order[size_t(vi) * p.m_stride + j], b);
+    bool act = j < n_act;
+    if (act) {
+        const size_t o = size_t(vi) * p.m_stride + j;
+        b.si = p.sorted_si[o];
+        b.s = p.sorted_s[o];
+        b.sg = p.segs + size_t(vi) * p.E + b.si;
+        const cdr_segment* sg = b.sg;
+        b.xq = D2{sg->q0[0] + (sg->q1[0] - sg->q0[0]) * b.s, sg->q0[1] + (sg->q1[1] - sg->q0[1]) * b.s};
+        int px = int(floor(b.xq.x)), py = int(floor(b.xq.y));
+        px = px < 0 ? 0 : (px > cam.W - 1 ? cam.W - 1 : px);
+        py = py < 0 ? 0 : (py > cam.H - 1 ? cam.H - 1 : py);
+        b.adj = ld3(p.adj + 3 * (p.pix_off[p.calls[vi].slot] + size_t(py) * cam.W + px));
+    }
     const int samples = p.calls[vi].samples;
     const double total_len = p.totals[3 * vi];
     double weighted = 0;
@@ -468,6 +487,9 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     c->b_key.ensure(nm);
     c->b_slot.ensure(nm);
     c->b_order.ensure(nm);
+    c->b_s.ensure(nm);
+    c->b_sorted_si.ensure(nm);
+    c->b_sorted_s.ensure(nm);
     CDR_CUDA_CHECK(cudaMemsetAsync(c->b_seg_count.p, 0, sizeof(int32_t) * size_t(n_views) * E, c->stream));
     BParams p{};
     p.sc = shade_scene(c);
@@ -494,6 +516,9 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     p.key = c->b_key.p;
     p.slot = c->b_slot.p;
     p.order = c->b_order.p;
+    p.s_param = c->b_s.p;
+    p.sorted_si = c->b_sorted_si.p;
+    p.sorted_s = c->b_sorted_s.p;
     dim3 grid((samples + kBlock - 1) / kBlock, n_views);
     { ++c->launches; k_bsample<<<grid, kBlock, 0, c->stream>>>(p); }
     { ++c->launches; k_bscan<<<n_views, 1024, 0, c->stream>>>(p.seg_count, p.count, E, p.seg_off, p.n_active); }
@@ -503,3 +528,13 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
 }
 
 }  // namespace cdr
+
+#ifdef CDR_TRACE_STATS
+// debug builds: traversal counters of the boundary probes (this translation unit)
+extern "C" int cdr_debug_trace_stats_boundary(unsigned long long out[4]) {
+    cudaMemcpyFromSymbol(out, cdr::g_trace_stats, sizeof(unsigned long long) * 4);
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(cdr::g_trace_stats, z, sizeof(z));
+    return 0;
+}
+#endif

@@ -24,7 +24,8 @@ namespace {
 struct ViewCall {
     int slot;
     int pad;
-    double scale;  // lambda / n_valid
+    double scale;     // lambda / n_valid
+    uint64_t h_view;  // hash_combine(seed, gid + 0x9e01)
 };
 
 struct Params {
@@ -34,6 +35,7 @@ struct Params {
     const ViewCall* calls;
     size_t* pix_off;  // per slot
     int spp, k, TW, TH;
+    double inv_k;
     uint64_t seed;
     double gamma;
     int use_mask, write_hits;
@@ -71,7 +73,7 @@ __device__ __forceinline__ void raise_nonfinite(ErrorInfo* e, int x, int y) {
 #endif
 __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
     const ViewCall vc = p.calls[blockIdx.y];
-    const DevCamera& cam = p.cams[vc.slot];
+    const DevCamera cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
     const int tiles_x = (W + p.TW - 1) / p.TW;
     const int tiles_y = (H + p.TH - 1) / p.TH;
@@ -84,7 +86,7 @@ __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params
     const int y = (blockIdx.x / tiles_x) * p.TH + pix / p.TW;
     if (!(pix < P && x < W && y < H)) return;
     const size_t pidx = p.pix_off[vc.slot] + size_t(y) * W + x;
-    D2 ps = pixel_sample_position(p.seed, cam.gid, x, y, W, s, spp, p.k);
+    D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
     D3 dir = primary_dir(cam, ps);
     Hit h = trace(p.sc.nodes, p.sc.recs, p.sc.n_tris, D3{cam.o[0], cam.o[1], cam.o[2]}, dir, p.info->t_min);
     p.hit[pidx * spp + s] = h.tri;
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     double t = 0, b1 = 0, b2 = 0;
     D3 dir{0, 0, 1};
     if (valid) {
-        D2 ps = pixel_sample_position(p.seed, cam.gid, x, y, W, s, spp, p.k);
+        D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
         dir = primary_dir(cam, ps);
         tri = p.hit[pidx * spp + s];
         if (tri >= 0) {
@@ -483,6 +485,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         calls[i].slot = view_slots[i];
         calls[i].pad = 0;
         calls[i].scale = loss_scales ? loss_scales[i] : 0.0;
+        calls[i].h_view = hash_combine(a.seed, uint64_t(c->views[view_slots[i]].cam.gid) + 0x9e01);
         maxW = std::max(maxW, c->views[view_slots[i]].cam.W);
         maxH = std::max(maxH, c->views[view_slots[i]].cam.H);
     }
@@ -510,6 +513,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     p.pix_off = st.pix_off.p;
     p.spp = a.spp;
     p.k = a.k;
+    p.inv_k = (a.k > 0 && (a.k & (a.k - 1)) == 0) ? 1.0 / a.k : 0.0;
     int P = kThreads / a.spp;
     int TW = 1;
     while (TW * TW * 4 <= P) TW *= 2;  // near-square power-of-two width
@@ -556,3 +560,14 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
 }
 
 }  // namespace cdr
+
+#ifdef CDR_TRACE_STATS
+// debug builds: traversal counters of the primary-visibility kernels in this
+// translation unit (rays, node visits, leaf tests); read-and-reset
+extern "C" int cdr_debug_trace_stats(unsigned long long out[4]) {
+    cudaMemcpyFromSymbol(out, cdr::g_trace_stats, sizeof(unsigned long long) * 4);
+    unsigned long long z[4] = {0, 0, 0, 0};
+    cudaMemcpyToSymbol(cdr::g_trace_stats, z, sizeof(z));
+    return 0;
+}
+#endif

@@ -234,3 +234,25 @@ def test_gpu_matches_reference_directly(sphere):
     for v in range(len(sphere.cameras)):
         np.testing.assert_array_equal(r.render(v, RenderSettings(spp=spp, seed=seed))[2],
                                       ref.render(v, spp, seed)[2])
+
+
+def test_grazing_rays_near_silhouettes_exact(sphere):
+    """Rays within a few ulps to 1e-3 px of silhouette edges (the boundary
+    probes' regime, where BVH pruning and the fp32 pre-test are most
+    stressed): triangle IDs must equal the exact oracle's."""
+    sc = blob_scene(freq=8, tex=16, views=2, image=64)
+    r, o = _pair(sc)
+    rng = np.random.default_rng(7)
+    for v in range(2):
+        segs, _ = o.silhouettes(v)
+        t = rng.uniform(0, 1, size=(len(segs), 8))
+        q0, q1 = segs["q0"][:, None, :], segs["q1"][:, None, :]
+        pts = q0 + (q1 - q0) * t[..., None]
+        tang = (q1 - q0) / np.linalg.norm(q1 - q0, axis=-1, keepdims=True)
+        nrm = np.stack([-tang[..., 1], tang[..., 0]], axis=-1)
+        offs = rng.choice([0.0, 1e-12, -1e-12, 1e-9, -1e-9, 1e-6, -1e-6, 1e-3, -1e-3, 0.5, -0.5],
+                          size=t.shape)[..., None]
+        xy = (pts + nrm * offs).reshape(-1, 2)
+        _, tg = r.radiance_at(v, xy)
+        _, to = o.radiance_at(v, xy)
+        np.testing.assert_array_equal(tg, to)
