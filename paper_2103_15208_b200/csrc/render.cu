@@ -255,11 +255,13 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
         if (n_len < 1e-14) {
             act = false;  // diff_render.cpp:101
         } else {
-            D3 n_hat = nt / n_len;
+            // gradient path (tolerance, not bit-exact): divisions as reciprocals
+            const double inv_len = rcp(n_len);
+            D3 n_hat = nt * inv_len;
             double mu = dot(n_hat, -dir);
             TexSample3 ts = sample_maps(p.sc.tex, p.sc.tw, p.sc.th, uv, true);
-            Brdf br = eval_brdf(ts.dv, ts.sv, ts.rv, mu, true);
-            const double inv_r2 = 1.0 / (t * t);
+            Brdf br = eval_brdf_grad(ts.dv, ts.sv, ts.rv, mu);
+            const double inv_r2 = rcp(t * t);
             const double Lc[3] = {p.sc.L[0], p.sc.L[1], p.sc.L[2]};
             const double ac[3] = {a.x, a.y, a.z};
             tex0 = ts.texel[0];
@@ -280,9 +282,10 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
                              m[2] * (m[3] * m[7] - m[4] * m[6]);
                 if (fabs(det) >= 1e-18) {
                     double cs = 0, cu = 0, cv = 0, cm = 0;
+                    const double m2_r3 = -2.0 * inv_r2 * rcp(t);  // -2 / t^3
                     for (int c = 0; c < 3; ++c) {
                         double w = ac[c] * Lc[c] * inv_r2;
-                        cs += ac[c] * Lc[c] * (-2.0 * comp(br.value, c) / (t * t * t));
+                        cs += ac[c] * Lc[c] * (comp(br.value, c) * m2_r3);
                         double gu = br.d_diffuse * comp(ts.ddu, c) + br.d_specular * comp(ts.sdu, c) +
                                     comp(br.d_rough, c) * ts.rdu;
                         double gv = br.d_diffuse * comp(ts.ddv, c) + br.d_specular * comp(ts.sdv, c) +
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
                     if (!isfinite(cs + cu + cv + cm)) {
                         raise_nonfinite(p.err, x, y);
                     } else {
-                        double inv = 1.0 / det;
+                        double inv = rcp(det);
                         D3 r0{(m[4] * m[8] - m[5] * m[7]) * inv, (m[2] * m[7] - m[1] * m[8]) * inv,
                               (m[1] * m[5] - m[2] * m[4]) * inv};
                         D3 r1{(m[5] * m[6] - m[3] * m[8]) * inv, (m[0] * m[8] - m[2] * m[6]) * inv,
@@ -302,9 +305,9 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
                         D3 r2{(m[3] * m[7] - m[4] * m[6]) * inv, (m[1] * m[6] - m[0] * m[7]) * inv,
                               (m[0] * m[4] - m[1] * m[3]) * inv};
                         // h = normalize_jacobian(n_tilde) * v_hat (vec.hpp:179-183)
-                        D3 n = nt / n_len;
+                        D3 n = n_hat;
                         D3 v = -dir;
-                        double sc = 1.0 / n_len;
+                        double sc = inv_len;
                         double J[9] = {(1 - n.x * n.x) * sc, (0 - n.x * n.y) * sc, (0 - n.x * n.z) * sc,
                                        (0 - n.y * n.x) * sc, (1 - n.y * n.y) * sc, (0 - n.y * n.z) * sc,
                                        (0 - n.z * n.x) * sc, (0 - n.z * n.y) * sc, (1 - n.z * n.z) * sc};
@@ -322,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     }
 
     // texel scatter through the bilinear weights (diff_render.cpp:110-128)
+#ifndef CDR_EXP_NO_TEXEL
     {
         const int key = act ? tex0 : -1 - (tid & 31);
         const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -349,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
             }
         }
     }
+#endif
     if (p.lay_l >= 0) {  // light intensity (diff_render.cpp:129-131)
         for (int o = 16; o > 0; o >>= 1)
             for (int c = 0; c < 3; ++c) lv[c] += __shfl_xor_sync(0xffffffffu, lv[c], o);
@@ -358,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     }
     // intersection response + normal-chain input, per triangle corner
     // (diff_render.cpp:170-184; the chain itself is applied in finalize.cu)
+#ifndef CDR_EXP_NO_POS
     {
         const int key = pact ? tri : -1 - (tid & 31);
         const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -376,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
             }
         }
     }
+#endif
 }
 
 __global__ void k_tone(const double* __restrict__ in, size_t n, double gamma, double* __restrict__ out) {
