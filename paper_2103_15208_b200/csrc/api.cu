@@ -141,6 +141,9 @@ void zero_grad(cdr_ctx* c, int64_t total) {
     c->corner_acc.ensure(std::max<size_t>(1, size_t(c->T) * 18));
     CDR_CUDA_CHECK(cudaMemsetAsync(c->corner_acc.p, 0, sizeof(double) * std::max<size_t>(1, size_t(c->T) * 18),
                                    c->stream));
+    const size_t nt = std::max<size_t>(1, size_t(c->tw) * c->th);
+    c->tex_acc.ensure(nt);
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->tex_acc.p, 0, sizeof(TexAcc) * nt, c->stream));
 }
 
 void reset_flags(cdr_ctx* c) {
@@ -272,7 +275,7 @@ void cdr_destroy(cdr_ctx* c) {
     c->target.release(); c->target_mask.release(); c->img.release(); c->mask.release(); c->adj.release();
     c->hit.release(); c->sil_flag.release(); c->sil_block_count.release(); c->sil_block_off.release();
     c->sil_count.release(); c->segs.release(); c->cdf.release(); c->total_len.release();
-    c->degenerate.release(); c->grad.release(); c->corner_acc.release(); c->qvec.release();
+    c->degenerate.release(); c->grad.release(); c->corner_acc.release(); c->tex_acc.release(); c->qvec.release();
     c->loss_acc.release(); c->errinfo.release(); c->counters.release();
     cudaStreamDestroy(c->stream);
     delete c;
@@ -617,6 +620,7 @@ int cdr_interior_pass(cdr_ctx* c, int32_t view, const double* adjoint, const cdr
     RenderArgs a = render_args(c, st, lay);
     int slot = view;
     launch_render(c, &slot, 1, a, false, false, true, nullptr);
+    launch_texel_flush(c, lay->diffuse, lay->specular, lay->roughness);
     launch_finalize_positions(c, lay->positions);
     sync(c);
     raise_device_error(c);
@@ -739,6 +743,7 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
     CDR_CUDA_CHECK(cudaEventRecord(ev[3], s));
     if (st->boundary_term) launch_boundary(c, n, max_samples, st->seed, CDR_PROBE_RADIANCE, lay->positions);
     CDR_CUDA_CHECK(cudaEventRecord(ev[4], s));
+    launch_texel_flush(c, lay->diffuse, lay->specular, lay->roughness);
     launch_finalize_positions(c, lay->positions);
     const bool lap_here = c->rank == 0;  // computed once across ranks
     if (lap_here) launch_laplacian(c, lap_mode, lambda_lap, c->grad.p + lay->positions);

@@ -126,6 +126,7 @@ struct cdr_ctx {
     int64_t grad_n = 0;
     cdr::DBuf<double> grad;
     cdr::DBuf<double> corner_acc;  // T x 3 corners x (g[3], h[3])
+    cdr::DBuf<cdr::TexAcc> tex_acc;  // texel-major interior texel gradients
     cdr::DBuf<double> qvec;        // V x 3: Jn_v * H_v
     cdr::DBuf<double> loss_acc;    // per view: Σ m |d|
     cdr::DBuf<cdr::ErrorInfo> errinfo;

@@ -70,6 +70,8 @@ void launch_laplacian(cdr_ctx* c, int mode, double lambda, double* grad_pos /* n
 // generic loss kernel over device images (cdr_view_loss)
 // Φ(target) for all target pixels (losses.cpp:38 evaluates it per pixel)
 void launch_tone_targets(cdr_ctx* c, double gamma);
+// add the texel-major accumulators into the gradient's texture segments
+void launch_texel_flush(cdr_ctx* c, int64_t lay_d, int64_t lay_s, int64_t lay_r);
 // radiance_at for n pixel positions of one view (device buffers)
 void launch_radiance_points(cdr_ctx* c, int slot, int n, const double* xy, double* rgb, int32_t* tri);
 // pack diffuse/specular/roughness (fp64, device) into 32-byte fp32 texel records

@@ -50,6 +50,7 @@ struct Params {
     double* grad;
     int64_t lay_d, lay_s, lay_r, lay_l;
     double* corner;
+    TexAcc* texacc;  // per texel: diffuse rgb, specular rgb, roughness
     double* loss_acc;
     ErrorInfo* err;
     Counters* counters;
@@ -344,12 +345,11 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
             v[6] = wr0 * w;
             reduce_peers<7>(0xffffffffu, peers, v);
             if (leader) {
+                // texel-major accumulator: the 7 values of a texel share 2 sectors
                 const int64_t tx = int64_t((kq < 2 ? y0 : y1)) * tw + ((kq & 1) ? x1 : x0);
-                for (int c = 0; c < 3; ++c) {
-                    if (v[c] != 0) atomicAdd(p.grad + p.lay_d + 3 * tx + c, v[c]);
-                    if (v[3 + c] != 0) atomicAdd(p.grad + p.lay_s + 3 * tx + c, v[3 + c]);
-                }
-                if (v[6] != 0) atomicAdd(p.grad + p.lay_r + tx, v[6]);
+                TexAcc* dst = p.texacc + tx;
+                for (int i = 0; i < 7; ++i)
+                    if (v[i] != 0) atomicAdd(&dst->v[i], TexAccT(v[i]));
             }
         }
     }
@@ -388,6 +388,19 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
 __global__ void k_tone(const double* __restrict__ in, size_t n, double gamma, double* __restrict__ out) {
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
         out[i] = tone_map(in[i], gamma);
+}
+
+// texel-major accumulators -> the diffuse / specular / roughness segments
+__global__ void k_texel_flush(const TexAcc* __restrict__ acc, int n, double* __restrict__ grad, int64_t lay_d,
+                              int64_t lay_s, int64_t lay_r) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const TexAcc a = acc[t];
+    for (int c = 0; c < 3; ++c) {
+        grad[lay_d + 3 * int64_t(t) + c] += double(a.v[c]);
+        grad[lay_s + 3 * int64_t(t) + c] += double(a.v[3 + c]);
+    }
+    grad[lay_r + t] += double(a.v[6]);
 }
 
 __global__ void k_view_loss(int n, const double* __restrict__ r, const double* __restrict__ tg,
@@ -454,6 +467,13 @@ void launch_tone_targets(cdr_ctx* c, double gamma) {
     if (n == 0) return;
     int nb = int(std::min<size_t>((n + 255) / 256, 148 * 16));
     { ++c->launches; k_tone<<<nb, 256, 0, c->stream>>>(c->target.p, n, gamma, c->target_tone.p); }
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_texel_flush(cdr_ctx* c, int64_t lay_d, int64_t lay_s, int64_t lay_r) {
+    const int n = c->tw * c->th;
+    if (n <= 0) return;
+    { ++c->launches; k_texel_flush<<<(n + 255) / 256, 256, 0, c->stream>>>(c->tex_acc.p, n, c->grad.p, lay_d, lay_s, lay_r); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -545,6 +565,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     p.lay_r = a.lay_roughness;
     p.lay_l = a.lay_light;
     p.corner = c->corner_acc.p;
+    p.texacc = c->tex_acc.p;
     p.loss_acc = c->loss_acc.p;
     p.err = c->errinfo.p;
     p.counters = c->counters.p;
