@@ -37,6 +37,14 @@ struct __align__(16) TriRec {
     int pad;
 };
 
+#ifdef CDR_TRACE_STATS
+// debug build only: [0] rays, [1] node visits, [2] leaf (triangle) tests
+static __device__ unsigned long long g_trace_stats[4];  // per translation unit
+#define CDR_STAT(i, v) atomicAdd(&g_trace_stats[i], (unsigned long long)(v))
+#else
+#define CDR_STAT(i, v)
+#endif
+
 struct Hit {
     int tri;
     double t, b1, b2;
@@ -82,6 +90,7 @@ __device__ __forceinline__ void leaf_test(const TriRec* __restrict__ recs, int l
     double2 a = __ldg(&p->a), b = __ldg(&p->b), c = __ldg(&p->c), dd = __ldg(&p->d);
     double e = __ldg(&p->e);
     int tri = __ldg(&p->tri);
+    CDR_STAT(2, 1);
     double t, b1, b2;
     if (ray_triangle(o, d, D3{a.x, a.y, b.x}, D3{b.y, c.x, c.y}, D3{dd.x, dd.y, e}, t, b1, b2) &&
         t > t_min && (t < best.t || (t == best.t && tri < best.tri))) {
@@ -108,12 +117,14 @@ __device__ __forceinline__ Hit trace(const BNode* __restrict__ nodes,
         return best;
     }
     FRay r = make_fray(o, d);
+    CDR_STAT(0, 1);
     int stack[64];
     int sp = 0;
     int node = 0;
     float tb = FLT_MAX;
     while (true) {
         const BNode* np = nodes + node;
+        CDR_STAT(1, 1);
         float4 a = __ldg(&np->a), b = __ldg(&np->b), c = __ldg(&np->c);
         int4 k = __ldg(&np->k);
         float t0, t1;
