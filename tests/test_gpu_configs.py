@@ -1,0 +1,60 @@
+"""Parity at the configurations' own sizes and shapes:
+one full cfg2 view (69,620-tri blob, 512^2 textures, 512^2 x 16 spp), the
+cfg4 torus-knot family (thin tube, many silhouettes), cfg1 in full, and the
+library's NCCL all-reduce path with a one-rank communicator."""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import Oracle, layout_for, settings
+from paper_2103_15208_b200 import scenes as S
+from paper_2103_15208_b200.api import RenderSettings, Renderer
+from tests.scenes_util import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare(scene, spp, seed, lam_lap=0.1, nccl=False):
+    tgt = S.perturbed_target_scene(scene)
+    to = Oracle(tgt)
+    targets = np.stack([to.render(v, spp, seed + 0x7A9)[0] for v in range(len(scene.cameras))])
+    lay = layout_for(scene)
+    o = Oracle(scene)
+    lo, go, ro = o.loss_grad(targets, settings(spp, seed), lay, lam_lap=lam_lap, want_rendered=True)
+    r = Renderer(0, scene)
+    if nccl:
+        r.comm_init(Renderer.nccl_unique_id(), 1, 0)
+    for k in range(len(scene.cameras)):
+        r.set_target(k, targets[k])
+    lg, gg, stats, rg = r.loss_grad(np.arange(len(scene.cameras)), RenderSettings(spp=spp, seed=seed), lay,
+                                    1.0, lam_lap, want_rendered=True)
+    for v in range(len(scene.cameras)):
+        np.testing.assert_array_equal(r.render(v, RenderSettings(spp=spp, seed=seed))[2], o.render(v, spp, seed)[2])
+    np.testing.assert_array_equal(rg, ro.ravel())
+    assert abs(lg[0] - lo[0]) <= 1e-10 * abs(lo[0])
+    P = 3 * scene.mesh.V
+    assert rel_l2(gg[:P], go[:P]) <= 1e-4
+    assert rel_l2(gg[P:], go[P:]) <= 1e-4
+    return stats
+
+
+def test_cfg2_full_view():
+    sc = S.make_scene(S.blob(59), 512, 1, 512)
+    st = _compare(sc, 16, 1)
+    assert st.samples == 512 * 512 * 16 and st.segments > 100
+
+
+def test_cfg4_torus_knot_family():
+    knot = S.torus_knot(250, 24)  # same (2,3) tube, reduced resolution
+    sc = S.make_scene(knot, 64, 2, 192)
+    st = _compare(sc, 4, 3)
+    assert st.boundary_active > 0
+
+
+def test_cfg1_full():
+    sc, spp = S.config_scene("cfg1")
+    _compare(sc, spp, 1)
+
+
+def test_nccl_single_rank_allreduce_path():
+    sc = S.make_scene(S.blob(6), 16, 2, 32)
+    _compare(sc, 4, 2, nccl=True)
