@@ -37,10 +37,23 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fwd+adjoint Msamples/s at 1/2/4/8 B200; ms per optimisation iteration"
 UNIT = "Msamples/s"
-VIEWS_PER_GPU = 50
-WORKLOAD = ("cfg2: 70k-tri blob (geodesic f=59 + make_blob field, 69,620 tris), 512^2 SVBRDF "
-            "textures, 50 views/GPU at 512^2, 16 spp, boundary term M=W*H, cotangent Laplacian")
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+# BASELINE.json configs (SURVEY.md §8(d) shapes). cfg2 (configs[1]) is the
+# default and the driver's line; the others are reachable with --config.
+# weak: every rank owns `views` views; strong: `views` views split over ranks.
+CONFIGS = {
+    "cfg1": dict(mesh="geodesic_sphere(11): 2,420 tris", tex=128, views=4, image=128, spp=4, scaling="weak"),
+    "cfg2": dict(mesh="blob(59): 69,620 tris", tex=512, views=50, image=512, spp=16, scaling="weak"),
+    "cfg3": dict(mesh="blob(59): 69,620 tris", tex=1024, views=100, image=512, spp=16, scaling="strong"),
+    "cfg4": dict(mesh="torus_knot(1000x100): 200,000 tris", tex=1024, views=64, image=1024, spp=16,
+                 scaling="strong"),
+    "cfg5": dict(mesh="blob(59): 69,620 tris", tex=1024, views=400, image=512, spp=16, scaling="strong"),
+}
+
+
+def workload_text(name, cfg, views):
+    return (f"{name}: {cfg['mesh']}, {cfg['tex']}^2 SVBRDF textures, {views} views at {cfg['image']}^2, "
+            f"{cfg['spp']} spp, boundary term M=W*H, cotangent Laplacian ({cfg['scaling']} scaling)")
 
 
 def _env_int(k, d):
@@ -56,20 +69,27 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--views", type=int, default=VIEWS_PER_GPU, help="views per GPU (default: cfg2's 50)")
+    p.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    p.add_argument("--views", type=int, default=None, help="override the config's view count")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
 
 
-def build_workload(rank, world, n_views):
+def build_workload(name, rank, world, n_views=None):
     from paper_2103_15208_b200 import scenes as S
-    mesh = S.blob(59)
-    d, s, r = S.random_maps(512, seed=7)
-    cams = S.sample_views_on_sphere(n_views * world, 2.5, 11, 40.0, 512, 512)
-    gids = list(range(rank * n_views, (rank + 1) * n_views))
+    from paper_2103_15208_b200.shard import shard_views, weak_views
+    cfg = CONFIGS[name]
+    mesh = {"cfg1": lambda: S.geodesic_sphere(11), "cfg4": lambda: S.torus_knot()}.get(name, lambda: S.blob(59))()
+    d, s, r = S.random_maps(cfg["tex"], seed=7)
+    views = n_views or cfg["views"]
+    if cfg["scaling"] == "weak":
+        total, gids = views * world, weak_views(views, rank)
+    else:
+        total, gids = views, shard_views(views, world, rank)
+    cams = S.sample_views_on_sphere(total, 2.5, 11, 40.0, cfg["image"], cfg["image"])
     scene = S.Scene(mesh, d, s, r, [cams[g] for g in gids])
-    return scene, gids
+    return scene, gids, cfg, total
 
 
 def peaks():
@@ -127,7 +147,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline_sample(scene, spp, seed, lay, threads, kind_pref="reference"):
+def cpu_baseline_sample(scene, spp, seed, lay, threads, kind_pref="reference", label="cfg2"):
     """Reference total_loss on ONE view of the workload (bounded sample)."""
     from oracle import pyoracle
     from paper_2103_15208_b200 import scenes as S
@@ -158,30 +178,31 @@ def cpu_baseline_sample(scene, spp, seed, lay, threads, kind_pref="reference"):
     cam = one.cameras[0]
     samples = cam.width * cam.height * spp
     return {"value": samples / dt / 1e6, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"1 cfg2 view (512^2 x {spp} spp, 69,620 tris, 512^2 tex) through total_loss, "
-                      f"{dt:.2f} s wall", "seconds": dt}
+            "sample": f"1 {label} view ({cam.width}^2 x {spp} spp, {scene.mesh.T:,} tris, {scene.tex_res[0]}^2 tex) "
+                      f"through total_loss, {dt:.2f} s wall", "seconds": dt}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return 0
     from paper_2103_15208_b200 import api
-    scene, gids = build_workload(0, 1, 1)
+    scene, gids, cfg, _ = build_workload(args.config, 0, 1, 1)
     lay = api.param_layout(scene)
     threads = os.cpu_count() or 1
     vals = []
     cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline_sample(scene, 16, 1, lay, threads)
+        cb = cpu_baseline_sample(scene, cfg["spp"], 1, lay, threads, label=args.config)
         if i >= args.warmup:
             vals.append(cb["seconds"])
     dt = sum(vals)
-    samples = 512 * 512 * 16 * len(vals)
+    samples = cfg["image"] * cfg["image"] * cfg["spp"] * len(vals)
     v = samples / dt / 1e6
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / len(vals), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "sample": "1 view per step (bounded CPU sample)",
+            "config": {"workload": workload_text(args.config, cfg, cfg["views"]),
+                       "sample": "1 view per step (bounded CPU sample)",
                        "threads": threads},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
                              "sample": cb["sample"]},
@@ -206,8 +227,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2103_15208_b200 import api
 
-    spp, seed = 16, 1
-    scene, gids = build_workload(rank, world, args.views)
+    seed = 1
+    scene, gids, cfg, total_views = build_workload(args.config, rank, world, args.views)
+    spp = cfg["spp"]
     r = api.Renderer(local, scene, view_ids=gids)
     if world > 1:
         uid = [api.Renderer.nccl_unique_id() if rank == 0 else None]
@@ -258,7 +280,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     t_max = float(t.item())
     samples_rank = sum(c.width * c.height for c in scene.cameras) * spp
-    total_samples = samples_rank * world * args.steps
+    samples_all = sum(cfg["image"] ** 2 for _ in range(total_views)) * spp
+    total_samples = samples_all * args.steps
     value = total_samples / (t_max / 1e3) / 1e6
 
     # ---- roofline of the dominant kernel (fused trace/shade/loss/interior)
@@ -310,7 +333,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline_sample(scene, spp, seed, lay, os.cpu_count() or 1)
+        cb = cpu_baseline_sample(scene, spp, seed, lay, os.cpu_count() or 1, label=args.config)
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
@@ -318,9 +341,10 @@ def main():
                   ("ms_prepare", "ms_trace", "ms_render", "ms_silhouette", "ms_boundary", "ms_finalize", "ms_total")}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "views_per_gpu": len(scene.cameras), "spp": spp,
-                           "samples_per_step": samples_rank * world, "parallelism": f"views sharded x{world}",
+                "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_text(args.config, cfg, total_views), "name": args.config,
+                           "views_per_gpu": len(scene.cameras), "spp": spp,
+                           "samples_per_step": samples_all, "parallelism": f"views sharded x{world}",
                            "l2": "flushed (256 MB write) before every timed step; step working set ~2 GB"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(sum(x["kernel_launches"] for x in stats)),
