@@ -231,9 +231,12 @@ def main():
     scene, gids, cfg, total_views = build_workload(args.config, rank, world, args.views)
     spp = cfg["spp"]
     r = api.Renderer(local, scene, view_ids=gids)
-    if world > 1:
+    if world > 1 or os.environ.get("CDR_FORCE_COMM") == "1":
+        # one NCCL communicator per GPU for the gradient all-reduce inside
+        # cdr_loss_grad; the 128-byte id travels over torch.distributed
         uid = [api.Renderer.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
+        if dist is not None:
+            dist.broadcast_object_list(uid, src=0)
         r.comm_init(uid[0], world, rank)
     # targets: the perturbed scene rendered by the same engine (gradcheck.cpp:49-73)
     from paper_2103_15208_b200 import scenes as S
@@ -326,7 +329,9 @@ def main():
         te = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
         if dist is not None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        h2d = pos_h.nbytes + d_h.nbytes + s_h.nbytes + r_h.nbytes
+        # positions + maps up; the caller's gradient buffer goes up and comes
+        # back (cdr_loss_grad accumulates += on the device)
+        h2d = pos_h.nbytes + d_h.nbytes + s_h.nbytes + r_h.nbytes + g_h.nbytes
         d2h = g_h.nbytes + 16
         e2e = {"value": total_samples / float(te.item()) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(te.item()) / args.steps}

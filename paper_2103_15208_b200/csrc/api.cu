@@ -161,14 +161,16 @@ void raise_device_error(cdr_ctx* c) {
         throw ApiErr(CDR_ERR_NONFINITE, "non-finite boundary gradient at segment " + std::to_string(e.segment));
 }
 
-// D2H of a device gradient slice and += into the caller's host buffer.
+// += of a device gradient slice into the caller's host buffer, done on the
+// device: upload the caller's values, add, download in place (two copies at
+// full speed when the caller's buffer is pinned; no host-side loop).
 void add_grad_to_host(cdr_ctx* c, double* host, int64_t off, int64_t n) {
     if (!host || n <= 0) return;
-    std::vector<double> tmp(n);
-    CDR_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), c->grad.p + off, sizeof(double) * n, cudaMemcpyDeviceToHost,
-                                   c->stream));
+    c->grad_tmp.ensure(size_t(n));
+    CDR_CUDA_CHECK(cudaMemcpyAsync(c->grad_tmp.p, host + off, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    launch_axpy(c, c->grad_tmp.p, c->grad.p + off, n);  // grad_tmp += grad
+    CDR_CUDA_CHECK(cudaMemcpyAsync(host + off, c->grad_tmp.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
     sync(c);
-    for (int64_t i = 0; i < n; ++i) host[off + i] += tmp[i];
 }
 
 void ensure_hit_arena(cdr_ctx* c, int spp) {
@@ -275,7 +277,7 @@ void cdr_destroy(cdr_ctx* c) {
     c->target.release(); c->target_mask.release(); c->img.release(); c->mask.release(); c->adj.release();
     c->hit.release(); c->sil_flag.release(); c->sil_block_count.release(); c->sil_block_off.release();
     c->sil_count.release(); c->segs.release(); c->cdf.release(); c->total_len.release();
-    c->degenerate.release(); c->grad.release(); c->corner_acc.release(); c->tex_acc.release(); c->qvec.release();
+    c->degenerate.release(); c->grad.release(); c->grad_tmp.release(); c->corner_acc.release(); c->tex_acc.release(); c->qvec.release();
     c->loss_acc.release(); c->errinfo.release(); c->counters.release();
     cudaStreamDestroy(c->stream);
     delete c;
@@ -756,13 +758,7 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
     double lap_sq = 0;
     CDR_CUDA_CHECK(cudaMemcpyAsync(lacc.data(), c->loss_acc.p, sizeof(double) * lacc.size(), cudaMemcpyDeviceToHost, s));
     CDR_CUDA_CHECK(cudaMemcpyAsync(&lap_sq, c->lap_partial.p, sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (grad) {
-        static thread_local std::vector<double> tmp;
-        tmp.resize(size_t(lay->total));
-        CDR_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), c->grad.p, sizeof(double) * lay->total, cudaMemcpyDeviceToHost, s));
-        sync(c);
-        for (int64_t i = 0; i < lay->total; ++i) grad[i] += tmp[i];
-    }
+    if (grad) add_grad_to_host(c, grad, 0, lay->total);
     size_t ro = 0, mo = 0;
     for (int i = 0; i < n; ++i) {
         const ViewData& v = c->views[slots[i]];

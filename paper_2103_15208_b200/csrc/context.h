@@ -125,6 +125,7 @@ struct cdr_ctx {
     // gradient + accumulators
     int64_t grad_n = 0;
     cdr::DBuf<double> grad;
+    cdr::DBuf<double> grad_tmp;    // staging of the caller's += buffer
     cdr::DBuf<double> corner_acc;  // T x 3 corners x (g[3], h[3])
     cdr::DBuf<cdr::TexAcc> tex_acc;  // texel-major interior texel gradients
     cdr::DBuf<double> qvec;        // V x 3: Jn_v * H_v

@@ -70,6 +70,8 @@ void launch_laplacian(cdr_ctx* c, int mode, double lambda, double* grad_pos /* n
 // generic loss kernel over device images (cdr_view_loss)
 // Φ(target) for all target pixels (losses.cpp:38 evaluates it per pixel)
 void launch_tone_targets(cdr_ctx* c, double gamma);
+// y += x over n doubles
+void launch_axpy(cdr_ctx* c, double* y, const double* x, int64_t n);
 // add the texel-major accumulators into the gradient's texture segments
 void launch_texel_flush(cdr_ctx* c, int64_t lay_d, int64_t lay_s, int64_t lay_r);
 // radiance_at for n pixel positions of one view (device buffers)

@@ -390,6 +390,11 @@ __global__ void k_tone(const double* __restrict__ in, size_t n, double gamma, do
         out[i] = tone_map(in[i], gamma);
 }
 
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        y[i] += x[i];
+}
+
 // texel-major accumulators -> the diffuse / specular / roughness segments
 __global__ void k_texel_flush(const TexAcc* __restrict__ acc, int n, double* __restrict__ grad, int64_t lay_d,
                               int64_t lay_s, int64_t lay_r) {
@@ -467,6 +472,13 @@ void launch_tone_targets(cdr_ctx* c, double gamma) {
     if (n == 0) return;
     int nb = int(std::min<size_t>((n + 255) / 256, 148 * 16));
     { ++c->launches; k_tone<<<nb, 256, 0, c->stream>>>(c->target.p, n, gamma, c->target_tone.p); }
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_axpy(cdr_ctx* c, double* y, const double* x, int64_t n) {
+    if (n <= 0) return;
+    int nb = int(std::min<int64_t>((n + 255) / 256, 148 * 8));
+    { ++c->launches; k_axpy<<<nb, 256, 0, c->stream>>>(y, x, n); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
