@@ -25,7 +25,7 @@ METRICS = {
     "grid": ("launch__grid_size", 1.0),
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
-              "msecond": 1e6, "second": 1e9}
+              "msecond": 1e6, "second": 1e9, "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9}
 
 
 def raw(rep):
