@@ -126,11 +126,11 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     int tri = -1;
     double t = 0, b1 = 0, b2 = 0;
     D3 dir{0, 0, 1};
-    if (valid) {
+    if (valid) tri = p.hit[pidx * spp + s];
+    if (tri >= 0) {  // misses need no ray: their radiance is the background
         D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
         dir = primary_dir(cam, ps);
-        tri = p.hit[pidx * spp + s];
-        if (tri >= 0) {
+        {
             int a = p.sc.tris[3 * tri], b = p.sc.tris[3 * tri + 1], c = p.sc.tris[3 * tri + 2];
             if (!ray_triangle(org, dir, ld3(p.sc.pos + 3 * a), ld3(p.sc.pos + 3 * b), ld3(p.sc.pos + 3 * c), t, b1, b2))
                 tri = -1;
@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
                 double a = 0;
                 if (m != 0) {
                     // losses.cpp:37-44; Φ'(r) = Φ(r) / (γ r) for r in (0, 1)
-                    double tr = tone_map(mean, p.gamma);
+                    // Φ(0) = pow(0, 1/γ) = +0 exactly: skip pow on background
+                    double tr = mean <= 0.0 ? 0.0 : tone_map(mean, p.gamma);
                     double d = tr - p.target_tone[3 * qi + c];
                     loss_part += m * fabs(d);
                     double sg = double((d > 0) - (d < 0));
