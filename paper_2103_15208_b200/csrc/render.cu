@@ -224,7 +224,9 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
             if (nh) atomicAdd(&p.counters->hit_samples, (unsigned long long)nh);
             if (na) atomicAdd(&p.counters->adjoint_samples, (unsigned long long)na);
         }
+        if (na == 0) return;  // background / zero-adjoint tile (uniform per CTA)
     }
+    if (!__any_sync(0xffffffffu, act)) return;  // no barrier follows: warp-level exit is safe
     a = a / double(spp);  // diff_render.cpp:82
 
     // Compute everything the scatter needs first, so the large temporaries
