@@ -258,32 +258,41 @@ __device__ __forceinline__ bool boundary_setup(const BParams& p, int vi, int64_t
     return !(b.adj.x == 0 && b.adj.y == 0 && b.adj.z == 0);
 }
 
-// pass 1: classify every sample, count active samples per segment
+// Samples are binned by (segment, position along it): kSBins buckets of s per
+// segment, so a warp of the probe kernel traces nearly identical rays.
+#ifndef CDR_SBINS
+#define CDR_SBINS 8
+#endif
+constexpr int kSBins = CDR_SBINS;
+
+// pass 1: classify every sample, count active samples per (segment, s bucket)
 __global__ void __launch_bounds__(kBlock) k_bsample(BParams p) {
     const int vi = blockIdx.y;
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     BSample b;
     bool act = i < p.m_stride && boundary_setup(p, vi, i, b);
-    const int key = act ? b.si : -1 - int(threadIdx.x & 31);
+    const int bin = act ? b.si * kSBins + min(kSBins - 1, int(b.s * kSBins)) : 0;
+    const int key = act ? bin : -1 - int(threadIdx.x & 31);
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(peers) - 1;
     int base = 0;
-    if (act && lane == leader) base = atomicAdd(&p.seg_count[size_t(vi) * p.E + b.si], __popc(peers));
+    if (act && lane == leader) base = atomicAdd(&p.seg_count[size_t(vi) * p.E * kSBins + bin], __popc(peers));
     base = __shfl_sync(0xffffffffu, base, leader);
     if (i < p.m_stride) {
         size_t o = size_t(vi) * p.m_stride + i;
-        p.key[o] = act ? b.si : -1;
+        p.key[o] = act ? bin : -1;
         p.slot[o] = base + __popc(peers & ((1u << lane) - 1u));
         if (act) p.s_param[o] = b.s;
     }
 }
 
-// pass 2 (one CTA per view): exclusive scan of the per-segment counts
+// pass 2 (one CTA per view): exclusive scan of the per-bin counts
 __global__ void k_bscan(const int32_t* __restrict__ count, const int32_t* __restrict__ nseg, int E,
                         int32_t* __restrict__ off, int32_t* __restrict__ n_active) {
     const int vi = blockIdx.x;
-    const int n = nseg[vi];
+    const int n = nseg[vi] * kSBins;
+    E *= kSBins;  // per-view stride of the bin arrays
     __shared__ int32_t sh[1024];
     __shared__ int32_t carry;
     if (threadIdx.x == 0) carry = 0;
@@ -315,9 +324,9 @@ __global__ void k_bscatter(BParams p) {
     size_t o = size_t(vi) * p.m_stride + i;
     int k = p.key[o];
     if (k < 0) return;
-    size_t d = size_t(vi) * p.m_stride + p.seg_off[size_t(vi) * p.E + k] + p.slot[o];
+    size_t d = size_t(vi) * p.m_stride + p.seg_off[size_t(vi) * p.E * kSBins + k] + p.slot[o];
     p.order[d] = int32_t(i);
-    p.sorted_si[d] = k;
+    p.sorted_si[d] = k / kSBins;
     p.sorted_s[d] = p.s_param[o];
 }
 
@@ -481,8 +490,8 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
                                    cudaMemcpyHostToDevice, c->stream));
     const int E = std::max(1, c->E);
     const size_t nm = size_t(n_views) * samples;
-    c->b_seg_count.ensure(size_t(n_views) * E);
-    c->b_seg_off.ensure(size_t(n_views) * E);
+    c->b_seg_count.ensure(size_t(n_views) * E * kSBins);
+    c->b_seg_off.ensure(size_t(n_views) * E * kSBins);
     c->b_n_active.ensure(n_views);
     c->b_key.ensure(nm);
     c->b_slot.ensure(nm);
@@ -490,7 +499,7 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     c->b_s.ensure(nm);
     c->b_sorted_si.ensure(nm);
     c->b_sorted_s.ensure(nm);
-    CDR_CUDA_CHECK(cudaMemsetAsync(c->b_seg_count.p, 0, sizeof(int32_t) * size_t(n_views) * E, c->stream));
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->b_seg_count.p, 0, sizeof(int32_t) * size_t(n_views) * E * kSBins, c->stream));
     BParams p{};
     p.sc = shade_scene(c);
     p.info = c->info.p;
