@@ -261,7 +261,7 @@ __device__ __forceinline__ bool boundary_setup(const BParams& p, int vi, int64_t
 // Samples are binned by (segment, position along it): kSBins buckets of s per
 // segment, so a warp of the probe kernel traces nearly identical rays.
 #ifndef CDR_SBINS
-#define CDR_SBINS 8
+#define CDR_SBINS 32
 #endif
 constexpr int kSBins = CDR_SBINS;
 
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kBlock) k_bsample(BParams p) {
 }
 
 // pass 2 (one CTA per view): exclusive scan of the per-bin counts
-__global__ void k_bscan(const int32_t* __restrict__ count, const int32_t* __restrict__ nseg, int E,
+__global__ void k_bscan(int32_t* __restrict__ count, const int32_t* __restrict__ nseg, int E,
                         int32_t* __restrict__ off, int32_t* __restrict__ n_active) {
     const int vi = blockIdx.x;
     const int n = nseg[vi] * kSBins;
@@ -299,7 +299,11 @@ __global__ void k_bscan(const int32_t* __restrict__ count, const int32_t* __rest
     __syncthreads();
     for (int base = 0; base < n; base += 1024) {
         int i = base + threadIdx.x;
-        int v = i < n ? count[size_t(vi) * E + i] : 0;
+        int v = 0;
+        if (i < n) {
+            v = count[size_t(vi) * E + i];
+            count[size_t(vi) * E + i] = 0;  // counters are left zeroed for the next call
+        }
         sh[threadIdx.x] = v;
         __syncthreads();
         for (int o = 1; o < 1024; o <<= 1) {
@@ -490,8 +494,12 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
                                    cudaMemcpyHostToDevice, c->stream));
     const int E = std::max(1, c->E);
     const size_t nm = size_t(n_views) * samples;
-    c->b_seg_count.ensure(size_t(n_views) * E * kSBins);
-    c->b_seg_off.ensure(size_t(n_views) * E * kSBins);
+    const size_t nbins = size_t(n_views) * E * kSBins;
+    if (c->b_seg_count.n < nbins) {  // zeroed once; k_bscan re-zeroes what it consumed
+        c->b_seg_count.ensure(nbins);
+        CDR_CUDA_CHECK(cudaMemsetAsync(c->b_seg_count.p, 0, sizeof(int32_t) * nbins, c->stream));
+    }
+    c->b_seg_off.ensure(nbins);
     c->b_n_active.ensure(n_views);
     c->b_key.ensure(nm);
     c->b_slot.ensure(nm);
@@ -499,7 +507,6 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     c->b_s.ensure(nm);
     c->b_sorted_si.ensure(nm);
     c->b_sorted_s.ensure(nm);
-    CDR_CUDA_CHECK(cudaMemsetAsync(c->b_seg_count.p, 0, sizeof(int32_t) * size_t(n_views) * E * kSBins, c->stream));
     BParams p{};
     p.sc = shade_scene(c);
     p.info = c->info.p;
