@@ -273,7 +273,10 @@ void cdr_destroy(cdr_ctx* c) {
     c->lap_val.release(); c->lap_lv.release(); c->lap_grad.release(); c->lap_partial.release();
     c->info.release(); c->bbox_partial.release(); c->keys.release(); c->keys_alt.release();
     c->sort_tmp.release(); c->parent_internal.release(); c->parent_leaf.release(); c->refit_flag.release();
-    c->node_box.release(); c->nodes.release(); c->recs.release(); c->tex.release(); c->d_cams.release();
+    c->node_box.release(); c->nodes.release(); c->recs.release();
+    c->beam_hdr.release(); c->beam_pool.release(); c->beam_used.release();
+    c->beam_pix_list.release(); c->beam_pix_cnt.release();
+    if (c->beam_used_host) cudaFreeHost(c->beam_used_host); c->tex.release(); c->d_cams.release();
     c->target.release(); c->target_mask.release(); c->img.release(); c->mask.release(); c->adj.release();
     c->hit.release(); c->sil_flag.release(); c->sil_block_count.release(); c->sil_block_off.release();
     c->sil_count.release(); c->segs.release(); c->cdf.release(); c->total_len.release();

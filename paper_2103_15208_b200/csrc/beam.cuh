@@ -1,0 +1,141 @@
+// beam.cuh — tile-frustum ("beam") traversal of the LBVH for primary rays.
+//
+// All primary rays of a pixel tile leave the camera origin through one small
+// pixel rectangle, so their BVH paths nearly coincide. Instead of every sample
+// traversing the tree (13 node visits and a stack per ray), ONE frustum
+// traversal per tile collects the candidate triangles: every leaf whose padded
+// box is not entirely outside one of the tile frustum's five planes. A sample
+// then scans the tile's candidates in order of a lower bound on their hit
+// distance, rejects most with an fp32 screen-space edge test, runs the exact
+// fp64 Moller-Trumbore (bvh.cuh leaf_test) on the rest, and stops as soon as
+// the next candidate's bound exceeds its best hit.
+//
+// Exactness: a triangle any ray of the tile can hit intersects
+// the tile frustum, so its box survives the conservative plane tests and it is
+// a candidate; the 2D test only rejects sample points farther than 0.01 px
+// outside the projected triangle (fp32 error is ~1e-5 px), and triangles whose
+// projection is unreliable (a vertex near or behind the camera plane, edge-on)
+// always go to the exact test; the distance bound is a lower bound on t
+// (rays are unit length), compared strictly, so ties to a lower triangle index
+// are never cut off. The answer is the brute-force oracle's, as for trace().
+// Tiles with more than kBeamCap candidates fall back to per-ray traversal.
+#pragma once
+
+#include "bvh.cuh"
+
+namespace cdr {
+
+constexpr int kBeamCap = 64;    // candidates per tile; more -> per-ray traversal
+constexpr int kPixCap = 16;     // candidates per pixel list; more -> scan the tile list
+constexpr int kFrontCap = 128;  // builder frontier per tile; more -> per-ray traversal
+
+// Candidate record (48 B): three edge functions E_i = A_i x + B_i y + C_i
+// (pixel coordinates relative to the tile origin, margin folded into C_i;
+// E_i >= 0 for all i -> possible hit), the distance bound, the leaf index and
+// flags (bit 0: always run the exact test).
+struct __align__(16) BeamCand {
+    float4 e0;  // A0 B0 C0 A1
+    float4 e1;  // B1 C1 A2 B2
+    float4 e2;  // C2 dmin leaf flags
+};
+
+struct TileHdr {
+    int off;  // first candidate in the pool
+    int cnt;  // candidates, or -1: overflow (per-ray traversal)
+};
+
+struct FrustumPlanes {
+    float n[5][3];  // inward normals through the camera origin
+};
+
+// Inward plane normals of the frustum through pixel rectangle [x0,x1]x[y0,y1]
+// (camera.cpp:29-34: pixel x <-> (q.r)/(q.f) = (2x/W - 1) th aspect, y <-> (q.u)/(q.f) = (1 - 2y/H) th).
+__device__ __forceinline__ FrustumPlanes tile_frustum(const DevCamera& c, double x0, double x1, double y0,
+                                                      double y1) {
+    const double s0 = (2.0 * x0 / c.W - 1.0) * c.th * c.aspect, s1 = (2.0 * x1 / c.W - 1.0) * c.th * c.aspect;
+    const double v0 = (1.0 - 2.0 * y0 / c.H) * c.th, v1 = (1.0 - 2.0 * y1 / c.H) * c.th;
+    FrustumPlanes fp;
+    for (int k = 0; k < 3; ++k) {
+        fp.n[0][k] = float(c.r[k] - s0 * c.f[k]);  // x >= x0
+        fp.n[1][k] = float(s1 * c.f[k] - c.r[k]);  // x <= x1
+        fp.n[2][k] = float(v0 * c.f[k] - c.u[k]);  // y >= y0
+        fp.n[3][k] = float(c.u[k] - v1 * c.f[k]);  // y <= y1
+        fp.n[4][k] = float(c.f[k]);                // in front of the camera
+    }
+    return fp;
+}
+
+// Conservative: true only if the box is certainly outside one plane.
+__device__ __forceinline__ bool box_outside(const FrustumPlanes& fp, const float o[3], float lx, float ly,
+                                            float lz, float hx, float hy, float hz) {
+    const float cx = 0.5f * (lx + hx) - o[0], cy = 0.5f * (ly + hy) - o[1], cz = 0.5f * (lz + hz) - o[2];
+    const float ex = 0.5f * (hx - lx), ey = 0.5f * (hy - ly), ez = 0.5f * (hz - lz);
+    const float mag = fabsf(cx) + fabsf(cy) + fabsf(cz) + ex + ey + ez;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const float* n = fp.n[k];
+        const float d = n[0] * cx + n[1] * cy + n[2] * cz;
+        const float r = fabsf(n[0]) * ex + fabsf(n[1]) * ey + fabsf(n[2]) * ez;
+        const float slack = 1e-5f * (fabsf(n[0]) + fabsf(n[1]) + fabsf(n[2])) * mag;
+        if (d + r < -slack) return true;
+    }
+    return false;
+}
+
+// Conservative overlap of a candidate's (margined) projected triangle with the
+// pixel rectangle [x0,x0+1]x[y0,y0+1] (tile-relative): false only if one edge
+// function is negative on all four corners.
+__device__ __forceinline__ bool cand_overlaps_pixel(const BeamCand& c, float x0, float y0) {
+    if (__float_as_int(c.e2.w) & 1) return true;
+    const float x1 = x0 + 1.0f, y1 = y0 + 1.0f;
+    const float A[3] = {c.e0.x, c.e0.w, c.e1.z}, B[3] = {c.e0.y, c.e1.x, c.e1.w}, C[3] = {c.e0.z, c.e1.y, c.e2.x};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float m = A[i] * (A[i] > 0 ? x1 : x0) + B[i] * (B[i] > 0 ? y1 : y0) + C[i];
+        if (m < 0.0f) return false;
+    }
+    return true;
+}
+
+// Nearest hit of one sample ray using its tile's candidate list (smem or
+// global). Same result as trace(): exact fp64 test, strict t_min < t, ties to
+// the lowest triangle index.
+__device__ __forceinline__ Hit trace_beam(const BeamCand* __restrict__ cand, int n, const TriRec* __restrict__ recs,
+                                          D3 o, D3 d, double t_min, float px, float py) {
+    Hit best{-1, 1e300, 0.0, 0.0};
+    for (int k = 0; k < n; ++k) {
+        const float4 e2 = cand[k].e2;
+        if (double(e2.y) > best.t) break;  // every remaining candidate is farther
+        const int flags = __float_as_int(e2.w);
+        bool pass = true;
+        if (!(flags & 1)) {
+            const float4 e0 = cand[k].e0, e1 = cand[k].e1;
+            pass = e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
+                   e1.z * px + e1.w * py + e2.x >= 0.0f;
+        }
+        if (pass) leaf_test(recs, __float_as_int(e2.z), o, d, t_min, best);
+    }
+    return best;
+}
+
+// Same scan over an index list (a pixel's candidates, in distance order).
+__device__ __forceinline__ Hit trace_beam_list(const BeamCand* __restrict__ cand, const unsigned char* __restrict__ idx,
+                                               int n, const TriRec* __restrict__ recs, D3 o, D3 d, double t_min,
+                                               float px, float py) {
+    Hit best{-1, 1e300, 0.0, 0.0};
+    for (int j = 0; j < n; ++j) {
+        const int k = idx[j];
+        const float4 e2 = cand[k].e2;
+        if (double(e2.y) > best.t) break;
+        bool pass = true;
+        if (!(__float_as_int(e2.w) & 1)) {
+            const float4 e0 = cand[k].e0, e1 = cand[k].e1;
+            pass = e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
+                   e1.z * px + e1.w * py + e2.x >= 0.0f;
+        }
+        if (pass) leaf_test(recs, __float_as_int(e2.z), o, d, t_min, best);
+    }
+    return best;
+}
+
+}  // namespace cdr

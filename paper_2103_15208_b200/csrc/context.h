@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/cdr.h"
+#include "beam.cuh"
 #include "bvh.cuh"
 #include "common.cuh"
 
@@ -94,6 +95,13 @@ struct cdr_ctx {
     cdr::DBuf<float> node_box;  // internal node boxes (6 floats) for the refit
     cdr::DBuf<cdr::BNode> nodes;
     cdr::DBuf<cdr::TriRec> recs;
+    // beam traversal (beam.cuh): per-tile headers and the candidate pool
+    cdr::DBuf<cdr::TileHdr> beam_hdr;
+    cdr::DBuf<cdr::BeamCand> beam_pool;
+    cdr::DBuf<int> beam_used;
+    cdr::DBuf<unsigned char> beam_pix_list, beam_pix_cnt;
+    int* beam_used_host = nullptr;   // pinned; previous call's pool use
+    int beam_used_last = 0;
     double t_min_host = 1e-8;
 
     // materials, light

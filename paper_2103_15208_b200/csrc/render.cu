@@ -16,6 +16,7 @@
 // The one-ring normal chain is deferred: per-corner sums of coeff_mu*b_j*h feed
 // the finalize kernels (finalize.cu), which apply it once per iteration.
 #include "kernels.h"
+#include "beam.cuh"
 #include "shade.cuh"
 
 namespace cdr {
@@ -23,13 +24,14 @@ namespace {
 
 struct ViewCall {
     int slot;
-    int pad;
+    int tile_base;  // first tile of this view in the beam tile arrays
     double scale;     // lambda / n_valid
     uint64_t h_view;  // hash_combine(seed, gid + 0x9e01)
 };
 
 struct Params {
     ShadeScene sc;
+    const BNode* sc_bin;  // binary LBVH (per-ray traversal and the beam builder)
     const SceneInfo* info;
     const DevCamera* cams;
     const ViewCall* calls;
@@ -54,6 +56,14 @@ struct Params {
     double* loss_acc;
     ErrorInfo* err;
     Counters* counters;
+    // beam traversal (beam.cuh): per-tile candidate lists
+    TileHdr* tile_hdr;
+    BeamCand* pool;
+    int pool_cap;
+    int* pool_used;
+    unsigned char* pix_list;  // per (tile, pixel): kPixCap candidate indices
+    unsigned char* pix_cnt;   // per (tile, pixel): count, 255 = scan the tile list
+    int use_beam;
 };
 
 constexpr int kThreads = 256;
@@ -66,13 +76,173 @@ __device__ __forceinline__ void raise_nonfinite(ErrorInfo* e, int x, int y) {
     }
 }
 
+// Beam lists, one warp per (view, tile): breadth-first frustum traversal of the
+// LBVH (lanes take frontier nodes), candidates sorted by their distance bound
+// (rank across lanes), screen-space edge functions, and per-pixel candidate
+// lists (conservative triangle/pixel overlap) so a sample scans only the few
+// triangles that can cover its pixel.
+constexpr int kListWarps = 4;
+__global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
+    __shared__ int s_front[kListWarps][2][kFrontCap];
+    __shared__ int s_leaf[kListWarps][kBeamCap];
+    __shared__ float s_d[kListWarps][kBeamCap];
+    __shared__ BeamCand s_cand[kListWarps][kBeamCap];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const unsigned lt = (1u << lane) - 1u;
+    const ViewCall vc = p.calls[blockIdx.y];
+    const DevCamera cam = p.cams[vc.slot];
+    const int tiles_x = (cam.W + p.TW - 1) / p.TW, tiles_y = (cam.H + p.TH - 1) / p.TH;
+    const int b = blockIdx.x * kListWarps + w;
+    if (b >= tiles_x * tiles_y) return;  // warp-uniform
+    const size_t tile = size_t(vc.tile_base) + b;
+    TileHdr* hdr = p.tile_hdr + tile;
+    const int X0 = (b % tiles_x) * p.TW, Y0 = (b / tiles_x) * p.TH;
+    const int X1 = min(X0 + p.TW, cam.W), Y1 = min(Y0 + p.TH, cam.H);
+    const FrustumPlanes fp = tile_frustum(cam, X0 - 0.01, X1 + 0.01, Y0 - 0.01, Y1 + 0.01);
+    const float of[3] = {float(cam.o[0]), float(cam.o[1]), float(cam.o[2])};
+    const int T = p.sc.n_tris;
+    int nl = 0, nf = 0, cur = 0;
+    bool over = false;
+    if (T == 1) {
+        if (lane == 0) s_leaf[w][0] = 0;
+        nl = 1;
+    } else if (T > 1) {
+        if (lane == 0) s_front[w][0][0] = 0;
+        nf = 1;
+    }
+    __syncwarp();
+    while (nf > 0) {
+        int nn = 0;
+        for (int base = 0; base < nf; base += 32) {
+            const int i = base + lane;
+            bool leaf0 = false, leaf1 = false, int0 = false, int1 = false;
+            int4 k = make_int4(0, 0, 0, 0);
+            if (i < nf) {
+                const BNode* np = p.sc_bin + s_front[w][cur][i];
+                const float4 a = __ldg(&np->a), bb = __ldg(&np->b), c = __ldg(&np->c);
+                k = __ldg(&np->k);
+                const bool in0 = !box_outside(fp, of, a.x, a.y, a.z, a.w, bb.x, bb.y);
+                const bool in1 = !box_outside(fp, of, bb.z, bb.w, c.x, c.y, c.z, c.w);
+                leaf0 = in0 && k.x < 0;
+                int0 = in0 && k.x >= 0;
+                leaf1 = in1 && k.y < 0;
+                int1 = in1 && k.y >= 0;
+            }
+            const unsigned m0 = __ballot_sync(0xffffffffu, leaf0), m1 = __ballot_sync(0xffffffffu, leaf1);
+            const int p0 = nl + __popc(m0 & lt), p1 = nl + __popc(m0) + __popc(m1 & lt);
+            if (leaf0 && p0 < kBeamCap) s_leaf[w][p0] = ~k.x;
+            if (leaf1 && p1 < kBeamCap) s_leaf[w][p1] = ~k.y;
+            nl += __popc(m0) + __popc(m1);
+            const unsigned q0 = __ballot_sync(0xffffffffu, int0), q1 = __ballot_sync(0xffffffffu, int1);
+            const int f0 = nn + __popc(q0 & lt), f1 = nn + __popc(q0) + __popc(q1 & lt);
+            if (int0 && f0 < kFrontCap) s_front[w][cur ^ 1][f0] = k.x;
+            if (int1 && f1 < kFrontCap) s_front[w][cur ^ 1][f1] = k.y;
+            nn += __popc(q0) + __popc(q1);
+        }
+        __syncwarp();
+        if (nl > kBeamCap || nn > kFrontCap) {
+            over = true;
+            break;
+        }
+        nf = nn;
+        cur ^= 1;
+    }
+    if (over) {
+        if (lane == 0) *hdr = TileHdr{0, -1};
+        return;
+    }
+    // lower bound on t (unit rays): distance from the origin to the triangle's box
+    for (int i = lane; i < nl; i += 32) {
+        const TriRec* r = p.sc.recs + s_leaf[w][i];
+        const double2 ra = r->a, rb = r->b, rc = r->c, rd = r->d;
+        const double re = r->e;
+        const double P[3][3] = {{ra.x, rb.y, rd.x}, {ra.y, rc.x, rd.y}, {rb.x, rc.y, re}};
+        double dd = 0;
+        for (int k = 0; k < 3; ++k) {
+            const double lo = fmin(P[k][0], fmin(P[k][1], P[k][2])), hi = fmax(P[k][0], fmax(P[k][1], P[k][2]));
+            const double g = fmax(fmax(lo - cam.o[k], cam.o[k] - hi), 0.0);
+            dd += g * g;
+        }
+        s_d[w][i] = __double2float_rd(sqrt(dd)) * 0.999999f;
+    }
+    __syncwarp();
+    const D3 o{cam.o[0], cam.o[1], cam.o[2]}, fw{cam.f[0], cam.f[1], cam.f[2]}, rt{cam.r[0], cam.r[1], cam.r[2]},
+        up{cam.u[0], cam.u[1], cam.u[2]};
+    for (int i = lane; i < nl; i += 32) {
+        const float di = s_d[w][i];
+        int rank = 0;  // distance order, ties by list position
+        for (int j = 0; j < nl; ++j) {
+            const float dj = s_d[w][j];
+            rank += (dj < di) || (dj == di && j < i);
+        }
+        const int leaf = s_leaf[w][i];
+        const TriRec* r = p.sc.recs + leaf;
+        const double2 ra = r->a, rb = r->b, rc = r->c, rd = r->d;
+        const D3 V[3] = {D3{ra.x, ra.y, rb.x}, D3{rb.y, rc.x, rc.y}, D3{rd.x, rd.y, r->e}};
+        double sx[3], sy[3];
+        int flags = 0;
+        for (int k = 0; k < 3; ++k) {  // project (camera.cpp:36-45), tile-relative pixels
+            const D3 q = V[k] - o;
+            const double cz = dot(q, fw);
+            if (!(cz > 1e-7 * (fabs(q.x) + fabs(q.y) + fabs(q.z)))) flags = 1;
+            sx[k] = (dot(q, rt) / (cz * cam.th * cam.aspect) + 1.0) * 0.5 * cam.W - X0;
+            sy[k] = (1.0 - dot(q, up) / (cz * cam.th)) * 0.5 * cam.H - Y0;
+            if (!(fabs(sx[k]) < 1e4 && fabs(sy[k]) < 1e4)) flags = 1;
+        }
+        const double area2 = (sx[1] - sx[0]) * (sy[2] - sy[0]) - (sx[2] - sx[0]) * (sy[1] - sy[0]);
+        if (!(fabs(area2) > 1e-9)) flags = 1;
+        const double sg = area2 < 0 ? -1.0 : 1.0;
+        float E[9];
+        for (int k = 0; k < 3; ++k) {  // E = cross(edge, point - start) >= -0.01 px * |edge|
+            const int j = k == 2 ? 0 : k + 1;
+            const double dx = sx[j] - sx[k], dy = sy[j] - sy[k];
+            E[3 * k] = float(-dy * sg);
+            E[3 * k + 1] = float(dx * sg);
+            E[3 * k + 2] = float((dy * sx[k] - dx * sy[k]) * sg + 0.01 * sqrt(dx * dx + dy * dy));
+        }
+        BeamCand bc;
+        bc.e0 = make_float4(E[0], E[1], E[2], E[3]);
+        bc.e1 = make_float4(E[4], E[5], E[6], E[7]);
+        bc.e2 = make_float4(E[8], di, __int_as_float(leaf), __int_as_float(flags));
+        s_cand[w][rank] = bc;
+    }
+    __syncwarp();
+    int off = 0;
+    if (lane == 0 && nl) off = atomicAdd(p.pool_used, nl);
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (off + nl > p.pool_cap) {
+        if (lane == 0) *hdr = TileHdr{0, -1};
+        return;
+    }
+    const float4* src = reinterpret_cast<const float4*>(&s_cand[w][0]);
+    float4* dst = reinterpret_cast<float4*>(p.pool + off);
+    for (int i = lane; i < 3 * nl; i += 32) dst[i] = src[i];
+    // per-pixel lists, in distance order
+    const int P = kThreads / p.spp;
+    for (int q = lane; q < P; q += 32) {
+        const float qx = float(q % p.TW), qy = float(q / p.TW);
+        unsigned char* lst = p.pix_list + (tile * P + q) * kPixCap;
+        int cnt = 0;
+        for (int k = 0; k < nl; ++k)
+            if (cand_overlaps_pixel(s_cand[w][k], qx, qy)) {
+                if (cnt < kPixCap) lst[cnt] = (unsigned char)k;
+                ++cnt;
+            }
+        p.pix_cnt[tile * P + q] = (unsigned char)(cnt > kPixCap ? 255 : cnt);
+    }
+    if (lane == 0) *hdr = TileHdr{off, nl};
+}
+
 // Primary visibility: one thread per sample, tile order as k_render, writes the
 // hit cache (the bit-exact output). Kept slim so it runs at high occupancy —
 // traversal is latency-bound, not bandwidth-bound.
 #ifndef CDR_TRACE_MIN_BLOCKS
 #define CDR_TRACE_MIN_BLOCKS 4
 #endif
+template <bool kBeam>
 __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
+    __shared__ BeamCand s_c[kBeam ? kBeamCap : 1];
+    __shared__ TileHdr s_h;
     const ViewCall vc = p.calls[blockIdx.y];
     const DevCamera cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
@@ -83,13 +253,44 @@ __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params
     const int spp = p.spp;
     const int P = kThreads / spp;
     const int pix = tid / spp, s = tid - (tid / spp) * spp;
-    const int x = (blockIdx.x % tiles_x) * p.TW + pix % p.TW;
-    const int y = (blockIdx.x / tiles_x) * p.TH + pix / p.TW;
+    const int X0 = (blockIdx.x % tiles_x) * p.TW, Y0 = (blockIdx.x / tiles_x) * p.TH;
+    const int x = X0 + pix % p.TW;
+    const int y = Y0 + pix / p.TW;
+    int n = -1;
+    __shared__ __align__(16) unsigned char s_pl[kBeam ? kThreads * kPixCap : 16];
+    __shared__ unsigned char s_pc[kBeam ? kThreads : 1];
+    if (kBeam) {  // stage the tile's candidates and pixel lists in shared memory
+        if (tid == 0) s_h = p.tile_hdr[vc.tile_base + blockIdx.x];
+        __syncthreads();
+        n = s_h.cnt;
+        if (n >= 0) {
+            for (int i = tid; i < 3 * n; i += kThreads)
+                reinterpret_cast<float4*>(s_c)[i] = __ldg(reinterpret_cast<const float4*>(p.pool + s_h.off) + i);
+            const size_t tile = size_t(vc.tile_base) + blockIdx.x;
+            const uint4* gl = reinterpret_cast<const uint4*>(p.pix_list + tile * P * kPixCap);
+            for (int i = tid; i < P * kPixCap / 16; i += kThreads) reinterpret_cast<uint4*>(s_pl)[i] = __ldg(gl + i);
+            if (tid < P) s_pc[tid] = p.pix_cnt[tile * P + tid];
+        }
+        __syncthreads();
+    }
     if (!(pix < P && x < W && y < H)) return;
     const size_t pidx = p.pix_off[vc.slot] + size_t(y) * W + x;
-    D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
-    D3 dir = primary_dir(cam, ps);
-    Hit h = trace(p.sc.nodes, p.sc.recs, p.sc.n_tris, D3{cam.o[0], cam.o[1], cam.o[2]}, dir, p.info->t_min);
+    const D3 org{cam.o[0], cam.o[1], cam.o[2]};
+    Hit h{-1, 1e300, 0.0, 0.0};
+    if (kBeam && n >= 0) {
+        const int cnt = s_pc[pix];
+        if (cnt != 0) {  // an empty pixel list means no triangle can cover the pixel: no ray needed
+            D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
+            D3 dir = primary_dir(cam, ps);
+            const float fx = float(ps.x - X0), fy = float(ps.y - Y0);
+            h = cnt == 255 ? trace_beam(s_c, n, p.sc.recs, org, dir, p.info->t_min, fx, fy)
+                           : trace_beam_list(s_c, s_pl + pix * kPixCap, cnt, p.sc.recs, org, dir, p.info->t_min, fx, fy);
+        }
+    } else {
+        D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
+        D3 dir = primary_dir(cam, ps);
+        h = trace(p.sc_bin, p.sc.recs, p.sc.n_tris, org, dir, p.info->t_min);
+    }
     p.hit[pidx * spp + s] = h.tri;
 }
 
@@ -523,9 +724,17 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     RenderStatics& st = statics(c);
     std::vector<ViewCall> calls(n_views);
     int maxW = 0, maxH = 0;
+    const int P = kThreads / a.spp;
+    int TW = 1;
+    while (TW * TW * 4 <= P) TW *= 2;  // near-square power-of-two width
+    int TH = (P + TW - 1) / TW;
+    while (TW * TH > P) --TH;
+    int tile_total = 0;
     for (int i = 0; i < n_views; ++i) {
         calls[i].slot = view_slots[i];
-        calls[i].pad = 0;
+        const DevCamera& vcam = c->views[view_slots[i]].cam;
+        calls[i].tile_base = tile_total;
+        tile_total += ((vcam.W + TW - 1) / TW) * ((vcam.H + TH - 1) / TH);
         calls[i].scale = loss_scales ? loss_scales[i] : 0.0;
         calls[i].h_view = hash_combine(a.seed, uint64_t(c->views[view_slots[i]].cam.gid) + 0x9e01);
         maxW = std::max(maxW, c->views[view_slots[i]].cam.W);
@@ -556,12 +765,9 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     p.spp = a.spp;
     p.k = a.k;
     p.inv_k = (a.k > 0 && (a.k & (a.k - 1)) == 0) ? 1.0 / a.k : 0.0;
-    int P = kThreads / a.spp;
-    int TW = 1;
-    while (TW * TW * 4 <= P) TW *= 2;  // near-square power-of-two width
     p.TW = TW;
-    p.TH = (P + TW - 1) / TW;
-    while (TW * p.TH > P) --p.TH;
+    p.TH = TH;
+    p.sc_bin = c->nodes.p;
     p.seed = a.seed;
     p.gamma = a.gamma;
     p.use_mask = a.use_mask;
@@ -587,7 +793,33 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
 
     int tiles = ((maxW + p.TW - 1) / p.TW) * ((maxH + p.TH - 1) / p.TH);
     dim3 grid(tiles, n_views);
-    if (trace) { ++c->launches; k_trace<<<grid, kThreads, 0, c->stream>>>(p); }
+    p.use_beam = trace && c->T > 0 && !std::getenv("CDR_NO_BEAM");
+    if (c->beam_used_host) c->beam_used_last = *c->beam_used_host;  // previous call has completed
+    if (p.use_beam) {
+        // candidate pool sized from the previous call's use (overflowing tiles
+        // fall back to per-ray traversal, so the size only affects speed)
+        size_t want = std::max<size_t>(size_t(tile_total) * 8, size_t(c->beam_used_last) * 3 / 2 + 1024);
+        if (c->beam_pool.n < want) c->beam_pool.ensure(want);
+        c->beam_hdr.ensure(std::max(1, tile_total));
+        c->beam_used.ensure(1);
+        CDR_CUDA_CHECK(cudaMemsetAsync(c->beam_used.p, 0, sizeof(int), c->stream));
+        p.tile_hdr = c->beam_hdr.p;
+        p.pool = c->beam_pool.p;
+        p.pool_cap = int(std::min<size_t>(c->beam_pool.n, 0x7fffffff));
+        p.pool_used = c->beam_used.p;
+        const size_t npix = size_t(tile_total) * P;
+        c->beam_pix_list.ensure(std::max<size_t>(16, npix * kPixCap));
+        c->beam_pix_cnt.ensure(std::max<size_t>(1, npix));
+        p.pix_list = c->beam_pix_list.p;
+        p.pix_cnt = c->beam_pix_cnt.p;
+        dim3 lgrid((tiles + kListWarps - 1) / kListWarps, n_views);
+        { ++c->launches; k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(p); }
+        if (!c->beam_used_host) CDR_CUDA_CHECK(cudaHostAlloc(&c->beam_used_host, sizeof(int), cudaHostAllocDefault));
+        CDR_CUDA_CHECK(cudaMemcpyAsync(c->beam_used_host, c->beam_used.p, sizeof(int), cudaMemcpyDeviceToHost,
+                                       c->stream));
+    }
+    if (trace && p.use_beam) { ++c->launches; k_trace<true><<<grid, kThreads, 0, c->stream>>>(p); }
+    if (trace && !p.use_beam) { ++c->launches; k_trace<false><<<grid, kThreads, 0, c->stream>>>(p); }
     if (after_trace) CDR_CUDA_CHECK(cudaEventRecord(after_trace, c->stream));
     if (trace && loss && interior)
         { ++c->launches; k_render<true, true, true><<<grid, kThreads, 0, c->stream>>>(p); }
