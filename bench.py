@@ -356,7 +356,8 @@ def main():
                 "gpu_launches": int(sum(x["kernel_launches"] for x in stats)),
                 "clocks": clk, "stages_ms": stages,
                 "counters": {k: s0[k] for k in ("pixels", "samples", "hit_samples", "adjoint_samples",
-                                                "boundary_samples", "boundary_active", "segments")}}
+                                                "boundary_samples", "boundary_active", "segments",
+                                                "beam_fallback_tiles")}}
         print(json.dumps(line), flush=True)
     r.close()
     if dist is not None:

@@ -119,7 +119,8 @@ typedef struct cdr_stats {
     double ms_finalize;        /* normal chain + position gather + Laplacian */
     double ms_total;
     int64_t kernel_launches;   /* kernels this library launched in the call */
-    double ms_trace;           /* primary-visibility kernel (part of ms_render) */
+    double ms_trace;           /* primary-visibility kernels (part of ms_render) */
+    int64_t beam_fallback_tiles; /* pixel tiles traced per ray (candidate-list overflow) */
 } cdr_stats;
 
 int cdr_abi_version(void);

@@ -71,7 +71,7 @@ class cdr_stats(C.Structure):
                 ("degenerate_skipped", C.c_int32), ("nonfinite", C.c_int32),
                 ("ms_prepare", C.c_double), ("ms_render", C.c_double), ("ms_silhouette", C.c_double),
                 ("ms_boundary", C.c_double), ("ms_finalize", C.c_double), ("ms_total", C.c_double),
-                ("kernel_launches", C.c_int64), ("ms_trace", C.c_double)]
+                ("kernel_launches", C.c_int64), ("ms_trace", C.c_double), ("beam_fallback_tiles", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -807,6 +807,7 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
         stats->hit_samples = int64_t(k.hit_samples);
         stats->adjoint_samples = int64_t(k.adjoint_samples);
         stats->boundary_active = int64_t(k.boundary_active);
+        stats->beam_fallback_tiles = int64_t(k.beam_fallback_tiles);
         if (st->boundary_term) {
             std::vector<int32_t> cnt(n), deg(n);
             CDR_CUDA_CHECK(cudaMemcpy(cnt.data(), c->sil_count.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));

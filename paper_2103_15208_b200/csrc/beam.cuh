@@ -25,9 +25,9 @@
 
 namespace cdr {
 
-constexpr int kBeamCap = 64;    // candidates per tile; more -> per-ray traversal
+constexpr int kBeamCap = 128;   // candidates per tile; more -> per-ray traversal
 constexpr int kPixCap = 16;     // candidates per pixel list; more -> scan the tile list
-constexpr int kFrontCap = 128;  // builder frontier per tile; more -> per-ray traversal
+constexpr int kFrontCap = 256;  // builder frontier per tile; more -> per-ray traversal
 
 // Candidate record (48 B): three edge functions E_i = A_i x + B_i y + C_i
 // (pixel coordinates relative to the tile origin, margin folded into C_i;

@@ -58,6 +58,7 @@ struct Counters {  // device-side work counters (cdr_stats)
     unsigned long long hit_samples;
     unsigned long long adjoint_samples;
     unsigned long long boundary_active;
+    unsigned long long beam_fallback_tiles;  // tiles traced per ray (list overflow)
     double loss_sum[1];
 };
 

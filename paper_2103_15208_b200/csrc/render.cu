@@ -148,7 +148,10 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
         cur ^= 1;
     }
     if (over) {
-        if (lane == 0) *hdr = TileHdr{0, -1};
+        if (lane == 0) {
+            *hdr = TileHdr{0, -1};
+            atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+        }
         return;
     }
     // lower bound on t (unit rays): distance from the origin to the triangle's box
@@ -211,7 +214,10 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
     if (lane == 0 && nl) off = atomicAdd(p.pool_used, nl);
     off = __shfl_sync(0xffffffffu, off, 0);
     if (off + nl > p.pool_cap) {
-        if (lane == 0) *hdr = TileHdr{0, -1};
+        if (lane == 0) {
+            *hdr = TileHdr{0, -1};
+            atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+        }
         return;
     }
     const float4* src = reinterpret_cast<const float4*>(&s_cand[w][0]);
@@ -798,7 +804,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     if (p.use_beam) {
         // candidate pool sized from the previous call's use (overflowing tiles
         // fall back to per-ray traversal, so the size only affects speed)
-        size_t want = std::max<size_t>(size_t(tile_total) * 8, size_t(c->beam_used_last) * 3 / 2 + 1024);
+        size_t want = std::max<size_t>(size_t(tile_total) * 24, size_t(c->beam_used_last) * 3 / 2 + 1024);
         if (c->beam_pool.n < want) c->beam_pool.ensure(want);
         c->beam_hdr.ensure(std::max(1, tile_total));
         c->beam_used.ensure(1);
