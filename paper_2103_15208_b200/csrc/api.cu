@@ -746,7 +746,8 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
         launch_cdf(c, n);
     }
     CDR_CUDA_CHECK(cudaEventRecord(ev[3], s));
-    if (st->boundary_term) launch_boundary(c, n, max_samples, st->seed, CDR_PROBE_RADIANCE, lay->positions);
+    if (st->boundary_term)  // the render above built candidate lists for exactly these views
+        launch_boundary(c, n, max_samples, st->seed, CDR_PROBE_RADIANCE, lay->positions, /*use_beam=*/true);
     CDR_CUDA_CHECK(cudaEventRecord(ev[4], s));
     launch_texel_flush(c, lay->diffuse, lay->specular, lay->roughness);
     launch_finalize_positions(c, lay->positions);

@@ -138,4 +138,44 @@ __device__ __forceinline__ Hit trace_beam_list(const BeamCand* __restrict__ cand
     return best;
 }
 
+// Per-call view of the beam lists for consumers other than k_trace (the
+// boundary probes): tile geometry of the render call and its per-view bases.
+struct BeamView {
+    const TileHdr* hdr;
+    const BeamCand* pool;
+    const unsigned char* pix_list;
+    const unsigned char* pix_cnt;
+    const int* tile_base;  // per view index of the call
+    int TW, TH, P;
+    int valid;
+};
+
+// Nearest hit for a ray through continuous pixel point x of view vi, using
+// the candidate list of the pixel containing x; per-ray traversal when x is
+// outside the image, the tile overflowed, or no lists exist for this call.
+__device__ __forceinline__ Hit trace_point(const BeamView& bv, int vi, const DevCamera& cam, const BNode* nodes,
+                                           const TriRec* recs, int n_tris, D2 x, D3 d, double t_min) {
+    const D3 o{cam.o[0], cam.o[1], cam.o[2]};
+    if (bv.valid) {
+        const double fx = floor(x.x), fy = floor(x.y);
+        if (fx >= 0 && fy >= 0 && fx < cam.W && fy < cam.H) {
+            const int px = int(fx), py = int(fy);
+            const int tiles_x = (cam.W + bv.TW - 1) / bv.TW;
+            const int tx = px / bv.TW, ty = py / bv.TH;
+            const size_t tile = size_t(bv.tile_base[vi]) + ty * tiles_x + tx;
+            const TileHdr h = bv.hdr[tile];
+            if (h.cnt >= 0) {
+                const int q = (py - ty * bv.TH) * bv.TW + (px - tx * bv.TW);
+                const int cnt = bv.pix_cnt[tile * bv.P + q];
+                const float lx = float(x.x - tx * bv.TW), ly = float(x.y - ty * bv.TH);
+                if (cnt == 0) return Hit{-1, 1e300, 0.0, 0.0};
+                if (cnt == 255) return trace_beam(bv.pool + h.off, h.cnt, recs, o, d, t_min, lx, ly);
+                return trace_beam_list(bv.pool + h.off, bv.pix_list + (tile * bv.P + q) * kPixCap, cnt, recs, o, d,
+                                       t_min, lx, ly);
+            }
+        }
+    }
+    return trace(nodes, recs, n_tris, o, d, t_min);
+}
+
 }  // namespace cdr

@@ -193,6 +193,7 @@ __global__ void k_cdf(const cdr_segment* __restrict__ segs, const int32_t* __res
 
 struct BParams {
     ShadeScene sc;
+    BeamView beam;  // candidate lists of the render call (beam.cuh)
     const SceneInfo* info;
     const DevCamera* cams;
     const SilCall* calls;
@@ -373,8 +374,13 @@ __global__ void __launch_bounds__(kBlock, CDR_BOUNDARY_MIN_BLOCKS) k_boundary(BP
         const double t_min = p.info->t_min;
         D3 delta;
         if (p.probe == CDR_PROBE_RADIANCE) {
-            D3 lo3 = radiance_at(p.sc, cam, xm, t_min, nullptr);
-            D3 hi3 = radiance_at(p.sc, cam, xp, t_min, nullptr);
+            // radiance_at (render.cpp:24-33) through the pixels' candidate lists
+            const D3 dm = primary_dir(cam, xm), dp = primary_dir(cam, xp);
+            const Hit hm = trace_point(p.beam, vi, cam, p.sc.nodes, p.sc.recs, p.sc.n_tris, xm, dm, t_min);
+            const Hit hp = trace_point(p.beam, vi, cam, p.sc.nodes, p.sc.recs, p.sc.n_tris, xp, dp, t_min);
+            const D3 bg{p.sc.bg[0], p.sc.bg[1], p.sc.bg[2]};
+            D3 lo3 = hm.tri >= 0 ? shade_hit(p.sc, hm, dm) : bg;
+            D3 hi3 = hp.tri >= 0 ? shade_hit(p.sc, hp, dp) : bg;
             delta = lo3 - hi3;
         } else {
             D3 org{cam.o[0], cam.o[1], cam.o[2]};
@@ -483,7 +489,7 @@ void launch_cdf(cdr_ctx* c, int n_views) {
 }
 
 void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int probe,
-                     int64_t lay_pos) {
+                     int64_t lay_pos, bool use_beam) {
     if (n_views <= 0 || samples <= 0) return;
     BStatics& st = bstatics(c);
     size_t nslots = c->views.size();
@@ -532,6 +538,8 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     p.key = c->b_key.p;
     p.slot = c->b_slot.p;
     p.order = c->b_order.p;
+    p.beam = c->beam_view;
+    p.beam.valid = c->beam_view.valid && use_beam;
     p.s_param = c->b_s.p;
     p.sorted_si = c->b_sorted_si.p;
     p.sorted_s = c->b_sorted_s.p;

@@ -58,8 +58,10 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
 void set_view_calls(cdr_ctx* c, const int* view_slots, const int* samples, int n_views);
 void launch_silhouettes(cdr_ctx* c, int n_views);
 void launch_cdf(cdr_ctx* c, int n_views);
+// use_beam: probes may use the candidate lists the preceding render call built
+// for the same view list (cdr_loss_grad); otherwise per-ray traversal
 void launch_boundary(cdr_ctx* c, int n_views, int max_samples, uint64_t seed, int probe,
-                     int64_t lay_pos);
+                     int64_t lay_pos, bool use_beam = false);
 
 // finalize.cu — position gradient assembly: per-corner interior sums, the
 // one-ring normal chain (diff_render.cpp:174-184) restated as q_v x d_{f,w},

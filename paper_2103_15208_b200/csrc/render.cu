@@ -800,6 +800,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     int tiles = ((maxW + p.TW - 1) / p.TW) * ((maxH + p.TH - 1) / p.TH);
     dim3 grid(tiles, n_views);
     p.use_beam = trace && c->T > 0 && !std::getenv("CDR_NO_BEAM");
+    c->beam_view.valid = 0;
     if (c->beam_used_host) c->beam_used_last = *c->beam_used_host;  // previous call has completed
     if (p.use_beam) {
         // candidate pool sized from the previous call's use (overflowing tiles
@@ -820,6 +821,13 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         p.pix_cnt = c->beam_pix_cnt.p;
         dim3 lgrid((tiles + kListWarps - 1) / kListWarps, n_views);
         { ++c->launches; k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(p); }
+        // publish the lists for the boundary probes of the same call
+        std::vector<int> bases(n_views);
+        for (int i = 0; i < n_views; ++i) bases[i] = calls[i].tile_base;
+        c->beam_tile_base.ensure(n_views);
+        CDR_CUDA_CHECK(cudaMemcpyAsync(c->beam_tile_base.p, bases.data(), sizeof(int) * n_views,
+                                       cudaMemcpyHostToDevice, c->stream));
+        c->beam_view = BeamView{p.tile_hdr, p.pool, p.pix_list, p.pix_cnt, c->beam_tile_base.p, TW, TH, P, 1};
         if (!c->beam_used_host) CDR_CUDA_CHECK(cudaHostAlloc(&c->beam_used_host, sizeof(int), cudaHostAllocDefault));
         CDR_CUDA_CHECK(cudaMemcpyAsync(c->beam_used_host, c->beam_used.p, sizeof(int), cudaMemcpyDeviceToHost,
                                        c->stream));
