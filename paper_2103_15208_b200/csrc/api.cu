@@ -266,6 +266,7 @@ void cdr_destroy(cdr_ctx* c) {
     if (c->nccl_comm && nccl().ok) nccl().commDestroy(c->nccl_comm);
     cudaStreamSynchronize(c->stream);
     for (auto& e : c->ev) cudaEventDestroy(e);
+    for (auto& e : c->chunk_ev) cudaEventDestroy(e);
     // DBufs are released with the process/context; free the big ones explicitly
     c->pos.release(); c->uv.release(); c->normals.release(); c->accum.release(); c->fnormal.release();
     c->tris.release(); c->edges.release(); c->vf_start.release(); c->vf_list.release();
@@ -822,9 +823,7 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
         for (int i = 0; i < 6; ++i) CDR_CUDA_CHECK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
         stats->ms_prepare = ms[0];
         stats->ms_render = ms[1];
-        float mt;
-        CDR_CUDA_CHECK(cudaEventElapsedTime(&mt, ev[1], ev[7]));
-        stats->ms_trace = mt;
+        stats->ms_trace = render_trace_ms(c);
         stats->ms_silhouette = ms[2];
         stats->ms_boundary = ms[3];
         stats->ms_finalize = ms[4];

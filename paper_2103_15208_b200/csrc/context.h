@@ -146,6 +146,8 @@ struct cdr_ctx {
 
     // timing and launch accounting (cdr_stats::kernel_launches)
     std::vector<cudaEvent_t> ev;
+    std::vector<cudaEvent_t> chunk_ev;  // per view chunk of a timed render: start, after trace
+    int chunk_ev_used = 0;
     int64_t launches = 0;
 
     // multi-GPU

@@ -51,6 +51,8 @@ struct RenderArgs {
 void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a,
                    bool trace, bool loss, bool interior, const double* loss_scales,
                    cudaEvent_t after_trace = nullptr);
+// Σ over the view chunks of the last timed launch_render: lists + trace time (ms)
+float render_trace_ms(cdr_ctx* c);
 
 // boundary.cu — extract_silhouettes (silhouette.cpp:55-106), the CDF of
 // boundary_pass (diff_render.cpp:213-228) and its edge samples (:230-278).

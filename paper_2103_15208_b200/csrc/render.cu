@@ -300,141 +300,10 @@ __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params
     p.hit[pidx * spp + s] = h.tri;
 }
 
-// kShade: radiance + pixel mean/mask; kLoss: loss + adjoint; kInterior: scatter.
-// The hit triangle comes from the hit cache and is re-intersected with
-// ray_triangle, exactly as interior_pass replays it (diff_render.cpp:84-93).
-#ifndef CDR_RENDER_MIN_BLOCKS
-#define CDR_RENDER_MIN_BLOCKS 3
-#endif
-template <bool kShade, bool kLoss, bool kInterior>
-__global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
-    __shared__ double s_rad[kThreads][3];
-    __shared__ double s_adj[kThreads][3];  // per pixel (index = pixel in tile)
-    __shared__ unsigned char s_hit[kThreads];
-
-    const ViewCall vc = p.calls[blockIdx.y];
-    const DevCamera& cam = p.cams[vc.slot];
-    const int W = cam.W, H = cam.H;
-    const int tiles_x = (W + p.TW - 1) / p.TW;
-    const int tiles_y = (H + p.TH - 1) / p.TH;
-    if (int(blockIdx.x) >= tiles_x * tiles_y) return;  // uniform per CTA
-    const int tid = threadIdx.x;
-    const int spp = p.spp;
-    const int P = kThreads / spp;
-    const int pix = tid / spp, s = tid - (tid / spp) * spp;
-    const int x = (blockIdx.x % tiles_x) * p.TW + pix % p.TW;
-    const int y = (blockIdx.x / tiles_x) * p.TH + pix / p.TW;
-    const bool valid = pix < P && x < W && y < H;
-    const size_t pbase = p.pix_off[vc.slot];
-    const size_t pidx = pbase + size_t(y) * W + x;  // arena pixel index
-    const D3 org{cam.o[0], cam.o[1], cam.o[2]};
-
-    // ---------------- phase 1: cached triangle -> (t, b1, b2), radiance
-    int tri = -1;
-    double t = 0, b1 = 0, b2 = 0;
-    D3 dir{0, 0, 1};
-    if (valid) tri = p.hit[pidx * spp + s];
-    if (tri >= 0) {  // misses need no ray: their radiance is the background
-        D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
-        dir = primary_dir(cam, ps);
-        {
-            int a = p.sc.tris[3 * tri], b = p.sc.tris[3 * tri + 1], c = p.sc.tris[3 * tri + 2];
-            if (!ray_triangle(org, dir, ld3(p.sc.pos + 3 * a), ld3(p.sc.pos + 3 * b), ld3(p.sc.pos + 3 * c), t, b1, b2))
-                tri = -1;
-        }
-    }
-    if (kShade) {
-        D3 rad{p.sc.bg[0], p.sc.bg[1], p.sc.bg[2]};
-        if (tri >= 0) rad = shade_hit(p.sc, Hit{tri, t, b1, b2}, dir);
-        s_rad[tid][0] = rad.x;
-        s_rad[tid][1] = rad.y;
-        s_rad[tid][2] = rad.z;
-        s_hit[tid] = tri >= 0;
-    }
-    __syncthreads();
-
-    // ---------------- phase 2: pixel mean / mask / loss / adjoint
-    // One thread per (pixel, channel): channels are independent, each sums its
-    // pixel's samples in sample order (render.cpp:48-57), so the mean is the
-    // reference's bit for bit; the tone map of the target is precomputed.
-    double loss_part = 0;
-    for (int item = tid; item < 3 * P; item += kThreads) {
-        const int q = item % P, c = item / P;
-        const int px = (blockIdx.x % tiles_x) * p.TW + q % p.TW;
-        const int py = (blockIdx.x / tiles_x) * p.TH + q / p.TW;
-        if (px < W && py < H) {
-            const size_t qi = pbase + size_t(py) * W + px;
-            double mean = 0;
-            if (kShade) {
-                double sum = 0;
-                int hits = 0;
-                for (int j = 0; j < spp; ++j) {
-                    sum = sum + s_rad[q * spp + j][c];
-                    hits += s_hit[q * spp + j];
-                }
-                mean = sum / double(spp);
-                p.img[3 * qi + c] = mean;
-                if (c == 0) p.mask[qi] = double(hits) / double(spp);
-            }
-            if (kLoss) {
-                double m = (p.use_mask && p.has_mask[vc.slot]) ? p.target_mask[qi] : 1.0;
-                double a = 0;
-                if (m != 0) {
-                    // losses.cpp:37-44; Φ'(r) = Φ(r) / (γ r) for r in (0, 1)
-                    // Φ(0) = pow(0, 1/γ) = +0 exactly: skip pow on background
-                    double tr = mean <= 0.0 ? 0.0 : tone_map(mean, p.gamma);
-                    double d = tr - p.target_tone[3 * qi + c];
-                    loss_part += m * fabs(d);
-                    double sg = double((d > 0) - (d < 0));
-                    double der = (mean <= 0.0 || mean >= 1.0) ? 0.0 : tr / (p.gamma * mean);
-                    a = vc.scale * m * sg * der;
-                }
-                p.adj[3 * qi + c] = a;
-                s_adj[q][c] = a;
-            }
-        }
-    }
-    if (kLoss) {
-        // CTA reduction of the loss partial (one fp64 atomic per CTA)
-        for (int o = 16; o > 0; o >>= 1) loss_part += __shfl_xor_sync(0xffffffffu, loss_part, o);
-        __shared__ double s_red[kThreads / 32];
-        if ((tid & 31) == 0) s_red[tid >> 5] = loss_part;
-        __syncthreads();
-        if (tid == 0) {
-            double tot = 0;
-            for (int w = 0; w < kThreads / 32; ++w) tot += s_red[w];
-            if (tot != 0) atomicAdd(&p.loss_acc[vc.slot], tot);
-        }
-    }
-    if (!kInterior) {
-        if (kShade) {
-            int nh = __syncthreads_count(valid && tri >= 0);
-            if (tid == 0 && nh) atomicAdd(&p.counters->hit_samples, (unsigned long long)nh);
-        }
-        return;
-    }
-
-    // ---------------- phase 3: interior adjoint scatter
-    D3 a{0, 0, 0};
-    if (valid && tri >= 0) {
-        if (kLoss) {
-            a = D3{s_adj[pix][0], s_adj[pix][1], s_adj[pix][2]};
-        } else {
-            a = ld3(p.adj + 3 * pidx);
-        }
-    }
-    bool act = valid && tri >= 0 && !(a.x == 0 && a.y == 0 && a.z == 0);
-    {
-        int nh = __syncthreads_count(valid && tri >= 0);
-        int na = __syncthreads_count(act);
-        if (tid == 0) {
-            if (nh) atomicAdd(&p.counters->hit_samples, (unsigned long long)nh);
-            if (na) atomicAdd(&p.counters->adjoint_samples, (unsigned long long)na);
-        }
-        if (na == 0) return;  // background / zero-adjoint tile (uniform per CTA)
-    }
-    if (!__any_sync(0xffffffffu, act)) return;  // no barrier follows: warp-level exit is safe
-    a = a / double(spp);  // diff_render.cpp:82
+// Phase 3 of k_render: the interior adjoint of one sample (diff_render.cpp:78-184).
+__device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x, int y, int spp, int tri, double t,
+                                              double b1, double b2, D3 dir, D3 a, bool act) {
+    a = (spp & (spp - 1)) == 0 ? a * (1.0 / spp) : a / double(spp);  // diff_render.cpp:82 (x/2^n exact as x*2^-n)
 
     // Compute everything the scatter needs first, so the large temporaries
     // (texture sample, BRDF partials, vertex data) are dead before the
@@ -535,12 +404,21 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
         }
     }
 
-    // texel scatter through the bilinear weights (diff_render.cpp:110-128)
+    // Samples of a warp sharing a texel quad (or a triangle) are summed with
+    // a log-depth shuffle tree first (reduce_peers), then the group leader
+    // issues the REDs. Measured alternatives, both slower at cfg2 (DESIGN.md
+    // §5): staging the leaders' sums in shared memory so one warp-wide RED
+    // covers several records (+2%: the L2 is not the limiter), and a
+    // shared-memory transpose in which lane (group, component) sums a column
+    // (+10%: fewer instructions, but a serial load-add chain per lane; this
+    // kernel is latency-bound at 6 warps per scheduler, not issue-bound).
+    const int lane = tid & 31;
 #ifndef CDR_EXP_NO_TEXEL
     {
-        const int key = act ? tex0 : -1 - (tid & 31);
+        // texel scatter through the bilinear weights (diff_render.cpp:110-128)
+        const int key = act ? tex0 : -1 - lane;
         const unsigned peers = __match_any_sync(0xffffffffu, key);
-        const bool leader = act && (__ffs(peers) - 1) == (tid & 31);
+        const bool leader = act && (__ffs(peers) - 1) == lane;
         const int tw = p.sc.tw, th = p.sc.th;
         const int x0 = tex0 % tw, y0 = tex0 / tw;
         const int x1 = x0 + 1 == tw ? 0 : x0 + 1, y1 = y0 + 1 == th ? 0 : y0 + 1;
@@ -567,7 +445,7 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     if (p.lay_l >= 0) {  // light intensity (diff_render.cpp:129-131)
         for (int o = 16; o > 0; o >>= 1)
             for (int c = 0; c < 3; ++c) lv[c] += __shfl_xor_sync(0xffffffffu, lv[c], o);
-        if ((tid & 31) == 0)
+        if (lane == 0)
             for (int c = 0; c < 3; ++c)
                 if (lv[c] != 0) atomicAdd(p.grad + p.lay_l + c, lv[c]);
     }
@@ -575,9 +453,9 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     // (diff_render.cpp:170-184; the chain itself is applied in finalize.cu)
 #ifndef CDR_EXP_NO_POS
     {
-        const int key = pact ? tri : -1 - (tid & 31);
+        const int key = pact ? tri : -1 - lane;
         const unsigned peers = __match_any_sync(0xffffffffu, key);
-        const bool leader = pact && (__ffs(peers) - 1) == (tid & 31);
+        const bool leader = pact && (__ffs(peers) - 1) == lane;
 #pragma unroll 1
         for (int j = 0; j < 3; ++j) {
             const double bj = j == 0 ? b0 : (j == 1 ? b1 : b2);
@@ -593,6 +471,165 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
         }
     }
 #endif
+}
+
+// kShade: radiance + pixel mean/mask; kLoss: loss + adjoint; kInterior: scatter.
+// The hit triangle comes from the hit cache and is re-intersected with
+// ray_triangle, exactly as interior_pass replays it (diff_render.cpp:84-93).
+#ifndef CDR_RENDER_MIN_BLOCKS
+#define CDR_RENDER_MIN_BLOCKS 3
+#endif
+template <bool kShade, bool kLoss, bool kInterior>
+__global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
+    __shared__ double s_rad[kThreads][3];
+    __shared__ double s_adj[kThreads][3];  // per pixel (index = pixel in tile)
+    __shared__ unsigned char s_hit[kThreads];
+
+    const ViewCall vc = p.calls[blockIdx.y];
+    const DevCamera& cam = p.cams[vc.slot];
+    const int W = cam.W, H = cam.H;
+    const int tiles_x = (W + p.TW - 1) / p.TW;
+    const int tiles_y = (H + p.TH - 1) / p.TH;
+    if (int(blockIdx.x) >= tiles_x * tiles_y) return;  // uniform per CTA
+    const int tid = threadIdx.x;
+    const int spp = p.spp;
+    const int P = kThreads / spp;
+    const int pix = tid / spp, s = tid - (tid / spp) * spp;
+    const int x = (blockIdx.x % tiles_x) * p.TW + pix % p.TW;
+    const int y = (blockIdx.x / tiles_x) * p.TH + pix / p.TW;
+    const bool valid = pix < P && x < W && y < H;
+    const size_t pbase = p.pix_off[vc.slot];
+    const size_t pidx = pbase + size_t(y) * W + x;  // arena pixel index
+    const D3 org{cam.o[0], cam.o[1], cam.o[2]};
+
+    // ---------------- phase 1: cached triangle -> (t, b1, b2), radiance
+    int tri = -1;
+    double t = 0, b1 = 0, b2 = 0;
+    D3 dir{0, 0, 1};
+    if (valid) tri = p.hit[pidx * spp + s];
+    if (tri >= 0) {  // misses need no ray: their radiance is the background
+        D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
+        dir = primary_dir(cam, ps);
+        {
+            int a = p.sc.tris[3 * tri], b = p.sc.tris[3 * tri + 1], c = p.sc.tris[3 * tri + 2];
+            if (!ray_triangle(org, dir, ld3(p.sc.pos + 3 * a), ld3(p.sc.pos + 3 * b), ld3(p.sc.pos + 3 * c), t, b1, b2))
+                tri = -1;
+        }
+    }
+    if (kShade) {
+        D3 rad{p.sc.bg[0], p.sc.bg[1], p.sc.bg[2]};
+        if (tri >= 0) rad = shade_hit(p.sc, Hit{tri, t, b1, b2}, dir);
+        s_rad[tid][0] = rad.x;
+        s_rad[tid][1] = rad.y;
+        s_rad[tid][2] = rad.z;
+        s_hit[tid] = tri >= 0;
+    }
+    // When spp divides 32 a warp holds whole pixels: phase 2 is warp-local and
+    // no CTA barrier separates the phases (warps overlap one another's pixel
+    // reductions with their scatter); the per-warp tallies meet once, at the
+    // end. Otherwise pixels straddle warps and phase 2 is CTA-wide.
+    const int lane = tid & 31, wib = tid >> 5;
+    const bool warp_local = (32 % spp) == 0;
+    __shared__ double s_wloss[kThreads / 32];
+    __shared__ int s_wcnt[kThreads / 32][2];
+    if (warp_local) __syncwarp();
+    else __syncthreads();
+
+    // ---------------- phase 2: pixel mean / mask / loss / adjoint
+    // One thread per (pixel, channel): channels are independent, each sums its
+    // pixel's samples in sample order (render.cpp:48-57), so the mean is the
+    // reference's bit for bit; the tone map of the target is precomputed.
+    double loss_part = 0;
+    {
+        const int ppw = warp_local ? 32 / spp : P;  // pixels per phase-2 group
+        const int n_items = 3 * ppw;
+        const int first = warp_local ? lane : tid, stride = warp_local ? 32 : kThreads;
+        for (int item = first; item < n_items; item += stride) {
+            const int q = (warp_local ? wib * ppw : 0) + item % ppw, c = item / ppw;
+            const int px = (blockIdx.x % tiles_x) * p.TW + q % p.TW;
+            const int py = (blockIdx.x / tiles_x) * p.TH + q / p.TW;
+            if (px < W && py < H) {
+                const size_t qi = pbase + size_t(py) * W + px;
+                double mean = 0;
+                if (kShade) {
+                    double sum = 0;
+                    int hits = 0;
+                    for (int j = 0; j < spp; ++j) {
+                        sum = sum + s_rad[q * spp + j][c];
+                        hits += s_hit[q * spp + j];
+                    }
+                    mean = sum / double(spp);
+                    p.img[3 * qi + c] = mean;
+                    if (c == 0) p.mask[qi] = double(hits) / double(spp);
+                }
+                if (kLoss) {
+                    double m = (p.use_mask && p.has_mask[vc.slot]) ? p.target_mask[qi] : 1.0;
+                    double a = 0;
+                    if (m != 0) {
+                        // losses.cpp:37-44; Φ'(r) = Φ(r) / (γ r) for r in (0, 1)
+                        // Φ(0) = pow(0, 1/γ) = +0 exactly: skip pow on background
+                        double tr = mean <= 0.0 ? 0.0 : tone_map(mean, p.gamma);
+                        double d = tr - p.target_tone[3 * qi + c];
+                        loss_part += m * fabs(d);
+                        double sg = double((d > 0) - (d < 0));
+                        double der = (mean <= 0.0 || mean >= 1.0) ? 0.0 : tr / (p.gamma * mean);
+                        a = vc.scale * m * sg * der;
+                    }
+                    p.adj[3 * qi + c] = a;
+                    s_adj[q][c] = a;
+                }
+            }
+        }
+    }
+    // per-warp tallies: loss partial, hit samples, adjoint samples
+    D3 a{0, 0, 0};
+    bool act;
+    {
+        if (kLoss)
+            for (int o = 16; o > 0; o >>= 1) loss_part += __shfl_xor_sync(0xffffffffu, loss_part, o);
+        if (warp_local) __syncwarp();
+        else __syncthreads();  // s_adj complete
+        if (kInterior && valid && tri >= 0) {
+            if (kLoss) {
+                a = D3{s_adj[pix][0], s_adj[pix][1], s_adj[pix][2]};
+            } else {
+                a = ld3(p.adj + 3 * pidx);
+            }
+        }
+        act = kInterior && valid && tri >= 0 && !(a.x == 0 && a.y == 0 && a.z == 0);
+        const int nh = __popc(__ballot_sync(0xffffffffu, valid && tri >= 0));
+        const int na = __popc(__ballot_sync(0xffffffffu, act));
+        if (lane == 0) {
+            s_wloss[wib] = loss_part;
+            s_wcnt[wib][0] = nh;
+            s_wcnt[wib][1] = na;
+        }
+    }
+
+    // ---------------- phase 3: interior adjoint scatter
+    if (kInterior && __any_sync(0xffffffffu, act)) interior_scatter(p, tid, x, y, spp, tri, t, b1, b2, dir, a, act);
+
+    // ---------------- publish the CTA's tallies (warp 0 waits for the others)
+    __threadfence_block();
+    if (wib == 0) {
+        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+        if (lane == 0) {
+            double tot = 0;
+            unsigned long long nh = 0, na = 0;
+            for (int w = 0; w < kThreads / 32; ++w) {
+                tot += s_wloss[w];
+                nh += s_wcnt[w][0];
+                na += s_wcnt[w][1];
+            }
+            if (kLoss && tot != 0) atomicAdd(&p.loss_acc[vc.slot], tot);
+            if (kShade || kInterior) {
+                if (nh) atomicAdd(&p.counters->hit_samples, nh);
+                if (na) atomicAdd(&p.counters->adjoint_samples, na);
+            }
+        }
+    } else {
+        asm volatile("bar.arrive 1, %0;" ::"n"(kThreads) : "memory");
+    }
 }
 
 __global__ void k_tone(const double* __restrict__ in, size_t n, double gamma, double* __restrict__ out) {
@@ -724,6 +761,20 @@ static RenderStatics& statics(cdr_ctx* c) {
     return *reg.back().second;
 }
 
+static void launch_render_kernel(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
+    ++c->launches;
+    if (trace && loss && interior)
+        k_render<true, true, true><<<grid, kThreads, 0, c->stream>>>(p);
+    else if (trace && !loss && !interior)
+        k_render<true, false, false><<<grid, kThreads, 0, c->stream>>>(p);
+    else if (!trace && !loss && interior)
+        k_render<false, false, true><<<grid, kThreads, 0, c->stream>>>(p);
+    else if (trace && loss && !interior)
+        k_render<true, true, false><<<grid, kThreads, 0, c->stream>>>(p);
+    else
+        throw std::runtime_error("unsupported render mode");
+}
+
 void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a, bool trace,
                    bool loss, bool interior, const double* loss_scales, cudaEvent_t after_trace) {
     if (n_views <= 0) return;
@@ -798,7 +849,6 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     p.counters = c->counters.p;
 
     int tiles = ((maxW + p.TW - 1) / p.TW) * ((maxH + p.TH - 1) / p.TH);
-    dim3 grid(tiles, n_views);
     p.use_beam = trace && c->T > 0 && !std::getenv("CDR_NO_BEAM");
     c->beam_view.valid = 0;
     if (c->beam_used_host) c->beam_used_last = *c->beam_used_host;  // previous call has completed
@@ -819,8 +869,6 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         c->beam_pix_cnt.ensure(std::max<size_t>(1, npix));
         p.pix_list = c->beam_pix_list.p;
         p.pix_cnt = c->beam_pix_cnt.p;
-        dim3 lgrid((tiles + kListWarps - 1) / kListWarps, n_views);
-        { ++c->launches; k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(p); }
         // publish the lists for the boundary probes of the same call
         std::vector<int> bases(n_views);
         for (int i = 0; i < n_views; ++i) bases[i] = calls[i].tile_base;
@@ -828,24 +876,60 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         CDR_CUDA_CHECK(cudaMemcpyAsync(c->beam_tile_base.p, bases.data(), sizeof(int) * n_views,
                                        cudaMemcpyHostToDevice, c->stream));
         c->beam_view = BeamView{p.tile_hdr, p.pool, p.pix_list, p.pix_cnt, c->beam_tile_base.p, TW, TH, P, 1};
+    }
+    // Views can go through lists -> trace -> shade in chunks whose hit cache
+    // (4 B per sample) fits in L2, so the shading kernel's first load hits L2.
+    // Measured slower at cfg2 (the extra launch tails cost more than the L2
+    // hits save: DESIGN.md §5), so off unless CDR_CHUNK_MB is set.
+    size_t chunk_bytes = 0;
+    if (const char* e = std::getenv("CDR_CHUNK_MB")) chunk_bytes = size_t(std::max(0, std::atoi(e))) << 20;
+    const size_t per_view = size_t(maxW) * maxH * size_t(a.spp) * sizeof(int32_t);
+    int chunk = n_views;
+    if (trace && chunk_bytes > 0) chunk = int(std::max<size_t>(1, std::min<size_t>(n_views, chunk_bytes / per_view)));
+    const int n_chunks = (n_views + chunk - 1) / chunk;
+    const bool timed = after_trace != nullptr;
+    if (timed) {
+        while (c->chunk_ev.size() < size_t(2 * n_chunks + 1)) {
+            cudaEvent_t e;
+            CDR_CUDA_CHECK(cudaEventCreate(&e));
+            c->chunk_ev.push_back(e);
+        }
+        c->chunk_ev_used = n_chunks;
+    }
+    for (int k = 0; k < n_chunks; ++k) {
+        const int v0 = k * chunk, nv = std::min(chunk, n_views - v0);
+        Params pc = p;
+        pc.calls = st.calls.p + v0;
+        dim3 grid(tiles, nv);
+        if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k], c->stream));
+        if (p.use_beam) {
+            dim3 lgrid((tiles + kListWarps - 1) / kListWarps, nv);
+            ++c->launches;
+            k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(pc);
+        }
+        if (trace && p.use_beam) { ++c->launches; k_trace<true><<<grid, kThreads, 0, c->stream>>>(pc); }
+        if (trace && !p.use_beam) { ++c->launches; k_trace<false><<<grid, kThreads, 0, c->stream>>>(pc); }
+        if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k + 1], c->stream));
+        launch_render_kernel(pc, grid, c, trace, loss, interior);
+    }
+    if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * n_chunks], c->stream));
+    if (p.use_beam) {
         if (!c->beam_used_host) CDR_CUDA_CHECK(cudaHostAlloc(&c->beam_used_host, sizeof(int), cudaHostAllocDefault));
         CDR_CUDA_CHECK(cudaMemcpyAsync(c->beam_used_host, c->beam_used.p, sizeof(int), cudaMemcpyDeviceToHost,
                                        c->stream));
     }
-    if (trace && p.use_beam) { ++c->launches; k_trace<true><<<grid, kThreads, 0, c->stream>>>(p); }
-    if (trace && !p.use_beam) { ++c->launches; k_trace<false><<<grid, kThreads, 0, c->stream>>>(p); }
     if (after_trace) CDR_CUDA_CHECK(cudaEventRecord(after_trace, c->stream));
-    if (trace && loss && interior)
-        { ++c->launches; k_render<true, true, true><<<grid, kThreads, 0, c->stream>>>(p); }
-    else if (trace && !loss && !interior)
-        { ++c->launches; k_render<true, false, false><<<grid, kThreads, 0, c->stream>>>(p); }
-    else if (!trace && !loss && interior)
-        { ++c->launches; k_render<false, false, true><<<grid, kThreads, 0, c->stream>>>(p); }
-    else if (trace && loss && !interior)
-        { ++c->launches; k_render<true, true, false><<<grid, kThreads, 0, c->stream>>>(p); }
-    else
-        throw std::runtime_error("unsupported render mode");
     CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+float render_trace_ms(cdr_ctx* c) {
+    float tot = 0;
+    for (int k = 0; k < c->chunk_ev_used; ++k) {
+        float ms = 0;
+        CDR_CUDA_CHECK(cudaEventElapsedTime(&ms, c->chunk_ev[2 * k], c->chunk_ev[2 * k + 1]));
+        tot += ms;
+    }
+    return tot;
 }
 
 }  // namespace cdr
