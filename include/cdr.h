@@ -204,6 +204,30 @@ int cdr_loss_grad(cdr_ctx* ctx, const int32_t* views, int32_t n_views,
                   int32_t laplacian_mode, int32_t use_target_mask, const cdr_layout* layout,
                   double* loss_out, double* grad_inout, double* rendered_rgb,
                   double* rendered_mask, cdr_stats* stats);
+/* LossWeights (losses.hpp:14-23) of the four mesh / material regularisers.
+ * The reference defaults are normal 0.01, edge 1, spec 0.01, roug 0.001,
+ * sigma1 2, sigma2 0.1. */
+typedef struct cdr_reg_weights {
+    double normal, edge, spec, roug, sigma1, sigma2;
+} cdr_reg_weights;
+
+/* total_loss (losses.hpp:94-96, losses.cpp:244-297): cdr_loss_grad plus
+ * normal_consistency_loss, edge_length_loss, specular_correlation_loss and
+ * roughness_tv_loss (losses.cpp:80-238) on the context's mesh and maps. Under
+ * a communicator the mesh/material terms are computed once (rank 0) and summed
+ * with the view shards. breakdown_out[7] = total, rend, lap, normal, edge,
+ * spec, roug (LossBreakdown, losses.hpp:25-28). Other arguments as cdr_loss_grad. */
+int cdr_total_loss(cdr_ctx* ctx, const int32_t* views, int32_t n_views, const cdr_settings* settings,
+                   double lambda_rend, double lambda_lap, const cdr_reg_weights* reg, int32_t laplacian_mode,
+                   int32_t use_target_mask, const cdr_layout* layout, double* breakdown_out,
+                   double* grad_inout, double* rendered_rgb, double* rendered_mask, cdr_stats* stats);
+
+/* The four regularisers alone. values_out[4] = normal, edge, spec, roug.
+ * grad_inout (ParamLayout order) receives +=; with NULL the gradients are
+ * added to the device gradient (cdr_grad_device_ptr) instead. */
+int cdr_regularisers(cdr_ctx* ctx, const cdr_reg_weights* reg, const cdr_layout* layout,
+                     double* values_out, double* grad_inout);
+
 int cdr_get_grad(cdr_ctx* ctx, double* grad_out, int64_t n);
 int cdr_grad_device_ptr(cdr_ctx* ctx, void** ptr, int64_t* n);
 

@@ -12,9 +12,9 @@
 //   grad_image_loss      diff_render.hpp:65-67  -> cdr_loss_grad (one view)
 //   extract_silhouettes  silhouette.hpp:36      -> cdr_extract_silhouettes
 //   cotangent_laplacian  laplacian.hpp:14-15    -> cdr_laplacian_matrix
-//   total_loss           losses.hpp:94-96       -> cdr_loss_grad (+ the
-//                        out-of-scope regularisers through the reference's own
-//                        host functions, exactly as losses.cpp:272-292 adds them)
+//   total_loss           losses.hpp:94-96       -> cdr_total_loss (rendering,
+//                        Laplacian and the four mesh/material regularisers of
+//                        losses.cpp:272-292, all on the device)
 //
 // The reference objects that also define these symbols are linked with them
 // weakened (objcopy --weaken-symbol, integration/Makefile), so the unmodified
@@ -355,14 +355,21 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
         rgb.resize(3 * np);
         mask.resize(np);
     }
-    double loss[2] = {0, 0};
-    d.check(cdr_loss_grad(d.ctx, views.data(), n, &st, weights.rend, weights.lap,
-                          options.laplacian_mode == LaplacianMode::Uniform ? CDR_LAPLACIAN_UNIFORM
-                                                                            : CDR_LAPLACIAN_COTANGENT,
-                          options.use_target_masks ? 1 : 0, &lay, loss, res.grad.values.data(),
-                          want_rendered ? rgb.data() : nullptr, want_rendered ? mask.data() : nullptr, nullptr));
-    res.breakdown.rend = loss[0];
-    res.breakdown.lap = loss[1];
+    const cdr_reg_weights reg{weights.normal, weights.edge, weights.spec, weights.roug, weights.sigma1,
+                              weights.sigma2};
+    double bd[7] = {0, 0, 0, 0, 0, 0, 0};
+    d.check(cdr_total_loss(d.ctx, views.data(), n, &st, weights.rend, weights.lap, &reg,
+                           options.laplacian_mode == LaplacianMode::Uniform ? CDR_LAPLACIAN_UNIFORM
+                                                                             : CDR_LAPLACIAN_COTANGENT,
+                           options.use_target_masks ? 1 : 0, &lay, bd, res.grad.values.data(),
+                           want_rendered ? rgb.data() : nullptr, want_rendered ? mask.data() : nullptr, nullptr));
+    res.breakdown.total = bd[0];
+    res.breakdown.rend = bd[1];
+    res.breakdown.lap = bd[2];
+    res.breakdown.normal = bd[3];
+    res.breakdown.edge = bd[4];
+    res.breakdown.spec = bd[5];
+    res.breakdown.roug = bd[6];
     if (want_rendered) {
         size_t o = 0;
         for (const auto& c : scene.views) {
@@ -374,24 +381,6 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
             o += np;
         }
     }
-    // out-of-scope regularisers: the reference's own host code (losses.cpp:272-292)
-    MeshLossResult nrm = normal_consistency_loss(scene.mesh, weights.normal);
-    MeshLossResult edg = edge_length_loss(scene.mesh, weights.edge);
-    res.breakdown.normal = nrm.value;
-    res.breakdown.edge = edg.value;
-    for (int v = 0; v < scene.mesh.vertex_count(); ++v) res.grad.add_position(v, nrm.grad[v] + edg.grad[v]);
-    SpecularLossResult spec = specular_correlation_loss(scene.maps, weights);
-    res.breakdown.spec = spec.value;
-    for (size_t i = 0; i < spec.grad_specular.data.size(); ++i)
-        if (spec.grad_specular.data[i] != 0) res.grad.add(SegmentId::Specular, i, spec.grad_specular.data[i]);
-    for (size_t i = 0; i < spec.grad_diffuse.data.size(); ++i)
-        if (spec.grad_diffuse.data[i] != 0) res.grad.add(SegmentId::Diffuse, i, spec.grad_diffuse.data[i]);
-    RoughnessLossResult roug = roughness_tv_loss(scene.maps, weights.roug);
-    res.breakdown.roug = roug.value;
-    for (size_t i = 0; i < roug.grad.data.size(); ++i)
-        if (roug.grad.data[i] != 0) res.grad.add(SegmentId::Roughness, i, roug.grad.data[i]);
-    res.breakdown.total = res.breakdown.rend + res.breakdown.lap + res.breakdown.normal + res.breakdown.edge +
-                          res.breakdown.spec + res.breakdown.roug;
     return res;
 }
 

@@ -81,9 +81,11 @@ int main(int argc, char** argv) {
     mean /= std::max<size_t>(1, it_s.size());
     std::printf("{\"tris\": %d, \"views\": %d, \"image\": %d, \"spp\": %d, \"threads\": %d, "
                 "\"ms_per_iteration\": %.3f, \"ms_total_loss\": %.3f, \"loss0\": %.9g, \"rend0\": %.9g, "
-                "\"lap0\": %.9g, \"loss_last\": %.9g, \"iterations\": %zu}\n",
+                "\"lap0\": %.9g, \"normal0\": %.9g, \"edge0\": %.9g, \"spec0\": %.9g, \"roug0\": %.9g, "
+                "\"loss_last\": %.9g, \"iterations\": %zu}\n",
                 gt.mesh.triangle_count(), views, image, spp, threads, 1e3 * mean, 1e3 * t_loss,
-                tl.breakdown.total, tl.breakdown.rend, tl.breakdown.lap,
+                tl.breakdown.total, tl.breakdown.rend, tl.breakdown.lap, tl.breakdown.normal, tl.breakdown.edge,
+                tl.breakdown.spec, tl.breakdown.roug,
                 r.log.empty() ? 0.0 : r.log.back().loss.total, r.log.size());
     return 0;
 }

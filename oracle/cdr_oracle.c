@@ -1092,6 +1092,155 @@ int orc_loss_grad(const orc_ctx* c, const double* targets_rgb, const double* tar
     return 0;
 }
 
+/* ---- mesh / material regularisers (losses.cpp:80-238), SURVEY §8(f) row 1.
+ * w[6] = normal, edge, spec, roug, sigma1, sigma2; values[4] = the four terms.
+ * Gradients are WRITTEN (zeroed first): grad_pos nv x 3, grad_d / grad_s
+ * tw*th*3, grad_r tw*th; any may be NULL. Sequential, in the reference order. */
+static double sgnd(double v) { return (double)((v > 0) - (v < 0)); } /* losses.cpp:12 */
+
+static d3 face_normal_unnorm(const orc_scene* s, int f) { /* mesh.hpp:30-33 */
+    const int32_t* t = s->tris + 3 * (size_t)f;
+    d3 a = ld3(s->pos + 3 * (size_t)t[0]);
+    return cross3(sub3(ld3(s->pos + 3 * (size_t)t[1]), a), sub3(ld3(s->pos + 3 * (size_t)t[2]), a));
+}
+
+int orc_regularisers(const orc_scene* s, const double* w, double* values, double* grad_pos, double* grad_d,
+                     double* grad_s, double* grad_r) {
+    const int nv = s->nv, ne = s->ne, tw = s->tw, th = s->th, nt = tw * th;
+    double* gn = (double*)calloc(3 * (size_t)nv + 1, sizeof(double));
+    double* ge = (double*)calloc(3 * (size_t)nv + 1, sizeof(double));
+    for (int i = 0; i < 4; ++i) values[i] = 0;
+    /* normal_consistency_loss (losses.cpp:80-115) */
+    if (w[0] != 0)
+        for (int i = 0; i < ne; ++i) {
+            const int32_t* e = s->edges + 4 * (size_t)i;
+            if (e[3] < 0) continue;
+            d3 m0 = face_normal_unnorm(s, e[2]), m1 = face_normal_unnorm(s, e[3]);
+            double l0 = len3(m0), l1 = len3(m1);
+            if (l0 < 1e-14 || l1 < 1e-14) continue;
+            d3 n0 = div3(m0, l0), n1 = div3(m1, l1);
+            double r = 1.0 - dot3(n0, n1);
+            values[0] += w[0] * r * r;
+            m33 j0 = normalize_jacobian(m0), j1 = normalize_jacobian(m1);
+            d3 h0 = mv33(&j0, n1), h1 = mv33(&j1, n0);
+            double wt = -2.0 * w[0] * r;
+            for (int which = 0; which < 2; ++which) {
+                const int32_t* t = s->tris + 3 * (size_t)(which == 0 ? e[2] : e[3]);
+                d3 h = which == 0 ? h0 : h1;
+                d3 a = ld3(s->pos + 3 * (size_t)t[0]), b = ld3(s->pos + 3 * (size_t)t[1]),
+                   c = ld3(s->pos + 3 * (size_t)t[2]);
+                m33 da = skew33(sub3(c, b)), db = skew33(sub3(a, c)), dc = skew33(sub3(b, a));
+                d3 ga = mul3(mtv33(&da, h), wt), gb = mul3(mtv33(&db, h), wt), gc = mul3(mtv33(&dc, h), wt);
+                double* q;
+                q = gn + 3 * (size_t)t[0]; q[0] += ga.x; q[1] += ga.y; q[2] += ga.z;
+                q = gn + 3 * (size_t)t[1]; q[0] += gb.x; q[1] += gb.y; q[2] += gb.z;
+                q = gn + 3 * (size_t)t[2]; q[0] += gc.x; q[1] += gc.y; q[2] += gc.z;
+            }
+        }
+    /* edge_length_loss (losses.cpp:117-134) */
+    if (w[1] != 0 && ne > 0) {
+        double sum_sq = 0;
+        for (int i = 0; i < ne; ++i) {
+            d3 d = sub3(ld3(s->pos + 3 * (size_t)s->edges[4 * i]), ld3(s->pos + 3 * (size_t)s->edges[4 * i + 1]));
+            sum_sq += dot3(d, d);
+        }
+        if (sum_sq > 0) {
+            double root = sqrt(sum_sq);
+            values[1] = w[1] * root;
+            double wt = w[1] / root;
+            for (int i = 0; i < ne; ++i) {
+                int a = s->edges[4 * i], b = s->edges[4 * i + 1];
+                d3 d = mul3(sub3(ld3(s->pos + 3 * (size_t)a), ld3(s->pos + 3 * (size_t)b)), wt);
+                ge[3 * (size_t)a] += d.x; ge[3 * (size_t)a + 1] += d.y; ge[3 * (size_t)a + 2] += d.z;
+                ge[3 * (size_t)b] -= d.x; ge[3 * (size_t)b + 1] -= d.y; ge[3 * (size_t)b + 2] -= d.z;
+            }
+        }
+    }
+    if (grad_pos)
+        for (size_t i = 0; i < 3 * (size_t)nv; ++i) grad_pos[i] = gn[i] + ge[i]; /* nrm + edg, losses.cpp:276 */
+    free(gn);
+    free(ge);
+    /* specular_correlation_loss (losses.cpp:136-213) */
+    double* gs = (double*)calloc(3 * (size_t)nt + 1, sizeof(double));
+    double* gd = (double*)calloc(3 * (size_t)nt + 1, sizeof(double));
+    if (w[2] != 0 && nt > 0) {
+        const double lw[3] = {0.2126, 0.7152, 0.0722};
+        const double i1 = 1.0 / (2.0 * w[4] * w[4]), i2 = 1.0 / (2.0 * w[5] * w[5]);
+        double* lum = (double*)malloc(sizeof(double) * (size_t)nt);
+        for (int i = 0; i < nt; ++i) lum[i] = dot3(ld3(s->diffuse + 3 * (size_t)i), v3(lw[0], lw[1], lw[2]));
+        for (int p = 0; p < nt; ++p) {
+            int px = p % tw, py = p / tw, cnt = 0, qs[49];
+            double mus[49], mu_sum = 0;
+            d3 avg = v3(0, 0, 0);
+            for (int dy = -3; dy <= 3; ++dy) {
+                int qy = py + dy;
+                if (qy < 0 || qy >= th) continue;
+                for (int dx = -3; dx <= 3; ++dx) {
+                    int qx = px + dx;
+                    if (qx < 0 || qx >= tw) continue;
+                    int q = qy * tw + qx;
+                    double dl = lum[p] - lum[q];
+                    double mu = exp(-(dx * dx + dy * dy) * i1 - dl * dl * i2);
+                    mus[cnt] = mu;
+                    qs[cnt++] = q;
+                    mu_sum += mu;
+                    avg = add3(avg, mul3(ld3(s->specular + 3 * (size_t)q), mu));
+                }
+            }
+            avg = div3(avg, mu_sum);
+            d3 ctr = ld3(s->specular + 3 * (size_t)p);
+            double sg[3];
+            for (int c = 0; c < 3; ++c) {
+                double d = comp3(ctr, c) - comp3(avg, c);
+                values[2] += w[2] * fabs(d);
+                sg[c] = sgnd(d);
+            }
+            for (int c = 0; c < 3; ++c) gs[3 * (size_t)p + c] += w[2] * sg[c];
+            for (int k = 0; k < cnt; ++k) {
+                int q = qs[k];
+                double mu = mus[k], dtm = 0;
+                for (int c = 0; c < 3; ++c) gs[3 * (size_t)q + c] -= w[2] * sg[c] * mu / mu_sum;
+                d3 asq = ld3(s->specular + 3 * (size_t)q);
+                for (int c = 0; c < 3; ++c) dtm += -w[2] * sg[c] * (comp3(asq, c) - comp3(avg, c)) / mu_sum;
+                double dl = lum[p] - lum[q];
+                double dp_ = mu * (-2.0 * dl * i2), dq = -dp_;
+                for (int c = 0; c < 3; ++c) {
+                    gd[3 * (size_t)p + c] += dtm * dp_ * lw[c];
+                    gd[3 * (size_t)q + c] += dtm * dq * lw[c];
+                }
+            }
+        }
+        free(lum);
+    }
+    if (grad_s) memcpy(grad_s, gs, sizeof(double) * 3 * (size_t)nt);
+    if (grad_d) memcpy(grad_d, gd, sizeof(double) * 3 * (size_t)nt);
+    free(gs);
+    free(gd);
+    /* roughness_tv_loss (losses.cpp:215-238) */
+    double* gr = (double*)calloc((size_t)nt + 1, sizeof(double));
+    if (w[3] != 0)
+        for (int y = 0; y < th; ++y)
+            for (int x = 0; x < tw; ++x) {
+                int i = y * tw + x;
+                double v = s->roughness[i];
+                if (x + 1 < tw) {
+                    double d = s->roughness[i + 1] - v, sv = w[3] * sgnd(d);
+                    values[3] += w[3] * fabs(d);
+                    gr[i + 1] += sv;
+                    gr[i] -= sv;
+                }
+                if (y + 1 < th) {
+                    double d = s->roughness[i + tw] - v, sv = w[3] * sgnd(d);
+                    values[3] += w[3] * fabs(d);
+                    gr[i + tw] += sv;
+                    gr[i] -= sv;
+                }
+            }
+    if (grad_r) memcpy(grad_r, gr, sizeof(double) * (size_t)nt);
+    free(gr);
+    return 0;
+}
+
 /* build_adjacency (mesh.cpp:27-63): edges sorted by (min, max); faces in
  * ascending face order; f1 = -1 on boundary; -1 return = non-manifold. */
 typedef struct { int64_t key; int f; } ekey;

@@ -74,6 +74,11 @@ int orc_boundary(const orc_ctx* c, int32_t view, const double* adjoint, int32_t 
                  int32_t* degenerate);
 int orc_laplacian(const orc_scene* s, int32_t mode, double lambda, double* value, double* grad,
                   int32_t* outer, int32_t* inner, double* vals);
+/* normal_consistency / edge_length / specular_correlation / roughness_tv
+ * (losses.cpp:80-238). w = normal, edge, spec, roug, sigma1, sigma2; values[4];
+ * gradients written (any may be NULL). */
+int orc_regularisers(const orc_scene* s, const double* w, double* values, double* grad_pos, double* grad_d,
+                     double* grad_s, double* grad_r);
 double orc_tone_map(double v, double gamma);
 double orc_tone_map_derivative(double v, double gamma);
 int orc_project(const cdr_camera* cam, const double* p, double* q, double* depth);

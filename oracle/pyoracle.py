@@ -136,6 +136,14 @@ class _SceneArrays:
         self.tw, self.th = scene.tex_res
 
 
+def _regularisers(fn, handle, scene, w, chk):
+    V, n = scene.mesh.V, scene.diffuse.shape[0] * scene.diffuse.shape[1]
+    vals = np.zeros(4)
+    gp, gd, gs, gr = np.zeros((V, 3)), np.zeros((n, 3)), np.zeros((n, 3)), np.zeros(n)
+    chk(fn(handle, dp(np.asarray(w, dtype=np.float64)), dp(vals), dp(gp), dp(gd), dp(gs), dp(gr)))
+    return vals, gp, gd, gs, gr
+
+
 class Oracle:
     """C restatement (oracle/cdr_oracle.c) over one scene."""
 
@@ -250,6 +258,11 @@ class Oracle:
         self.lib.orc_laplacian(C.byref(self.s), mode, C.c_double(lam), C.byref(v), dp(grad),
                                ip(outer), ip(inner), dp(vals))
         return v.value, grad, (outer, inner, vals)
+
+    def regularisers(self, w):
+        """(values[4], grad_pos V x 3, grad_d, grad_s tex x 3, grad_r tex) of
+        normal / edge / spec / roug; w = (normal, edge, spec, roug, sigma1, sigma2)."""
+        return _regularisers(self.lib.orc_regularisers, C.byref(self.s), self.scene, w, self._chk)
 
     def loss_grad(self, targets_rgb, st, lay, lam_rend=1.0, lam_lap=0.1, lap_mode=0,
                   targets_mask=None, use_mask=False, want_rendered=False):
@@ -387,6 +400,9 @@ class RefLib:
         self._chk(self.lib.ref_laplacian(self.h, mode, C.c_double(lam), C.byref(v), dp(grad), ip(outer),
                                          ip(inner), dp(vals), C.byref(nnz)))
         return v.value, grad, (outer, inner, vals)
+
+    def regularisers(self, w):
+        return _regularisers(self.lib.ref_regularisers, self.h, self.scene, w, self._chk)
 
     def total_loss(self, targets_rgb, spp, seed, lay, threads=1, lam_rend=1.0, lam_lap=0.1,
                    boundary_term=1, boundary_samples=0, gamma=2.2, lap_mode=0,

@@ -449,6 +449,40 @@ int ref_laplacian(void* s, int32_t mode, double lambda, double* value, double* g
     })
 }
 
+// The four mesh/material regularisers (losses.cpp:80-238) with explicit
+// sigmas. w = normal, edge, spec, roug, sigma1, sigma2. Gradients written
+// (positions: nrm + edg as total_loss sums them, losses.cpp:276).
+int ref_regularisers(void* s, const double* w, double* values, double* grad_pos, double* grad_d,
+                     double* grad_s, double* grad_r) {
+    GUARD({
+        auto* rs = static_cast<RefScene*>(s);
+        const Scene& sc = rs->scene;
+        MeshLossResult nrm = normal_consistency_loss(sc.mesh, w[0]);
+        MeshLossResult edg = edge_length_loss(sc.mesh, w[1]);
+        LossWeights lw;
+        lw.spec = w[2];
+        lw.sigma1 = w[4];
+        lw.sigma2 = w[5];
+        SpecularLossResult spec = specular_correlation_loss(sc.maps, lw);
+        RoughnessLossResult roug = roughness_tv_loss(sc.maps, w[3]);
+        values[0] = nrm.value;
+        values[1] = edg.value;
+        values[2] = spec.value;
+        values[3] = roug.value;
+        if (grad_pos)
+            for (size_t v = 0; v < nrm.grad.size(); ++v) {
+                Vec3 g = nrm.grad[v] + edg.grad[v];
+                grad_pos[3 * v] = g.x;
+                grad_pos[3 * v + 1] = g.y;
+                grad_pos[3 * v + 2] = g.z;
+            }
+        if (grad_d) std::memcpy(grad_d, spec.grad_diffuse.data.data(), spec.grad_diffuse.data.size() * sizeof(double));
+        if (grad_s)
+            std::memcpy(grad_s, spec.grad_specular.data.data(), spec.grad_specular.data.size() * sizeof(double));
+        if (grad_r) std::memcpy(grad_r, roug.grad.data.data(), roug.grad.data.size() * sizeof(double));
+    })
+}
+
 // total_loss (losses.cpp:244-297). weights[0..5] = rend, lap, normal, edge,
 // spec, roug (sigma1/2 stay default). breakdown[0..6] = total, rend, lap,
 // normal, edge, spec, roug. grad is written (fresh GradVector, losses.cpp:250).

@@ -64,6 +64,11 @@ class cdr_layout(C.Structure):
                 ("roughness", C.c_int64), ("light", C.c_int64), ("total", C.c_int64)]
 
 
+class cdr_reg_weights(C.Structure):
+    _fields_ = [("normal", C.c_double), ("edge", C.c_double), ("spec", C.c_double), ("roug", C.c_double),
+                ("sigma1", C.c_double), ("sigma2", C.c_double)]
+
+
 class cdr_stats(C.Structure):
     _fields_ = [("pixels", C.c_int64), ("samples", C.c_int64), ("hit_samples", C.c_int64),
                 ("adjoint_samples", C.c_int64), ("boundary_samples", C.c_int64),
@@ -121,6 +126,10 @@ def load_library(path: str = LIB_PATH):
     L.cdr_loss_grad.argtypes = [_vp, _i, C.c_int32, C.POINTER(cdr_settings), C.c_double, C.c_double,
                                 C.c_int32, C.c_int32, C.POINTER(cdr_layout), _d, _d, _d, _d,
                                 C.POINTER(cdr_stats)]
+    L.cdr_total_loss.argtypes = [_vp, _i, C.c_int32, C.POINTER(cdr_settings), C.c_double, C.c_double,
+                                 C.POINTER(cdr_reg_weights), C.c_int32, C.c_int32, C.POINTER(cdr_layout), _d, _d,
+                                 _d, _d, C.POINTER(cdr_stats)]
+    L.cdr_regularisers.argtypes = [_vp, C.POINTER(cdr_reg_weights), C.POINTER(cdr_layout), _d, _d]
     L.cdr_get_grad.argtypes = [_vp, _d, C.c_int64]
     L.cdr_grad_device_ptr.argtypes = [_vp, C.POINTER(_vp), C.POINTER(C.c_int64)]
     L.cdr_laplacian_matrix.argtypes = [_vp, C.c_int32, _i, _i, _d, C.POINTER(C.c_int64)]
@@ -160,6 +169,22 @@ class RenderSettings:
     def c(self):
         return cdr_settings(int(self.spp), int(bool(self.boundary_term)), int(self.boundary_samples), 0,
                             int(self.seed) & (2 ** 64 - 1), float(self.gamma))
+
+
+@dataclass
+class LossWeights:
+    """LossWeights (losses.hpp:14-23), the reference defaults."""
+    rend: float = 1.0
+    lap: float = 0.1
+    normal: float = 0.01
+    edge: float = 1.0
+    spec: float = 0.01
+    roug: float = 0.001
+    sigma1: float = 2.0
+    sigma2: float = 0.1
+
+    def c_reg(self):
+        return cdr_reg_weights(self.normal, self.edge, self.spec, self.roug, self.sigma1, self.sigma2)
 
 
 def param_layout(scene: Scene, optimize_light: bool = False) -> dict:
@@ -363,22 +388,45 @@ class Renderer:
         return loss, g, stats, rend
 
     def total_loss(self, targets, settings: RenderSettings, layout, lambda_rend=1.0, lambda_lap=0.1,
-                   laplacian_mode=0, use_target_masks=False, target_masks=None):
-        """total_loss (losses.cpp:244-297) with the out-of-scope regularisers at
-        weight zero: breakdown {rend, lap, total}, fresh gradient, rendered images."""
+                   laplacian_mode=0, use_target_masks=False, target_masks=None, weights=None):
+        """total_loss (losses.cpp:244-297): breakdown {total, rend, lap, normal,
+        edge, spec, roug}, fresh gradient, rendered images. `weights`
+        (LossWeights) gives every term its weight; without it the call keeps the
+        lambda_rend / lambda_lap arguments and the four regularisers at zero."""
         if len(targets) != len(self.cameras):
             raise SizeMismatch("target count does not match views")
         for k, t in enumerate(targets):
             self.set_target(k, t, None if target_masks is None else target_masks[k])
-        loss, g, stats, rend = self.loss_grad(np.arange(len(self.cameras)), settings, layout, lambda_rend,
-                                              lambda_lap, laplacian_mode, use_target_masks, want_rendered=True)
+        w = weights if weights is not None else LossWeights(lambda_rend, lambda_lap, 0.0, 0.0, 0.0, 0.0)
+        views = np.arange(len(self.cameras), dtype=np.int32)
+        st = settings.c()
+        lay = _clayout(layout)
+        reg = w.c_reg()
+        bd = np.zeros(7)
+        g = np.zeros(layout["total"])
+        rend = np.zeros(sum(3 * c.width * c.height for c in self.cameras))
+        stats = cdr_stats()
+        self._chk(self.L.cdr_total_loss(self.h, _ip(views), len(views), C.byref(st), w.rend, w.lap, C.byref(reg),
+                                        laplacian_mode, int(use_target_masks), C.byref(lay), _dp(bd), _dp(g),
+                                        _dp(rend), None, C.byref(stats)))
         rendered, off = [], 0
         for cam in self.cameras:
             n = cam.width * cam.height * 3
             rendered.append(rend[off:off + n].reshape(cam.height, cam.width, 3))
             off += n
-        bd = {"rend": loss[0], "lap": loss[1], "total": loss[0] + loss[1]}
-        return bd, g, rendered
+        keys = ("total", "rend", "lap", "normal", "edge", "spec", "roug")
+        return dict(zip(keys, bd.tolist())), g, rendered
+
+    def regularisers(self, weights, layout, grad=None):
+        """normal_consistency / edge_length / specular_correlation / roughness_tv
+        (losses.cpp:80-238). Returns ({normal, edge, spec, roug}, grad) with the
+        gradients += into `grad` (ParamLayout order; fresh zeros by default)."""
+        reg = weights.c_reg()
+        lay = _clayout(layout)
+        vals = np.zeros(4)
+        g = np.zeros(layout["total"]) if grad is None else grad
+        self._chk(self.L.cdr_regularisers(self.h, C.byref(reg), C.byref(lay), _dp(vals), _dp(g)))
+        return dict(zip(("normal", "edge", "spec", "roug"), vals.tolist())), g
 
     def grad_image_loss(self, view, target, settings: RenderSettings, lambda_rend, use_target_mask, layout,
                         grad=None, target_mask=None):

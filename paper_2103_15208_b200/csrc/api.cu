@@ -428,12 +428,11 @@ int cdr_set_textures(cdr_ctx* c, const double* diffuse, const double* specular, 
     c->tw = w;
     c->th = h;
     c->tex.ensure(n);
-    // fp64 inputs are staged on the device and packed into fp32 texel records
-    static thread_local DBuf<double> sd, ss, sr;
-    h2d(sd, diffuse, 3 * n, c->stream);
-    h2d(ss, specular, 3 * n, c->stream);
-    h2d(sr, roughness, n, c->stream);
-    launch_pack_textures(c, sd.p, ss.p, sr.p, int(n));
+    // fp64 maps stay resident (regularisers); shading reads fp32 texel records
+    h2d(c->map_d, diffuse, 3 * n, c->stream);
+    h2d(c->map_s, specular, 3 * n, c->stream);
+    h2d(c->map_r, roughness, n, c->stream);
+    launch_pack_textures(c, c->map_d.p, c->map_s.p, c->map_r.p, int(n));
     sync(c);
     API_END
 }
@@ -700,10 +699,12 @@ int cdr_boundary_pass(cdr_ctx* c, int32_t view, const double* adjoint, const cdr
     API_END
 }
 
-int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_settings* st, double lambda_rend,
-                  double lambda_lap, int32_t lap_mode, int32_t use_mask, const cdr_layout* lay, double* loss_out,
-                  double* grad, double* rendered_rgb, double* rendered_mask, cdr_stats* stats) {
-    API_BEGIN(c)
+// The fused total_loss pipeline (losses.cpp:244-297). terms[6] = rend, lap,
+// normal, edge, spec, roug; reg == nullptr leaves the last four at 0.
+static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_settings* st, double lambda_rend,
+                    double lambda_lap, const cdr_reg_weights* reg, int32_t lap_mode, int32_t use_mask,
+                    const cdr_layout* lay, double* terms_out, double* grad, double* rendered_rgb,
+                    double* rendered_mask, cdr_stats* stats) {
     if (!st || n < 0 || (n > 0 && !views)) throw ApiErr(CDR_ERR_INVALID_ARG, "bad arguments");
     check_layout(c, lay);
     check_ready(c);
@@ -754,6 +755,9 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
     launch_finalize_positions(c, lay->positions);
     const bool lap_here = c->rank == 0;  // computed once across ranks
     if (lap_here) launch_laplacian(c, lap_mode, lambda_lap, c->grad.p + lay->positions);
+    c->reg_vals.ensure(4);
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->reg_vals.p, 0, sizeof(double) * 4, s));
+    if (lap_here && reg) launch_regularisers(c, *reg, *lay, c->grad.p, c->reg_vals.p);
     CDR_CUDA_CHECK(cudaEventRecord(ev[5], s));
     if (c->nccl_comm)
         nccl_check(nccl().allReduce(c->grad.p, c->grad.p, size_t(lay->total), kNcclFloat64, kNcclSum, c->nccl_comm, s),
@@ -763,6 +767,8 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
     double lap_sq = 0;
     CDR_CUDA_CHECK(cudaMemcpyAsync(lacc.data(), c->loss_acc.p, sizeof(double) * lacc.size(), cudaMemcpyDeviceToHost, s));
     CDR_CUDA_CHECK(cudaMemcpyAsync(&lap_sq, c->lap_partial.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    double regv[4] = {0, 0, 0, 0};
+    CDR_CUDA_CHECK(cudaMemcpyAsync(regv, c->reg_vals.p, sizeof(regv), cudaMemcpyDeviceToHost, s));
     if (grad) add_grad_to_host(c, grad, 0, lay->total);
     size_t ro = 0, mo = 0;
     for (int i = 0; i < n; ++i) {
@@ -780,22 +786,19 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
     sync(c);
     raise_device_error(c);
     // rendering term in view order, each view scale * Σ m|d| (losses.cpp:44-47, :257)
-    double terms[2] = {0.0, lap_here ? lambda_lap * lap_sq : 0.0};
+    double terms[6] = {0.0, lap_here ? lambda_lap * lap_sq : 0.0, regv[0], regv[1], regv[2], regv[3]};
     for (int i = 0; i < n; ++i) terms[0] += scales[i] * lacc[slots[i]];
     if (c->nccl_comm) {  // sum the loss terms of all view shards
-        c->lap_lv.ensure(2);
         static thread_local DBuf<double> dterm;
-        dterm.ensure(2);
+        dterm.ensure(6);
         CDR_CUDA_CHECK(cudaMemcpyAsync(dterm.p, terms, sizeof(terms), cudaMemcpyHostToDevice, s));
-        nccl_check(nccl().allReduce(dterm.p, dterm.p, 2, kNcclFloat64, kNcclSum, c->nccl_comm, s),
+        nccl_check(nccl().allReduce(dterm.p, dterm.p, 6, kNcclFloat64, kNcclSum, c->nccl_comm, s),
                    "ncclAllReduce(loss)");
         CDR_CUDA_CHECK(cudaMemcpyAsync(terms, dterm.p, sizeof(terms), cudaMemcpyDeviceToHost, s));
         sync(c);
     }
-    if (loss_out) {
-        loss_out[0] = terms[0];
-        loss_out[1] = terms[1];
-    }
+    if (terms_out)
+        for (int i = 0; i < 6; ++i) terms_out[i] = terms[i];
     if (stats) {
         Counters k;
         CDR_CUDA_CHECK(cudaMemcpy(&k, c->counters.p, sizeof(k), cudaMemcpyDeviceToHost));
@@ -831,6 +834,68 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
         CDR_CUDA_CHECK(cudaEventElapsedTime(&tot, ev[0], ev[6]));
         stats->ms_total = tot;
         stats->kernel_launches = c->launches;
+    }
+}
+
+
+
+int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_settings* st, double lambda_rend,
+                  double lambda_lap, int32_t lap_mode, int32_t use_mask, const cdr_layout* lay, double* loss_out,
+                  double* grad, double* rendered_rgb, double* rendered_mask, cdr_stats* stats) {
+    API_BEGIN(c)
+    double terms[6];
+    loss_grad_impl(c, views, n, st, lambda_rend, lambda_lap, nullptr, lap_mode, use_mask, lay, terms, grad,
+                   rendered_rgb, rendered_mask, stats);
+    if (loss_out) {
+        loss_out[0] = terms[0];
+        loss_out[1] = terms[1];
+    }
+    API_END
+}
+
+int cdr_total_loss(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_settings* st, double lambda_rend,
+                   double lambda_lap, const cdr_reg_weights* reg, int32_t lap_mode, int32_t use_mask,
+                   const cdr_layout* lay, double* breakdown, double* grad, double* rendered_rgb,
+                   double* rendered_mask, cdr_stats* stats) {
+    API_BEGIN(c)
+    if (!reg) throw ApiErr(CDR_ERR_INVALID_ARG, "reg weights are required");
+    double t[6];
+    loss_grad_impl(c, views, n, st, lambda_rend, lambda_lap, reg, lap_mode, use_mask, lay, t, grad, rendered_rgb,
+                   rendered_mask, stats);
+    if (breakdown) {  // LossBreakdown, total in the reference's order (losses.cpp:294-295)
+        breakdown[0] = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
+        for (int i = 0; i < 6; ++i) breakdown[1 + i] = t[i];
+    }
+    API_END
+}
+
+int cdr_regularisers(cdr_ctx* c, const cdr_reg_weights* reg, const cdr_layout* lay, double* values,
+                     double* grad) {
+    API_BEGIN(c)
+    if (!reg) throw ApiErr(CDR_ERR_INVALID_ARG, "reg weights are required");
+    check_layout(c, lay);
+    check_ready(c);
+    c->reg_vals.ensure(4);
+    double* gdev = nullptr;
+    if (grad) {  // private zeroed gradient, then += into the caller's buffer
+        c->reg_grad.ensure(std::max<int64_t>(1, lay->total));
+        CDR_CUDA_CHECK(cudaMemsetAsync(c->reg_grad.p, 0, sizeof(double) * std::max<int64_t>(1, lay->total),
+                                       c->stream));
+        gdev = c->reg_grad.p;
+    } else {
+        if (c->grad_n != lay->total) zero_grad(c, lay->total);
+        gdev = c->grad.p;
+    }
+    launch_regularisers(c, *reg, *lay, gdev, c->reg_vals.p);
+    double v[4];
+    CDR_CUDA_CHECK(cudaMemcpyAsync(v, c->reg_vals.p, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (values)
+        for (int i = 0; i < 4; ++i) values[i] = v[i];
+    if (grad) {
+        std::vector<double> g(size_t(lay->total));
+        CDR_CUDA_CHECK(cudaMemcpy(g.data(), gdev, sizeof(double) * g.size(), cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < g.size(); ++i) grad[i] += g[i];
     }
     API_END
 }

@@ -110,6 +110,8 @@ struct cdr_ctx {
     // materials, light
     int tw = 0, th = 0;
     cdr::DBuf<cdr::Texel> tex;
+    cdr::DBuf<double> map_d, map_s, map_r;  // fp64 maps, resident (the regularisers read them)
+    cdr::DBuf<double> reg_part, reg_lum, reg_stats, reg_vals, reg_grad;
     double light[3] = {1, 1, 1};
     double background[3] = {0, 0, 0};
 

@@ -51,6 +51,10 @@ struct RenderArgs {
 void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a,
                    bool trace, bool loss, bool interior, const double* loss_scales,
                    cudaEvent_t after_trace = nullptr);
+// normal / edge / specular / roughness regularisers (regularisers.cu):
+// values_dev[0..3] written, gradients += into grad (ParamLayout order) if given
+void launch_regularisers(cdr_ctx* c, const cdr_reg_weights& w, const cdr_layout& lay, double* grad,
+                         double* values_dev);
 // Σ over the view chunks of the last timed launch_render: lists + trace time (ms)
 float render_trace_ms(cdr_ctx* c);
 

@@ -6,7 +6,9 @@ sources (oracle/_ref). Run where /root/reference exists:
 Each fixture stores the inputs (so it is self-contained) and the reference's
 outputs: hit caches, images, masks, per-view loss + adjoint, interior and
 boundary gradients, silhouette segments, the Laplacian (CSC, value, gradient)
-and the hot subset of total_loss (loss terms + gradient).
+the hot subset of total_loss (loss terms + gradient), the four mesh/material
+regularisers at two weight sets (REG_WEIGHTS) and total_loss with every term
+at the reference default weights (LossWeights, losses.hpp:14-23).
 """
 import os
 import sys
@@ -18,6 +20,10 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
 from oracle.pyoracle import RefLib, layout_for  # noqa: E402
 from paper_2103_15208_b200 import scenes as S  # noqa: E402
+
+# (normal, edge, spec, roug, sigma1, sigma2): the reference defaults, then a
+# second set with other sigmas so the window weights are exercised off-default
+REG_WEIGHTS = {"default": (0.01, 1.0, 0.01, 0.001, 2.0, 0.1), "alt": (0.3, 0.7, 0.05, 0.02, 1.3, 0.25)}
 
 CASES = {
     "sphere_f4": dict(mesh=lambda: S.geodesic_sphere(4), tex=8, views=2, image=24, spp=4, seed=3, light=True),
@@ -51,6 +57,12 @@ def make(name, c):
     out.update(lap_value=np.array(val), lap_grad=grad, lap_outer=o_, lap_inner=i_, lap_vals=x_)
     bd, g, _ = ref.total_loss(targets, spp, seed, lay)
     out["total_breakdown"], out["total_grad"] = bd, g
+    for k, w in REG_WEIGHTS.items():
+        vals, gp, gd, gs, gr = ref.regularisers(w)
+        out.update({f"reg_{k}_values": vals, f"reg_{k}_pos": gp, f"reg_{k}_diffuse": gd, f"reg_{k}_specular": gs,
+                    f"reg_{k}_roughness": gr, f"reg_{k}_w": np.array(w)})
+    bd, g, _ = ref.total_loss(targets, spp, seed, lay, others=REG_WEIGHTS["default"][:4])
+    out["full_breakdown"], out["full_grad"] = bd, g
     np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
     print(name, os.path.getsize(os.path.join(HERE, name + ".npz")), "bytes")
 
