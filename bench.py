@@ -337,6 +337,39 @@ def main():
         e2e = {"value": total_samples / float(te.item()) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(te.item()) / args.steps}
 
+    # ---- the four mesh/material regularisers of total_loss (losses.cpp:272-292)
+    # at the reference's default weights: texture-size work, not per sample, so
+    # timed on their own (device events on the library stream)
+    regs = None
+    if rank == 0:
+        lw = api.LossWeights()
+        r.regularisers(lw, lay, device_only=True)
+        rev = []
+        for _ in range(max(3, args.steps)):
+            with torch.cuda.stream(stream):
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+            vals, _ = r.regularisers(lw, lay, device_only=True)
+            with torch.cuda.stream(stream):
+                b.record(stream)
+            rev.append((a, b))
+        torch.cuda.synchronize(local)
+        regs = {"ms": statistics.median(a.elapsed_time(b) for a, b in rev), "values": vals,
+                "texels": int(scene.diffuse.shape[0] * scene.diffuse.shape[1]), "tris": scene.mesh.T,
+                "weights": "LossWeights defaults (losses.hpp:14-23)"}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                from oracle.pyoracle import RefLib
+                ref = RefLib(scene)
+                t0 = time.perf_counter()
+                ref.regularisers((lw.normal, lw.edge, lw.spec, lw.roug, lw.sigma1, lw.sigma2))
+                regs["cpu_ms"] = 1e3 * (time.perf_counter() - t0)
+                regs["cpu_kind"] = "reference (oracle/_ref), 1 thread: the reference functions are serial"
+            except Exception as e:  # noqa: BLE001 — the CPU leg is optional
+                regs["cpu_ms"] = None
+                regs["cpu_kind"] = f"unavailable: {e}"
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline_sample(scene, spp, seed, lay, os.cpu_count() or 1, label=args.config)
@@ -352,7 +385,7 @@ def main():
                            "views_per_gpu": len(scene.cameras), "spp": spp,
                            "samples_per_step": samples_all, "parallelism": f"views sharded x{world}",
                            "l2": "flushed (256 MB write) before every timed step; step working set ~2 GB"},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "regularisers": regs,
                 "gpu_launches": int(sum(x["kernel_launches"] for x in stats)),
                 "clocks": clk, "stages_ms": stages,
                 "counters": {k: s0[k] for k in ("pixels", "samples", "hit_samples", "adjoint_samples",

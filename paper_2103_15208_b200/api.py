@@ -417,14 +417,15 @@ class Renderer:
         keys = ("total", "rend", "lap", "normal", "edge", "spec", "roug")
         return dict(zip(keys, bd.tolist())), g, rendered
 
-    def regularisers(self, weights, layout, grad=None):
+    def regularisers(self, weights, layout, grad=None, device_only=False):
         """normal_consistency / edge_length / specular_correlation / roughness_tv
         (losses.cpp:80-238). Returns ({normal, edge, spec, roug}, grad) with the
-        gradients += into `grad` (ParamLayout order; fresh zeros by default)."""
+        gradients += into `grad` (ParamLayout order; fresh zeros by default), or
+        into the device gradient with device_only (grad is then None)."""
         reg = weights.c_reg()
         lay = _clayout(layout)
         vals = np.zeros(4)
-        g = np.zeros(layout["total"]) if grad is None else grad
+        g = None if device_only else (np.zeros(layout["total"]) if grad is None else grad)
         self._chk(self.L.cdr_regularisers(self.h, C.byref(reg), C.byref(lay), _dp(vals), _dp(g)))
         return dict(zip(("normal", "edge", "spec", "roug"), vals.tolist())), g
 
