@@ -34,7 +34,7 @@ def raw(rep):
     hdr, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
-        d = {"kernel": r[hdr.index("Kernel Name")]}
+        d = {"kernel": r[hdr.index("Kernel Name")], "id": r[hdr.index("ID")]}
         for k, (m, sc) in METRICS.items():
             if m in hdr:
                 i = hdr.index(m)
@@ -55,11 +55,12 @@ def raw(rep):
 
 
 def stalls(rep):
+    """Warp-state / scheduler / occupancy details, per launch ID."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
-    keep = {}
+    keep = defaultdict(dict)
     for r in csv.reader(io.StringIO(out)):
         if len(r) > 14 and r[11] in ("Warp State Statistics", "Scheduler Statistics", "Occupancy") and r[14]:
-            keep[r[12]] = r[14] + (" " + r[13] if r[13] else "")
+            keep[r[0]][r[12]] = r[14] + (" " + r[13] if r[13] else "")
     return keep
 
 
@@ -79,7 +80,8 @@ if __name__ == "__main__":
     tag, lcsv, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     doc = {"tag": tag, "launch_list": launches(lcsv), "kernels": {}}
     for rep in reps:
-        for d in raw(rep):
-            d["details"] = stalls(rep)
+        st = stalls(rep)
+        for d in raw(rep):  # the last launch of each kernel name is kept
+            d["details"] = st.get(d["id"], {})
             doc["kernels"][d["kernel"]] = d
     print(json.dumps(doc, indent=1))
