@@ -323,16 +323,14 @@ def main():
         for _ in range(args.steps):
             r.update_positions(pos_h)
             r.set_textures(d_h, s_h, r_h)
-            g_h[:] = 0
-            r.loss_grad(views, st, lay, grad=g_h)
+            r.loss_grad(views, st, lay, grad=g_h, overwrite=True)  # fresh gradient, as total_loss
         barrier()
         dt = time.perf_counter() - t0
         te = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
         if dist is not None:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        # positions + maps up; the caller's gradient buffer goes up and comes
-        # back (cdr_loss_grad accumulates += on the device)
-        h2d = pos_h.nbytes + d_h.nbytes + s_h.nbytes + r_h.nbytes + g_h.nbytes
+        # positions + maps up; the step's gradient (and the two loss terms) down
+        h2d = pos_h.nbytes + d_h.nbytes + s_h.nbytes + r_h.nbytes
         d2h = g_h.nbytes + 16
         e2e = {"value": total_samples / float(te.item()) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(te.item()) / args.steps}

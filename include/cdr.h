@@ -70,12 +70,17 @@ typedef struct cdr_camera {
     int32_t height;
 } cdr_camera;
 
+/* cdr_settings.flags */
+#define CDR_FLAG_GRAD_OVERWRITE 1 /* cdr_loss_grad / cdr_total_loss: grad_inout receives =
+                                     (the fresh GradVector total_loss returns,
+                                     losses.cpp:250) instead of +=, and is not read */
+
 /* RenderSettings (render.hpp:27-35); `threads` has no meaning on the GPU. */
 typedef struct cdr_settings {
     int32_t spp;
     int32_t boundary_term;    /* 0/1 */
     int32_t boundary_samples; /* 0 -> W*H (diff_render.cpp:300-301) */
-    int32_t reserved;
+    int32_t flags;            /* CDR_FLAG_* */
     uint64_t seed;
     double gamma;
 } cdr_settings;

@@ -346,6 +346,7 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
     std::vector<int32_t> views(n);
     for (int k = 0; k < n; ++k) views[k] = k;
     cdr_settings st = settings_of(options.render);
+    st.flags |= CDR_FLAG_GRAD_OVERWRITE;  // res.grad is the fresh GradVector (losses.cpp:250)
     cdr_layout lay = layout_of(*layout);
     const bool want_rendered = !std::getenv("CDR_SKIP_RENDERED");
     std::vector<double> rgb, mask;

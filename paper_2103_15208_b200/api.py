@@ -56,12 +56,15 @@ _vp = C.c_void_p
 
 class cdr_settings(C.Structure):
     _fields_ = [("spp", C.c_int32), ("boundary_term", C.c_int32), ("boundary_samples", C.c_int32),
-                ("reserved", C.c_int32), ("seed", C.c_uint64), ("gamma", C.c_double)]
+                ("flags", C.c_int32), ("seed", C.c_uint64), ("gamma", C.c_double)]
 
 
 class cdr_layout(C.Structure):
     _fields_ = [("positions", C.c_int64), ("diffuse", C.c_int64), ("specular", C.c_int64),
                 ("roughness", C.c_int64), ("light", C.c_int64), ("total", C.c_int64)]
+
+
+CDR_FLAG_GRAD_OVERWRITE = 1
 
 
 class cdr_reg_weights(C.Structure):
@@ -370,10 +373,16 @@ class Renderer:
         return g, deg.value
 
     def loss_grad(self, views, settings: RenderSettings, layout, lambda_rend=1.0, lambda_lap=0.1,
-                  laplacian_mode=0, use_target_mask=False, grad=None, want_rendered=False, device_only=False):
-        """Hot subset of total_loss over `views` (slots). Returns (loss[2], grad, stats, rendered)."""
+                  laplacian_mode=0, use_target_mask=False, grad=None, want_rendered=False, device_only=False,
+                  overwrite=False):
+        """Rendering + Laplacian part of total_loss over `views` (slots). Returns
+        (loss[2], grad, stats, rendered). The gradient is added to `grad` (fresh
+        zeros by default), or written over it with overwrite=True (the caller's
+        buffer is then not read: CDR_FLAG_GRAD_OVERWRITE)."""
         views = np.ascontiguousarray(views, dtype=np.int32)
         st = settings.c()
+        if overwrite:
+            st.flags |= CDR_FLAG_GRAD_OVERWRITE
         lay = _clayout(layout)
         loss = np.zeros(2)
         g = None if device_only else (np.zeros(layout["total"]) if grad is None else grad)
@@ -400,10 +409,11 @@ class Renderer:
         w = weights if weights is not None else LossWeights(lambda_rend, lambda_lap, 0.0, 0.0, 0.0, 0.0)
         views = np.arange(len(self.cameras), dtype=np.int32)
         st = settings.c()
+        st.flags |= CDR_FLAG_GRAD_OVERWRITE  # a fresh GradVector (losses.cpp:250)
         lay = _clayout(layout)
         reg = w.c_reg()
         bd = np.zeros(7)
-        g = np.zeros(layout["total"])
+        g = np.empty(layout["total"])
         rend = np.zeros(sum(3 * c.width * c.height for c in self.cameras))
         stats = cdr_stats()
         self._chk(self.L.cdr_total_loss(self.h, _ip(views), len(views), C.byref(st), w.rend, w.lap, C.byref(reg),

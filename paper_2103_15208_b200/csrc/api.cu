@@ -769,7 +769,10 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
     CDR_CUDA_CHECK(cudaMemcpyAsync(&lap_sq, c->lap_partial.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     double regv[4] = {0, 0, 0, 0};
     CDR_CUDA_CHECK(cudaMemcpyAsync(regv, c->reg_vals.p, sizeof(regv), cudaMemcpyDeviceToHost, s));
-    if (grad) add_grad_to_host(c, grad, 0, lay->total);
+    if (grad && (st->flags & CDR_FLAG_GRAD_OVERWRITE))
+        CDR_CUDA_CHECK(cudaMemcpyAsync(grad, c->grad.p, sizeof(double) * lay->total, cudaMemcpyDeviceToHost, s));
+    else if (grad)
+        add_grad_to_host(c, grad, 0, lay->total);
     size_t ro = 0, mo = 0;
     for (int i = 0; i < n; ++i) {
         const ViewData& v = c->views[slots[i]];

@@ -256,3 +256,21 @@ def test_grazing_rays_near_silhouettes_exact(sphere):
         _, tg = r.radiance_at(v, xy)
         _, to = o.radiance_at(v, xy)
         np.testing.assert_array_equal(tg, to)
+
+
+def test_grad_overwrite_flag(sphere):
+    """CDR_FLAG_GRAD_OVERWRITE writes the fresh gradient; the default adds."""
+    r, _ = _pair(sphere)
+    spp, seed = 4, 1
+    tg = targets_for(sphere, spp, seed, Oracle)
+    for k in range(len(sphere.cameras)):
+        r.set_target(k, tg[k])
+    lay = param_layout(sphere)
+    views = np.arange(len(sphere.cameras))
+    st = RenderSettings(spp=spp, seed=seed)
+    _, g0, _, _ = r.loss_grad(views, st, lay)
+    junk = np.full(lay["total"], 7.0)
+    _, g1, _, _ = r.loss_grad(views, st, lay, grad=junk.copy(), overwrite=True)
+    assert rel_l2(g1, g0) <= 1e-12  # runs differ only by fp64 RED order
+    _, g2, _, _ = r.loss_grad(views, st, lay, grad=junk.copy())
+    assert rel_l2(g2 - 7.0, g0) <= 1e-12
