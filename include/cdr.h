@@ -245,6 +245,16 @@ int cdr_laplacian_matrix(cdr_ctx* ctx, int32_t mode, int32_t* outer, int32_t* in
 int cdr_laplacian_loss(cdr_ctx* ctx, int32_t mode, double lambda, double* value_out,
                        double* grad_positions_inout);
 
+/* self_intersects (mesh.hpp:67, mesh.cpp:184-214) on an arbitrary mesh (it
+ * need not be the context's render mesh, nor manifold): result = 1 iff two
+ * triangles sharing no vertex overlap (triangles_intersect, tol 1e-10). With
+ * pairs (cap x 2, nullable) and/or n_pairs (nullable) every offending pair
+ * (f < g) is found; pairs receives the first `cap` of them sorted by (f, g)
+ * and n_pairs their count. Without either, the search stops at the first. */
+int cdr_self_intersects(cdr_ctx* ctx, const double* positions, int32_t n_vertices,
+                        const int32_t* triangles, int32_t n_triangles, int32_t* result,
+                        int32_t* pairs, int64_t cap, int64_t* n_pairs);
+
 /* Multi-GPU view sharding: one context per GPU/rank, gradient all-reduce over
  * NCCL (loaded at run time). id is an ncclUniqueId (128 bytes). */
 int cdr_nccl_unique_id(char id_out[128]);

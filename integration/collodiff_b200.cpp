@@ -12,6 +12,8 @@
 //   grad_image_loss      diff_render.hpp:65-67  -> cdr_loss_grad (one view)
 //   extract_silhouettes  silhouette.hpp:36      -> cdr_extract_silhouettes
 //   cotangent_laplacian  laplacian.hpp:14-15    -> cdr_laplacian_matrix
+//   self_intersects      mesh.hpp:67            -> cdr_self_intersects (pairs
+//                        sorted by (f, g); the reference's follow its BVH)
 //   total_loss           losses.hpp:94-96       -> cdr_total_loss (rendering,
 //                        Laplacian and the four mesh/material regularisers of
 //                        losses.cpp:272-292, all on the device)
@@ -315,6 +317,32 @@ double grad_image_loss(const Scene& scene, const GradContext&, int view, const I
     d.check(cdr_loss_grad(d.ctx, &v, 1, &st, lambda_rend, 0.0, CDR_LAPLACIAN_COTANGENT, use_target_mask ? 1 : 0,
                           &lay, loss, grad.values.data(), nullptr, nullptr, nullptr));
     return loss[0];
+}
+
+bool self_intersects(const Mesh& mesh, std::vector<std::pair<int, int>>* pairs) {
+    if (pairs) pairs->clear();
+    Device& d = dev();
+    const int nv = mesh.vertex_count(), nt = mesh.triangle_count();
+    std::vector<double> pos(3 * size_t(nv));
+    for (int v = 0; v < nv; ++v) {
+        pos[3 * v] = mesh.positions[v].x;
+        pos[3 * v + 1] = mesh.positions[v].y;
+        pos[3 * v + 2] = mesh.positions[v].z;
+    }
+    std::vector<int32_t> tris(3 * size_t(nt));
+    for (int f = 0; f < nt; ++f)
+        for (int k = 0; k < 3; ++k) tris[3 * f + k] = mesh.triangles[f][k];
+    int32_t res = 0;
+    if (!pairs) {
+        d.check(cdr_self_intersects(d.ctx, pos.data(), nv, tris.data(), nt, &res, nullptr, 0, nullptr));
+        return res != 0;
+    }
+    int64_t n = 0;
+    d.check(cdr_self_intersects(d.ctx, pos.data(), nv, tris.data(), nt, &res, nullptr, 0, &n));
+    std::vector<int32_t> pr(2 * size_t(n));
+    if (n > 0) d.check(cdr_self_intersects(d.ctx, pos.data(), nv, tris.data(), nt, &res, pr.data(), n, &n));
+    for (int64_t i = 0; i < n; ++i) pairs->push_back({pr[2 * i], pr[2 * i + 1]});
+    return res != 0;
 }
 
 Eigen::SparseMatrix<double> cotangent_laplacian(const Mesh& mesh, LaplacianMode mode) {

@@ -1241,6 +1241,80 @@ int orc_regularisers(const orc_scene* s, const double* w, double* values, double
     return 0;
 }
 
+/* ---- self_intersects (mesh.cpp:137-214), SURVEY §8(f) row 2. Brute force
+ * over all pairs f < g with an exact fp64 AABB prefilter (a pair whose boxes
+ * are disjoint cannot pass the separating-axis test), pairs in (f, g) order.
+ * pairs (cap x 2) and n_pairs may be NULL. */
+static int sat_separated(d3 axis, const d3* ta, const d3* tb, double tol) { /* mesh.cpp:147-157 */
+    double l2 = dot3(axis, axis);
+    if (l2 < 1e-24) return 0;
+    double alo = dot3(axis, ta[0]), ahi = alo, blo = dot3(axis, tb[0]), bhi = blo;
+    for (int i = 1; i < 3; ++i) {
+        double da = dot3(axis, ta[i]), db = dot3(axis, tb[i]);
+        alo = da < alo ? da : alo;
+        ahi = ahi < da ? da : ahi;
+        blo = db < blo ? db : blo;
+        bhi = bhi < db ? db : bhi;
+    }
+    double g0 = blo - ahi, g1 = alo - bhi, gap = g0 < g1 ? g1 : g0;
+    return gap > -tol * sqrt(l2);
+}
+
+int orc_triangles_intersect(const double* a0, const double* a1, const double* a2, const double* b0,
+                            const double* b1, const double* b2, double tol) { /* mesh.cpp:160-182 */
+    d3 ta[3] = {ld3(a0), ld3(a1), ld3(a2)}, tb[3] = {ld3(b0), ld3(b1), ld3(b2)};
+    d3 ea[3] = {sub3(ta[1], ta[0]), sub3(ta[2], ta[1]), sub3(ta[0], ta[2])};
+    d3 eb[3] = {sub3(tb[1], tb[0]), sub3(tb[2], tb[1]), sub3(tb[0], tb[2])};
+    if (sat_separated(cross3(ea[0], ea[1]), ta, tb, tol)) return 0;
+    if (sat_separated(cross3(eb[0], eb[1]), ta, tb, tol)) return 0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            if (sat_separated(cross3(ea[i], eb[j]), ta, tb, tol)) return 0;
+    return 1;
+}
+
+int orc_self_intersects(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, int32_t* result,
+                        int32_t* pairs, int64_t cap, int64_t* n_pairs) {
+    (void)nv;
+    int64_t n = 0;
+    double* box = (double*)malloc(sizeof(double) * 6 * ((size_t)nt + 1));
+    for (int f = 0; f < nt; ++f)
+        for (int k = 0; k < 3; ++k) {
+            double a = pos[3 * (size_t)tris[3 * f] + k], b = pos[3 * (size_t)tris[3 * f + 1] + k],
+                   c = pos[3 * (size_t)tris[3 * f + 2] + k];
+            box[6 * (size_t)f + k] = fmin(a, fmin(b, c));
+            box[6 * (size_t)f + 3 + k] = fmax(a, fmax(b, c));
+        }
+    const int want = pairs != NULL || n_pairs != NULL;
+    for (int f = 0; f < nt && (want || n == 0); ++f) {
+        const int32_t* t = tris + 3 * (size_t)f;
+        for (int g = f + 1; g < nt; ++g) {
+            const int32_t* u = tris + 3 * (size_t)g;
+            const double *bf = box + 6 * (size_t)f, *bg = box + 6 * (size_t)g;
+            if (bf[0] > bg[3] || bf[3] < bg[0] || bf[1] > bg[4] || bf[4] < bg[1] || bf[2] > bg[5] || bf[5] < bg[2])
+                continue;
+            int share = 0;
+            for (int i = 0; i < 3; ++i)
+                for (int j = 0; j < 3; ++j) share |= t[i] == u[j];
+            if (share) continue;
+            if (orc_triangles_intersect(pos + 3 * (size_t)t[0], pos + 3 * (size_t)t[1], pos + 3 * (size_t)t[2],
+                                        pos + 3 * (size_t)u[0], pos + 3 * (size_t)u[1], pos + 3 * (size_t)u[2],
+                                        1e-10)) {
+                if (pairs && n < cap) {
+                    pairs[2 * n] = f;
+                    pairs[2 * n + 1] = g;
+                }
+                ++n;
+                if (!want) break;
+            }
+        }
+    }
+    free(box);
+    *result = n > 0;
+    if (n_pairs) *n_pairs = n;
+    return 0;
+}
+
 /* build_adjacency (mesh.cpp:27-63): edges sorted by (min, max); faces in
  * ascending face order; f1 = -1 on boundary; -1 return = non-manifold. */
 typedef struct { int64_t key; int f; } ekey;

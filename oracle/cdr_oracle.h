@@ -79,6 +79,12 @@ int orc_laplacian(const orc_scene* s, int32_t mode, double lambda, double* value
  * gradients written (any may be NULL). */
 int orc_regularisers(const orc_scene* s, const double* w, double* values, double* grad_pos, double* grad_d,
                      double* grad_s, double* grad_r);
+/* self_intersects / triangles_intersect (mesh.cpp:137-214): brute force, pairs
+ * sorted by (f, g); pairs / n_pairs may be NULL. */
+int orc_triangles_intersect(const double* a0, const double* a1, const double* a2, const double* b0,
+                            const double* b1, const double* b2, double tol);
+int orc_self_intersects(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, int32_t* result,
+                        int32_t* pairs, int64_t cap, int64_t* n_pairs);
 double orc_tone_map(double v, double gamma);
 double orc_tone_map_derivative(double v, double gamma);
 int orc_project(const cdr_camera* cam, const double* p, double* q, double* depth);

@@ -136,6 +136,51 @@ class _SceneArrays:
         self.tw, self.th = scene.tex_res
 
 
+def _self_intersects(fn, pos, tris, want_pairs):
+    pos = np.ascontiguousarray(pos, dtype=np.float64)
+    tris = np.ascontiguousarray(tris, dtype=np.int32)
+    res = C.c_int32()
+    n = C.c_int64()
+    if not want_pairs:
+        rc = fn(dp(pos), len(pos), ip(tris), len(tris), C.byref(res), None, C.c_int64(0), None)
+        return bool(res.value), None, rc
+    cap = max(16, 4 * len(tris))
+    pairs = np.zeros((cap, 2), np.int32)
+    rc = fn(dp(pos), len(pos), ip(tris), len(tris), C.byref(res), ip(pairs), C.c_int64(cap), C.byref(n))
+    if rc == 0 and n.value > cap:
+        cap = n.value
+        pairs = np.zeros((cap, 2), np.int32)
+        rc = fn(dp(pos), len(pos), ip(tris), len(tris), C.byref(res), ip(pairs), C.c_int64(cap), C.byref(n))
+    return bool(res.value), pairs[:n.value].copy(), rc
+
+
+def oracle_self_intersects(pos, tris, want_pairs=True):
+    """self_intersects (mesh.cpp:184-214), C restatement: (bool, pairs sorted by (f, g))."""
+    L = C.CDLL(build_oracle())
+    b, pr, rc = _self_intersects(L.orc_self_intersects, pos, tris, want_pairs)
+    assert rc == 0
+    return b, pr
+
+
+def ref_self_intersects(pos, tris, want_pairs=True):
+    """The reference's own self_intersects (oracle/_ref), pairs sorted by (f, g)."""
+    L = C.CDLL(build_ref())
+    b, pr, rc = _self_intersects(L.ref_self_intersects, pos, tris, want_pairs)
+    if rc != 0:
+        raise RuntimeError(f"reference status {rc}")
+    return b, pr
+
+
+def triangles_intersect(a, b, tol=1e-10, ref=False):
+    """triangles_intersect (mesh.cpp:160-182) of two 3x3 vertex arrays."""
+    L = C.CDLL(build_ref() if ref else build_oracle())
+    fn = L.ref_triangles_intersect if ref else L.orc_triangles_intersect
+    fn.argtypes = [C.POINTER(C.c_double)] * 6 + [C.c_double]
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    return bool(fn(*(dp(np.ascontiguousarray(x)) for x in (a[0], a[1], a[2], b[0], b[1], b[2])), tol))
+
+
 def _regularisers(fn, handle, scene, w, chk):
     V, n = scene.mesh.V, scene.diffuse.shape[0] * scene.diffuse.shape[1]
     vals = np.zeros(4)

@@ -6,6 +6,7 @@
 // cpu_baseline leg. It never participates in the product path.
 //
 // Every ref_* call forwards to the reference function named beside it.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -481,6 +482,35 @@ int ref_regularisers(void* s, const double* w, double* values, double* grad_pos,
             std::memcpy(grad_s, spec.grad_specular.data.data(), spec.grad_specular.data.size() * sizeof(double));
         if (grad_r) std::memcpy(grad_r, roug.grad.data.data(), roug.grad.data.size() * sizeof(double));
     })
+}
+
+// self_intersects (mesh.cpp:184-214) with pairs, sorted by (f, g) for
+// comparison (the reference's order follows its BVH traversal), and
+// triangles_intersect (mesh.cpp:160-182).
+int ref_self_intersects(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, int32_t* result,
+                        int32_t* pairs, int64_t cap, int64_t* n_pairs) {
+    GUARD({
+        Mesh m;
+        m.positions.resize(nv);
+        for (int i = 0; i < nv; ++i) m.positions[i] = Vec3(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]);
+        m.triangles.resize(nt);
+        for (int f = 0; f < nt; ++f) m.triangles[f] = {tris[3 * f], tris[3 * f + 1], tris[3 * f + 2]};
+        std::vector<std::pair<int, int>> pr;
+        const bool want = pairs || n_pairs;
+        *result = self_intersects(m, want ? &pr : nullptr) ? 1 : 0;
+        std::sort(pr.begin(), pr.end());
+        for (int64_t i = 0; i < std::min<int64_t>(cap, int64_t(pr.size())); ++i) {
+            pairs[2 * i] = pr[size_t(i)].first;
+            pairs[2 * i + 1] = pr[size_t(i)].second;
+        }
+        if (n_pairs) *n_pairs = int64_t(pr.size());
+    })
+}
+
+int ref_triangles_intersect(const double* a0, const double* a1, const double* a2, const double* b0,
+                            const double* b1, const double* b2, double tol) {
+    auto v = [](const double* p) { return Vec3(p[0], p[1], p[2]); };
+    return triangles_intersect(v(a0), v(a1), v(a2), v(b0), v(b1), v(b2), tol) ? 1 : 0;
 }
 
 // total_loss (losses.cpp:244-297). weights[0..5] = rend, lap, normal, edge,

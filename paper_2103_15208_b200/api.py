@@ -133,6 +133,8 @@ def load_library(path: str = LIB_PATH):
                                  C.POINTER(cdr_reg_weights), C.c_int32, C.c_int32, C.POINTER(cdr_layout), _d, _d,
                                  _d, _d, C.POINTER(cdr_stats)]
     L.cdr_regularisers.argtypes = [_vp, C.POINTER(cdr_reg_weights), C.POINTER(cdr_layout), _d, _d]
+    L.cdr_self_intersects.argtypes = [_vp, _d, C.c_int32, _i, C.c_int32, _i, _i, C.c_int64,
+                                      C.POINTER(C.c_int64)]
     L.cdr_get_grad.argtypes = [_vp, _d, C.c_int64]
     L.cdr_grad_device_ptr.argtypes = [_vp, C.POINTER(_vp), C.POINTER(C.c_int64)]
     L.cdr_laplacian_matrix.argtypes = [_vp, C.c_int32, _i, _i, _d, C.POINTER(C.c_int64)]
@@ -460,6 +462,27 @@ class Renderer:
         v = C.c_double()
         self._chk(self.L.cdr_laplacian_loss(self.h, mode, lam, C.byref(v), _dp(g)))
         return v.value, g
+
+    def self_intersects(self, positions, triangles, want_pairs=False):
+        """self_intersects (mesh.hpp:67) of any mesh (not necessarily this
+        renderer's): (bool, pairs (n x 2, sorted by (f, g)) or None)."""
+        pos = np.ascontiguousarray(positions, dtype=np.float64)
+        tris = np.ascontiguousarray(triangles, dtype=np.int32)
+        res = C.c_int32()
+        if not want_pairs:
+            self._chk(self.L.cdr_self_intersects(self.h, _dp(pos), len(pos), _ip(tris), len(tris), C.byref(res),
+                                                 None, 0, None))
+            return bool(res.value), None
+        n = C.c_int64()
+        cap = max(16, 4 * len(tris))
+        pairs = np.zeros((cap, 2), np.int32)
+        self._chk(self.L.cdr_self_intersects(self.h, _dp(pos), len(pos), _ip(tris), len(tris), C.byref(res),
+                                             _ip(pairs), cap, C.byref(n)))
+        if n.value > cap:
+            pairs = np.zeros((n.value, 2), np.int32)
+            self._chk(self.L.cdr_self_intersects(self.h, _dp(pos), len(pos), _ip(tris), len(tris), C.byref(res),
+                                                 _ip(pairs), n.value, C.byref(n)))
+        return bool(res.value), pairs[:n.value].copy()
 
     def grad_device(self):
         p = _vp()

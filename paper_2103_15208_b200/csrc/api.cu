@@ -263,6 +263,8 @@ int cdr_create(int device, cdr_ctx** out) {
 void cdr_destroy(cdr_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
+    if (c->geo) cdr_destroy(c->geo);
+    c->si_pairs.release();
     if (c->nccl_comm && nccl().ok) nccl().commDestroy(c->nccl_comm);
     cudaStreamSynchronize(c->stream);
     for (auto& e : c->ev) cudaEventDestroy(e);
@@ -951,6 +953,59 @@ int cdr_laplacian_loss(cdr_ctx* c, int32_t mode, double lambda, double* value, d
     if (value) *value = lambda * sq;
     if (grad)
         for (size_t i = 0; i < g.size(); ++i) grad[i] += g[i];
+    API_END
+}
+
+int cdr_self_intersects(cdr_ctx* c, const double* positions, int32_t nv, const int32_t* triangles, int32_t nt,
+                        int32_t* result, int32_t* pairs, int64_t cap, int64_t* n_pairs) {
+    API_BEGIN(c)
+    if (nv < 0 || nt < 0 || (nv > 0 && !positions) || (nt > 0 && !triangles) || !result || cap < 0 ||
+        (cap > 0 && !pairs))
+        throw ApiErr(CDR_ERR_INVALID_ARG, "bad self_intersects arguments");
+    for (int64_t i = 0; i < 3 * int64_t(nt); ++i)
+        if (triangles[i] < 0 || triangles[i] >= nv)
+            throw ApiErr(CDR_ERR_INVALID_ARG, "triangle references a vertex out of range");
+    *result = 0;
+    if (n_pairs) *n_pairs = 0;
+    if (nt < 2) return;  // mesh.cpp:186
+    if (!c->geo) {  // a geometry-only context: the render mesh stays untouched
+        const int rc = cdr_create(c->device, &c->geo);
+        if (rc != CDR_OK) throw ApiErr(rc, "cannot create the geometry context");
+    }
+    cdr_ctx* g = c->geo;
+    cudaStream_t s = g->stream;
+    // topology cached across calls (robust_evolve passes one topology many times)
+    if (g->T != nt || g->V != nv || std::memcmp(g->h_tris.data(), triangles, sizeof(int32_t) * 3 * size_t(nt)) != 0) {
+        g->V = nv;
+        g->T = nt;
+        g->h_tris.assign(triangles, triangles + 3 * size_t(nt));
+        h2d(g->tris, triangles, 3 * size_t(nt), s);
+    }
+    h2d(g->pos, positions, 3 * size_t(nv), s);
+    launch_bvh(g, 0.0);
+    const bool want = pairs != nullptr || n_pairs != nullptr;
+    long long n = 0;
+    if (!want) {
+        n = launch_self_intersect(g, nullptr, 0);
+    } else {
+        size_t capd = std::max<size_t>(4096, c->si_pairs.n);
+        while (true) {
+            c->si_pairs.ensure(capd);
+            n = launch_self_intersect(g, c->si_pairs.p, (long long)c->si_pairs.n);
+            if (n <= (long long)c->si_pairs.n) break;
+            capd = size_t(n);  // rerun with room for every pair
+        }
+        std::vector<int2> h(static_cast<size_t>(n));
+        if (n > 0)
+            CDR_CUDA_CHECK(cudaMemcpy(h.data(), c->si_pairs.p, sizeof(int2) * size_t(n), cudaMemcpyDeviceToHost));
+        std::sort(h.begin(), h.end(), [](int2 a, int2 b) { return a.x != b.x ? a.x < b.x : a.y < b.y; });
+        for (int64_t i = 0; i < std::min<int64_t>(cap, n); ++i) {
+            pairs[2 * i] = h[size_t(i)].x;
+            pairs[2 * i + 1] = h[size_t(i)].y;
+        }
+        if (n_pairs) *n_pairs = n;
+    }
+    *result = n > 0 ? 1 : 0;
     API_END
 }
 

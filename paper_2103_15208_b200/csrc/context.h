@@ -70,6 +70,8 @@ struct Timer {
 
 struct cdr_ctx {
     int device = 0;
+    cdr_ctx* geo = nullptr;  // geometry-only context of cdr_self_intersects (lazy)
+    cdr::DBuf<int2> si_pairs;
     cudaStream_t stream = nullptr;
     std::string err;
 

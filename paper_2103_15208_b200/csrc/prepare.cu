@@ -242,11 +242,19 @@ inline int blocks(long n, int b = kBlock) { return int((n + b - 1) / b); }
 void launch_prepare(cdr_ctx* c, double cam_abs_max) {
     cudaStream_t s = c->stream;
     const int V = c->V, T = c->T;
-    c->info.ensure(1);
     if (T > 0) { ++c->launches; k_face_normals<<<blocks(T), kBlock, 0, s>>>(c->pos.p, c->tris.p, T, c->fnormal.p); }
     if (V > 0)
         { ++c->launches; k_vertex_normals<<<blocks(V), kBlock, 0, s>>>(c->fnormal.p, c->vf_start.p, c->vf_list.p, V,
                                                       c->normals.p, c->accum.p); }
+    launch_bvh(c, cam_abs_max);
+}
+
+// Bounding box + t_min + LBVH only (no normals): also the build of the
+// geometry-only context behind cdr_self_intersects.
+void launch_bvh(cdr_ctx* c, double cam_abs_max) {
+    cudaStream_t s = c->stream;
+    const int V = c->V, T = c->T;
+    c->info.ensure(1);
     int nb = std::max(1, std::min(blocks(V), 1184));
     c->bbox_partial.ensure(size_t(nb) * 6);
     { ++c->launches; k_bbox_partial<<<nb, kBlock, 0, s>>>(c->pos.p, V, c->bbox_partial.p); }

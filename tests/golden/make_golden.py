@@ -8,7 +8,8 @@ outputs: hit caches, images, masks, per-view loss + adjoint, interior and
 boundary gradients, silhouette segments, the Laplacian (CSC, value, gradient)
 the hot subset of total_loss (loss terms + gradient), the four mesh/material
 regularisers at two weight sets (REG_WEIGHTS) and total_loss with every term
-at the reference default weights (LossWeights, losses.hpp:14-23).
+at the reference default weights (LossWeights, losses.hpp:14-23); and
+selfint.npz: self_intersects pairs of clean, broken and noisy meshes.
 """
 import os
 import sys
@@ -18,7 +19,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-from oracle.pyoracle import RefLib, layout_for  # noqa: E402
+from oracle.pyoracle import RefLib, layout_for, ref_self_intersects  # noqa: E402
 from paper_2103_15208_b200 import scenes as S  # noqa: E402
 
 # (normal, edge, spec, roug, sigma1, sigma2): the reference defaults, then a
@@ -67,6 +68,36 @@ def make(name, c):
     print(name, os.path.getsize(os.path.join(HERE, name + ".npz")), "bytes")
 
 
+def selfint_cases():
+    """Meshes for self_intersects (mesh.cpp:184-214): clean, broken and noisy."""
+    rng = np.random.default_rng(11)
+    out = {}
+    ico = S.icosphere(2)
+    out["ico2"] = (ico.positions, ico.triangles)
+    p = ico.positions.copy()
+    p[0] = -p[0] * 1.2  # test_mesh.cpp:126-131
+    out["ico2_punched"] = (p, ico.triangles)
+    out["two_tris"] = (np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0.3, 0.3, -1], [0.5, 0.1, 1], [0.1, 0.5, 1.0]]),
+                       np.array([[0, 1, 2], [3, 4, 5]], np.int32))  # test_mesh.cpp:116-124
+    for name, m in (("sphere_f12", S.geodesic_sphere(12)), ("knot_small", S.torus_knot(120, 10))):
+        out[name] = (m.positions, m.triangles)
+        scale = np.ptp(m.positions, axis=0).max()
+        for k, sd in enumerate((0.002, 0.01, 0.04)):
+            out[f"{name}_noise{k}"] = (m.positions + rng.normal(0, sd * scale, m.positions.shape), m.triangles)
+    return out
+
+
+def make_selfint():
+    out = {}
+    for name, (pos, tris) in selfint_cases().items():
+        b, pairs = ref_self_intersects(pos, tris)
+        out[f"{name}_pos"], out[f"{name}_tris"] = np.asarray(pos, np.float64), np.asarray(tris, np.int32)
+        out[f"{name}_result"], out[f"{name}_pairs"] = np.array(int(b)), pairs
+        print(name, len(tris), "tris", int(b), len(pairs), "pairs")
+    np.savez_compressed(os.path.join(HERE, "selfint.npz"), names=np.array(sorted(selfint_cases())), **out)
+
+
 if __name__ == "__main__":
     for n, c in CASES.items():
         make(n, c)
+    make_selfint()
