@@ -245,6 +245,12 @@ int cdr_laplacian_matrix(cdr_ctx* ctx, int32_t mode, int32_t* outer, int32_t* in
 int cdr_laplacian_loss(cdr_ctx* ctx, int32_t mode, double lambda, double* value_out,
                        double* grad_positions_inout);
 
+/* Image and mask of `view` from the last cdr_render / cdr_loss_grad /
+ * cdr_total_loss that rendered it (the rendered outputs of total_loss,
+ * losses.cpp:259), read straight into the caller's W x H x 3 and W x H
+ * buffers (either may be NULL). */
+int cdr_get_rendered(cdr_ctx* ctx, int32_t view, double* rgb_out, double* mask_out);
+
 /* self_intersects (mesh.hpp:67, mesh.cpp:184-214) on an arbitrary mesh (it
  * need not be the context's render mesh, nor manifold): result = 1 iff two
  * triangles sharing no vertex overlap (triangles_intersect, tol 1e-10). With

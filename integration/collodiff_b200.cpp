@@ -26,7 +26,9 @@
 // Device selection: env CDR_DEVICE (default 0). Env CDR_SKIP_RENDERED=1 makes
 // total_loss leave TotalLossResult::rendered empty (run_coarse_to_fine does
 // not read it; it costs a K-image download per iteration).
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -61,6 +63,7 @@ struct Device {
     cdr_ctx* ctx = nullptr;
     uint64_t topo_key = 0;
     uint64_t target_key = 0;
+    uint64_t view_key = 0;
     std::vector<int32_t> tris, edges;
     std::vector<double> buf;
 
@@ -129,6 +132,7 @@ struct Device {
 
     void views(const std::vector<Camera>& cams) {
         std::vector<cdr_camera> cc(cams.size());
+        std::memset(cc.data(), 0, sizeof(cdr_camera) * cc.size());  // hashed below: no padding garbage
         for (size_t i = 0; i < cams.size(); ++i) {
             const Camera& c = cams[i];
             const Vec3* src[4] = {&c.origin, &c.right, &c.up, &c.forward};
@@ -142,7 +146,12 @@ struct Device {
             cc[i].width = c.width;
             cc[i].height = c.height;
         }
+        // the cameras rarely change across iterations: re-sending them would
+        // reset the per-view slots and force every target to be re-uploaded
+        const uint64_t key = fnv1a(cc.data(), sizeof(cdr_camera) * cc.size(), 0xca3e + cc.size());
+        if (key == view_key && view_key != 0) return;
         check(cdr_set_views(ctx, cc.data(), nullptr, int32_t(cc.size())));
+        view_key = key;
         target_key = 0;  // set_views resets the per-view slots
     }
 
@@ -161,6 +170,35 @@ struct Device {
                                  t.has_mask() ? t.mask.data() : nullptr));
         }
         target_key = key;
+    }
+};
+
+// CDR_SHIM_PROFILE=1: wall time per shim entry point, printed at exit
+struct ShimProfile {
+    const bool on = std::getenv("CDR_SHIM_PROFILE") != nullptr;
+    double ms[8] = {};
+    long calls[8] = {};
+    ~ShimProfile() {
+        if (!on) return;
+        const char* names[8] = {"total_loss", "  scene+targets upload", "  cdr_total_loss", "  rendered copy",
+                                "self_intersects", "render", "", ""};
+        for (int i = 0; i < 8; ++i)
+            if (calls[i]) std::fprintf(stderr, "[cdr shim] %-24s %6ld calls %10.2f ms\n", names[i], calls[i], ms[i]);
+    }
+};
+ShimProfile& prof() {
+    static ShimProfile p;
+    return p;
+}
+struct ShimTimer {
+    int slot;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit ShimTimer(int s) : slot(s) {}
+    ~ShimTimer() {
+        ShimProfile& p = prof();
+        if (!p.on) return;
+        p.ms[slot] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        ++p.calls[slot];
     }
 };
 
@@ -320,6 +358,7 @@ double grad_image_loss(const Scene& scene, const GradContext&, int view, const I
 }
 
 bool self_intersects(const Mesh& mesh, std::vector<std::pair<int, int>>* pairs) {
+    ShimTimer timer(4);
     if (pairs) pairs->clear();
     Device& d = dev();
     const int nv = mesh.vertex_count(), nt = mesh.triangle_count();
@@ -366,10 +405,14 @@ Eigen::SparseMatrix<double> cotangent_laplacian(const Mesh& mesh, LaplacianMode 
 TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets, const LossWeights& weights,
                            const LossOptions& options, std::shared_ptr<const ParamLayout> layout) {
     if (targets.size() != scene.views.size()) throw SizeMismatch("target count does not match views");
+    ShimTimer timer(0);
     TotalLossResult res{LossBreakdown{}, GradVector(layout), {}};
     Device& d = dev();
-    d.scene(scene);
-    d.targets(targets);
+    {
+        ShimTimer t(1);
+        d.scene(scene);
+        d.targets(targets);
+    }
     const int n = int(scene.views.size());
     std::vector<int32_t> views(n);
     for (int k = 0; k < n; ++k) views[k] = k;
@@ -377,21 +420,17 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
     st.flags |= CDR_FLAG_GRAD_OVERWRITE;  // res.grad is the fresh GradVector (losses.cpp:250)
     cdr_layout lay = layout_of(*layout);
     const bool want_rendered = !std::getenv("CDR_SKIP_RENDERED");
-    std::vector<double> rgb, mask;
-    if (want_rendered) {
-        size_t np = 0;
-        for (const auto& c : scene.views) np += size_t(c.width) * c.height;
-        rgb.resize(3 * np);
-        mask.resize(np);
-    }
     const cdr_reg_weights reg{weights.normal, weights.edge, weights.spec, weights.roug, weights.sigma1,
                               weights.sigma2};
     double bd[7] = {0, 0, 0, 0, 0, 0, 0};
-    d.check(cdr_total_loss(d.ctx, views.data(), n, &st, weights.rend, weights.lap, &reg,
-                           options.laplacian_mode == LaplacianMode::Uniform ? CDR_LAPLACIAN_UNIFORM
-                                                                             : CDR_LAPLACIAN_COTANGENT,
-                           options.use_target_masks ? 1 : 0, &lay, bd, res.grad.values.data(),
-                           want_rendered ? rgb.data() : nullptr, want_rendered ? mask.data() : nullptr, nullptr));
+    {
+        ShimTimer t2(2);
+        d.check(cdr_total_loss(d.ctx, views.data(), n, &st, weights.rend, weights.lap, &reg,
+                               options.laplacian_mode == LaplacianMode::Uniform ? CDR_LAPLACIAN_UNIFORM
+                                                                                 : CDR_LAPLACIAN_COTANGENT,
+                               options.use_target_masks ? 1 : 0, &lay, bd, res.grad.values.data(), nullptr,
+                               nullptr, nullptr));
+    }
     res.breakdown.total = bd[0];
     res.breakdown.rend = bd[1];
     res.breakdown.lap = bd[2];
@@ -399,15 +438,14 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
     res.breakdown.edge = bd[4];
     res.breakdown.spec = bd[5];
     res.breakdown.roug = bd[6];
-    if (want_rendered) {
-        size_t o = 0;
-        for (const auto& c : scene.views) {
+    if (want_rendered) {  // straight from the device arena into the returned images
+        ShimTimer t3(3);
+        res.rendered.reserve(scene.views.size());
+        for (int k = 0; k < n; ++k) {
+            const Camera& c = scene.views[k];
             Image img(c.width, c.height, true);
-            size_t np = size_t(c.width) * c.height;
-            std::memcpy(img.pixels.data(), rgb.data() + 3 * o, sizeof(double) * 3 * np);
-            std::memcpy(img.mask.data(), mask.data() + o, sizeof(double) * np);
+            d.check(cdr_get_rendered(d.ctx, k, reinterpret_cast<double*>(img.pixels.data()), img.mask.data()));
             res.rendered.push_back(std::move(img));
-            o += np;
         }
     }
     return res;

@@ -133,6 +133,7 @@ def load_library(path: str = LIB_PATH):
                                  C.POINTER(cdr_reg_weights), C.c_int32, C.c_int32, C.POINTER(cdr_layout), _d, _d,
                                  _d, _d, C.POINTER(cdr_stats)]
     L.cdr_regularisers.argtypes = [_vp, C.POINTER(cdr_reg_weights), C.POINTER(cdr_layout), _d, _d]
+    L.cdr_get_rendered.argtypes = [_vp, C.c_int32, _d, _d]
     L.cdr_self_intersects.argtypes = [_vp, _d, C.c_int32, _i, C.c_int32, _i, _i, C.c_int64,
                                       C.POINTER(C.c_int64)]
     L.cdr_get_grad.argtypes = [_vp, _d, C.c_int64]
@@ -462,6 +463,14 @@ class Renderer:
         v = C.c_double()
         self._chk(self.L.cdr_laplacian_loss(self.h, mode, lam, C.byref(v), _dp(g)))
         return v.value, g
+
+    def rendered(self, view):
+        """(rgb H x W x 3, mask H x W) of the last pass that rendered `view`."""
+        cam = self.cameras[view]
+        rgb = np.zeros((cam.height, cam.width, 3))
+        mask = np.zeros((cam.height, cam.width))
+        self._chk(self.L.cdr_get_rendered(self.h, view, _dp(rgb), _dp(mask)))
+        return rgb, mask
 
     def self_intersects(self, positions, triangles, want_pairs=False):
         """self_intersects (mesh.hpp:67) of any mesh (not necessarily this

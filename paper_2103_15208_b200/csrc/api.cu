@@ -956,6 +956,22 @@ int cdr_laplacian_loss(cdr_ctx* c, int32_t mode, double lambda, double* value, d
     API_END
 }
 
+int cdr_get_rendered(cdr_ctx* c, int32_t view, double* rgb, double* mask) {
+    API_BEGIN(c)
+    check_view(c, view);
+    const ViewData& v = c->views[view];
+    const size_t np = size_t(v.cam.W) * v.cam.H;
+    if (c->img.n < v.pix_off + np) throw ApiErr(CDR_ERR_INVALID_ARG, "view has not been rendered");
+    if (rgb)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(rgb, c->img.p + 3 * v.pix_off, sizeof(double) * 3 * np, cudaMemcpyDeviceToHost,
+                                       c->stream));
+    if (mask)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(mask, c->mask.p + v.pix_off, sizeof(double) * np, cudaMemcpyDeviceToHost,
+                                       c->stream));
+    sync(c);
+    API_END
+}
+
 int cdr_self_intersects(cdr_ctx* c, const double* positions, int32_t nv, const int32_t* triangles, int32_t nt,
                         int32_t* result, int32_t* pairs, int64_t cap, int64_t* n_pairs) {
     API_BEGIN(c)

@@ -274,3 +274,23 @@ def test_grad_overwrite_flag(sphere):
     assert rel_l2(g1, g0) <= 1e-12  # runs differ only by fp64 RED order
     _, g2, _, _ = r.loss_grad(views, st, lay, grad=junk.copy())
     assert rel_l2(g2 - 7.0, g0) <= 1e-12
+
+
+def test_get_rendered_matches_pass_outputs(sphere):
+    """cdr_get_rendered returns the images the last loss pass rendered."""
+    r, _ = _pair(sphere)
+    spp, seed = 4, 2
+    tg = targets_for(sphere, spp, seed, Oracle)
+    for k in range(len(sphere.cameras)):
+        r.set_target(k, tg[k])
+    lay = param_layout(sphere)
+    _, _, _, rend = r.loss_grad(np.arange(len(sphere.cameras)), RenderSettings(spp=spp, seed=seed), lay,
+                                want_rendered=True)
+    off = 0
+    for v, cam in enumerate(sphere.cameras):
+        n = cam.width * cam.height * 3
+        rgb, mask = r.rendered(v)
+        np.testing.assert_array_equal(rgb.ravel(), rend[off:off + n])
+        img, m2, _ = r.render(v, RenderSettings(spp=spp, seed=seed))
+        np.testing.assert_array_equal(mask, m2)
+        off += n
