@@ -50,7 +50,8 @@ enum {
     CDR_ERR_ERROR = 3,
     CDR_ERR_CUDA = 4,
     CDR_ERR_INVALID_ARG = 5,
-    CDR_ERR_NO_DEVICE = 6
+    CDR_ERR_NO_DEVICE = 6,
+    CDR_ERR_SELF_INTERSECTING = 7 /* -> collodiff::InputSelfIntersecting (errors.hpp) */
 };
 
 enum { CDR_PROBE_RADIANCE = 0, CDR_PROBE_COVERAGE = 1 };  /* diff_render.hpp:38 */
@@ -234,6 +235,9 @@ int cdr_regularisers(cdr_ctx* ctx, const cdr_reg_weights* reg, const cdr_layout*
                      double* values_out, double* grad_inout);
 
 int cdr_get_grad(cdr_ctx* ctx, double* grad_out, int64_t n);
+/* Replace the device gradient (n values, ParamLayout order): e.g. a gradient
+ * assembled elsewhere, for cdr_adam_step. */
+int cdr_set_grad(cdr_ctx* ctx, const double* grad, int64_t n);
 int cdr_grad_device_ptr(cdr_ctx* ctx, void** ptr, int64_t* n);
 
 /* cotangent_laplacian (laplacian.hpp:14-15) as CSC (Eigen's default storage):
@@ -260,6 +264,36 @@ int cdr_get_rendered(cdr_ctx* ctx, int32_t view, double* rgb_out, double* mask_o
 int cdr_self_intersects(cdr_ctx* ctx, const double* positions, int32_t n_vertices,
                         const int32_t* triangles, int32_t n_triangles, int32_t* result,
                         int32_t* pairs, int64_t cap, int64_t* n_pairs);
+
+/* ---- resident optimiser --------------------------------
+ * AdamConfig (optimize.hpp:13-18). */
+typedef struct cdr_adam_config {
+    double beta1, beta2, epsilon, lr_positions, lr_textures, lr_light;
+} cdr_adam_config;
+
+/* AdamState(layout, config) (optimize.hpp:20-28) on the device: m = v = 0, step 0. */
+int cdr_adam_init(cdr_ctx* ctx, const cdr_adam_config* config, const cdr_layout* layout);
+/* adam_step (adam.cpp:9-54) + apply (params.cpp:103-134) on the resident
+ * parameters, with the device gradient of the last cdr_loss_grad /
+ * cdr_total_loss. Texture and light segments are updated and clamped in place
+ * (the next pass renders them); the position segment is not applied: its
+ * displacement stays on the device for cdr_evolve and is copied to
+ * displacement_out (V x 3, nullable). CDR_ERR_NONFINITE (nothing updated) if a
+ * gradient value is not finite. */
+int cdr_adam_step(cdr_ctx* ctx, double* displacement_out, int64_t* step_out);
+/* Moments and step for checkpoints / coarse-to-fine carries (layout order). */
+int cdr_adam_get_state(cdr_ctx* ctx, double* m_out, double* v_out, int64_t* step_out);
+int cdr_adam_set_state(cdr_ctx* ctx, const double* m, const double* v, int64_t step);
+/* robust_evolve (evolve.cpp:19-53) on the device: positions += s * d for the
+ * largest s in {1, 1/2, ..., 2^-8} that keeps every triangle area > 1e-12 and
+ * the mesh free of self-intersections, else unchanged (s = 0). d = displacement
+ * (V x 3) or, when NULL, the one of the last cdr_adam_step. scale_out and
+ * positions_out (V x 3) are nullable. CDR_ERR_SELF_INTERSECTING if the current
+ * mesh already self-intersects (evolve.cpp:23). */
+int cdr_evolve(cdr_ctx* ctx, const double* displacement, double* scale_out, double* positions_out);
+/* pack (params.cpp:70-100): the resident positions, maps and light in
+ * ParamLayout order. */
+int cdr_get_params(cdr_ctx* ctx, const cdr_layout* layout, double* params_out);
 
 /* Multi-GPU view sharding: one context per GPU/rank, gradient all-reduce over
  * NCCL (loaded at run time). id is an ncclUniqueId (128 bytes). */

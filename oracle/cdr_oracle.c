@@ -1315,6 +1315,75 @@ int orc_self_intersects(const double* pos, int32_t nv, const int32_t* tris, int3
     return 0;
 }
 
+/* ---- adam_step (adam.cpp:9-54) and robust_evolve (evolve.cpp:19-53), SURVEY
+ * §8(f) row 3. cfg = beta1, beta2, epsilon, lr_positions, lr_textures,
+ * lr_light. m, v, *step updated in place; params_out = params with texture /
+ * light segments stepped and clamped; disp_out = V x 3 position deltas.
+ * Returns CDR_ERR_NONFINITE (nothing updated) on a non-finite gradient. */
+int orc_adam_step(const double* cfg, const cdr_layout* L, int64_t nv, int64_t n_tex, int64_t* step, double* m,
+                  double* v, const double* params, const double* grad, double* params_out, double* disp_out) {
+    for (int64_t i = 0; i < L->total; ++i)
+        if (!isfinite(grad[i])) return CDR_ERR_NONFINITE;
+    *step += 1;
+    const double c1 = 1.0 - pow(cfg[0], (double)*step), c2 = 1.0 - pow(cfg[1], (double)*step);
+    memcpy(params_out, params, sizeof(double) * (size_t)L->total);
+    for (int64_t i = 0; i < L->total; ++i) {
+        double lr = cfg[4], lo = 0.0, hi = 1.0;
+        int pos = 0;
+        if (i >= L->positions && i < L->positions + 3 * nv) { lr = cfg[3]; pos = 1; }
+        else if (i >= L->roughness && i < L->roughness + n_tex) lo = 0.01; /* kAlphaMin */
+        else if (L->light >= 0 && i >= L->light && i < L->light + 3) { lr = cfg[5]; hi = 1e30; }
+        double g = grad[i];
+        m[i] = cfg[0] * m[i] + (1.0 - cfg[0]) * g;
+        v[i] = cfg[1] * v[i] + (1.0 - cfg[1]) * g * g;
+        double mh = m[i] / c1, vh = v[i] / c2;
+        double delta = -lr * mh / (sqrt(vh) + cfg[2]);
+        if (pos) disp_out[i - L->positions] = delta;
+        else {
+            double x = params_out[i] + delta;
+            params_out[i] = x < lo ? lo : (hi < x ? hi : x);
+        }
+    }
+    return 0;
+}
+
+static double min_area(const double* pos, const int32_t* tris, int32_t nt) { /* evolve.cpp:11-15 */
+    double best = 1e300;
+    for (int f = 0; f < nt; ++f) {
+        d3 a = ld3(pos + 3 * (size_t)tris[3 * f]);
+        double ar = 0.5 * len3(cross3(sub3(ld3(pos + 3 * (size_t)tris[3 * f + 1]), a),
+                                      sub3(ld3(pos + 3 * (size_t)tris[3 * f + 2]), a)));
+        best = ar < best ? ar : best;
+    }
+    return best;
+}
+
+int orc_robust_evolve(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, const double* disp,
+                      double* pos_out, double* scale_out) {
+    int32_t r = 0;
+    orc_self_intersects(pos, nv, tris, nt, &r, NULL, 0, NULL);
+    if (r) return CDR_ERR_SELF_INTERSECTING;
+    memcpy(pos_out, pos, sizeof(double) * 3 * (size_t)nv);
+    *scale_out = 0.0;
+    int any = 0;
+    for (int64_t i = 0; i < 3 * (int64_t)nv; ++i) any |= disp[i] != 0;
+    if (!any) { *scale_out = 1.0; return 0; }
+    double* cand = (double*)malloc(sizeof(double) * 3 * ((size_t)nv + 1));
+    double s = 1.0;
+    for (int attempt = 0; attempt <= 8; ++attempt, s *= 0.5) {
+        for (int64_t i = 0; i < 3 * (int64_t)nv; ++i) cand[i] = pos[i] + disp[i] * s;
+        if (min_area(cand, tris, nt) <= 1e-12) continue;
+        orc_self_intersects(cand, nv, tris, nt, &r, NULL, 0, NULL);
+        if (!r) {
+            memcpy(pos_out, cand, sizeof(double) * 3 * (size_t)nv);
+            *scale_out = s;
+            break;
+        }
+    }
+    free(cand);
+    return 0;
+}
+
 /* build_adjacency (mesh.cpp:27-63): edges sorted by (min, max); faces in
  * ascending face order; f1 = -1 on boundary; -1 return = non-manifold. */
 typedef struct { int64_t key; int f; } ekey;

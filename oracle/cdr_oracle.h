@@ -85,6 +85,11 @@ int orc_triangles_intersect(const double* a0, const double* a1, const double* a2
                             const double* b1, const double* b2, double tol);
 int orc_self_intersects(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, int32_t* result,
                         int32_t* pairs, int64_t cap, int64_t* n_pairs);
+/* adam_step (adam.cpp:9-54) and robust_evolve (evolve.cpp:19-53). */
+int orc_adam_step(const double* cfg, const cdr_layout* L, int64_t nv, int64_t n_tex, int64_t* step, double* m,
+                  double* v, const double* params, const double* grad, double* params_out, double* disp_out);
+int orc_robust_evolve(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, const double* disp,
+                      double* pos_out, double* scale_out);
 double orc_tone_map(double v, double gamma);
 double orc_tone_map_derivative(double v, double gamma);
 int orc_project(const cdr_camera* cam, const double* p, double* q, double* depth);

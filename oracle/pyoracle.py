@@ -181,6 +181,40 @@ def triangles_intersect(a, b, tol=1e-10, ref=False):
     return bool(fn(*(dp(np.ascontiguousarray(x)) for x in (a[0], a[1], a[2], b[0], b[1], b[2])), tol))
 
 
+def adam_step(cfg, lay, nv, tex_wh, step, m, v, params, grad, ref=False):
+    """adam_step (adam.cpp:9-54): oracle (C) or the reference itself. cfg =
+    (beta1, beta2, epsilon, lr_positions, lr_textures, lr_light). Returns
+    (status, step, m, v, params_out, displacement V x 3)."""
+    m, v = np.array(m, dtype=np.float64), np.array(v, dtype=np.float64)
+    out, disp = np.zeros(lay["total"]), np.zeros((nv, 3))
+    st = C.c_int64(step)
+    cf = np.asarray(cfg, dtype=np.float64)
+    pr, gr = np.ascontiguousarray(params, dtype=np.float64), np.ascontiguousarray(grad, dtype=np.float64)
+    if ref:
+        L = C.CDLL(build_ref())
+        rc = L.ref_adam_step(dp(cf), nv, tex_wh[0], tex_wh[1], int(lay["light"] >= 0), C.byref(st), dp(m), dp(v),
+                             dp(pr), dp(gr), dp(out), dp(disp))
+    else:
+        L = C.CDLL(build_oracle())
+        cl = c_layout(lay)
+        rc = L.orc_adam_step(dp(cf), C.byref(cl), C.c_int64(nv), C.c_int64(tex_wh[0] * tex_wh[1]), C.byref(st),
+                             dp(m), dp(v), dp(pr), dp(gr), dp(out), dp(disp))
+    return rc, st.value, m, v, out, disp
+
+
+def robust_evolve(pos, tris, disp, ref=False):
+    """robust_evolve (evolve.cpp:19-53): (status, positions, applied scale)."""
+    L = C.CDLL(build_ref() if ref else build_oracle())
+    fn = L.ref_robust_evolve if ref else L.orc_robust_evolve
+    pos = np.ascontiguousarray(pos, dtype=np.float64)
+    tris = np.ascontiguousarray(tris, dtype=np.int32)
+    d = np.ascontiguousarray(disp, dtype=np.float64)
+    out = np.zeros_like(pos)
+    sc = C.c_double()
+    rc = fn(dp(pos), len(pos), ip(tris), len(tris), dp(d), dp(out), C.byref(sc))
+    return rc, out, sc.value
+
+
 def _regularisers(fn, handle, scene, w, chk):
     V, n = scene.mesh.V, scene.diffuse.shape[0] * scene.diffuse.shape[1]
     vals = np.zeros(4)

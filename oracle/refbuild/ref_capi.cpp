@@ -23,6 +23,7 @@
 #include "collodiff/losses.hpp"
 #include "collodiff/material.hpp"
 #include "collodiff/mesh.hpp"
+#include "collodiff/optimize.hpp"
 #include "collodiff/params.hpp"
 #include "collodiff/render.hpp"
 #include "collodiff/rng.hpp"
@@ -49,6 +50,7 @@ int fail(const std::exception& e) {
     g_err = e.what();
     if (dynamic_cast<const SizeMismatch*>(&e)) return CDR_ERR_SIZE_MISMATCH;
     if (dynamic_cast<const NonFiniteGradient*>(&e)) return CDR_ERR_NONFINITE;
+    if (dynamic_cast<const InputSelfIntersecting*>(&e)) return CDR_ERR_SELF_INTERSECTING;
     return CDR_ERR_ERROR;
 }
 
@@ -511,6 +513,68 @@ int ref_triangles_intersect(const double* a0, const double* a1, const double* a2
                             const double* b1, const double* b2, double tol) {
     auto v = [](const double* p) { return Vec3(p[0], p[1], p[2]); };
     return triangles_intersect(v(a0), v(a1), v(a2), v(b0), v(b1), v(b2), tol) ? 1 : 0;
+}
+
+// adam_step (adam.cpp:9-54) on a layout of nv vertices and tw x th maps
+// (ParamLayout::for_scene). cfg = beta1, beta2, epsilon, lr_positions,
+// lr_textures, lr_light; m, v, step updated in place.
+int ref_adam_step(const double* cfg, int32_t nv, int32_t tw, int32_t th, int32_t light, int64_t* step, double* m,
+                  double* v, const double* params, const double* grad, double* params_out, double* disp_out) {
+    GUARD({
+        Scene sc;
+        sc.mesh.positions.assign(nv, Vec3());
+        sc.maps.diffuse = Texture::constant(tw, th, 3, Vec3());
+        sc.maps.specular = Texture::constant(tw, th, 3, Vec3());
+        sc.maps.roughness = Texture::constant(tw, th, 1, Vec3());
+        auto layout = ParamLayout::for_scene(sc, light != 0);
+        AdamConfig c;
+        c.beta1 = cfg[0];
+        c.beta2 = cfg[1];
+        c.epsilon = cfg[2];
+        c.lr_positions = cfg[3];
+        c.lr_textures = cfg[4];
+        c.lr_light = cfg[5];
+        AdamState st(layout, c);
+        const size_t n = layout->total;
+        st.m.assign(m, m + n);
+        st.v.assign(v, v + n);
+        st.step = *step;
+        ParamVector pv;
+        pv.layout = layout;
+        pv.values.assign(params, params + n);
+        GradVector gv(layout);
+        gv.values.assign(grad, grad + n);
+        AdamStepResult out = adam_step(st, pv, gv);
+        std::memcpy(m, st.m.data(), n * sizeof(double));
+        std::memcpy(v, st.v.data(), n * sizeof(double));
+        *step = st.step;
+        std::memcpy(params_out, out.params.values.data(), n * sizeof(double));
+        for (size_t i = 0; i < out.displacement.size(); ++i) {
+            disp_out[3 * i] = out.displacement[i].x;
+            disp_out[3 * i + 1] = out.displacement[i].y;
+            disp_out[3 * i + 2] = out.displacement[i].z;
+        }
+    })
+}
+
+// robust_evolve (evolve.cpp:19-53)
+int ref_robust_evolve(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, const double* disp,
+                      double* pos_out, double* scale_out) {
+    GUARD({
+        Mesh m;
+        m.positions.resize(nv);
+        for (int i = 0; i < nv; ++i) m.positions[i] = Vec3(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]);
+        m.triangles.resize(nt);
+        for (int f = 0; f < nt; ++f) m.triangles[f] = {tris[3 * f], tris[3 * f + 1], tris[3 * f + 2]};
+        std::vector<Vec3> d(nv);
+        for (int i = 0; i < nv; ++i) d[i] = Vec3(disp[3 * i], disp[3 * i + 1], disp[3 * i + 2]);
+        Mesh out = robust_evolve(m, d, scale_out);
+        for (int i = 0; i < nv; ++i) {
+            pos_out[3 * i] = out.positions[i].x;
+            pos_out[3 * i + 1] = out.positions[i].y;
+            pos_out[3 * i + 2] = out.positions[i].z;
+        }
+    })
 }
 
 // total_loss (losses.cpp:244-297). weights[0..5] = rend, lap, normal, edge,

@@ -49,6 +49,10 @@ class NoDevice(CollodiffError):
     pass
 
 
+class InputSelfIntersecting(CollodiffError):
+    """collodiff::InputSelfIntersecting (errors.hpp:32-34)."""
+
+
 _d = C.POINTER(C.c_double)
 _i = C.POINTER(C.c_int32)
 _vp = C.c_void_p
@@ -65,6 +69,11 @@ class cdr_layout(C.Structure):
 
 
 CDR_FLAG_GRAD_OVERWRITE = 1
+
+
+class cdr_adam_config(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("epsilon", C.c_double),
+                ("lr_positions", C.c_double), ("lr_textures", C.c_double), ("lr_light", C.c_double)]
 
 
 class cdr_reg_weights(C.Structure):
@@ -90,7 +99,7 @@ SEGMENT_DTYPE = np.dtype([("v0", "<i4"), ("v1", "<i4"), ("p0", "<f8", 3), ("p1",
                           ("z0", "<f8"), ("z1", "<f8"), ("length_px", "<f8")])
 
 _ERRORS = {1: SizeMismatch, 2: NonFiniteGradient, 3: CollodiffError, 4: CollodiffError,
-           5: CollodiffError, 6: NoDevice}
+           5: CollodiffError, 6: NoDevice, 7: InputSelfIntersecting}
 
 _lib = None
 
@@ -134,9 +143,16 @@ def load_library(path: str = LIB_PATH):
                                  _d, _d, C.POINTER(cdr_stats)]
     L.cdr_regularisers.argtypes = [_vp, C.POINTER(cdr_reg_weights), C.POINTER(cdr_layout), _d, _d]
     L.cdr_get_rendered.argtypes = [_vp, C.c_int32, _d, _d]
+    L.cdr_adam_init.argtypes = [_vp, C.POINTER(cdr_adam_config), C.POINTER(cdr_layout)]
+    L.cdr_adam_step.argtypes = [_vp, _d, C.POINTER(C.c_int64)]
+    L.cdr_adam_get_state.argtypes = [_vp, _d, _d, C.POINTER(C.c_int64)]
+    L.cdr_adam_set_state.argtypes = [_vp, _d, _d, C.c_int64]
+    L.cdr_evolve.argtypes = [_vp, _d, C.POINTER(C.c_double), _d]
+    L.cdr_get_params.argtypes = [_vp, C.POINTER(cdr_layout), _d]
     L.cdr_self_intersects.argtypes = [_vp, _d, C.c_int32, _i, C.c_int32, _i, _i, C.c_int64,
                                       C.POINTER(C.c_int64)]
     L.cdr_get_grad.argtypes = [_vp, _d, C.c_int64]
+    L.cdr_set_grad.argtypes = [_vp, _d, C.c_int64]
     L.cdr_grad_device_ptr.argtypes = [_vp, C.POINTER(_vp), C.POINTER(C.c_int64)]
     L.cdr_laplacian_matrix.argtypes = [_vp, C.c_int32, _i, _i, _d, C.POINTER(C.c_int64)]
     L.cdr_laplacian_loss.argtypes = [_vp, C.c_int32, C.c_double, _d, _d]
@@ -191,6 +207,24 @@ class LossWeights:
 
     def c_reg(self):
         return cdr_reg_weights(self.normal, self.edge, self.spec, self.roug, self.sigma1, self.sigma2)
+
+
+@dataclass
+class AdamConfig:
+    """AdamConfig (optimize.hpp:13-18)."""
+    beta1: float = 0.9
+    beta2: float = 0.999
+    epsilon: float = 1e-8
+    lr_positions: float = 1e-3
+    lr_textures: float = 1e-2
+    lr_light: float = 1e-2
+
+    def c(self):
+        return cdr_adam_config(self.beta1, self.beta2, self.epsilon, self.lr_positions, self.lr_textures,
+                               self.lr_light)
+
+    def tuple(self):
+        return (self.beta1, self.beta2, self.epsilon, self.lr_positions, self.lr_textures, self.lr_light)
 
 
 def param_layout(scene: Scene, optimize_light: bool = False) -> dict:
@@ -464,6 +498,45 @@ class Renderer:
         self._chk(self.L.cdr_laplacian_loss(self.h, mode, lam, C.byref(v), _dp(g)))
         return v.value, g
 
+    # ---- resident optimiser: total_loss -> adam -> evolve
+    def adam_init(self, config: AdamConfig, layout):
+        """AdamState(layout, config) on the device (m = v = 0, step 0)."""
+        self._adam_layout = layout
+        self._chk(self.L.cdr_adam_init(self.h, C.byref(config.c()), C.byref(_clayout(layout))))
+
+    def adam_step(self, want_displacement=True):
+        """adam_step + apply on the resident parameters with the device gradient
+        of the last loss pass. Returns (displacement V x 3 or None, step)."""
+        disp = np.zeros((self.V, 3)) if want_displacement else None
+        step = C.c_int64()
+        self._chk(self.L.cdr_adam_step(self.h, _dp(disp), C.byref(step)))
+        return disp, step.value
+
+    def adam_state(self):
+        n = self._adam_layout["total"]
+        m, v, step = np.zeros(n), np.zeros(n), C.c_int64()
+        self._chk(self.L.cdr_adam_get_state(self.h, _dp(m), _dp(v), C.byref(step)))
+        return m, v, step.value
+
+    def set_adam_state(self, m, v, step):
+        self._chk(self.L.cdr_adam_set_state(self.h, _dp(np.ascontiguousarray(m, dtype=np.float64)),
+                                            _dp(np.ascontiguousarray(v, dtype=np.float64)), int(step)))
+
+    def evolve(self, displacement=None, want_positions=True):
+        """robust_evolve on the device (the displacement of the last adam_step
+        when None). Returns (applied scale, positions V x 3 or None)."""
+        d = None if displacement is None else np.ascontiguousarray(displacement, dtype=np.float64)
+        out = np.zeros((self.V, 3)) if want_positions else None
+        sc = C.c_double()
+        self._chk(self.L.cdr_evolve(self.h, _dp(d), C.byref(sc), _dp(out)))
+        return sc.value, out
+
+    def params(self, layout):
+        """pack (params.cpp:70-100) of the resident state."""
+        out = np.zeros(layout["total"])
+        self._chk(self.L.cdr_get_params(self.h, C.byref(_clayout(layout)), _dp(out)))
+        return out
+
     def rendered(self, view):
         """(rgb H x W x 3, mask H x W) of the last pass that rendered `view`."""
         cam = self.cameras[view]
@@ -503,6 +576,10 @@ class Renderer:
         out = np.zeros(n)
         self._chk(self.L.cdr_get_grad(self.h, _dp(out), n))
         return out
+
+    def set_grad(self, g):
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        self._chk(self.L.cdr_set_grad(self.h, _dp(g), len(g)))
 
     # ---------------------------------------------------------------- multi-GPU
     @staticmethod

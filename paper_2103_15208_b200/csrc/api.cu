@@ -345,6 +345,8 @@ int cdr_set_mesh(cdr_ctx* c, const double* positions, int32_t nv, const int32_t*
         }
     }
     c->E = int(c->h_edges.size() / 4);
+    ++c->topo_version;
+    c->adam_ready = false;  // a new vertex set: the optimiser state no longer matches
     cudaStream_t s = c->stream;
     h2d(c->pos, positions, 3 * size_t(nv), s);
     c->has_uv = uvs != nullptr;
@@ -913,6 +915,16 @@ int cdr_get_grad(cdr_ctx* c, double* out, int64_t n) {
     API_END
 }
 
+int cdr_set_grad(cdr_ctx* c, const double* g, int64_t n) {
+    API_BEGIN(c)
+    if (n < 0 || (n > 0 && !g)) throw ApiErr(CDR_ERR_INVALID_ARG, "bad gradient");
+    c->grad.ensure(std::max<int64_t>(1, n));
+    c->grad_n = n;
+    if (n > 0) CDR_CUDA_CHECK(cudaMemcpyAsync(c->grad.p, g, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    sync(c);
+    API_END
+}
+
 int cdr_grad_device_ptr(cdr_ctx* c, void** ptr, int64_t* n) {
     if (!c || !ptr) return CDR_ERR_INVALID_ARG;
     *ptr = c->grad.p;
@@ -1022,6 +1034,166 @@ int cdr_self_intersects(cdr_ctx* c, const double* positions, int32_t nv, const i
         if (n_pairs) *n_pairs = n;
     }
     *result = n > 0 ? 1 : 0;
+    API_END
+}
+
+// ---- resident optimiser (optimize.cu) --------------------------------------
+namespace {
+cdr_ctx* geometry_ctx(cdr_ctx* c) {
+    if (!c->geo) {
+        const int rc = cdr_create(c->device, &c->geo);
+        if (rc != CDR_OK) throw ApiErr(rc, "cannot create the geometry context");
+    }
+    return c->geo;
+}
+
+// geo <- c's topology (device copy), tracked by version
+void sync_topology(cdr_ctx* c, cdr_ctx* g) {
+    if (g->topo_version == c->topo_version && g->T == c->T && g->V == c->V && g->h_tris.size() == c->h_tris.size())
+        return;
+    g->V = c->V;
+    g->T = c->T;
+    g->h_tris = c->h_tris;
+    g->tris.ensure(std::max<size_t>(1, 3 * size_t(c->T)));
+    CDR_CUDA_CHECK(cudaMemcpyAsync(g->tris.p, c->tris.p, sizeof(int32_t) * 3 * size_t(c->T), cudaMemcpyDeviceToDevice,
+                                   g->stream));
+    g->pos.ensure(std::max<size_t>(1, 3 * size_t(c->V)));
+    g->topo_version = c->topo_version;
+}
+
+// self_intersects of g's mesh (positions already in g->pos)
+bool geo_self_intersects(cdr_ctx* g) {
+    launch_bvh(g, 0.0);
+    return launch_self_intersect(g, nullptr, 0) > 0;
+}
+}  // namespace
+
+int cdr_adam_init(cdr_ctx* c, const cdr_adam_config* cfg, const cdr_layout* lay) {
+    API_BEGIN(c)
+    if (!cfg) throw ApiErr(CDR_ERR_INVALID_ARG, "config is required");
+    check_layout(c, lay);
+    c->adam_cfg = *cfg;
+    c->adam_lay = *lay;
+    c->adam_step = 0;
+    const size_t n = std::max<int64_t>(1, lay->total);
+    c->adam_m.ensure(n);
+    c->adam_v.ensure(n);
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->adam_m.p, 0, sizeof(double) * n, c->stream));
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->adam_v.p, 0, sizeof(double) * n, c->stream));
+    c->adam_disp.ensure(std::max<size_t>(1, 3 * size_t(c->V)));
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->adam_disp.p, 0, sizeof(double) * std::max<size_t>(1, 3 * size_t(c->V)),
+                                   c->stream));
+    c->adam_light.ensure(3);
+    c->adam_ready = true;
+    sync(c);
+    API_END
+}
+
+int cdr_adam_step(cdr_ctx* c, double* disp_out, int64_t* step_out) {
+    API_BEGIN(c)
+    if (!c->adam_ready) throw ApiErr(CDR_ERR_INVALID_ARG, "cdr_adam_init first (or again after cdr_set_mesh)");
+    const cdr_layout& L = c->adam_lay;
+    if (c->grad_n != L.total) throw SizeMismatchErr("adam state/params/grad layout mismatch");  // adam.cpp:10-11
+    if (any_nonfinite(c, c->grad.p, L.total))
+        throw ApiErr(CDR_ERR_NONFINITE, "non-finite gradient entering adam");  // adam.cpp:12-13
+    c->adam_step += 1;
+    const double corr1 = 1.0 - std::pow(c->adam_cfg.beta1, double(c->adam_step));
+    const double corr2 = 1.0 - std::pow(c->adam_cfg.beta2, double(c->adam_step));
+    CDR_CUDA_CHECK(cudaMemcpyAsync(c->adam_light.p, c->light, sizeof(double) * 3, cudaMemcpyHostToDevice, c->stream));
+    launch_adam(c, c->grad.p, corr1, corr2);
+    if (L.light >= 0)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(c->light, c->adam_light.p, sizeof(double) * 3, cudaMemcpyDeviceToHost,
+                                       c->stream));
+    if (c->tw > 0) launch_pack_textures(c, c->map_d.p, c->map_s.p, c->map_r.p, c->tw * c->th);
+    if (disp_out)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(disp_out, c->adam_disp.p, sizeof(double) * 3 * size_t(c->V),
+                                       cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (step_out) *step_out = c->adam_step;
+    API_END
+}
+
+int cdr_adam_get_state(cdr_ctx* c, double* m, double* v, int64_t* step) {
+    API_BEGIN(c)
+    if (!c->adam_ready) throw ApiErr(CDR_ERR_INVALID_ARG, "no optimiser state");
+    const size_t n = size_t(c->adam_lay.total);
+    if (m) CDR_CUDA_CHECK(cudaMemcpyAsync(m, c->adam_m.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    if (v) CDR_CUDA_CHECK(cudaMemcpyAsync(v, c->adam_v.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    if (step) *step = c->adam_step;
+    API_END
+}
+
+int cdr_adam_set_state(cdr_ctx* c, const double* m, const double* v, int64_t step) {
+    API_BEGIN(c)
+    if (!c->adam_ready) throw ApiErr(CDR_ERR_INVALID_ARG, "cdr_adam_init first");
+    const size_t n = size_t(c->adam_lay.total);
+    if (m) CDR_CUDA_CHECK(cudaMemcpyAsync(c->adam_m.p, m, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    if (v) CDR_CUDA_CHECK(cudaMemcpyAsync(c->adam_v.p, v, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    c->adam_step = step;
+    sync(c);
+    API_END
+}
+
+int cdr_evolve(cdr_ctx* c, const double* disp_host, double* scale_out, double* positions_out) {
+    API_BEGIN(c)
+    if (scale_out) *scale_out = 0.0;
+    cdr_ctx* g = geometry_ctx(c);
+    sync(c);
+    sync_topology(c, g);
+    const int64_t n = 3 * int64_t(c->V);
+    const double* disp = c->adam_disp.p;
+    if (disp_host) {
+        c->grad_tmp.ensure(std::max<int64_t>(1, n));
+        CDR_CUDA_CHECK(cudaMemcpyAsync(c->grad_tmp.p, disp_host, sizeof(double) * n, cudaMemcpyHostToDevice, g->stream));
+        disp = c->grad_tmp.p;
+    } else if (!c->adam_ready) {
+        throw ApiErr(CDR_ERR_INVALID_ARG, "no displacement: pass one or run cdr_adam_step");
+    }
+    // evolve.cpp:23: the input must be intersection-free
+    CDR_CUDA_CHECK(cudaMemcpyAsync(g->pos.p, c->pos.p, sizeof(double) * n, cudaMemcpyDeviceToDevice, g->stream));
+    if (geo_self_intersects(g)) throw ApiErr(CDR_ERR_SELF_INTERSECTING, "input mesh self-intersects");
+    double applied = 0.0;
+    if (!any_nonzero(g, disp, n)) {
+        applied = 1.0;  // evolve.cpp:26-35
+    } else {
+        double s = 1.0;
+        for (int attempt = 0; attempt <= 8; ++attempt, s *= 0.5) {  // evolve.cpp:39-48
+            launch_candidate(g, c->pos.p, disp, s, g->pos.p);
+            if (min_triangle_area(g, g->pos.p) <= 1e-12) continue;
+            if (!geo_self_intersects(g)) {
+                CDR_CUDA_CHECK(cudaMemcpyAsync(c->pos.p, g->pos.p, sizeof(double) * n, cudaMemcpyDeviceToDevice,
+                                               g->stream));
+                CDR_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+                c->geometry_dirty = true;
+                applied = s;
+                break;
+            }
+        }
+    }
+    CDR_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+    if (positions_out)
+        CDR_CUDA_CHECK(cudaMemcpy(positions_out, c->pos.p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+    if (scale_out) *scale_out = applied;
+    API_END
+}
+
+int cdr_get_params(cdr_ctx* c, const cdr_layout* lay, double* out) {
+    API_BEGIN(c)
+    check_layout(c, lay);
+    if (!out) throw ApiErr(CDR_ERR_INVALID_ARG, "params_out is required");
+    const size_t nt = size_t(c->tw) * c->th;
+    auto d2h = [&](int64_t off, const double* src, size_t n) {
+        if (off >= 0 && n)
+            CDR_CUDA_CHECK(cudaMemcpyAsync(out + off, src, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    };
+    d2h(lay->positions, c->pos.p, 3 * size_t(c->V));
+    d2h(lay->diffuse, c->map_d.p, 3 * nt);
+    d2h(lay->specular, c->map_s.p, 3 * nt);
+    d2h(lay->roughness, c->map_r.p, nt);
+    sync(c);
+    if (lay->light >= 0)
+        for (int i = 0; i < 3; ++i) out[lay->light + i] = c->light[i];
     API_END
 }
 

@@ -70,7 +70,14 @@ struct Timer {
 
 struct cdr_ctx {
     int device = 0;
-    cdr_ctx* geo = nullptr;  // geometry-only context of cdr_self_intersects (lazy)
+    cdr_ctx* geo = nullptr;  // geometry-only context of cdr_self_intersects / cdr_evolve (lazy)
+    uint64_t topo_version = 0;  // bumped by cdr_set_mesh; geo->topo_version = the copy it holds
+    // resident optimiser (optimize.cu): AdamState (optimize.hpp:20-28) on the device
+    bool adam_ready = false;
+    cdr_adam_config adam_cfg{};
+    cdr_layout adam_lay{};
+    int64_t adam_step = 0;
+    cdr::DBuf<double> adam_m, adam_v, adam_disp, adam_light;
     cdr::DBuf<int2> si_pairs;
     cudaStream_t stream = nullptr;
     std::string err;

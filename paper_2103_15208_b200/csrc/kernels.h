@@ -38,6 +38,12 @@ void launch_bvh(cdr_ctx* c, double cam_abs_max);  // bbox + t_min + LBVH (no nor
 // the number of intersecting pairs (early exit after the first when pairs ==
 // nullptr); pairs (f < g) written up to cap, in no particular order.
 long long launch_self_intersect(cdr_ctx* c, int2* pairs, long long cap);
+// optimize.cu: resident adam_step / robust_evolve building blocks
+bool any_nonfinite(cdr_ctx* c, const double* g, int64_t n);
+bool any_nonzero(cdr_ctx* c, const double* d, int64_t n);
+void launch_adam(cdr_ctx* c, const double* grad, double corr1, double corr2);
+double min_triangle_area(cdr_ctx* c, const double* pos);  // over c's triangles, positions `pos`
+void launch_candidate(cdr_ctx* c, const double* pos, const double* disp, double s, double* out);
 
 // render.cu — fused per-sample kernel. Modes:
 //   kTrace     primary-ray generation + LBVH traversal + shading (render.cpp:35-64)

@@ -9,7 +9,8 @@ boundary gradients, silhouette segments, the Laplacian (CSC, value, gradient)
 the hot subset of total_loss (loss terms + gradient), the four mesh/material
 regularisers at two weight sets (REG_WEIGHTS) and total_loss with every term
 at the reference default weights (LossWeights, losses.hpp:14-23); and
-selfint.npz: self_intersects pairs of clean, broken and noisy meshes.
+selfint.npz: self_intersects pairs of clean, broken and noisy meshes;
+optimize.npz: adam_step and robust_evolve cases.
 """
 import os
 import sys
@@ -19,7 +20,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-from oracle.pyoracle import RefLib, layout_for, ref_self_intersects  # noqa: E402
+from oracle.pyoracle import RefLib, adam_step, layout_for, ref_self_intersects, robust_evolve  # noqa: E402
 from paper_2103_15208_b200 import scenes as S  # noqa: E402
 
 # (normal, edge, spec, roug, sigma1, sigma2): the reference defaults, then a
@@ -97,7 +98,45 @@ def make_selfint():
     np.savez_compressed(os.path.join(HERE, "selfint.npz"), names=np.array(sorted(selfint_cases())), **out)
 
 
+ADAM_CFG = (0.9, 0.999, 1e-8, 2e-3, 1e-2, 5e-2)
+
+
+def make_optimize():
+    """adam_step (adam.cpp:9-54) and robust_evolve (evolve.cpp:19-53) cases."""
+    rng = np.random.default_rng(21)
+    out = {"adam_cfg": np.array(ADAM_CFG)}
+    sc = S.make_scene(S.icosphere(2), 8, 1, 16)
+    for light in (0, 1):
+        lay = layout_for(sc, optimize_light=bool(light))
+        n, V = lay["total"], sc.mesh.V
+        params = rng.uniform(-0.05, 1.05, n)  # some outside [0, 1]: the clamps
+        grad = rng.normal(0, 1, n)
+        grad[rng.uniform(size=n) < 0.2] = 0.0
+        m, v = rng.normal(0, 0.1, n), rng.uniform(0, 0.1, n)
+        for step in (0, 6):
+            rc, st, m2, v2, p2, d2 = adam_step(ADAM_CFG, lay, V, (8, 8), step, m, v, params, grad, ref=True)
+            k = f"adam_l{light}_s{step}"
+            out.update({f"{k}_params": params, f"{k}_grad": grad, f"{k}_m": m, f"{k}_v": v, f"{k}_m2": m2,
+                        f"{k}_v2": v2, f"{k}_p2": p2, f"{k}_d2": d2, f"{k}_step2": np.array(st)})
+    m = S.blob(4)
+    out["evolve_pos"], out["evolve_tris"] = m.positions, m.triangles
+    for k, sd in enumerate((0.0, 0.002, 0.02, 0.08, 0.5, 3.0, 40.0)):
+        d = rng.normal(0, sd, m.positions.shape)
+        rc, pos, scale = robust_evolve(m.positions, m.triangles, d, ref=True)
+        out.update({f"evolve{k}_d": d, f"evolve{k}_pos": pos, f"evolve{k}_scale": np.array(scale),
+                    f"evolve{k}_rc": np.array(rc)})
+        print("evolve", k, sd, rc, scale)
+    p = S.icosphere(2)
+    bad = p.positions.copy()
+    bad[0] = -bad[0] * 1.2
+    rc, _, _ = robust_evolve(bad, p.triangles, np.zeros_like(bad), ref=True)
+    out.update({"evolve_bad_pos": bad, "evolve_bad_tris": p.triangles, "evolve_bad_rc": np.array(rc)})
+    print("evolve bad input", rc)
+    np.savez_compressed(os.path.join(HERE, "optimize.npz"), **out)
+
+
 if __name__ == "__main__":
     for n, c in CASES.items():
         make(n, c)
     make_selfint()
+    make_optimize()

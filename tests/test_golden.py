@@ -11,8 +11,8 @@ from oracle.pyoracle import Oracle, layout_for
 from paper_2103_15208_b200 import scenes as S
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-# scene fixtures (selfint.npz holds meshes only: tests/test_selfint.py)
-FIXTURES = sorted(f for f in glob.glob(os.path.join(HERE, "*.npz")) if not f.endswith("selfint.npz"))
+# scene fixtures (selfint.npz / optimize.npz: tests/test_selfint.py, tests/test_optimize.py)
+FIXTURES = sorted(f for f in glob.glob(os.path.join(HERE, "*.npz")) if os.path.basename(f) not in ("selfint.npz", "optimize.npz"))
 
 
 def load(path):
