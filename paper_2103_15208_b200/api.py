@@ -464,6 +464,22 @@ class Renderer:
         keys = ("total", "rend", "lap", "normal", "edge", "spec", "roug")
         return dict(zip(keys, bd.tolist())), g, rendered
 
+    def total_loss_device(self, views, settings: RenderSettings, layout, weights=None, laplacian_mode=0,
+                          use_target_masks=False):
+        """cdr_total_loss over `views` (slots) with the targets already set and
+        the gradient left on the device (for adam_step): the resident form of
+        total_loss. Returns (breakdown dict, stats)."""
+        w = weights if weights is not None else LossWeights()
+        views = np.ascontiguousarray(views, dtype=np.int32)
+        st = settings.c()
+        bd = np.zeros(7)
+        stats = cdr_stats()
+        self._chk(self.L.cdr_total_loss(self.h, _ip(views), len(views), C.byref(st), w.rend, w.lap,
+                                        C.byref(w.c_reg()), laplacian_mode, int(use_target_masks),
+                                        C.byref(_clayout(layout)), _dp(bd), None, None, None, C.byref(stats)))
+        keys = ("total", "rend", "lap", "normal", "edge", "spec", "roug")
+        return dict(zip(keys, bd.tolist())), stats
+
     def regularisers(self, weights, layout, grad=None, device_only=False):
         """normal_consistency / edge_length / specular_correlation / roughness_tv
         (losses.cpp:80-238). Returns ({normal, edge, spec, roug}, grad) with the
