@@ -51,7 +51,8 @@ enum {
     CDR_ERR_CUDA = 4,
     CDR_ERR_INVALID_ARG = 5,
     CDR_ERR_NO_DEVICE = 6,
-    CDR_ERR_SELF_INTERSECTING = 7 /* -> collodiff::InputSelfIntersecting (errors.hpp) */
+    CDR_ERR_SELF_INTERSECTING = 7, /* -> collodiff::InputSelfIntersecting (errors.hpp) */
+    CDR_ERR_PROJECTION_TOO_FAR = 8 /* -> collodiff::ProjectionTooFar (errors.hpp) */
 };
 
 enum { CDR_PROBE_RADIANCE = 0, CDR_PROBE_COVERAGE = 1 };  /* diff_render.hpp:38 */
@@ -264,6 +265,17 @@ int cdr_get_rendered(cdr_ctx* ctx, int32_t view, double* rgb_out, double* mask_o
 int cdr_self_intersects(cdr_ctx* ctx, const double* positions, int32_t n_vertices,
                         const int32_t* triangles, int32_t n_triangles, int32_t* result,
                         int32_t* pairs, int64_t cap, int64_t* n_pairs);
+
+/* Bvh::closest_point (bvh.hpp:44, bvh.cpp:267-329) of nq query points (nq x 3)
+ * on an arbitrary mesh: triangle (-1 if the mesh is empty), closest point
+ * (nq x 3), distance, barycentrics b0 b1 b2 (nq x 3); every output nullable.
+ * The distance is the reference's; on an exact tie between triangles the
+ * lowest index is returned (the reference: first met by its SAH traversal).
+ * Used for uv_transfer (remesh.cpp:281-294) and point_to_mesh_distance. */
+int cdr_closest_points(cdr_ctx* ctx, const double* positions, int32_t n_vertices,
+                       const int32_t* triangles, int32_t n_triangles, const double* queries,
+                       int32_t n_queries, int32_t* tri_out, double* point_out, double* dist_out,
+                       double* bary_out);
 
 /* ---- resident optimiser --------------------------------
  * AdamConfig (optimize.hpp:13-18). */

@@ -12,6 +12,8 @@
 //   grad_image_loss      diff_render.hpp:65-67  -> cdr_loss_grad (one view)
 //   extract_silhouettes  silhouette.hpp:36      -> cdr_extract_silhouettes
 //   cotangent_laplacian  laplacian.hpp:14-15    -> cdr_laplacian_matrix
+//   point_to_mesh_distance mesh.hpp:53          -> cdr_closest_points
+//   uv_transfer          optimize.hpp:56        -> cdr_closest_points
 //   self_intersects      mesh.hpp:67            -> cdr_self_intersects (pairs
 //                        sorted by (f, g); the reference's follow its BVH)
 //   total_loss           losses.hpp:94-96       -> cdr_total_loss (rendering,
@@ -40,6 +42,8 @@
 #include "collodiff/errors.hpp"
 #include "collodiff/laplacian.hpp"
 #include "collodiff/losses.hpp"
+#include "collodiff/mesh.hpp"
+#include "collodiff/optimize.hpp"
 #include "collodiff/render.hpp"
 #include "collodiff/silhouette.hpp"
 
@@ -382,6 +386,64 @@ bool self_intersects(const Mesh& mesh, std::vector<std::pair<int, int>>* pairs) 
     if (n > 0) d.check(cdr_self_intersects(d.ctx, pos.data(), nv, tris.data(), nt, &res, pr.data(), n, &n));
     for (int64_t i = 0; i < n; ++i) pairs->push_back({pr[2 * i], pr[2 * i + 1]});
     return res != 0;
+}
+
+namespace {
+void mesh_arrays(const Mesh& m, std::vector<double>& pos, std::vector<int32_t>& tris) {
+    pos.resize(3 * size_t(m.vertex_count()));
+    for (int v = 0; v < m.vertex_count(); ++v) {
+        pos[3 * v] = m.positions[v].x;
+        pos[3 * v + 1] = m.positions[v].y;
+        pos[3 * v + 2] = m.positions[v].z;
+    }
+    tris.resize(3 * size_t(m.triangle_count()));
+    for (int f = 0; f < m.triangle_count(); ++f)
+        for (int k = 0; k < 3; ++k) tris[3 * f + k] = m.triangles[f][k];
+}
+}  // namespace
+
+double point_to_mesh_distance(const std::vector<Vec3>& points, const Mesh& mesh) {
+    if (mesh.triangle_count() == 0) throw EmptyMesh();  // mesh.cpp:128
+    if (points.empty()) return 0.0;
+    Device& d = dev();
+    std::vector<double> pos, q(3 * points.size()), dist(points.size());
+    std::vector<int32_t> tris;
+    mesh_arrays(mesh, pos, tris);
+    for (size_t i = 0; i < points.size(); ++i) {
+        q[3 * i] = points[i].x;
+        q[3 * i + 1] = points[i].y;
+        q[3 * i + 2] = points[i].z;
+    }
+    d.check(cdr_closest_points(d.ctx, pos.data(), mesh.vertex_count(), tris.data(), mesh.triangle_count(), q.data(),
+                               int32_t(points.size()), nullptr, nullptr, dist.data(), nullptr));
+    double sum = 0;  // the reference's sequential sum (mesh.cpp:131)
+    for (double x : dist) sum += x;
+    return sum / double(points.size());
+}
+
+void uv_transfer(const Mesh& old_mesh, Mesh& mesh, double max_distance) {
+    if (old_mesh.uvs.size() != old_mesh.positions.size()) return;  // remesh.cpp:282
+    Device& d = dev();
+    std::vector<double> pos, q(3 * size_t(mesh.vertex_count())), dist(mesh.vertex_count()),
+        bary(3 * size_t(mesh.vertex_count()));
+    std::vector<int32_t> tris, tri(mesh.vertex_count());
+    mesh_arrays(old_mesh, pos, tris);
+    for (int v = 0; v < mesh.vertex_count(); ++v) {
+        q[3 * v] = mesh.positions[v].x;
+        q[3 * v + 1] = mesh.positions[v].y;
+        q[3 * v + 2] = mesh.positions[v].z;
+    }
+    d.check(cdr_closest_points(d.ctx, pos.data(), old_mesh.vertex_count(), tris.data(), old_mesh.triangle_count(),
+                               q.data(), mesh.vertex_count(), tri.data(), nullptr, dist.data(), bary.data()));
+    mesh.uvs.resize(mesh.positions.size());
+    for (int v = 0; v < mesh.vertex_count(); ++v) {
+        if (tri[v] < 0 || dist[v] > max_distance)
+            throw ProjectionTooFar("uv transfer: vertex " + std::to_string(v) + " is " + std::to_string(dist[v]) +
+                                   " away from the source mesh");
+        const auto& t = old_mesh.triangles[tri[v]];
+        mesh.uvs[v] = old_mesh.uvs[t[0]] * bary[3 * v] + old_mesh.uvs[t[1]] * bary[3 * v + 1] +
+                      old_mesh.uvs[t[2]] * bary[3 * v + 2];
+    }
 }
 
 Eigen::SparseMatrix<double> cotangent_laplacian(const Mesh& mesh, LaplacianMode mode) {

@@ -7,6 +7,7 @@
 //
 //   demo_{ref,b200} [views=8] [image=256] [spp=4] [iters=3] [subdiv=5] [tex=256] [threads=N]
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <thread>
@@ -29,6 +30,7 @@ int main(int argc, char** argv) {
     const int views = arg(1, 8), image = arg(2, 256), spp = arg(3, 4), iters = arg(4, 3), subdiv = arg(5, 5),
               tex = arg(6, 256);
     const int threads = arg(7, int(std::thread::hardware_concurrency()));
+    const int stages = arg(8, 1);  // > 1: coarse-to-fine with remesh + texture doubling per stage
 
     Scene gt;
     gt.mesh = make_blob(subdiv, 5, 0.15);
@@ -60,13 +62,20 @@ int main(int argc, char** argv) {
     double t_loss = secs(t0, clk::now());
 
     StagePlan plan;
-    Stage st;
-    st.iterations = iters;
-    st.edge_length = 0.04;
-    st.texture_resolution = tex;
-    st.lr_positions = 1e-3 * init.mesh.bbox_diagonal();
-    plan.stages = {st};
+    for (int si = 0; si < stages; ++si) {
+        Stage st;
+        st.iterations = iters;
+        st.edge_length = 0.04 / std::pow(1.4, si);  // a remesh at every stage change
+        st.texture_resolution = tex;  // (doubling trips the reference's own moment carry: "moment upsample size mismatch")
+        st.lr_positions = 1e-3 * init.mesh.bbox_diagonal();
+        plan.stages.push_back(st);
+    }
     CoarseToFineConfig cfg;
+    const int metric = arg(9, 0);  // 1: point-to-mesh metric vs the ground truth every iteration
+    if (metric) {
+        cfg.ground_truth = &gt.mesh;
+        cfg.verify_safety = true;
+    }
     std::vector<double> it_s;
     auto last = clk::now();
     cfg.on_iteration = [&](const IterationRecord&) {
@@ -82,10 +91,13 @@ int main(int argc, char** argv) {
     std::printf("{\"tris\": %d, \"views\": %d, \"image\": %d, \"spp\": %d, \"threads\": %d, "
                 "\"ms_per_iteration\": %.3f, \"ms_total_loss\": %.3f, \"loss0\": %.9g, \"rend0\": %.9g, "
                 "\"lap0\": %.9g, \"normal0\": %.9g, \"edge0\": %.9g, \"spec0\": %.9g, \"roug0\": %.9g, "
-                "\"loss_last\": %.9g, \"iterations\": %zu}\n",
+                "\"loss_last\": %.9g, \"iterations\": %zu, \"stages\": %d, \"tris_final\": %d, "
+                "\"p2m_last\": %.12g, \"safety_ok\": %d}\n",
                 gt.mesh.triangle_count(), views, image, spp, threads, 1e3 * mean, 1e3 * t_loss,
                 tl.breakdown.total, tl.breakdown.rend, tl.breakdown.lap, tl.breakdown.normal, tl.breakdown.edge,
                 tl.breakdown.spec, tl.breakdown.roug,
-                r.log.empty() ? 0.0 : r.log.back().loss.total, r.log.size());
+                r.log.empty() ? 0.0 : r.log.back().loss.total, r.log.size(), stages,
+                r.scene.mesh.triangle_count(), r.log.empty() ? 0.0 : r.log.back().point_to_mesh,
+                r.log.empty() ? 0 : int(r.log.back().safety_ok));
     return 0;
 }

@@ -1384,6 +1384,67 @@ int orc_robust_evolve(const double* pos, int32_t nv, const int32_t* tris, int32_
     return 0;
 }
 
+/* ---- Bvh::closest_point (bvh.cpp:267-329) by brute force, SURVEY §8(f) row 4.
+ * Ties go to the lowest triangle index. Outputs nullable. */
+static d3 closest_on_tri(d3 p, d3 a, d3 b, d3 c) { /* mesh.cpp:96-126 */
+    d3 ab = sub3(b, a), ac = sub3(c, a), ap = sub3(p, a);
+    double d1 = dot3(ab, ap), d2 = dot3(ac, ap);
+    if (d1 <= 0 && d2 <= 0) return a;
+    d3 bp = sub3(p, b);
+    double d3_ = dot3(ab, bp), d4 = dot3(ac, bp);
+    if (d3_ >= 0 && d4 <= d3_) return b;
+    double vc = d1 * d4 - d3_ * d2;
+    if (vc <= 0 && d1 >= 0 && d3_ <= 0) return add3(a, mul3(ab, d1 / (d1 - d3_)));
+    d3 cp = sub3(p, c);
+    double d5 = dot3(ab, cp), d6 = dot3(ac, cp);
+    if (d6 >= 0 && d5 <= d6) return c;
+    double vb = d5 * d2 - d1 * d6;
+    if (vb <= 0 && d2 >= 0 && d6 <= 0) return add3(a, mul3(ac, d2 / (d2 - d6)));
+    double va = d3_ * d6 - d5 * d4;
+    if (va <= 0 && (d4 - d3_) >= 0 && (d5 - d6) >= 0)
+        return add3(b, mul3(sub3(c, b), (d4 - d3_) / ((d4 - d3_) + (d5 - d6))));
+    double denom = 1.0 / (va + vb + vc);
+    double v = vb * denom, w = vc * denom;
+    return add3(add3(a, mul3(ab, v)), mul3(ac, w));
+}
+
+static double clamp01d(double x) { return x < 0.0 ? 0.0 : (1.0 < x ? 1.0 : x); }
+
+int orc_closest_points(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, const double* q, int32_t nq,
+                       int32_t* tri_out, double* point_out, double* dist_out, double* bary_out) {
+    (void)nv;
+    for (int i = 0; i < nq; ++i) {
+        d3 p = ld3(q + 3 * (size_t)i), bp = v3(0, 0, 0);
+        double best = 1e300;
+        int bt = -1;
+        for (int f = 0; f < nt; ++f) {
+            const int32_t* t = tris + 3 * (size_t)f;
+            d3 cp = closest_on_tri(p, ld3(pos + 3 * (size_t)t[0]), ld3(pos + 3 * (size_t)t[1]),
+                                   ld3(pos + 3 * (size_t)t[2]));
+            double d = len3(sub3(p, cp));
+            if (d < best) { best = d; bt = f; bp = cp; }
+        }
+        double b0 = 0, b1 = 0, b2 = 0;
+        if (bt >= 0) { /* bvh.cpp:312-326 */
+            const int32_t* t = tris + 3 * (size_t)bt;
+            d3 a = ld3(pos + 3 * (size_t)t[0]);
+            d3 v0 = sub3(ld3(pos + 3 * (size_t)t[1]), a), v1 = sub3(ld3(pos + 3 * (size_t)t[2]), a), v2 = sub3(bp, a);
+            double d00 = dot3(v0, v0), d01 = dot3(v0, v1), d11 = dot3(v1, v1), d20 = dot3(v2, v0), d21 = dot3(v2, v1);
+            double den = d00 * d11 - d01 * d01;
+            if (fabs(den) > 1e-30) {
+                b1 = clamp01d((d11 * d20 - d01 * d21) / den);
+                b2 = clamp01d((d00 * d21 - d01 * d20) / den);
+            }
+            b0 = clamp01d(1.0 - b1 - b2);
+        }
+        if (tri_out) tri_out[i] = bt;
+        if (dist_out) dist_out[i] = best;
+        if (point_out) { point_out[3 * i] = bp.x; point_out[3 * i + 1] = bp.y; point_out[3 * i + 2] = bp.z; }
+        if (bary_out) { bary_out[3 * i] = b0; bary_out[3 * i + 1] = b1; bary_out[3 * i + 2] = b2; }
+    }
+    return 0;
+}
+
 /* build_adjacency (mesh.cpp:27-63): edges sorted by (min, max); faces in
  * ascending face order; f1 = -1 on boundary; -1 return = non-manifold. */
 typedef struct { int64_t key; int f; } ekey;

@@ -90,6 +90,9 @@ int orc_adam_step(const double* cfg, const cdr_layout* L, int64_t nv, int64_t n_
                   double* v, const double* params, const double* grad, double* params_out, double* disp_out);
 int orc_robust_evolve(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, const double* disp,
                       double* pos_out, double* scale_out);
+/* Bvh::closest_point (bvh.cpp:267-329), brute force, ties to the lowest index. */
+int orc_closest_points(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, const double* q, int32_t nq,
+                       int32_t* tri_out, double* point_out, double* dist_out, double* bary_out);
 double orc_tone_map(double v, double gamma);
 double orc_tone_map_derivative(double v, double gamma);
 int orc_project(const cdr_camera* cam, const double* p, double* q, double* depth);

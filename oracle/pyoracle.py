@@ -215,6 +215,45 @@ def robust_evolve(pos, tris, disp, ref=False):
     return rc, out, sc.value
 
 
+def closest_points(pos, tris, queries, ref=False):
+    """Bvh::closest_point (bvh.cpp:267-329) per query: oracle (brute force,
+    ties to the lowest index) or the reference. (tri, point, dist, bary)."""
+    L = C.CDLL(build_ref() if ref else build_oracle())
+    fn = L.ref_closest_points if ref else L.orc_closest_points
+    pos = np.ascontiguousarray(pos, dtype=np.float64)
+    tris = np.ascontiguousarray(tris, dtype=np.int32)
+    q = np.ascontiguousarray(queries, dtype=np.float64)
+    n = len(q)
+    tri, pt, di, ba = np.zeros(n, np.int32), np.zeros((n, 3)), np.zeros(n), np.zeros((n, 3))
+    rc = fn(dp(pos), len(pos), ip(tris), len(tris), dp(q), n, ip(tri), dp(pt), dp(di), dp(ba))
+    assert rc == 0
+    return tri, pt, di, ba
+
+
+def ref_point_to_mesh(pos, tris, queries):
+    L = C.CDLL(build_ref())
+    out = C.c_double()
+    q = np.ascontiguousarray(queries, dtype=np.float64)
+    rc = L.ref_point_to_mesh(dp(np.ascontiguousarray(pos, dtype=np.float64)), len(pos),
+                             ip(np.ascontiguousarray(tris, dtype=np.int32)), len(tris), dp(q), len(q), C.byref(out))
+    assert rc == 0
+    return out.value
+
+
+def ref_uv_transfer(old_pos, old_tris, old_uv, new_pos, max_distance):
+    """(status, uvs) of uv_transfer (remesh.cpp:281-294)."""
+    L = C.CDLL(build_ref())
+    L.ref_uv_transfer.argtypes = [_vp, C.c_int32, _vp, C.c_int32, _vp, _vp, C.c_int32, C.c_double, _vp]
+    op = np.ascontiguousarray(old_pos, dtype=np.float64)
+    ot = np.ascontiguousarray(old_tris, dtype=np.int32)
+    ou = np.ascontiguousarray(old_uv, dtype=np.float64)
+    npos = np.ascontiguousarray(new_pos, dtype=np.float64)
+    uv = np.zeros((len(npos), 2))
+    rc = L.ref_uv_transfer(op.ctypes.data, len(op), ot.ctypes.data, len(ot), ou.ctypes.data, npos.ctypes.data,
+                           len(npos), max_distance, uv.ctypes.data)
+    return rc, uv
+
+
 def _regularisers(fn, handle, scene, w, chk):
     V, n = scene.mesh.V, scene.diffuse.shape[0] * scene.diffuse.shape[1]
     vals = np.zeros(4)

@@ -51,6 +51,7 @@ int fail(const std::exception& e) {
     if (dynamic_cast<const SizeMismatch*>(&e)) return CDR_ERR_SIZE_MISMATCH;
     if (dynamic_cast<const NonFiniteGradient*>(&e)) return CDR_ERR_NONFINITE;
     if (dynamic_cast<const InputSelfIntersecting*>(&e)) return CDR_ERR_SELF_INTERSECTING;
+    if (dynamic_cast<const ProjectionTooFar*>(&e)) return CDR_ERR_PROJECTION_TOO_FAR;
     return CDR_ERR_ERROR;
 }
 
@@ -573,6 +574,67 @@ int ref_robust_evolve(const double* pos, int32_t nv, const int32_t* tris, int32_
             pos_out[3 * i] = out.positions[i].x;
             pos_out[3 * i + 1] = out.positions[i].y;
             pos_out[3 * i + 2] = out.positions[i].z;
+        }
+    })
+}
+
+// Bvh::closest_point (bvh.cpp:267-329) for nq queries
+int ref_closest_points(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, const double* q, int32_t nq,
+                       int32_t* tri_out, double* point_out, double* dist_out, double* bary_out) {
+    GUARD({
+        Mesh m;
+        m.positions.resize(nv);
+        for (int i = 0; i < nv; ++i) m.positions[i] = Vec3(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]);
+        m.triangles.resize(nt);
+        for (int f = 0; f < nt; ++f) m.triangles[f] = {tris[3 * f], tris[3 * f + 1], tris[3 * f + 2]};
+        Bvh bvh(m);
+        for (int i = 0; i < nq; ++i) {
+            ClosestPoint cp = bvh.closest_point(m, Vec3(q[3 * i], q[3 * i + 1], q[3 * i + 2]));
+            tri_out[i] = cp.tri;
+            dist_out[i] = cp.distance;
+            point_out[3 * i] = cp.point.x;
+            point_out[3 * i + 1] = cp.point.y;
+            point_out[3 * i + 2] = cp.point.z;
+            bary_out[3 * i] = cp.b0;
+            bary_out[3 * i + 1] = cp.b1;
+            bary_out[3 * i + 2] = cp.b2;
+        }
+    })
+}
+
+// point_to_mesh_distance (mesh.cpp:127-133) and uv_transfer (remesh.cpp:281-294)
+int ref_point_to_mesh(const double* pos, int32_t nv, const int32_t* tris, int32_t nt, const double* q, int32_t nq,
+                      double* out) {
+    GUARD({
+        Mesh m;
+        m.positions.resize(nv);
+        for (int i = 0; i < nv; ++i) m.positions[i] = Vec3(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]);
+        m.triangles.resize(nt);
+        for (int f = 0; f < nt; ++f) m.triangles[f] = {tris[3 * f], tris[3 * f + 1], tris[3 * f + 2]};
+        std::vector<Vec3> pts(nq);
+        for (int i = 0; i < nq; ++i) pts[i] = Vec3(q[3 * i], q[3 * i + 1], q[3 * i + 2]);
+        *out = point_to_mesh_distance(pts, m);
+    })
+}
+
+int ref_uv_transfer(const double* opos, int32_t onv, const int32_t* otris, int32_t ont, const double* ouv,
+                    const double* npos, int32_t nnv, double max_distance, double* uv_out) {
+    GUARD({
+        Mesh o, n;
+        o.positions.resize(onv);
+        o.uvs.resize(onv);
+        for (int i = 0; i < onv; ++i) {
+            o.positions[i] = Vec3(opos[3 * i], opos[3 * i + 1], opos[3 * i + 2]);
+            o.uvs[i] = Vec2(ouv[2 * i], ouv[2 * i + 1]);
+        }
+        o.triangles.resize(ont);
+        for (int f = 0; f < ont; ++f) o.triangles[f] = {otris[3 * f], otris[3 * f + 1], otris[3 * f + 2]};
+        n.positions.resize(nnv);
+        for (int i = 0; i < nnv; ++i) n.positions[i] = Vec3(npos[3 * i], npos[3 * i + 1], npos[3 * i + 2]);
+        uv_transfer(o, n, max_distance);
+        for (int i = 0; i < nnv; ++i) {
+            uv_out[2 * i] = n.uvs[i].x;
+            uv_out[2 * i + 1] = n.uvs[i].y;
         }
     })
 }

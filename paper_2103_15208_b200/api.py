@@ -53,6 +53,10 @@ class InputSelfIntersecting(CollodiffError):
     """collodiff::InputSelfIntersecting (errors.hpp:32-34)."""
 
 
+class ProjectionTooFar(CollodiffError):
+    """collodiff::ProjectionTooFar (errors.hpp:40)."""
+
+
 _d = C.POINTER(C.c_double)
 _i = C.POINTER(C.c_int32)
 _vp = C.c_void_p
@@ -99,7 +103,7 @@ SEGMENT_DTYPE = np.dtype([("v0", "<i4"), ("v1", "<i4"), ("p0", "<f8", 3), ("p1",
                           ("z0", "<f8"), ("z1", "<f8"), ("length_px", "<f8")])
 
 _ERRORS = {1: SizeMismatch, 2: NonFiniteGradient, 3: CollodiffError, 4: CollodiffError,
-           5: CollodiffError, 6: NoDevice, 7: InputSelfIntersecting}
+           5: CollodiffError, 6: NoDevice, 7: InputSelfIntersecting, 8: ProjectionTooFar}
 
 _lib = None
 
@@ -143,6 +147,7 @@ def load_library(path: str = LIB_PATH):
                                  _d, _d, C.POINTER(cdr_stats)]
     L.cdr_regularisers.argtypes = [_vp, C.POINTER(cdr_reg_weights), C.POINTER(cdr_layout), _d, _d]
     L.cdr_get_rendered.argtypes = [_vp, C.c_int32, _d, _d]
+    L.cdr_closest_points.argtypes = [_vp, _d, C.c_int32, _i, C.c_int32, _d, C.c_int32, _i, _d, _d, _d]
     L.cdr_adam_init.argtypes = [_vp, C.POINTER(cdr_adam_config), C.POINTER(cdr_layout)]
     L.cdr_adam_step.argtypes = [_vp, _d, C.POINTER(C.c_int64)]
     L.cdr_adam_get_state.argtypes = [_vp, _d, _d, C.POINTER(C.c_int64)]
@@ -560,6 +565,40 @@ class Renderer:
         mask = np.zeros((cam.height, cam.width))
         self._chk(self.L.cdr_get_rendered(self.h, view, _dp(rgb), _dp(mask)))
         return rgb, mask
+
+    def closest_points(self, positions, triangles, queries):
+        """Bvh::closest_point (bvh.cpp:267-329) of each query on any mesh:
+        (tri, point n x 3, distance, barycentrics n x 3)."""
+        pos = np.ascontiguousarray(positions, dtype=np.float64)
+        tris = np.ascontiguousarray(triangles, dtype=np.int32)
+        q = np.ascontiguousarray(queries, dtype=np.float64)
+        n = len(q)
+        tri, pt, di, ba = np.zeros(n, np.int32), np.zeros((n, 3)), np.zeros(n), np.zeros((n, 3))
+        self._chk(self.L.cdr_closest_points(self.h, _dp(pos), len(pos), _ip(tris), len(tris), _dp(q), n, _ip(tri),
+                                            _dp(pt), _dp(di), _dp(ba)))
+        return tri, pt, di, ba
+
+    def point_to_mesh_distance(self, points, positions, triangles):
+        """point_to_mesh_distance (mesh.cpp:127-133): mean closest distance."""
+        if len(triangles) == 0:
+            raise CollodiffError("mesh has no triangles")  # EmptyMesh
+        _, _, d, _ = self.closest_points(positions, triangles, points)
+        s = 0.0
+        for x in d:  # the reference's sequential sum
+            s += float(x)
+        return s / len(d) if len(d) else 0.0
+
+    def uv_transfer(self, old_positions, old_triangles, old_uvs, new_positions, max_distance):
+        """uv_transfer (remesh.cpp:281-294): UVs of new vertices from the
+        closest point on the old mesh; ProjectionTooFar past max_distance."""
+        tri, _, d, b = self.closest_points(old_positions, old_triangles, new_positions)
+        bad = np.nonzero((tri < 0) | (d > max_distance))[0]
+        if len(bad):
+            v = int(bad[0])
+            raise ProjectionTooFar(f"uv transfer: vertex {v} is {d[v]} away from the source mesh")
+        t = np.asarray(old_triangles)[tri]
+        uv = np.asarray(old_uvs, dtype=np.float64)
+        return (uv[t[:, 0]] * b[:, :1] + uv[t[:, 1]] * b[:, 1:2]) + uv[t[:, 2]] * b[:, 2:3]
 
     def self_intersects(self, positions, triangles, want_pairs=False):
         """self_intersects (mesh.hpp:67) of any mesh (not necessarily this

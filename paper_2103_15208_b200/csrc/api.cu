@@ -984,6 +984,72 @@ int cdr_get_rendered(cdr_ctx* c, int32_t view, double* rgb, double* mask) {
     API_END
 }
 
+namespace {
+// The geometry-only context (lazy): an arbitrary mesh for the query entry
+// points, its LBVH built; the render mesh stays untouched. The topology is
+// cached across calls (robust_evolve / uv_transfer pass one topology often).
+cdr_ctx* load_geometry(cdr_ctx* c, const double* positions, int32_t nv, const int32_t* triangles, int32_t nt) {
+    for (int64_t i = 0; i < 3 * int64_t(nt); ++i)
+        if (triangles[i] < 0 || triangles[i] >= nv)
+            throw ApiErr(CDR_ERR_INVALID_ARG, "triangle references a vertex out of range");
+    if (!c->geo) {
+        const int rc = cdr_create(c->device, &c->geo);
+        if (rc != CDR_OK) throw ApiErr(rc, "cannot create the geometry context");
+    }
+    cdr_ctx* g = c->geo;
+    cudaStream_t s = g->stream;
+    if (g->T != nt || g->V != nv || g->h_tris.size() != 3 * size_t(nt) ||
+        std::memcmp(g->h_tris.data(), triangles, sizeof(int32_t) * 3 * size_t(nt)) != 0) {
+        g->V = nv;
+        g->T = nt;
+        g->h_tris.assign(triangles, triangles + 3 * size_t(nt));
+        h2d(g->tris, triangles, 3 * size_t(nt), s);
+        g->topo_version = ~0ull;  // not a copy of c's topology (sync_topology re-copies)
+    }
+    h2d(g->pos, positions, 3 * size_t(nv), s);
+    launch_bvh(g, 0.0);
+    return g;
+}
+}  // namespace
+
+int cdr_closest_points(cdr_ctx* c, const double* positions, int32_t nv, const int32_t* triangles, int32_t nt,
+                       const double* queries, int32_t nq, int32_t* tri_out, double* point_out, double* dist_out,
+                       double* bary_out) {
+    API_BEGIN(c)
+    if (nv < 0 || nt < 0 || nq < 0 || (nv > 0 && !positions) || (nt > 0 && !triangles) || (nq > 0 && !queries))
+        throw ApiErr(CDR_ERR_INVALID_ARG, "bad closest_points arguments");
+    if (nq == 0) return;
+    if (nt == 0) {  // bvh.cpp:270: no nodes -> tri -1, distance 1e300
+        for (int i = 0; i < nq; ++i) {
+            if (tri_out) tri_out[i] = -1;
+            if (dist_out) dist_out[i] = 1e300;
+            for (int k = 0; k < 3; ++k) {
+                if (point_out) point_out[3 * i + k] = 0;
+                if (bary_out) bary_out[3 * i + k] = 0;
+            }
+        }
+        return;
+    }
+    cdr_ctx* g = load_geometry(c, positions, nv, triangles, nt);
+    static thread_local DBuf<double> q, pt, di, ba;
+    static thread_local DBuf<int32_t> tr;
+    h2d(q, queries, 3 * size_t(nq), g->stream);
+    tr.ensure(nq);
+    pt.ensure(3 * size_t(nq));
+    di.ensure(nq);
+    ba.ensure(3 * size_t(nq));
+    launch_closest(g, q.p, nq, tr.p, pt.p, di.p, ba.p);
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+        if (dst) CDR_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, g->stream));
+    };
+    d2h(tri_out, tr.p, sizeof(int32_t) * nq);
+    d2h(point_out, pt.p, sizeof(double) * 3 * nq);
+    d2h(dist_out, di.p, sizeof(double) * nq);
+    d2h(bary_out, ba.p, sizeof(double) * 3 * nq);
+    CDR_CUDA_CHECK(cudaStreamSynchronize(g->stream));
+    API_END
+}
+
 int cdr_self_intersects(cdr_ctx* c, const double* positions, int32_t nv, const int32_t* triangles, int32_t nt,
                         int32_t* result, int32_t* pairs, int64_t cap, int64_t* n_pairs) {
     API_BEGIN(c)
@@ -996,21 +1062,7 @@ int cdr_self_intersects(cdr_ctx* c, const double* positions, int32_t nv, const i
     *result = 0;
     if (n_pairs) *n_pairs = 0;
     if (nt < 2) return;  // mesh.cpp:186
-    if (!c->geo) {  // a geometry-only context: the render mesh stays untouched
-        const int rc = cdr_create(c->device, &c->geo);
-        if (rc != CDR_OK) throw ApiErr(rc, "cannot create the geometry context");
-    }
-    cdr_ctx* g = c->geo;
-    cudaStream_t s = g->stream;
-    // topology cached across calls (robust_evolve passes one topology many times)
-    if (g->T != nt || g->V != nv || std::memcmp(g->h_tris.data(), triangles, sizeof(int32_t) * 3 * size_t(nt)) != 0) {
-        g->V = nv;
-        g->T = nt;
-        g->h_tris.assign(triangles, triangles + 3 * size_t(nt));
-        h2d(g->tris, triangles, 3 * size_t(nt), s);
-    }
-    h2d(g->pos, positions, 3 * size_t(nv), s);
-    launch_bvh(g, 0.0);
+    cdr_ctx* g = load_geometry(c, positions, nv, triangles, nt);
     const bool want = pairs != nullptr || n_pairs != nullptr;
     long long n = 0;
     if (!want) {

@@ -10,7 +10,8 @@ the hot subset of total_loss (loss terms + gradient), the four mesh/material
 regularisers at two weight sets (REG_WEIGHTS) and total_loss with every term
 at the reference default weights (LossWeights, losses.hpp:14-23); and
 selfint.npz: self_intersects pairs of clean, broken and noisy meshes;
-optimize.npz: adam_step and robust_evolve cases.
+optimize.npz: adam_step and robust_evolve cases; closest.npz:
+Bvh::closest_point, point_to_mesh_distance and uv_transfer cases.
 """
 import os
 import sys
@@ -20,7 +21,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 
-from oracle.pyoracle import RefLib, adam_step, layout_for, ref_self_intersects, robust_evolve  # noqa: E402
+from oracle.pyoracle import (RefLib, adam_step, closest_points, layout_for, ref_point_to_mesh,  # noqa: E402
+                             ref_self_intersects, ref_uv_transfer, robust_evolve)
 from paper_2103_15208_b200 import scenes as S  # noqa: E402
 
 # (normal, edge, spec, roug, sigma1, sigma2): the reference defaults, then a
@@ -135,8 +137,28 @@ def make_optimize():
     np.savez_compressed(os.path.join(HERE, "optimize.npz"), **out)
 
 
+def make_closest():
+    """Bvh::closest_point, point_to_mesh_distance and uv_transfer cases."""
+    rng = np.random.default_rng(41)
+    m = S.blob(6)
+    q = np.concatenate([rng.normal(0, 0.6, (1500, 3)),              # volume: many edge/vertex ties
+                        m.positions[:300] * 1.0001,                  # just off vertices
+                        m.positions[rng.integers(0, m.V, 200)] + rng.normal(0, 1e-3, (200, 3))])
+    tri, pt, di, ba = closest_points(m.positions, m.triangles, q, ref=True)
+    out = {"pos": m.positions, "tris": m.triangles, "uvs": m.uvs, "q": q, "tri": tri, "pt": pt, "dist": di,
+           "bary": ba, "p2m": np.array(ref_point_to_mesh(m.positions, m.triangles, q))}
+    fine = S.blob(9)  # a finer sampling of the same surface: a remesh's new vertices
+    rc, uv = ref_uv_transfer(m.positions, m.triangles, m.uvs, fine.positions, 0.05)
+    out.update({"new_pos": fine.positions, "uv_rc": np.array(rc), "uv": uv})
+    rc2, _ = ref_uv_transfer(m.positions, m.triangles, m.uvs, fine.positions * 1.5, 0.05)
+    out["uv_far_rc"] = np.array(rc2)
+    print("closest", len(q), "queries; uv_transfer", rc, "far", rc2)
+    np.savez_compressed(os.path.join(HERE, "closest.npz"), **out)
+
+
 if __name__ == "__main__":
     for n, c in CASES.items():
         make(n, c)
     make_selfint()
     make_optimize()
+    make_closest()

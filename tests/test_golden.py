@@ -12,7 +12,7 @@ from paper_2103_15208_b200 import scenes as S
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 # scene fixtures (selfint.npz / optimize.npz: tests/test_selfint.py, tests/test_optimize.py)
-FIXTURES = sorted(f for f in glob.glob(os.path.join(HERE, "*.npz")) if os.path.basename(f) not in ("selfint.npz", "optimize.npz"))
+FIXTURES = sorted(f for f in glob.glob(os.path.join(HERE, "*.npz")) if os.path.basename(f) not in ("selfint.npz", "optimize.npz", "closest.npz"))
 
 
 def load(path):
