@@ -159,6 +159,10 @@ int cdr_set_views(cdr_ctx* ctx, const cdr_camera* cameras, const int32_t* global
                   int32_t n_views);
 /* Target image of a view slot (W x H x 3) and optional mask (W x H). */
 int cdr_set_target(cdr_ctx* ctx, int32_t view, const double* rgb, const double* mask);
+/* The same from fp32 data (PFM targets, texture.cpp:119-155, hold fp32): half
+ * the upload, widened exactly on the device; identical to cdr_set_target on
+ * the doubles the reference's load_pfm would produce. */
+int cdr_set_target_f32(cdr_ctx* ctx, int32_t view, const float* rgb, const float* mask);
 
 /* vertex_normals (mesh.cpp:65-95). */
 int cdr_vertex_normals(cdr_ctx* ctx, double* normals_out /* V x 3 */);

@@ -129,6 +129,7 @@ def load_library(path: str = LIB_PATH):
     L.cdr_set_light.argtypes = [_vp, _d, _d]
     L.cdr_set_views.argtypes = [_vp, _vp, _i, C.c_int32]
     L.cdr_set_target.argtypes = [_vp, C.c_int32, _d, _d]
+    L.cdr_set_target_f32.argtypes = [_vp, C.c_int32, C.POINTER(C.c_float), C.POINTER(C.c_float)]
     L.cdr_vertex_normals.argtypes = [_vp, _d]
     L.cdr_render.argtypes = [_vp, C.c_int32, C.POINTER(cdr_settings), _d, _d, _i]
     L.cdr_radiance_at.argtypes = [_vp, C.c_int32, C.c_int32, _d, _d, _i]
@@ -329,6 +330,15 @@ class Renderer:
         self.cameras = list(cameras)
 
     def set_target(self, view, rgb, mask=None):
+        """Target image (H x W x 3) and optional mask of a view slot; float32
+        arrays (PFM data) take the fp32 upload path (cdr_set_target_f32)."""
+        if np.asarray(rgb).dtype == np.float32:
+            fp = C.POINTER(C.c_float)
+            rgb = np.ascontiguousarray(rgb, dtype=np.float32)
+            mask = None if mask is None else np.ascontiguousarray(mask, dtype=np.float32)
+            self._chk(self.L.cdr_set_target_f32(self.h, view, rgb.ctypes.data_as(fp),
+                                                None if mask is None else mask.ctypes.data_as(fp)))
+            return
         rgb = np.ascontiguousarray(rgb, dtype=np.float64)
         mask = None if mask is None else np.ascontiguousarray(mask, dtype=np.float64)
         self._chk(self.L.cdr_set_target(self.h, view, _dp(rgb), _dp(mask)))

@@ -513,6 +513,29 @@ int cdr_set_target(cdr_ctx* c, int32_t view, const double* rgb, const double* ma
     API_END
 }
 
+int cdr_set_target_f32(cdr_ctx* c, int32_t view, const float* rgb, const float* mask) {
+    API_BEGIN(c)
+    check_view(c, view);
+    if (!rgb) throw ApiErr(CDR_ERR_INVALID_ARG, "target rgb is null");
+    ViewData& v = c->views[view];
+    const size_t np = size_t(v.cam.W) * v.cam.H;
+    static thread_local DBuf<float> stage;
+    h2d(stage, rgb, 3 * np, c->stream);
+    launch_widen(c, stage.p, int64_t(3 * np), c->target.p + 3 * v.pix_off);
+    v.has_target = true;
+    c->target_tone_gamma = -1;
+    v.has_target_mask = mask != nullptr;
+    v.target_mask_sum = 0;
+    if (mask) {
+        sync(c);  // the staging buffer is reused
+        for (size_t i = 0; i < np; ++i) v.target_mask_sum += double(mask[i]);  // losses.cpp:26 order
+        h2d(stage, mask, np, c->stream);
+        launch_widen(c, stage.p, int64_t(np), c->target_mask.p + v.pix_off);
+    }
+    sync(c);
+    API_END
+}
+
 int cdr_vertex_normals(cdr_ctx* c, double* out) {
     API_BEGIN(c)
     ensure_prepared(c);

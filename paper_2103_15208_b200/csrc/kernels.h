@@ -38,6 +38,7 @@ void launch_bvh(cdr_ctx* c, double cam_abs_max);  // bbox + t_min + LBVH (no nor
 // the number of intersecting pairs (early exit after the first when pairs ==
 // nullptr); pairs (f < g) written up to cap, in no particular order.
 long long launch_self_intersect(cdr_ctx* c, int2* pairs, long long cap);
+void launch_widen(cdr_ctx* c, const float* in, int64_t n, double* out);  // fp32 -> fp64 (exact)
 // closest.cu: Bvh::closest_point for nq queries on c's mesh + LBVH (device outputs)
 void launch_closest(cdr_ctx* c, const double* queries, int nq, int32_t* tri, double* point, double* dist,
                     double* bary);

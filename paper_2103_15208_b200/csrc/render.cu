@@ -637,6 +637,11 @@ __global__ void k_tone(const double* __restrict__ in, size_t n, double gamma, do
         out[i] = tone_map(in[i], gamma);
 }
 
+__global__ void k_widen(const float* __restrict__ in, int64_t n, double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = double(in[i]);
+}
+
 __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, int64_t n) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
         y[i] += x[i];
@@ -710,6 +715,14 @@ void launch_radiance_points(cdr_ctx* c, int slot, int n, const double* xy, doubl
 void launch_pack_textures(cdr_ctx* c, const double* d, const double* s, const double* r, int n) {
     if (n <= 0) return;
     { ++c->launches; k_pack_textures<<<(n + 255) / 256, 256, 0, c->stream>>>(d, s, r, n, c->tex.p); }
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_widen(cdr_ctx* c, const float* in, int64_t n, double* out) {
+    if (n <= 0) return;
+    const int nb = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+    ++c->launches;
+    k_widen<<<nb, 256, 0, c->stream>>>(in, n, out);
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -294,3 +294,28 @@ def test_get_rendered_matches_pass_outputs(sphere):
         img, m2, _ = r.render(v, RenderSettings(spp=spp, seed=seed))
         np.testing.assert_array_equal(mask, m2)
         off += n
+
+
+def test_fp32_targets_equal_widened_fp64(sphere):
+    """cdr_set_target_f32 (PFM data) == cdr_set_target of the widened doubles."""
+    spp, seed = 4, 6
+    tg = targets_for(sphere, spp, seed, Oracle)
+    rng = np.random.default_rng(2)
+    lay = param_layout(sphere)
+    views = np.arange(len(sphere.cameras))
+    st = RenderSettings(spp=spp, seed=seed)
+    t32 = [t.astype(np.float32) for t in tg]
+    m32 = [(rng.uniform(size=t.shape[:2]) > 0.3).astype(np.float32) * np.float32(0.75) for t in tg]
+    out = []
+    for f32 in (False, True):
+        r, _ = _pair(sphere)
+        for k in range(len(sphere.cameras)):
+            if f32:
+                r.set_target(k, t32[k], m32[k])
+            else:
+                r.set_target(k, t32[k].astype(np.float64), m32[k].astype(np.float64))
+        loss, g, _, _ = r.loss_grad(views, st, lay, use_target_mask=True)
+        out.append((loss, g))
+    # the per-view loss is an fp64 RED sum across CTAs: equal to rounding
+    np.testing.assert_allclose(out[0][0], out[1][0], rtol=1e-12, atol=0)
+    assert rel_l2(out[0][1], out[1][1]) <= 1e-12
