@@ -25,6 +25,7 @@ namespace {
 struct ViewCall {
     int slot;
     int tile_base;  // first tile of this view in the beam tile arrays
+    int tiles_x, tiles_y;  // the view's tile grid
     double scale;     // lambda / n_valid
     uint64_t h_view;  // hash_combine(seed, gid + 0x9e01)
 };
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
     const unsigned lt = (1u << lane) - 1u;
     const ViewCall vc = p.calls[blockIdx.y];
     const DevCamera cam = p.cams[vc.slot];
-    const int tiles_x = (cam.W + p.TW - 1) / p.TW, tiles_y = (cam.H + p.TH - 1) / p.TH;
+    const int tiles_x = vc.tiles_x, tiles_y = vc.tiles_y;
     const int b = blockIdx.x * kListWarps + w;
     if (b >= tiles_x * tiles_y) return;  // warp-uniform
     const size_t tile = size_t(vc.tile_base) + b;
@@ -245,34 +246,36 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
 #ifndef CDR_TRACE_MIN_BLOCKS
 #define CDR_TRACE_MIN_BLOCKS 4
 #endif
-template <bool kBeam>
+// Grids are (tile x, tile y, view call); kSPP = 16 makes the sample/tile
+// geometry compile-time (4x4 pixels x 16 samples), 0 reads it from Params.
+template <bool kBeam, int kSPP>
 __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
     __shared__ BeamCand s_c[kBeam ? kBeamCap : 1];
     __shared__ TileHdr s_h;
-    const ViewCall vc = p.calls[blockIdx.y];
+    const ViewCall vc = p.calls[blockIdx.z];
     const DevCamera cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
-    const int tiles_x = (W + p.TW - 1) / p.TW;
-    const int tiles_y = (H + p.TH - 1) / p.TH;
-    if (int(blockIdx.x) >= tiles_x * tiles_y) return;
+    if (int(blockIdx.x) >= vc.tiles_x || int(blockIdx.y) >= vc.tiles_y) return;
+    const int tile_in_view = int(blockIdx.y) * vc.tiles_x + int(blockIdx.x);
     const int tid = threadIdx.x;
-    const int spp = p.spp;
+    const int spp = kSPP ? kSPP : p.spp;
+    const int TW = kSPP == 16 ? 4 : p.TW, TH = kSPP == 16 ? 4 : p.TH;
     const int P = kThreads / spp;
     const int pix = tid / spp, s = tid - (tid / spp) * spp;
-    const int X0 = (blockIdx.x % tiles_x) * p.TW, Y0 = (blockIdx.x / tiles_x) * p.TH;
-    const int x = X0 + pix % p.TW;
-    const int y = Y0 + pix / p.TW;
+    const int X0 = int(blockIdx.x) * TW, Y0 = int(blockIdx.y) * TH;
+    const int x = X0 + pix % TW;
+    const int y = Y0 + pix / TW;
     int n = -1;
     __shared__ __align__(16) unsigned char s_pl[kBeam ? kThreads * kPixCap : 16];
     __shared__ unsigned char s_pc[kBeam ? kThreads : 1];
     if (kBeam) {  // stage the tile's candidates and pixel lists in shared memory
-        if (tid == 0) s_h = p.tile_hdr[vc.tile_base + blockIdx.x];
+        if (tid == 0) s_h = p.tile_hdr[vc.tile_base + tile_in_view];
         __syncthreads();
         n = s_h.cnt;
         if (n >= 0) {
             for (int i = tid; i < 3 * n; i += kThreads)
                 reinterpret_cast<float4*>(s_c)[i] = __ldg(reinterpret_cast<const float4*>(p.pool + s_h.off) + i);
-            const size_t tile = size_t(vc.tile_base) + blockIdx.x;
+            const size_t tile = size_t(vc.tile_base) + tile_in_view;
             const uint4* gl = reinterpret_cast<const uint4*>(p.pix_list + tile * P * kPixCap);
             for (int i = tid; i < P * kPixCap / 16; i += kThreads) reinterpret_cast<uint4*>(s_pl)[i] = __ldg(gl + i);
             if (tid < P) s_pc[tid] = p.pix_cnt[tile * P + tid];
@@ -479,24 +482,24 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
 #ifndef CDR_RENDER_MIN_BLOCKS
 #define CDR_RENDER_MIN_BLOCKS 3
 #endif
-template <bool kShade, bool kLoss, bool kInterior>
+template <bool kShade, bool kLoss, bool kInterior, int kSPP>
 __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
     __shared__ double s_rad[kThreads][3];
     __shared__ double s_adj[kThreads][3];  // per pixel (index = pixel in tile)
     __shared__ unsigned char s_hit[kThreads];
 
-    const ViewCall vc = p.calls[blockIdx.y];
+    const ViewCall vc = p.calls[blockIdx.z];
     const DevCamera& cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
-    const int tiles_x = (W + p.TW - 1) / p.TW;
-    const int tiles_y = (H + p.TH - 1) / p.TH;
-    if (int(blockIdx.x) >= tiles_x * tiles_y) return;  // uniform per CTA
+    if (int(blockIdx.x) >= vc.tiles_x || int(blockIdx.y) >= vc.tiles_y) return;  // uniform per CTA
     const int tid = threadIdx.x;
-    const int spp = p.spp;
+    const int spp = kSPP ? kSPP : p.spp;
+    const int TW = kSPP == 16 ? 4 : p.TW, TH = kSPP == 16 ? 4 : p.TH;
     const int P = kThreads / spp;
     const int pix = tid / spp, s = tid - (tid / spp) * spp;
-    const int x = (blockIdx.x % tiles_x) * p.TW + pix % p.TW;
-    const int y = (blockIdx.x / tiles_x) * p.TH + pix / p.TW;
+    const int X0 = int(blockIdx.x) * TW, Y0 = int(blockIdx.y) * TH;
+    const int x = X0 + pix % TW;
+    const int y = Y0 + pix / TW;
     const bool valid = pix < P && x < W && y < H;
     const size_t pbase = p.pix_off[vc.slot];
     const size_t pidx = pbase + size_t(y) * W + x;  // arena pixel index
@@ -546,8 +549,8 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
         const int first = warp_local ? lane : tid, stride = warp_local ? 32 : kThreads;
         for (int item = first; item < n_items; item += stride) {
             const int q = (warp_local ? wib * ppw : 0) + item % ppw, c = item / ppw;
-            const int px = (blockIdx.x % tiles_x) * p.TW + q % p.TW;
-            const int py = (blockIdx.x / tiles_x) * p.TH + q / p.TW;
+            const int px = X0 + q % TW;
+            const int py = Y0 + q / TW;
             if (px < W && py < H) {
                 const size_t qi = pbase + size_t(py) * W + px;
                 double mean = 0;
@@ -774,18 +777,32 @@ static RenderStatics& statics(cdr_ctx* c) {
     return *reg.back().second;
 }
 
-static void launch_render_kernel(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
-    ++c->launches;
+template <int kSPP>
+static void launch_render_kernel_t(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
     if (trace && loss && interior)
-        k_render<true, true, true><<<grid, kThreads, 0, c->stream>>>(p);
+        k_render<true, true, true, kSPP><<<grid, kThreads, 0, c->stream>>>(p);
     else if (trace && !loss && !interior)
-        k_render<true, false, false><<<grid, kThreads, 0, c->stream>>>(p);
+        k_render<true, false, false, kSPP><<<grid, kThreads, 0, c->stream>>>(p);
     else if (!trace && !loss && interior)
-        k_render<false, false, true><<<grid, kThreads, 0, c->stream>>>(p);
+        k_render<false, false, true, kSPP><<<grid, kThreads, 0, c->stream>>>(p);
     else if (trace && loss && !interior)
-        k_render<true, true, false><<<grid, kThreads, 0, c->stream>>>(p);
+        k_render<true, true, false, kSPP><<<grid, kThreads, 0, c->stream>>>(p);
     else
         throw std::runtime_error("unsupported render mode");
+}
+
+static void launch_render_kernel(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
+    ++c->launches;
+    if (p.spp == 16) launch_render_kernel_t<16>(p, grid, c, trace, loss, interior);
+    else launch_render_kernel_t<0>(p, grid, c, trace, loss, interior);
+}
+
+static void launch_trace_kernel(const Params& p, dim3 grid, cdr_ctx* c) {
+    ++c->launches;
+    if (p.use_beam && p.spp == 16) k_trace<true, 16><<<grid, kThreads, 0, c->stream>>>(p);
+    else if (p.use_beam) k_trace<true, 0><<<grid, kThreads, 0, c->stream>>>(p);
+    else if (p.spp == 16) k_trace<false, 16><<<grid, kThreads, 0, c->stream>>>(p);
+    else k_trace<false, 0><<<grid, kThreads, 0, c->stream>>>(p);
 }
 
 void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a, bool trace,
@@ -804,7 +821,9 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         calls[i].slot = view_slots[i];
         const DevCamera& vcam = c->views[view_slots[i]].cam;
         calls[i].tile_base = tile_total;
-        tile_total += ((vcam.W + TW - 1) / TW) * ((vcam.H + TH - 1) / TH);
+        calls[i].tiles_x = (vcam.W + TW - 1) / TW;
+        calls[i].tiles_y = (vcam.H + TH - 1) / TH;
+        tile_total += calls[i].tiles_x * calls[i].tiles_y;
         calls[i].scale = loss_scales ? loss_scales[i] : 0.0;
         calls[i].h_view = hash_combine(a.seed, uint64_t(c->views[view_slots[i]].cam.gid) + 0x9e01);
         maxW = std::max(maxW, c->views[view_slots[i]].cam.W);
@@ -913,15 +932,14 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         const int v0 = k * chunk, nv = std::min(chunk, n_views - v0);
         Params pc = p;
         pc.calls = st.calls.p + v0;
-        dim3 grid(tiles, nv);
+        dim3 grid((maxW + TW - 1) / TW, (maxH + TH - 1) / TH, nv);
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k], c->stream));
         if (p.use_beam) {
             dim3 lgrid((tiles + kListWarps - 1) / kListWarps, nv);
             ++c->launches;
             k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(pc);
         }
-        if (trace && p.use_beam) { ++c->launches; k_trace<true><<<grid, kThreads, 0, c->stream>>>(pc); }
-        if (trace && !p.use_beam) { ++c->launches; k_trace<false><<<grid, kThreads, 0, c->stream>>>(pc); }
+        if (trace) launch_trace_kernel(pc, grid, c);
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k + 1], c->stream));
         launch_render_kernel(pc, grid, c, trace, loss, interior);
     }
