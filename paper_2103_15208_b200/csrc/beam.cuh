@@ -25,9 +25,16 @@
 
 namespace cdr {
 
-constexpr int kBeamCap = 128;   // candidates per tile; more -> per-ray traversal
-constexpr int kPixCap = 16;     // candidates per pixel list; more -> scan the tile list
-constexpr int kFrontCap = 256;  // builder frontier per tile; more -> per-ray traversal
+#ifndef CDR_BEAM_CAP
+#define CDR_BEAM_CAP 128
+#endif
+#ifndef CDR_FRONT_CAP
+#define CDR_FRONT_CAP 256
+#endif
+constexpr int kBeamCap = CDR_BEAM_CAP;    // candidates per tile; more -> per-ray traversal
+constexpr int kPixCap = 16;               // candidates per pixel list; more -> scan the tile list
+constexpr int kBigPixCap = 64;            // the same for big tiles (over kBeamCap candidates)
+constexpr int kFrontCap = CDR_FRONT_CAP;  // builder frontier per tile; more -> per-ray traversal
 
 // Candidate record (48 B): three edge functions E_i = A_i x + B_i y + C_i
 // (pixel coordinates relative to the tile origin, margin folded into C_i;
@@ -42,6 +49,8 @@ struct __align__(16) BeamCand {
 struct TileHdr {
     int off;  // first candidate in the pool
     int cnt;  // candidates, or -1: overflow (per-ray traversal)
+    int big;  // index of the tile's kBigPixCap pixel lists, -1: the kPixCap ones
+    int pad;
 };
 
 struct FrustumPlanes {
@@ -145,6 +154,8 @@ struct BeamView {
     const BeamCand* pool;
     const unsigned char* pix_list;
     const unsigned char* pix_cnt;
+    const unsigned char* big_pix_list;
+    const unsigned char* big_pix_cnt;
     const int* tile_base;  // per view index of the call
     int TW, TH, P;
     int valid;
@@ -166,12 +177,13 @@ __device__ __forceinline__ Hit trace_point(const BeamView& bv, int vi, const Dev
             const TileHdr h = bv.hdr[tile];
             if (h.cnt >= 0) {
                 const int q = (py - ty * bv.TH) * bv.TW + (px - tx * bv.TW);
-                const int cnt = bv.pix_cnt[tile * bv.P + q];
+                const size_t li = h.big >= 0 ? size_t(h.big) * bv.P + q : tile * bv.P + q;
+                const int cnt = h.big >= 0 ? bv.big_pix_cnt[li] : bv.pix_cnt[li];
+                const unsigned char* lst = h.big >= 0 ? bv.big_pix_list + li * kBigPixCap : bv.pix_list + li * kPixCap;
                 const float lx = float(x.x - tx * bv.TW), ly = float(x.y - ty * bv.TH);
                 if (cnt == 0) return Hit{-1, 1e300, 0.0, 0.0};
                 if (cnt == 255) return trace_beam(bv.pool + h.off, h.cnt, recs, o, d, t_min, lx, ly);
-                return trace_beam_list(bv.pool + h.off, bv.pix_list + (tile * bv.P + q) * kPixCap, cnt, recs, o, d,
-                                       t_min, lx, ly);
+                return trace_beam_list(bv.pool + h.off, lst, cnt, recs, o, d, t_min, lx, ly);
             }
         }
     }

@@ -110,7 +110,10 @@ struct cdr_ctx {
     cdr::DBuf<cdr::BeamCand> beam_pool;
     cdr::DBuf<int> beam_used;
     cdr::DBuf<unsigned char> beam_pix_list, beam_pix_cnt;
-    cdr::DBuf<int> beam_tile_base;      // per view index of the last render call
+    cdr::DBuf<int> beam_tile_base;
+    cdr::DBuf<int2> beam_big_queue;  // tiles rebuilt with the big candidate cap
+    cdr::DBuf<int> beam_big_count;
+    cdr::DBuf<unsigned char> beam_big_pix_list, beam_big_pix_cnt;      // per view index of the last render call
     cdr::BeamView beam_view{};          // lists of the last render call (valid flag)
     int* beam_used_host = nullptr;   // pinned; previous call's pool use
     int beam_used_last = 0;

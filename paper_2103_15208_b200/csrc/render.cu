@@ -64,7 +64,12 @@ struct Params {
     int* pool_used;
     unsigned char* pix_list;  // per (tile, pixel): kPixCap candidate indices
     unsigned char* pix_cnt;   // per (tile, pixel): count, 255 = scan the tile list
+    unsigned char* big_pix_list;  // per (big tile, pixel): kBigPixCap indices
+    unsigned char* big_pix_cnt;
     int use_beam;
+    int2* big_queue;  // (call, tile) of the tiles over kBeamCap candidates
+    int* big_count;
+    int big_cap;
 };
 
 constexpr int kThreads = 256;
@@ -81,20 +86,36 @@ __device__ __forceinline__ void raise_nonfinite(ErrorInfo* e, int x, int y) {
 // LBVH (lanes take frontier nodes), candidates sorted by their distance bound
 // (rank across lanes), screen-space edge functions, and per-pixel candidate
 // lists (conservative triangle/pixel overlap) so a sample scans only the few
-// triangles that can cover its pixel.
-constexpr int kListWarps = 4;
-__global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
-    __shared__ int s_front[kListWarps][2][kFrontCap];
-    __shared__ int s_leaf[kListWarps][kBeamCap];
-    __shared__ float s_d[kListWarps][kBeamCap];
-    __shared__ BeamCand s_cand[kListWarps][kBeamCap];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// triangles that can cover its pixel. Returns false when the tile has more
+// than kCap candidates (or kFront frontier nodes); the header is then untouched.
+// Warp bitonic sort of n <= kN 64-bit keys in shared memory (ascending).
+template <int kN>
+__device__ void warp_bitonic_sort(unsigned long long* key, int n, int lane) {
+    for (int i = n + lane; i < kN; i += 32) key[i] = ~0ull;  // pad
+    __syncwarp();
+    for (int k = 2; k <= kN; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = lane; i < kN; i += 32) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const unsigned long long a = key[i], c = key[l];
+                    const bool up = (i & k) == 0;
+                    if ((a > c) == up) {
+                        key[i] = c;
+                        key[l] = a;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+}
+
+template <int kCap, int kFront, int kPix>
+__device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCamera& cam, int b, int lane,
+                                int (*s_front)[kFront], int* s_leaf, float* s_d, BeamCand* s_cand,
+                                unsigned long long* s_key, int big) {
+    const int tiles_x = vc.tiles_x;
     const unsigned lt = (1u << lane) - 1u;
-    const ViewCall vc = p.calls[blockIdx.y];
-    const DevCamera cam = p.cams[vc.slot];
-    const int tiles_x = vc.tiles_x, tiles_y = vc.tiles_y;
-    const int b = blockIdx.x * kListWarps + w;
-    if (b >= tiles_x * tiles_y) return;  // warp-uniform
     const size_t tile = size_t(vc.tile_base) + b;
     TileHdr* hdr = p.tile_hdr + tile;
     const int X0 = (b % tiles_x) * p.TW, Y0 = (b / tiles_x) * p.TH;
@@ -105,10 +126,10 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
     int nl = 0, nf = 0, cur = 0;
     bool over = false;
     if (T == 1) {
-        if (lane == 0) s_leaf[w][0] = 0;
+        if (lane == 0) s_leaf[0] = 0;
         nl = 1;
     } else if (T > 1) {
-        if (lane == 0) s_front[w][0][0] = 0;
+        if (lane == 0) s_front[0][0] = 0;
         nf = 1;
     }
     __syncwarp();
@@ -119,7 +140,7 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
             bool leaf0 = false, leaf1 = false, int0 = false, int1 = false;
             int4 k = make_int4(0, 0, 0, 0);
             if (i < nf) {
-                const BNode* np = p.sc_bin + s_front[w][cur][i];
+                const BNode* np = p.sc_bin + s_front[cur][i];
                 const float4 a = __ldg(&np->a), bb = __ldg(&np->b), c = __ldg(&np->c);
                 k = __ldg(&np->k);
                 const bool in0 = !box_outside(fp, of, a.x, a.y, a.z, a.w, bb.x, bb.y);
@@ -131,33 +152,27 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
             }
             const unsigned m0 = __ballot_sync(0xffffffffu, leaf0), m1 = __ballot_sync(0xffffffffu, leaf1);
             const int p0 = nl + __popc(m0 & lt), p1 = nl + __popc(m0) + __popc(m1 & lt);
-            if (leaf0 && p0 < kBeamCap) s_leaf[w][p0] = ~k.x;
-            if (leaf1 && p1 < kBeamCap) s_leaf[w][p1] = ~k.y;
+            if (leaf0 && p0 < kCap) s_leaf[p0] = ~k.x;
+            if (leaf1 && p1 < kCap) s_leaf[p1] = ~k.y;
             nl += __popc(m0) + __popc(m1);
             const unsigned q0 = __ballot_sync(0xffffffffu, int0), q1 = __ballot_sync(0xffffffffu, int1);
             const int f0 = nn + __popc(q0 & lt), f1 = nn + __popc(q0) + __popc(q1 & lt);
-            if (int0 && f0 < kFrontCap) s_front[w][cur ^ 1][f0] = k.x;
-            if (int1 && f1 < kFrontCap) s_front[w][cur ^ 1][f1] = k.y;
+            if (int0 && f0 < kFront) s_front[cur ^ 1][f0] = k.x;
+            if (int1 && f1 < kFront) s_front[cur ^ 1][f1] = k.y;
             nn += __popc(q0) + __popc(q1);
         }
         __syncwarp();
-        if (nl > kBeamCap || nn > kFrontCap) {
+        if (nl > kCap || nn > kFront) {
             over = true;
             break;
         }
         nf = nn;
         cur ^= 1;
     }
-    if (over) {
-        if (lane == 0) {
-            *hdr = TileHdr{0, -1};
-            atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
-        }
-        return;
-    }
+    if (over) return false;
     // lower bound on t (unit rays): distance from the origin to the triangle's box
     for (int i = lane; i < nl; i += 32) {
-        const TriRec* r = p.sc.recs + s_leaf[w][i];
+        const TriRec* r = p.sc.recs + s_leaf[i];
         const double2 ra = r->a, rb = r->b, rc = r->c, rd = r->d;
         const double re = r->e;
         const double P[3][3] = {{ra.x, rb.y, rd.x}, {ra.y, rc.x, rd.y}, {rb.x, rc.y, re}};
@@ -167,19 +182,31 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
             const double g = fmax(fmax(lo - cam.o[k], cam.o[k] - hi), 0.0);
             dd += g * g;
         }
-        s_d[w][i] = __double2float_rd(sqrt(dd)) * 0.999999f;
+        s_d[i] = __double2float_rd(sqrt(dd)) * 0.999999f;
     }
     __syncwarp();
     const D3 o{cam.o[0], cam.o[1], cam.o[2]}, fw{cam.f[0], cam.f[1], cam.f[2]}, rt{cam.r[0], cam.r[1], cam.r[2]},
         up{cam.u[0], cam.u[1], cam.u[2]};
+    if (s_key) {  // big tiles: sort (distance bits, list position): the same order as the ranks below
+        for (int i = lane; i < nl; i += 32)
+            s_key[i] = (static_cast<unsigned long long>(__float_as_uint(s_d[i])) << 32) | unsigned(i);
+        warp_bitonic_sort<256>(s_key, nl, lane);
+    }
     for (int i = lane; i < nl; i += 32) {
-        const float di = s_d[w][i];
         int rank = 0;  // distance order, ties by list position
-        for (int j = 0; j < nl; ++j) {
-            const float dj = s_d[w][j];
-            rank += (dj < di) || (dj == di && j < i);
+        int src = i;
+        if (s_key) {
+            rank = i;
+            src = int(unsigned(s_key[i]));
+        } else {
+            const float di = s_d[i];
+            for (int j = 0; j < nl; ++j) {
+                const float dj = s_d[j];
+                rank += (dj < di) || (dj == di && j < i);
+            }
         }
-        const int leaf = s_leaf[w][i];
+        const float di = s_d[src];
+        const int leaf = s_leaf[src];
         const TriRec* r = p.sc.recs + leaf;
         const double2 ra = r->a, rb = r->b, rc = r->c, rd = r->d;
         const D3 V[3] = {D3{ra.x, ra.y, rb.x}, D3{rb.y, rc.x, rc.y}, D3{rd.x, rd.y, r->e}};
@@ -208,7 +235,7 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
         bc.e0 = make_float4(E[0], E[1], E[2], E[3]);
         bc.e1 = make_float4(E[4], E[5], E[6], E[7]);
         bc.e2 = make_float4(E[8], di, __int_as_float(leaf), __int_as_float(flags));
-        s_cand[w][rank] = bc;
+        s_cand[rank] = bc;
     }
     __syncwarp();
     int off = 0;
@@ -216,28 +243,89 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
     off = __shfl_sync(0xffffffffu, off, 0);
     if (off + nl > p.pool_cap) {
         if (lane == 0) {
-            *hdr = TileHdr{0, -1};
+            *hdr = TileHdr{0, -1, -1, 0};
             atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
         }
-        return;
+        return true;  // pool full: per-ray traversal
     }
-    const float4* src = reinterpret_cast<const float4*>(&s_cand[w][0]);
+    const float4* src = reinterpret_cast<const float4*>(&s_cand[0]);
     float4* dst = reinterpret_cast<float4*>(p.pool + off);
     for (int i = lane; i < 3 * nl; i += 32) dst[i] = src[i];
     // per-pixel lists, in distance order
     const int P = kThreads / p.spp;
     for (int q = lane; q < P; q += 32) {
         const float qx = float(q % p.TW), qy = float(q / p.TW);
-        unsigned char* lst = p.pix_list + (tile * P + q) * kPixCap;
+        const size_t li = big >= 0 ? size_t(big) * P + q : tile * P + q;
+        unsigned char* lst = (big >= 0 ? p.big_pix_list : p.pix_list) + li * kPix;
         int cnt = 0;
         for (int k = 0; k < nl; ++k)
-            if (cand_overlaps_pixel(s_cand[w][k], qx, qy)) {
-                if (cnt < kPixCap) lst[cnt] = (unsigned char)k;
+            if (cand_overlaps_pixel(s_cand[k], qx, qy)) {
+                if (cnt < kPix) lst[cnt] = (unsigned char)k;
                 ++cnt;
             }
-        p.pix_cnt[tile * P + q] = (unsigned char)(cnt > kPixCap ? 255 : cnt);
+        (big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li] = (unsigned char)(cnt > kPix ? 255 : cnt);
     }
-    if (lane == 0) *hdr = TileHdr{off, nl};
+    if (lane == 0) *hdr = TileHdr{off, nl, big, 0};
+    return true;
+}
+
+// Fast pass: 4 warps per CTA, kBeamCap candidates. Tiles that overflow are
+// queued for the big pass (silhouette tiles, whose frustum grazes the surface:
+// ~1 % of the tiles but a third of the boundary probes).
+#ifndef CDR_LIST_WARPS
+#define CDR_LIST_WARPS 4
+#endif
+constexpr int kListWarps = CDR_LIST_WARPS;
+#ifndef CDR_BIG_FRONT
+#define CDR_BIG_FRONT 1024
+#endif
+#ifndef CDR_BIG_WARPS
+#define CDR_BIG_WARPS 1
+#endif
+constexpr int kBigCap = 255;              // candidates of a big tile (pixel lists index with a byte)
+constexpr int kBigFront = CDR_BIG_FRONT;  // its builder frontier
+constexpr int kBigWarps = CDR_BIG_WARPS;  // big-tile builders per CTA
+__global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
+    __shared__ int s_front[kListWarps][2][kFrontCap];
+    __shared__ int s_leaf[kListWarps][kBeamCap];
+    __shared__ float s_d[kListWarps][kBeamCap];
+    __shared__ BeamCand s_cand[kListWarps][kBeamCap];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const ViewCall vc = p.calls[blockIdx.y];
+    const DevCamera cam = p.cams[vc.slot];
+    const int b = blockIdx.x * kListWarps + w;
+    if (b >= vc.tiles_x * vc.tiles_y) return;  // warp-uniform
+    if (build_tile_list<kBeamCap, kFrontCap, kPixCap>(p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], s_cand[w],
+                                                       nullptr, -1))
+        return;
+    if (lane == 0) {
+        p.tile_hdr[size_t(vc.tile_base) + b] = TileHdr{0, -1, -1, 0};
+        const int i = atomicAdd(p.big_count, 1);
+        if (i < p.big_cap) p.big_queue[i] = make_int2(int(blockIdx.y), b);
+        else atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+    }
+}
+
+// Big pass: one warp per CTA over the queue (persistent grid), kBigCap
+// candidates; what still overflows is traced per ray.
+__global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
+    __shared__ int s_front[kBigWarps][2][kBigFront];
+    __shared__ int s_leaf[kBigWarps][kBigCap];
+    __shared__ float s_d[kBigWarps][kBigCap];
+    __shared__ BeamCand s_cand[kBigWarps][kBigCap];
+    __shared__ unsigned long long s_key[kBigWarps][256];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = min(*p.big_count, p.big_cap);
+    for (int i = blockIdx.x * kBigWarps + w; i < n; i += gridDim.x * kBigWarps) {
+        const int2 e = p.big_queue[i];
+        const ViewCall vc = p.calls[e.x];
+        const DevCamera& cam = p.cams[vc.slot];
+        if (!build_tile_list<kBigCap, kBigFront, kBigPixCap>(p, vc, cam, e.y, lane, s_front[w], s_leaf[w], s_d[w],
+                                                             s_cand[w], s_key[w], i) &&
+            lane == 0)
+            atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+        __syncwarp();
+    }
 }
 
 // Primary visibility: one thread per sample, tile order as k_render, writes the
@@ -250,7 +338,7 @@ __global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
 // geometry compile-time (4x4 pixels x 16 samples), 0 reads it from Params.
 template <bool kBeam, int kSPP>
 __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
-    __shared__ BeamCand s_c[kBeam ? kBeamCap : 1];
+    __shared__ BeamCand s_c[kBeam ? kBigCap : 1];  // big tiles too
     __shared__ TileHdr s_h;
     const ViewCall vc = p.calls[blockIdx.z];
     const DevCamera cam = p.cams[vc.slot];
@@ -276,9 +364,12 @@ __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params
             for (int i = tid; i < 3 * n; i += kThreads)
                 reinterpret_cast<float4*>(s_c)[i] = __ldg(reinterpret_cast<const float4*>(p.pool + s_h.off) + i);
             const size_t tile = size_t(vc.tile_base) + tile_in_view;
-            const uint4* gl = reinterpret_cast<const uint4*>(p.pix_list + tile * P * kPixCap);
-            for (int i = tid; i < P * kPixCap / 16; i += kThreads) reinterpret_cast<uint4*>(s_pl)[i] = __ldg(gl + i);
-            if (tid < P) s_pc[tid] = p.pix_cnt[tile * P + tid];
+            const int cap = s_h.big >= 0 ? kBigPixCap : kPixCap;
+            const size_t li = s_h.big >= 0 ? size_t(s_h.big) * P : tile * P;
+            const uint4* gl =
+                reinterpret_cast<const uint4*>((s_h.big >= 0 ? p.big_pix_list : p.pix_list) + li * cap);
+            for (int i = tid; i < P * cap / 16; i += kThreads) reinterpret_cast<uint4*>(s_pl)[i] = __ldg(gl + i);
+            if (tid < P) s_pc[tid] = (s_h.big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li + tid];
         }
         __syncthreads();
     }
@@ -292,8 +383,10 @@ __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params
             D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
             D3 dir = primary_dir(cam, ps);
             const float fx = float(ps.x - X0), fy = float(ps.y - Y0);
-            h = cnt == 255 ? trace_beam(s_c, n, p.sc.recs, org, dir, p.info->t_min, fx, fy)
-                           : trace_beam_list(s_c, s_pl + pix * kPixCap, cnt, p.sc.recs, org, dir, p.info->t_min, fx, fy);
+            const BeamCand* cands = s_c;
+            h = cnt == 255 ? trace_beam(cands, n, p.sc.recs, org, dir, p.info->t_min, fx, fy)
+                           : trace_beam_list(cands, s_pl + pix * (s_h.big >= 0 ? kBigPixCap : kPixCap), cnt,
+                                             p.sc.recs, org, dir, p.info->t_min, fx, fy);
         }
     } else {
         D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
@@ -901,13 +994,26 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         c->beam_pix_cnt.ensure(std::max<size_t>(1, npix));
         p.pix_list = c->beam_pix_list.p;
         p.pix_cnt = c->beam_pix_cnt.p;
+        // big tiles: up to 1/16 of the tiles, and only while their pixel lists
+        // fit k_trace's staging buffer (P <= 64, spp >= 4)
+        const int big_cap = P * kBigPixCap <= kThreads * kPixCap ? std::max(64, tile_total / 16) : 0;
+        c->beam_big_queue.ensure(std::max(1, big_cap));
+        c->beam_big_count.ensure(1);
+        c->beam_big_pix_list.ensure(std::max<size_t>(16, size_t(big_cap) * P * kBigPixCap));
+        c->beam_big_pix_cnt.ensure(std::max<size_t>(1, size_t(big_cap) * P));
+        p.big_queue = c->beam_big_queue.p;
+        p.big_count = c->beam_big_count.p;
+        p.big_cap = big_cap;
+        p.big_pix_list = c->beam_big_pix_list.p;
+        p.big_pix_cnt = c->beam_big_pix_cnt.p;
         // publish the lists for the boundary probes of the same call
         std::vector<int> bases(n_views);
         for (int i = 0; i < n_views; ++i) bases[i] = calls[i].tile_base;
         c->beam_tile_base.ensure(n_views);
         CDR_CUDA_CHECK(cudaMemcpyAsync(c->beam_tile_base.p, bases.data(), sizeof(int) * n_views,
                                        cudaMemcpyHostToDevice, c->stream));
-        c->beam_view = BeamView{p.tile_hdr, p.pool, p.pix_list, p.pix_cnt, c->beam_tile_base.p, TW, TH, P, 1};
+        c->beam_view = BeamView{p.tile_hdr,     p.pool, p.pix_list, p.pix_cnt, p.big_pix_list, p.big_pix_cnt,
+                                c->beam_tile_base.p, TW,   TH,         P,         1};
     }
     // Views can go through lists -> trace -> shade in chunks whose hit cache
     // (4 B per sample) fits in L2, so the shading kernel's first load hits L2.
@@ -936,8 +1042,11 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k], c->stream));
         if (p.use_beam) {
             dim3 lgrid((tiles + kListWarps - 1) / kListWarps, nv);
+            CDR_CUDA_CHECK(cudaMemsetAsync(pc.big_count, 0, sizeof(int), c->stream));
             ++c->launches;
             k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(pc);
+            ++c->launches;
+            k_tile_lists_big<<<148 * 8 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
         }
         if (trace) launch_trace_kernel(pc, grid, c);
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k + 1], c->stream));
