@@ -396,6 +396,17 @@ __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params
     p.hit[pidx * spp + s] = h.tri;
 }
 
+// Type of the warp partial sums of the scatter. fp64 by default (the whole
+// path is fp64). -DCDR_REDUCE_F32 sums the <= 32 per-group terms in fp32
+// (the global REDs stay fp64): shading 17.1 -> 16.0 ms at cfg2, gradients
+// still ~1e-7 from the reference (tolerance 1e-4), but not an fp64 path, so
+// it is an opt-in build and never the benchmarked one.
+#ifdef CDR_REDUCE_F32
+using RedT = float;
+#else
+using RedT = double;
+#endif
+
 // Phase 3 of k_render: the interior adjoint of one sample (diff_render.cpp:78-184).
 __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x, int y, int spp, int tri, double t,
                                               double b1, double b2, D3 dir, D3 a, bool act) {
@@ -520,13 +531,13 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
         const int x1 = x0 + 1 == tw ? 0 : x0 + 1, y1 = y0 + 1 == th ? 0 : y0 + 1;
 #pragma unroll 1
         for (int kq = 0; kq < 4; ++kq) {
-            double v[7];
+            RedT v[7];
             const double w = wq[kq];
             for (int c = 0; c < 3; ++c) {
-                v[c] = aL[c] * (w * wd0);
-                v[3 + c] = aL[c] * (w * ws0);
+                v[c] = RedT(aL[c] * (w * wd0));
+                v[3 + c] = RedT(aL[c] * (w * ws0));
             }
-            v[6] = wr0 * w;
+            v[6] = RedT(wr0 * w);
             reduce_peers<7>(0xffffffffu, peers, v);
             if (leader) {
                 // texel-major accumulator: the 7 values of a texel share 2 sectors
@@ -555,14 +566,15 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
 #pragma unroll 1
         for (int j = 0; j < 3; ++j) {
             const double bj = j == 0 ? b0 : (j == 1 ? b1 : b2);
-            double v[6] = {gc.x * bj, gc.y * bj, gc.z * bj, hm.x * bj, hm.y * bj, hm.z * bj};
+            RedT v[6] = {RedT(gc.x * bj), RedT(gc.y * bj), RedT(gc.z * bj),
+                         RedT(hm.x * bj), RedT(hm.y * bj), RedT(hm.z * bj)};
             if (!pact)
                 for (int i = 0; i < 6; ++i) v[i] = 0;
             reduce_peers<6>(0xffffffffu, peers, v);
             if (leader) {
                 double* dst = p.corner + (size_t(tri) * 3 + j) * 6;
                 for (int i = 0; i < 6; ++i)
-                    if (v[i] != 0) atomicAdd(dst + i, v[i]);
+                    if (v[i] != 0) atomicAdd(dst + i, double(v[i]));
             }
         }
     }
