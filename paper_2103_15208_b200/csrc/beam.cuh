@@ -190,4 +190,83 @@ __device__ __forceinline__ Hit trace_point(const BeamView& bv, int vi, const Dev
     return trace(nodes, recs, n_tris, o, d, t_min);
 }
 
+// Two probes at once (the boundary pass traces x - n/2 and x + n/2 of every
+// edge sample): the same scans as trace_point, stepped in one loop so each
+// thread keeps two independent candidate -> triangle load chains in flight.
+// Per-ray traversal (off-image points, overflowing tiles) runs afterwards.
+struct ProbeScan {
+    const BeamCand* cand;
+    const unsigned char* lst;  // nullptr: scan the whole tile list
+    int n, j;
+    float lx, ly;
+    int mode;  // 0 done, 1 scanning, 2 per-ray traversal
+    Hit best;
+};
+
+__device__ __forceinline__ void probe_setup(const BeamView& bv, int vi, const DevCamera& cam, D2 x, ProbeScan& s) {
+    s.best = Hit{-1, 1e300, 0.0, 0.0};
+    s.mode = 2;
+    s.j = 0;
+    if (!bv.valid) return;
+    const double fx = floor(x.x), fy = floor(x.y);
+    if (!(fx >= 0 && fy >= 0 && fx < cam.W && fy < cam.H)) return;
+    const int px = int(fx), py = int(fy);
+    const int tiles_x = (cam.W + bv.TW - 1) / bv.TW;
+    const int tx = px / bv.TW, ty = py / bv.TH;
+    const size_t tile = size_t(bv.tile_base[vi]) + ty * tiles_x + tx;
+    const TileHdr h = bv.hdr[tile];
+    if (h.cnt < 0) return;
+    const int q = (py - ty * bv.TH) * bv.TW + (px - tx * bv.TW);
+    const size_t li = h.big >= 0 ? size_t(h.big) * bv.P + q : tile * bv.P + q;
+    const int cnt = h.big >= 0 ? bv.big_pix_cnt[li] : bv.pix_cnt[li];
+    s.cand = bv.pool + h.off;
+    s.lx = float(x.x - tx * bv.TW);
+    s.ly = float(x.y - ty * bv.TH);
+    if (cnt == 255) {
+        s.lst = nullptr;
+        s.n = h.cnt;
+    } else {
+        s.lst = h.big >= 0 ? bv.big_pix_list + li * kBigPixCap : bv.pix_list + li * kPixCap;
+        s.n = cnt;
+    }
+    s.mode = s.n > 0 ? 1 : 0;
+}
+
+// one candidate of trace_beam / trace_beam_list
+__device__ __forceinline__ void probe_step(ProbeScan& s, const TriRec* __restrict__ recs, D3 o, D3 d, double t_min) {
+    if (s.j >= s.n) {
+        s.mode = 0;
+        return;
+    }
+    const int k = s.lst ? int(s.lst[s.j]) : s.j;
+    ++s.j;
+    const float4 e2 = s.cand[k].e2;
+    if (double(e2.y) > s.best.t) {  // every remaining candidate is farther
+        s.mode = 0;
+        return;
+    }
+    bool pass = true;
+    if (!(__float_as_int(e2.w) & 1)) {
+        const float4 e0 = s.cand[k].e0, e1 = s.cand[k].e1;
+        pass = e0.x * s.lx + e0.y * s.ly + e0.z >= 0.0f && e0.w * s.lx + e1.x * s.ly + e1.y >= 0.0f &&
+               e1.z * s.lx + e1.w * s.ly + e2.x >= 0.0f;
+    }
+    if (pass) leaf_test(recs, __float_as_int(e2.z), o, d, t_min, s.best);
+}
+
+__device__ __forceinline__ void trace_points2(const BeamView& bv, int vi, const DevCamera& cam, const BNode* nodes,
+                                              const TriRec* recs, int n_tris, D2 xa, D3 da, D2 xb, D3 db,
+                                              double t_min, Hit& ha, Hit& hb) {
+    const D3 o{cam.o[0], cam.o[1], cam.o[2]};
+    ProbeScan a, b;
+    probe_setup(bv, vi, cam, xa, a);
+    probe_setup(bv, vi, cam, xb, b);
+    while (a.mode == 1 || b.mode == 1) {
+        if (a.mode == 1) probe_step(a, recs, o, da, t_min);
+        if (b.mode == 1) probe_step(b, recs, o, db, t_min);
+    }
+    ha = a.mode == 2 ? trace(nodes, recs, n_tris, o, da, t_min) : a.best;
+    hb = b.mode == 2 ? trace(nodes, recs, n_tris, o, db, t_min) : b.best;
+}
+
 }  // namespace cdr

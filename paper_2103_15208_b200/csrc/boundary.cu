@@ -376,8 +376,13 @@ __global__ void __launch_bounds__(kBlock, CDR_BOUNDARY_MIN_BLOCKS) k_boundary(BP
         if (p.probe == CDR_PROBE_RADIANCE) {
             // radiance_at (render.cpp:24-33) through the pixels' candidate lists
             const D3 dm = primary_dir(cam, xm), dp = primary_dir(cam, xp);
+#ifdef CDR_PROBES_SEQUENTIAL
             const Hit hm = trace_point(p.beam, vi, cam, p.sc.nodes, p.sc.recs, p.sc.n_tris, xm, dm, t_min);
             const Hit hp = trace_point(p.beam, vi, cam, p.sc.nodes, p.sc.recs, p.sc.n_tris, xp, dp, t_min);
+#else
+            Hit hm, hp;
+            trace_points2(p.beam, vi, cam, p.sc.nodes, p.sc.recs, p.sc.n_tris, xm, dm, xp, dp, t_min, hm, hp);
+#endif
             const D3 bg{p.sc.bg[0], p.sc.bg[1], p.sc.bg[2]};
             D3 lo3 = hm.tri >= 0 ? shade_hit(p.sc, hm, dm) : bg;
             D3 hi3 = hp.tri >= 0 ? shade_hit(p.sc, hp, dp) : bg;
