@@ -112,8 +112,8 @@ __device__ void warp_bitonic_sort(unsigned long long* key, int n, int lane) {
 
 template <int kCap, int kFront, int kPix>
 __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCamera& cam, int b, int lane,
-                                int (*s_front)[kFront], int* s_leaf, float* s_d, BeamCand* s_cand,
-                                unsigned long long* s_key, int big) {
+                                int (*s_front)[kFront], int* s_leaf, float* s_d, unsigned long long* s_key,
+                                int big) {
     const int tiles_x = vc.tiles_x;
     const unsigned lt = (1u << lane) - 1u;
     const size_t tile = size_t(vc.tile_base) + b;
@@ -187,6 +187,18 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
     __syncwarp();
     const D3 o{cam.o[0], cam.o[1], cam.o[2]}, fw{cam.f[0], cam.f[1], cam.f[2]}, rt{cam.r[0], cam.r[1], cam.r[2]},
         up{cam.u[0], cam.u[1], cam.u[2]};
+    // candidates go straight to their sorted slots in the pool (no staging)
+    int off = 0;
+    if (lane == 0 && nl) off = atomicAdd(p.pool_used, nl);
+    off = __shfl_sync(0xffffffffu, off, 0);
+    if (off + nl > p.pool_cap) {
+        if (lane == 0) {
+            *hdr = TileHdr{0, -1, -1, 0};
+            atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+        }
+        return true;  // pool full: per-ray traversal
+    }
+    BeamCand* s_cand = p.pool + off;
     if (s_key) {  // big tiles: sort (distance bits, list position): the same order as the ranks below
         for (int i = lane; i < nl; i += 32)
             s_key[i] = (static_cast<unsigned long long>(__float_as_uint(s_d[i])) << 32) | unsigned(i);
@@ -237,20 +249,7 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
         bc.e2 = make_float4(E[8], di, __int_as_float(leaf), __int_as_float(flags));
         s_cand[rank] = bc;
     }
-    __syncwarp();
-    int off = 0;
-    if (lane == 0 && nl) off = atomicAdd(p.pool_used, nl);
-    off = __shfl_sync(0xffffffffu, off, 0);
-    if (off + nl > p.pool_cap) {
-        if (lane == 0) {
-            *hdr = TileHdr{0, -1, -1, 0};
-            atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
-        }
-        return true;  // pool full: per-ray traversal
-    }
-    const float4* src = reinterpret_cast<const float4*>(&s_cand[0]);
-    float4* dst = reinterpret_cast<float4*>(p.pool + off);
-    for (int i = lane; i < 3 * nl; i += 32) dst[i] = src[i];
+    __syncwarp();  // orders the lanes' pool writes for the per-pixel pass
     // per-pixel lists, in distance order
     const int P = kThreads / p.spp;
     for (int q = lane; q < P; q += 32) {
@@ -285,18 +284,20 @@ constexpr int kListWarps = CDR_LIST_WARPS;
 constexpr int kBigCap = 255;              // candidates of a big tile (pixel lists index with a byte)
 constexpr int kBigFront = CDR_BIG_FRONT;  // its builder frontier
 constexpr int kBigWarps = CDR_BIG_WARPS;  // big-tile builders per CTA
-__global__ void __launch_bounds__(32 * kListWarps) k_tile_lists(Params p) {
+#ifndef CDR_LIST_MIN_BLOCKS
+#define CDR_LIST_MIN_BLOCKS 8  // 32 warps per SM: the builder is latency-bound (level-by-level BFS)
+#endif
+__global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_lists(Params p) {
     __shared__ int s_front[kListWarps][2][kFrontCap];
     __shared__ int s_leaf[kListWarps][kBeamCap];
     __shared__ float s_d[kListWarps][kBeamCap];
-    __shared__ BeamCand s_cand[kListWarps][kBeamCap];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const ViewCall vc = p.calls[blockIdx.y];
     const DevCamera cam = p.cams[vc.slot];
     const int b = blockIdx.x * kListWarps + w;
     if (b >= vc.tiles_x * vc.tiles_y) return;  // warp-uniform
-    if (build_tile_list<kBeamCap, kFrontCap, kPixCap>(p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], s_cand[w],
-                                                       nullptr, -1))
+    if (build_tile_list<kBeamCap, kFrontCap, kPixCap>(p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], nullptr,
+                                                       -1))
         return;
     if (lane == 0) {
         p.tile_hdr[size_t(vc.tile_base) + b] = TileHdr{0, -1, -1, 0};
@@ -312,7 +313,6 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
     __shared__ int s_front[kBigWarps][2][kBigFront];
     __shared__ int s_leaf[kBigWarps][kBigCap];
     __shared__ float s_d[kBigWarps][kBigCap];
-    __shared__ BeamCand s_cand[kBigWarps][kBigCap];
     __shared__ unsigned long long s_key[kBigWarps][256];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = min(*p.big_count, p.big_cap);
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
         const ViewCall vc = p.calls[e.x];
         const DevCamera& cam = p.cams[vc.slot];
         if (!build_tile_list<kBigCap, kBigFront, kBigPixCap>(p, vc, cam, e.y, lane, s_front[w], s_leaf[w], s_d[w],
-                                                             s_cand[w], s_key[w], i) &&
+                                                             s_key[w], i) &&
             lane == 0)
             atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
         __syncwarp();
