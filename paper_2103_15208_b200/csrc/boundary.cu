@@ -338,7 +338,7 @@ __global__ void k_bscatter(BParams p) {
 // pass 4: the two radiance probes and the vertex deposit, in segment order so a
 // warp traces neighbouring rays along one silhouette edge (diff_render.cpp:246-277)
 #ifndef CDR_BOUNDARY_MIN_BLOCKS
-#define CDR_BOUNDARY_MIN_BLOCKS 3
+#define CDR_BOUNDARY_MIN_BLOCKS 5  // latency-bound probes: occupancy beats the extra spill
 #endif
 __global__ void __launch_bounds__(kBlock, CDR_BOUNDARY_MIN_BLOCKS) k_boundary(BParams p) {
     const int vi = blockIdx.y;
