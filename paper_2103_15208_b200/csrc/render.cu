@@ -67,6 +67,7 @@ struct Params {
     unsigned char* big_pix_list;  // per (big tile, pixel): kBigPixCap indices
     unsigned char* big_pix_cnt;
     int use_beam;
+    int fast_cap;     // candidate cap of the fast pass (kBeamCap; lower only to test the big pass)
     int2* big_queue;  // (call, tile) of the tiles over kBeamCap candidates
     int* big_count;
     int big_cap;
@@ -162,7 +163,7 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
             nn += __popc(q0) + __popc(q1);
         }
         __syncwarp();
-        if (nl > kCap || nn > kFront) {
+        if (nl > (kCap == kBeamCap ? p.fast_cap : kCap) || nn > kFront) {
             over = true;
             break;
         }
@@ -987,6 +988,8 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
 
     int tiles = ((maxW + p.TW - 1) / p.TW) * ((maxH + p.TH - 1) / p.TH);
     p.use_beam = trace && c->T > 0 && !std::getenv("CDR_NO_BEAM");
+    p.fast_cap = kBeamCap;  // CDR_BEAM_FAST_CAP < kBeamCap pushes tiles to the big pass (tests)
+    if (const char* e = std::getenv("CDR_BEAM_FAST_CAP")) p.fast_cap = std::max(0, std::min(kBeamCap, std::atoi(e)));
     c->beam_view.valid = 0;
     if (c->beam_used_host) c->beam_used_last = *c->beam_used_host;  // previous call has completed
     if (p.use_beam) {

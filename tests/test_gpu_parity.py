@@ -319,3 +319,25 @@ def test_fp32_targets_equal_widened_fp64(sphere):
     # the per-view loss is an fp64 RED sum across CTAs: equal to rounding
     np.testing.assert_allclose(out[0][0], out[1][0], rtol=1e-12, atol=0)
     assert rel_l2(out[0][1], out[1][1]) <= 1e-12
+
+
+@pytest.mark.parametrize("fast_cap", ["0", "3"])
+def test_big_tile_lists_exact(sphere, monkeypatch, fast_cap):
+    """Tiles over the fast pass's candidate cap are rebuilt by the big pass
+    (255 candidates, 64-entry pixel lists). Forcing (almost) every tile there
+    must leave hit caches and images bit-exact and gradients in tolerance."""
+    monkeypatch.setenv("CDR_BEAM_FAST_CAP", fast_cap)
+    blob = blob_scene(freq=8, tex=32, views=2, image=48)
+    for sc in (sphere, blob):
+        r, o = _pair(sc)
+        for spp in (4, 16):
+            st = RenderSettings(spp=spp, seed=5)
+            for v in range(len(sc.cameras)):
+                rgb, mask, hit = r.render(v, st)
+                ro, mo, ho = o.render(v, spp, 5)
+                np.testing.assert_array_equal(hit, ho)
+                np.testing.assert_array_equal(mask, mo)
+                np.testing.assert_array_equal(rgb, ro)
+    # (with every tile forced into it, the big queue, sized for 1/16 of the
+    # tiles, overflows too: those tiles are traced per ray, also exact)
+    _loss_grad_check(sphere, 16, 2, param_layout(sphere))
