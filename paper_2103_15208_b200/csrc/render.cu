@@ -277,7 +277,7 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
 #endif
 constexpr int kListWarps = CDR_LIST_WARPS;
 #ifndef CDR_BIG_FRONT
-#define CDR_BIG_FRONT 1024
+#define CDR_BIG_FRONT 512
 #endif
 #ifndef CDR_BIG_WARPS
 #define CDR_BIG_WARPS 1
@@ -311,10 +311,11 @@ __global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_l
 // Big pass: one warp per CTA over the queue (persistent grid), kBigCap
 // candidates; what still overflows is traced per ray.
 __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
-    __shared__ int s_front[kBigWarps][2][kBigFront];
+    // the sort keys reuse the frontier (the BFS is over before the sort)
+    static_assert(2 * kBigFront * sizeof(int) >= 256 * sizeof(unsigned long long), "key space");
+    __shared__ __align__(8) int s_front[kBigWarps][2][kBigFront];
     __shared__ int s_leaf[kBigWarps][kBigCap];
     __shared__ float s_d[kBigWarps][kBigCap];
-    __shared__ unsigned long long s_key[kBigWarps][256];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = min(*p.big_count, p.big_cap);
     for (int i = blockIdx.x * kBigWarps + w; i < n; i += gridDim.x * kBigWarps) {
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
         const ViewCall vc = p.calls[e.x];
         const DevCamera& cam = p.cams[vc.slot];
         if (!build_tile_list<kBigCap, kBigFront, kBigPixCap>(p, vc, cam, e.y, lane, s_front[w], s_leaf[w], s_d[w],
-                                                             s_key[w], i) &&
+                                                             reinterpret_cast<unsigned long long*>(s_front[w]), i) &&
             lane == 0)
             atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
         __syncwarp();
@@ -1061,7 +1062,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             ++c->launches;
             k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(pc);
             ++c->launches;
-            k_tile_lists_big<<<148 * 8 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
+            k_tile_lists_big<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
         }
         if (trace) launch_trace_kernel(pc, grid, c);
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k + 1], c->stream));
