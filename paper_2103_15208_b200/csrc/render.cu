@@ -68,6 +68,7 @@ struct Params {
     unsigned char* big_pix_cnt;
     int use_beam;
     int fast_cap;     // candidate cap of the fast pass (kBeamCap; lower only to test the big pass)
+    int no_shared_top;  // 1: every tile walks the BVH from the root (A/B and tests)
     int2* big_queue;  // (call, tile) of the tiles over kBeamCap candidates
     int* big_count;
     int big_cap;
@@ -114,7 +115,7 @@ __device__ void warp_bitonic_sort(unsigned long long* key, int n, int lane) {
 template <int kCap, int kFront, int kPix>
 __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCamera& cam, int b, int lane,
                                 int (*s_front)[kFront], int* s_leaf, float* s_d, unsigned long long* s_key,
-                                int big) {
+                                int big, const int* init_front = nullptr, int init_n = 0) {
     const int tiles_x = vc.tiles_x;
     const unsigned lt = (1u << lane) - 1u;
     const size_t tile = size_t(vc.tile_base) + b;
@@ -129,6 +130,9 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
     if (T == 1) {
         if (lane == 0) s_leaf[0] = 0;
         nl = 1;
+    } else if (T > 1 && init_n > 0) {  // start below the levels the CTA walked together
+        for (int i = lane; i < init_n; i += 32) s_front[0][i] = init_front[i];
+        nf = init_n;
     } else if (T > 1) {
         if (lane == 0) s_front[0][0] = 0;
         nf = 1;
@@ -288,17 +292,80 @@ constexpr int kBigWarps = CDR_BIG_WARPS;  // big-tile builders per CTA
 #ifndef CDR_LIST_MIN_BLOCKS
 #define CDR_LIST_MIN_BLOCKS 8  // 32 warps per SM: the builder is latency-bound (level-by-level BFS)
 #endif
+// The top levels of the BVH are the same for neighbouring tiles: one warp
+// walks them once against the union frustum of the CTA's tiles (one tile row)
+// until the frontier fills a warp or a leaf would appear; every warp then
+// starts its own tile's BFS from that frontier. A node outside the union
+// frustum is outside each tile's, so nothing a tile needs is dropped.
+constexpr int kTopCap = 64;
+__device__ int shared_top_levels(const Params& p, const DevCamera& cam, int X0, int X1, int Y0, int Y1, int lane,
+                                 int (*scratch)[kFrontCap], int* out) {
+    const FrustumPlanes fp = tile_frustum(cam, X0 - 0.01, X1 + 0.01, Y0 - 0.01, Y1 + 0.01);
+    const float of[3] = {float(cam.o[0]), float(cam.o[1]), float(cam.o[2])};
+    const unsigned lt = (1u << lane) - 1u;
+    int nf = 1, cur = 0;
+    if (lane == 0) scratch[0][0] = 0;
+    __syncwarp();
+    while (nf < 32) {
+        int nn = 0;
+        bool leafy = false;
+        for (int base = 0; base < nf; base += 32) {
+            const int i = base + lane;
+            bool int0 = false, int1 = false, lf = false;
+            int4 k = make_int4(0, 0, 0, 0);
+            if (i < nf) {
+                const BNode* np = p.sc_bin + scratch[cur][i];
+                const float4 a = __ldg(&np->a), bb = __ldg(&np->b), c = __ldg(&np->c);
+                k = __ldg(&np->k);
+                const bool in0 = !box_outside(fp, of, a.x, a.y, a.z, a.w, bb.x, bb.y);
+                const bool in1 = !box_outside(fp, of, bb.z, bb.w, c.x, c.y, c.z, c.w);
+                lf = (in0 && k.x < 0) || (in1 && k.y < 0);
+                int0 = in0 && k.x >= 0;
+                int1 = in1 && k.y >= 0;
+            }
+            leafy |= __any_sync(0xffffffffu, lf);
+            const unsigned q0 = __ballot_sync(0xffffffffu, int0), q1 = __ballot_sync(0xffffffffu, int1);
+            const int f0 = nn + __popc(q0 & lt), f1 = nn + __popc(q0) + __popc(q1 & lt);
+            if (int0 && f0 < kTopCap) scratch[cur ^ 1][f0] = k.x;
+            if (int1 && f1 < kTopCap) scratch[cur ^ 1][f1] = k.y;
+            nn += __popc(q0) + __popc(q1);
+        }
+        __syncwarp();
+        if (leafy || nn > kTopCap || nn == 0) break;  // keep the current level
+        nf = nn;
+        cur ^= 1;
+    }
+    for (int i = lane; i < nf; i += 32) out[i] = scratch[cur][i];
+    return nf;
+}
+
 __global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_lists(Params p) {
     __shared__ int s_front[kListWarps][2][kFrontCap];
     __shared__ int s_leaf[kListWarps][kBeamCap];
     __shared__ float s_d[kListWarps][kBeamCap];
+    __shared__ int s_top[kTopCap];
+    __shared__ int s_ntop;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const ViewCall vc = p.calls[blockIdx.y];
     const DevCamera cam = p.cams[vc.slot];
-    const int b = blockIdx.x * kListWarps + w;
-    if (b >= vc.tiles_x * vc.tiles_y) return;  // warp-uniform
+    const int n_tiles = vc.tiles_x * vc.tiles_y;
+    const int b0 = blockIdx.x * kListWarps;
+    if (b0 >= n_tiles) return;  // CTA-uniform
+    const int b1 = min(b0 + kListWarps, n_tiles) - 1;
+    const bool share = p.sc.n_tris > 1 && b0 / vc.tiles_x == b1 / vc.tiles_x && !p.no_shared_top;
+    if (share) {
+        if (w == 0) {
+            const int X0 = (b0 % vc.tiles_x) * p.TW, X1 = min((b1 % vc.tiles_x) * p.TW + p.TW, cam.W);
+            const int Y0 = (b0 / vc.tiles_x) * p.TH, Y1 = min(Y0 + p.TH, cam.H);
+            const int n = shared_top_levels(p, cam, X0, X1, Y0, Y1, lane, s_front[0], s_top);
+            if (lane == 0) s_ntop = n;
+        }
+        __syncthreads();
+    }
+    const int b = b0 + w;
+    if (b > b1) return;  // warp-uniform (after the only barrier)
     if (build_tile_list<kBeamCap, kFrontCap, kPixCap>(p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], nullptr,
-                                                       -1))
+                                                       -1, share ? s_top : nullptr, share ? s_ntop : 0))
         return;
     if (lane == 0) {
         p.tile_hdr[size_t(vc.tile_base) + b] = TileHdr{0, -1, -1, 0};
@@ -990,6 +1057,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     int tiles = ((maxW + p.TW - 1) / p.TW) * ((maxH + p.TH - 1) / p.TH);
     p.use_beam = trace && c->T > 0 && !std::getenv("CDR_NO_BEAM");
     p.fast_cap = kBeamCap;  // CDR_BEAM_FAST_CAP < kBeamCap pushes tiles to the big pass (tests)
+    p.no_shared_top = std::getenv("CDR_NO_SHARED_TOP") != nullptr;
     if (const char* e = std::getenv("CDR_BEAM_FAST_CAP")) p.fast_cap = std::max(0, std::min(kBeamCap, std::atoi(e)));
     c->beam_view.valid = 0;
     if (c->beam_used_host) c->beam_used_last = *c->beam_used_host;  // previous call has completed
