@@ -407,8 +407,6 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
 // geometry compile-time (4x4 pixels x 16 samples), 0 reads it from Params.
 template <bool kBeam, int kSPP>
 __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
-    __shared__ BeamCand s_c[kBeam ? kBigCap : 1];  // big tiles too
-    __shared__ TileHdr s_h;
     const ViewCall vc = p.calls[blockIdx.z];
     const DevCamera cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
@@ -422,40 +420,28 @@ __global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params
     const int X0 = int(blockIdx.x) * TW, Y0 = int(blockIdx.y) * TH;
     const int x = X0 + pix % TW;
     const int y = Y0 + pix / TW;
-    int n = -1;
-    __shared__ __align__(16) unsigned char s_pl[kBeam ? kThreads * kPixCap : 16];
-    __shared__ unsigned char s_pc[kBeam ? kThreads : 1];
-    if (kBeam) {  // stage the tile's candidates and pixel lists in shared memory
-        if (tid == 0) s_h = p.tile_hdr[vc.tile_base + tile_in_view];
-        __syncthreads();
-        n = s_h.cnt;
-        if (n >= 0) {
-            for (int i = tid; i < 3 * n; i += kThreads)
-                reinterpret_cast<float4*>(s_c)[i] = __ldg(reinterpret_cast<const float4*>(p.pool + s_h.off) + i);
-            const size_t tile = size_t(vc.tile_base) + tile_in_view;
-            const int cap = s_h.big >= 0 ? kBigPixCap : kPixCap;
-            const size_t li = s_h.big >= 0 ? size_t(s_h.big) * P : tile * P;
-            const uint4* gl =
-                reinterpret_cast<const uint4*>((s_h.big >= 0 ? p.big_pix_list : p.pix_list) + li * cap);
-            for (int i = tid; i < P * cap / 16; i += kThreads) reinterpret_cast<uint4*>(s_pl)[i] = __ldg(gl + i);
-            if (tid < P) s_pc[tid] = (s_h.big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li + tid];
-        }
-        __syncthreads();
-    }
     if (!(pix < P && x < W && y < H)) return;
     const size_t pidx = p.pix_off[vc.slot] + size_t(y) * W + x;
     const D3 org{cam.o[0], cam.o[1], cam.o[2]};
     Hit h{-1, 1e300, 0.0, 0.0};
-    if (kBeam && n >= 0) {
-        const int cnt = s_pc[pix];
+    // No staging and no barrier: each sample reads the tile header (one
+    // broadcast transaction per warp), its own pixel's list and the candidate
+    // records, which the tile's 256 samples share through L1.
+    TileHdr th{0, -1, -1, 0};
+    if (kBeam) th = p.tile_hdr[vc.tile_base + tile_in_view];
+    if (kBeam && th.cnt >= 0) {
+        const size_t tile = size_t(vc.tile_base) + tile_in_view;
+        const size_t li = th.big >= 0 ? size_t(th.big) * P + pix : tile * P + pix;
+        const int cnt = (th.big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li];
         if (cnt != 0) {  // an empty pixel list means no triangle can cover the pixel: no ray needed
             D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
             D3 dir = primary_dir(cam, ps);
             const float fx = float(ps.x - X0), fy = float(ps.y - Y0);
-            const BeamCand* cands = s_c;
-            h = cnt == 255 ? trace_beam(cands, n, p.sc.recs, org, dir, p.info->t_min, fx, fy)
-                           : trace_beam_list(cands, s_pl + pix * (s_h.big >= 0 ? kBigPixCap : kPixCap), cnt,
-                                             p.sc.recs, org, dir, p.info->t_min, fx, fy);
+            const BeamCand* cands = p.pool + th.off;
+            h = cnt == 255 ? trace_beam(cands, th.cnt, p.sc.recs, org, dir, p.info->t_min, fx, fy)
+                           : trace_beam_list(cands,
+                                             (th.big >= 0 ? p.big_pix_list + li * kBigPixCap : p.pix_list + li * kPixCap),
+                                             cnt, p.sc.recs, org, dir, p.info->t_min, fx, fy);
         }
     } else {
         D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
