@@ -75,6 +75,10 @@ struct Params {
 };
 
 constexpr int kThreads = 256;
+#ifndef CDR_RENDER_THREADS16
+#define CDR_RENDER_THREADS16 128  // 4 x 2 pixels: a CTA waits for its slowest warp; smaller is better down to 128
+#endif
+constexpr int kRenderThreads16 = CDR_RENDER_THREADS16;  // k_render CTA at spp 16 (64 per pixel row of 4)
 
 __device__ __forceinline__ void raise_nonfinite(ErrorInfo* e, int x, int y) {
     if (atomicCAS(&e->flag, 0, 1) == 0) {
@@ -643,19 +647,23 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
 #define CDR_RENDER_MIN_BLOCKS 3
 #endif
 template <bool kShade, bool kLoss, bool kInterior, int kSPP>
-__global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
-    __shared__ double s_rad[kThreads][3];
-    __shared__ double s_adj[kThreads][3];  // per pixel (index = pixel in tile)
-    __shared__ unsigned char s_hit[kThreads];
+__global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
+                                  kSPP == 16 ? CDR_RENDER_MIN_BLOCKS * kThreads / kRenderThreads16
+                                             : CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
+    // spp 16: kRenderThreads16 threads = (kRenderThreads16 / 64) x 4 pixels x 16 samples
+    constexpr int kRT = kSPP == 16 ? kRenderThreads16 : kThreads;
+    __shared__ double s_rad[kRT][3];
+    __shared__ double s_adj[kRT][3];  // per pixel (index = pixel in tile)
+    __shared__ unsigned char s_hit[kRT];
 
     const ViewCall vc = p.calls[blockIdx.z];
     const DevCamera& cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
-    if (int(blockIdx.x) >= vc.tiles_x || int(blockIdx.y) >= vc.tiles_y) return;  // uniform per CTA
     const int tid = threadIdx.x;
     const int spp = kSPP ? kSPP : p.spp;
-    const int TW = kSPP == 16 ? 4 : p.TW, TH = kSPP == 16 ? 4 : p.TH;
-    const int P = kThreads / spp;
+    const int TW = kSPP == 16 ? 4 : p.TW, TH = kSPP == 16 ? kRT / 64 : p.TH;
+    if (int(blockIdx.x) * TW >= W || int(blockIdx.y) * TH >= H) return;  // uniform per CTA
+    const int P = kRT / spp;
     const int pix = tid / spp, s = tid - (tid / spp) * spp;
     const int X0 = int(blockIdx.x) * TW, Y0 = int(blockIdx.y) * TH;
     const int x = X0 + pix % TW;
@@ -693,8 +701,8 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     // end. Otherwise pixels straddle warps and phase 2 is CTA-wide.
     const int lane = tid & 31, wib = tid >> 5;
     const bool warp_local = (32 % spp) == 0;
-    __shared__ double s_wloss[kThreads / 32];
-    __shared__ int s_wcnt[kThreads / 32][2];
+    __shared__ double s_wloss[kRT / 32];
+    __shared__ int s_wcnt[kRT / 32][2];
     if (warp_local) __syncwarp();
     else __syncthreads();
 
@@ -706,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     {
         const int ppw = warp_local ? 32 / spp : P;  // pixels per phase-2 group
         const int n_items = 3 * ppw;
-        const int first = warp_local ? lane : tid, stride = warp_local ? 32 : kThreads;
+        const int first = warp_local ? lane : tid, stride = warp_local ? 32 : kRT;
         for (int item = first; item < n_items; item += stride) {
             const int q = (warp_local ? wib * ppw : 0) + item % ppw, c = item / ppw;
             const int px = X0 + q % TW;
@@ -775,11 +783,11 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
     // ---------------- publish the CTA's tallies (warp 0 waits for the others)
     __threadfence_block();
     if (wib == 0) {
-        asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(kRT) : "memory");
         if (lane == 0) {
             double tot = 0;
             unsigned long long nh = 0, na = 0;
-            for (int w = 0; w < kThreads / 32; ++w) {
+            for (int w = 0; w < kRT / 32; ++w) {
                 tot += s_wloss[w];
                 nh += s_wcnt[w][0];
                 na += s_wcnt[w][1];
@@ -791,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, CDR_RENDER_MIN_BLOCKS) k_render(Para
             }
         }
     } else {
-        asm volatile("bar.arrive 1, %0;" ::"n"(kThreads) : "memory");
+        asm volatile("bar.arrive 1, %0;" ::"n"(kRT) : "memory");
     }
 }
 
@@ -939,21 +947,25 @@ static RenderStatics& statics(cdr_ctx* c) {
 
 template <int kSPP>
 static void launch_render_kernel_t(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
+    constexpr int bs = kSPP == 16 ? kRenderThreads16 : kThreads;
     if (trace && loss && interior)
-        k_render<true, true, true, kSPP><<<grid, kThreads, 0, c->stream>>>(p);
+        k_render<true, true, true, kSPP><<<grid, bs, 0, c->stream>>>(p);
     else if (trace && !loss && !interior)
-        k_render<true, false, false, kSPP><<<grid, kThreads, 0, c->stream>>>(p);
+        k_render<true, false, false, kSPP><<<grid, bs, 0, c->stream>>>(p);
     else if (!trace && !loss && interior)
-        k_render<false, false, true, kSPP><<<grid, kThreads, 0, c->stream>>>(p);
+        k_render<false, false, true, kSPP><<<grid, bs, 0, c->stream>>>(p);
     else if (trace && loss && !interior)
-        k_render<true, true, false, kSPP><<<grid, kThreads, 0, c->stream>>>(p);
+        k_render<true, true, false, kSPP><<<grid, bs, 0, c->stream>>>(p);
     else
         throw std::runtime_error("unsupported render mode");
 }
 
 static void launch_render_kernel(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
     ++c->launches;
-    if (p.spp == 16) launch_render_kernel_t<16>(p, grid, c, trace, loss, interior);
+    if (p.spp == 16) {
+        grid.y = (grid.y * 4 + kRenderThreads16 / 64 - 1) / (kRenderThreads16 / 64);  // rows of kRT/64 pixels
+        launch_render_kernel_t<16>(p, grid, c, trace, loss, interior);
+    }
     else launch_render_kernel_t<0>(p, grid, c, trace, loss, interior);
 }
 
