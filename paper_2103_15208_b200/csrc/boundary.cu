@@ -340,7 +340,11 @@ __global__ void k_bscatter(BParams p) {
 #ifndef CDR_BOUNDARY_MIN_BLOCKS
 #define CDR_BOUNDARY_MIN_BLOCKS 5  // latency-bound probes: occupancy beats the extra spill
 #endif
-__global__ void __launch_bounds__(kBlock, CDR_BOUNDARY_MIN_BLOCKS) k_boundary(BParams p) {
+#ifndef CDR_BND_BLOCK
+#define CDR_BND_BLOCK 128
+#endif
+constexpr int kBndBlock = CDR_BND_BLOCK;  // probe costs vary per warp: a CTA waits for its slowest
+__global__ void __launch_bounds__(kBndBlock, CDR_BOUNDARY_MIN_BLOCKS * 256 / kBndBlock) k_boundary(BParams p) {
     const int vi = blockIdx.y;
     const int lane = threadIdx.x & 31;
     const DevCamera cam = p.cams[p.calls[vi].slot];
@@ -552,7 +556,8 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     { ++c->launches; k_bsample<<<grid, kBlock, 0, c->stream>>>(p); }
     { ++c->launches; k_bscan<<<n_views, 1024, 0, c->stream>>>(p.seg_count, p.count, E, p.seg_off, p.n_active); }
     { ++c->launches; k_bscatter<<<grid, kBlock, 0, c->stream>>>(p); }
-    { ++c->launches; k_boundary<<<grid, kBlock, 0, c->stream>>>(p); }
+    dim3 bgrid((samples + kBndBlock - 1) / kBndBlock, n_views);
+    { ++c->launches; k_boundary<<<bgrid, kBndBlock, 0, c->stream>>>(p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -78,7 +78,11 @@ constexpr int kThreads = 256;
 #ifndef CDR_RENDER_THREADS16
 #define CDR_RENDER_THREADS16 128  // 4 x 2 pixels: a CTA waits for its slowest warp; smaller is better down to 128
 #endif
-constexpr int kRenderThreads16 = CDR_RENDER_THREADS16;  // k_render CTA at spp 16 (64 per pixel row of 4)
+constexpr int kRenderThreads16 = CDR_RENDER_THREADS16;
+#ifndef CDR_TRACE_THREADS16
+#define CDR_TRACE_THREADS16 128  // half a beam tile: 6,563 -> 6,709 Msamples/s at cfg2
+#endif
+constexpr int kTraceThreads16 = CDR_TRACE_THREADS16;  // k_trace CTA at spp 16 (64, 128 or 256)  // k_render CTA at spp 16 (64 per pixel row of 4)
 
 __device__ __forceinline__ void raise_nonfinite(ErrorInfo* e, int x, int y) {
     if (atomicCAS(&e->flag, 0, 1) == 0) {
@@ -410,18 +414,24 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
 // Grids are (tile x, tile y, view call); kSPP = 16 makes the sample/tile
 // geometry compile-time (4x4 pixels x 16 samples), 0 reads it from Params.
 template <bool kBeam, int kSPP>
-__global__ void __launch_bounds__(kThreads, CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
+__global__ void __launch_bounds__(kSPP == 16 ? kTraceThreads16 : kThreads,
+                                  kSPP == 16 ? CDR_TRACE_MIN_BLOCKS * kThreads / kTraceThreads16
+                                             : CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
+    // spp 16: a CTA covers kTraceThreads16 / 64 rows of a 4 x 4 beam tile
+    constexpr int kCR = kSPP == 16 ? kTraceThreads16 / 64 : 0;  // pixel rows per CTA
     const ViewCall vc = p.calls[blockIdx.z];
     const DevCamera cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
-    if (int(blockIdx.x) >= vc.tiles_x || int(blockIdx.y) >= vc.tiles_y) return;
-    const int tile_in_view = int(blockIdx.y) * vc.tiles_x + int(blockIdx.x);
     const int tid = threadIdx.x;
     const int spp = kSPP ? kSPP : p.spp;
     const int TW = kSPP == 16 ? 4 : p.TW, TH = kSPP == 16 ? 4 : p.TH;
-    const int P = kThreads / spp;
-    const int pix = tid / spp, s = tid - (tid / spp) * spp;
-    const int X0 = int(blockIdx.x) * TW, Y0 = int(blockIdx.y) * TH;
+    const int P = kThreads / spp;  // pixels per beam tile (its pixel lists)
+    const int cpix = tid / spp, s = tid - (tid / spp) * spp;  // pixel within the CTA
+    const int ty = kSPP == 16 ? int(blockIdx.y) * kCR / 4 : int(blockIdx.y);
+    if (int(blockIdx.x) >= vc.tiles_x || ty >= vc.tiles_y) return;
+    const int tile_in_view = ty * vc.tiles_x + int(blockIdx.x);
+    const int X0 = int(blockIdx.x) * TW, Y0 = ty * TH;
+    const int pix = kSPP == 16 ? (int(blockIdx.y) * kCR - Y0) * 4 + cpix : cpix;  // pixel within the beam tile
     const int x = X0 + pix % TW;
     const int y = Y0 + pix / TW;
     if (!(pix < P && x < W && y < H)) return;
@@ -971,9 +981,11 @@ static void launch_render_kernel(const Params& p, dim3 grid, cdr_ctx* c, bool tr
 
 static void launch_trace_kernel(const Params& p, dim3 grid, cdr_ctx* c) {
     ++c->launches;
-    if (p.use_beam && p.spp == 16) k_trace<true, 16><<<grid, kThreads, 0, c->stream>>>(p);
+    dim3 g16 = grid;
+    g16.y = grid.y * (kThreads / kTraceThreads16);
+    if (p.use_beam && p.spp == 16) k_trace<true, 16><<<g16, kTraceThreads16, 0, c->stream>>>(p);
     else if (p.use_beam) k_trace<true, 0><<<grid, kThreads, 0, c->stream>>>(p);
-    else if (p.spp == 16) k_trace<false, 16><<<grid, kThreads, 0, c->stream>>>(p);
+    else if (p.spp == 16) k_trace<false, 16><<<g16, kTraceThreads16, 0, c->stream>>>(p);
     else k_trace<false, 0><<<grid, kThreads, 0, c->stream>>>(p);
 }
 
