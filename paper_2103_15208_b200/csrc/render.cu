@@ -356,6 +356,27 @@ __global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_l
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const ViewCall vc = p.calls[blockIdx.y];
     const DevCamera cam = p.cams[vc.slot];
+#ifndef CDR_LIST_STRIP
+    // a 2 x 2 block of tiles per CTA (the union frustum is 8 x 8 pixels)
+    static_assert(kListWarps == 4, "2x2 tile blocks need 4 warps");
+    const int bx = (vc.tiles_x + 1) / 2, by = (vc.tiles_y + 1) / 2;
+    if (int(blockIdx.x) >= bx * by) return;  // CTA-uniform
+    const int cx = int(blockIdx.x) % bx, cy = int(blockIdx.x) / bx;
+    const int tx = 2 * cx + (w & 1), ty = 2 * cy + (w >> 1);
+    const bool mine = tx < vc.tiles_x && ty < vc.tiles_y;
+    const int b = ty * vc.tiles_x + tx;
+    const bool share = p.sc.n_tris > 1 && !p.no_shared_top;
+    if (share) {
+        if (w == 0) {
+            const int X0 = 2 * cx * p.TW, X1 = min(X0 + 2 * p.TW, cam.W);
+            const int Y0 = 2 * cy * p.TH, Y1 = min(Y0 + 2 * p.TH, cam.H);
+            const int n = shared_top_levels(p, cam, X0, X1, Y0, Y1, lane, s_front[0], s_top);
+            if (lane == 0) s_ntop = n;
+        }
+        __syncthreads();
+    }
+    if (!mine) return;  // warp-uniform (after the only barrier)
+#else
     const int n_tiles = vc.tiles_x * vc.tiles_y;
     const int b0 = blockIdx.x * kListWarps;
     if (b0 >= n_tiles) return;  // CTA-uniform
@@ -372,6 +393,7 @@ __global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_l
     }
     const int b = b0 + w;
     if (b > b1) return;  // warp-uniform (after the only barrier)
+#endif
     if (build_tile_list<kBeamCap, kFrontCap, kPixCap>(p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], nullptr,
                                                        -1, share ? s_top : nullptr, share ? s_ntop : 0))
         return;
@@ -1135,7 +1157,11 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         dim3 grid((maxW + TW - 1) / TW, (maxH + TH - 1) / TH, nv);
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k], c->stream));
         if (p.use_beam) {
+#ifndef CDR_LIST_STRIP
+            dim3 lgrid(((maxW + TW - 1) / TW + 1) / 2 * (((maxH + TH - 1) / TH + 1) / 2), nv);
+#else
             dim3 lgrid((tiles + kListWarps - 1) / kListWarps, nv);
+#endif
             CDR_CUDA_CHECK(cudaMemsetAsync(pc.big_count, 0, sizeof(int), c->stream));
             ++c->launches;
             k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(pc);
