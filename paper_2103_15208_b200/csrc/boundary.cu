@@ -163,32 +163,42 @@ __global__ void k_sil_write(const double* __restrict__ pos, const double* __rest
     if (f) make_segment(pos, fn, edges[i], cam, &segs[size_t(vi) * E + off]);
 }
 
-// Running CDF in segment order, one thread per view (diff_render.cpp:213-228).
-// info[vi] = {total_len (acc), extract_total, usable, degenerate}
-__global__ void k_cdf(const cdr_segment* __restrict__ segs, const int32_t* __restrict__ count, int E,
-                      int n_views, double* __restrict__ cdf, double* __restrict__ totals,
-                      int32_t* __restrict__ degenerate) {
-    int vi = blockIdx.x * blockDim.x + threadIdx.x;
+// Running CDF in segment order (diff_render.cpp:213-228), one warp per view:
+// the lanes load 32 segment lengths at once, then every lane steps through the
+// same sequence of 32 additions (shuffled in segment order) and keeps the
+// prefix at its own position, so each value is the reference's sequential
+// sum, bit for bit, without a load latency per segment.
+// totals[3 vi] = {total_len (acc), usable, extract_total}
+__global__ void __launch_bounds__(32) k_cdf(const cdr_segment* __restrict__ segs, const int32_t* __restrict__ count,
+                                            int E, int n_views, double* __restrict__ cdf,
+                                            double* __restrict__ totals, int32_t* __restrict__ degenerate) {
+    const int vi = blockIdx.x, lane = threadIdx.x;
     if (vi >= n_views) return;
-    int n = count[vi];
+    const int n = count[vi];
     double acc = 0, ext = 0;
     int usable = 0, deg = 0;
-    for (int i = 0; i < n; ++i) {
-        double len = segs[size_t(vi) * E + i].length_px;
-        ext += len;  // SilhouetteSet::total_length (silhouette.cpp:103)
-        if (len < 1e-12) {
-            ++deg;
-            len = 0;
-        } else {
-            ++usable;
+    for (int base = 0; base < n; base += 32) {
+        const int i = base + lane;
+        const double raw = i < n ? segs[size_t(vi) * E + i].length_px : 0.0;
+        const bool dg = i < n && raw < 1e-12;
+        const double len = dg ? 0.0 : raw;
+        deg += __popc(__ballot_sync(0xffffffffu, dg));
+        usable += __popc(__ballot_sync(0xffffffffu, i < n && !dg));
+        const int m = min(32, n - base);
+        double mine = 0;
+        for (int k = 0; k < m; ++k) {
+            ext += __shfl_sync(0xffffffffu, raw, k);  // SilhouetteSet::total_length (silhouette.cpp:103)
+            acc += __shfl_sync(0xffffffffu, len, k);
+            if (k == lane) mine = acc;
         }
-        acc += len;
-        cdf[size_t(vi) * E + i] = acc;
+        if (i < n) cdf[size_t(vi) * E + i] = mine;
     }
-    totals[3 * vi] = acc;
-    totals[3 * vi + 1] = (n == 0 || ext <= 0 || usable == 0 || acc <= 0) ? 0.0 : 1.0;
-    totals[3 * vi + 2] = ext;
-    degenerate[vi] = (n == 0 || ext <= 0) ? 0 : deg;
+    if (lane == 0) {
+        totals[3 * vi] = acc;
+        totals[3 * vi + 1] = (n == 0 || ext <= 0 || usable == 0 || acc <= 0) ? 0.0 : 1.0;
+        totals[3 * vi + 2] = ext;
+        degenerate[vi] = (n == 0 || ext <= 0) ? 0 : deg;
+    }
 }
 
 struct BParams {
@@ -492,7 +502,7 @@ void launch_silhouettes(cdr_ctx* c, int n_views) {
 
 void launch_cdf(cdr_ctx* c, int n_views) {
     if (n_views <= 0) return;
-    { ++c->launches; k_cdf<<<(n_views + 31) / 32, 32, 0, c->stream>>>(c->segs.p, c->sil_count.p, std::max(1, c->E),
+    { ++c->launches; k_cdf<<<n_views, 32, 0, c->stream>>>(c->segs.p, c->sil_count.p, std::max(1, c->E),
                                                      n_views, c->cdf.p, c->total_len.p, c->degenerate.p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
