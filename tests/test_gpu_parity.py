@@ -341,3 +341,24 @@ def test_big_tile_lists_exact(sphere, monkeypatch, fast_cap):
     # (with every tile forced into it, the big queue, sized for 1/16 of the
     # tiles, overflows too: those tiles are traced per ray, also exact)
     _loss_grad_check(sphere, 16, 2, param_layout(sphere))
+
+
+@pytest.mark.parametrize("wh", [(37, 29), (29, 37)])
+def test_odd_image_sizes_exact(wh):
+    """Partial tiles at the right and bottom edges, odd tile counts (the 2x2
+    tile blocks of the list builder, the 4x2-pixel shading CTAs, the half-tile
+    trace CTAs): hit caches and images bit-exact, gradients in tolerance."""
+    w, h = wh
+    m = S.blob(6)
+    d, s_, r_ = S.random_maps(16)
+    sc = S.Scene(m, d, s_, r_, S.sample_views_on_sphere(2, 2.5, 11, 40, w, h))
+    r, o = _pair(sc)
+    for spp in (16, 4):
+        st = RenderSettings(spp=spp, seed=9)
+        for v in range(len(sc.cameras)):
+            rgb, mask, hit = r.render(v, st)
+            ro, mo, ho = o.render(v, spp, 9)
+            np.testing.assert_array_equal(hit, ho)
+            np.testing.assert_array_equal(mask, mo)
+            np.testing.assert_array_equal(rgb, ro)
+    _loss_grad_check(sc, 16, 3, param_layout(sc))
