@@ -248,6 +248,10 @@ int cdr_create(int device, cdr_ctx** out) {
     try {
         CDR_CUDA_CHECK(cudaSetDevice(device));
         CDR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CDR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_sil, cudaEventDisableTiming));
+        CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_reg, cudaEventDisableTiming));
         c->errinfo.ensure(1);
         c->counters.ensure(1);
         c->info.ensure(1);
@@ -285,6 +289,13 @@ void cdr_destroy(cdr_ctx* c) {
     c->sil_count.release(); c->segs.release(); c->cdf.release(); c->total_len.release();
     c->degenerate.release(); c->grad.release(); c->grad_tmp.release(); c->corner_acc.release(); c->tex_acc.release(); c->qvec.release();
     c->loss_acc.release(); c->errinfo.release(); c->counters.release();
+    if (c->side) {
+        cudaStreamSynchronize(c->side);
+        cudaEventDestroy(c->ev_fork);
+        cudaEventDestroy(c->ev_sil);
+        cudaEventDestroy(c->ev_reg);
+        cudaStreamDestroy(c->side);
+    }
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -726,6 +737,13 @@ int cdr_boundary_pass(cdr_ctx* c, int32_t view, const double* adjoint, const cdr
     API_END
 }
 
+// Scope in which the context's launchers target its side stream.
+struct OnSideStream {
+    cdr_ctx* c;
+    explicit OnSideStream(cdr_ctx* ctx) : c(ctx) { std::swap(c->stream, c->side); }
+    ~OnSideStream() { std::swap(c->stream, c->side); }
+};
+
 // The fused total_loss pipeline (losses.cpp:244-297). terms[6] = rend, lap,
 // normal, edge, spec, roug; reg == nullptr leaves the last four at 0.
 static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_settings* st, double lambda_rend,
@@ -765,26 +783,45 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
         c->target_tone_gamma = st->gamma;
     }
     CDR_CUDA_CHECK(cudaEventRecord(ev[1], s));
+    // Side stream: silhouettes + CDF (they need only the prepared geometry) and
+    // the regularisers (mesh + maps, into their own gradient buffer) run
+    // beside the render; the main stream joins them where their results are used.
+    const bool lap_here = c->rank == 0;  // computed once across ranks (SURVEY §8(e))
+    const bool reg_here = lap_here && reg;
+    CDR_CUDA_CHECK(cudaEventRecord(c->ev_fork, s));
+    CDR_CUDA_CHECK(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    c->reg_vals.ensure(4);
+    {
+        OnSideStream side(c);
+        if (st->boundary_term) {
+            set_view_calls(c, slots.data(), samples.data(), n);
+            launch_silhouettes(c, n);
+            launch_cdf(c, n);
+        }
+        CDR_CUDA_CHECK(cudaEventRecord(c->ev_sil, c->stream));
+        CDR_CUDA_CHECK(cudaMemsetAsync(c->reg_vals.p, 0, sizeof(double) * 4, c->stream));
+        if (reg_here) {
+            c->reg_grad.ensure(std::max<int64_t>(1, lay->total));
+            CDR_CUDA_CHECK(cudaMemsetAsync(c->reg_grad.p, 0, sizeof(double) * std::max<int64_t>(1, lay->total),
+                                           c->stream));
+            launch_regularisers(c, *reg, *lay, c->reg_grad.p, c->reg_vals.p);
+        }
+        CDR_CUDA_CHECK(cudaEventRecord(c->ev_reg, c->stream));
+    }
     RenderArgs a = render_args(c, st, lay);
     a.use_mask = use_mask;
     launch_render(c, slots.data(), n, a, true, true, true, scales.data(), ev[7]);
     CDR_CUDA_CHECK(cudaEventRecord(ev[2], s));
-    if (st->boundary_term) {
-        set_view_calls(c, slots.data(), samples.data(), n);
-        launch_silhouettes(c, n);
-        launch_cdf(c, n);
-    }
+    CDR_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_sil, 0));  // segments + CDF for the boundary pass
     CDR_CUDA_CHECK(cudaEventRecord(ev[3], s));
     if (st->boundary_term)  // the render above built candidate lists for exactly these views
         launch_boundary(c, n, max_samples, st->seed, CDR_PROBE_RADIANCE, lay->positions, /*use_beam=*/true);
     CDR_CUDA_CHECK(cudaEventRecord(ev[4], s));
     launch_texel_flush(c, lay->diffuse, lay->specular, lay->roughness);
     launch_finalize_positions(c, lay->positions);
-    const bool lap_here = c->rank == 0;  // computed once across ranks (SURVEY §8(e))
     if (lap_here) launch_laplacian(c, lap_mode, lambda_lap, c->grad.p + lay->positions);
-    c->reg_vals.ensure(4);
-    CDR_CUDA_CHECK(cudaMemsetAsync(c->reg_vals.p, 0, sizeof(double) * 4, s));
-    if (lap_here && reg) launch_regularisers(c, *reg, *lay, c->grad.p, c->reg_vals.p);
+    CDR_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_reg, 0));  // the regularisers' gradient and values
+    if (reg_here) launch_axpy(c, c->grad.p, c->reg_grad.p, lay->total);  // grad += reg_grad
     CDR_CUDA_CHECK(cudaEventRecord(ev[5], s));
     if (c->nccl_comm)
         nccl_check(nccl().allReduce(c->grad.p, c->grad.p, size_t(lay->total), kNcclFloat64, kNcclSum, c->nccl_comm, s),

@@ -70,6 +70,8 @@ struct Timer {
 
 struct cdr_ctx {
     int device = 0;
+    cudaStream_t side = nullptr;  // silhouettes + CDF and the regularisers run here, beside the render
+    cudaEvent_t ev_fork = nullptr, ev_sil = nullptr, ev_reg = nullptr;
     cdr_ctx* geo = nullptr;  // geometry-only context of cdr_self_intersects / cdr_evolve (lazy)
     uint64_t topo_version = 0;  // bumped by cdr_set_mesh; geo->topo_version = the copy it holds
     // resident optimiser (optimize.cu): AdamState (optimize.hpp:20-28) on the device
