@@ -9,6 +9,8 @@
  *   CDR_ERR_SIZE_MISMATCH  -> collodiff::SizeMismatch       (errors.hpp:24-26)
  *   CDR_ERR_NONFINITE      -> collodiff::NonFiniteGradient  (errors.hpp:28-30)
  *   CDR_ERR_ERROR          -> collodiff::Error              (errors.hpp:8-10)
+ *   CDR_ERR_SELF_INTERSECTING  -> collodiff::InputSelfIntersecting (errors.hpp:32-34)
+ *   CDR_ERR_PROJECTION_TOO_FAR -> collodiff::ProjectionTooFar      (errors.hpp:40-42)
  *   CDR_ERR_CUDA / _NO_DEVICE / _INVALID_ARG -> collodiff::Error
  *
  * Each entry point names the reference interface it replaces (file:line is

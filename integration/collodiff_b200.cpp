@@ -53,6 +53,8 @@ namespace {
 [[noreturn]] void raise(int rc, const std::string& msg) {
     if (rc == CDR_ERR_SIZE_MISMATCH) throw SizeMismatch(msg);
     if (rc == CDR_ERR_NONFINITE) throw NonFiniteGradient(msg);
+    if (rc == CDR_ERR_SELF_INTERSECTING) throw InputSelfIntersecting();
+    if (rc == CDR_ERR_PROJECTION_TOO_FAR) throw ProjectionTooFar(msg);
     throw Error("cdr: " + msg);
 }
 
