@@ -115,7 +115,7 @@ def test_gpu_resident_loop_matches_oracle(light):
     """total_loss -> adam_step -> evolve, three iterations, entirely on the
     device; every step checked bit for bit against the oracle fed the same
     device gradient."""
-    from paper_2103_15208_b200.api import AdamConfig, LossWeights, RenderSettings, Renderer
+    from paper_2103_15208_b200.api import AdamConfig, RenderSettings, Renderer
     sc = S.make_scene(S.blob(4), 16, 2, 32)
     spp, seed = 4, 3
     tg = _targets(sc, spp, seed)
@@ -164,7 +164,6 @@ def test_gpu_resident_loop_matches_oracle(light):
         b = r2.render(k, st)
         np.testing.assert_array_equal(a[0], b[0])
         np.testing.assert_array_equal(a[2], b[2])
-    del LossWeights
 
 
 @pytest.mark.gpu
@@ -228,3 +227,32 @@ def test_gpu_evolve_rejects_self_intersecting_input():
     r = Renderer(0, S.Scene(m, d, s, rr, S.sample_views_on_sphere(1, 2.5, 11, 40, 8, 8)))
     with pytest.raises(InputSelfIntersecting):
         r.evolve(np.zeros_like(z["evolve_bad_pos"]))
+
+
+@pytest.mark.gpu
+def test_gpu_optimiser_and_query_errors():
+    """Error behaviour of the new entry points, as the reference's exceptions."""
+    from paper_2103_15208_b200.api import AdamConfig, CollodiffError, NonFiniteGradient, Renderer, SizeMismatch
+    sc = _adam_scene()
+    r = Renderer(0, sc)
+    lay = layout_for(sc)
+    with pytest.raises(CollodiffError):  # no optimiser state yet
+        r.adam_step()
+    r.adam_init(AdamConfig(), lay)
+    with pytest.raises(SizeMismatch):  # no gradient of this layout yet (adam.cpp:10-11)
+        r.adam_step()
+    g = np.zeros(lay["total"])
+    g[3] = np.inf
+    r.set_grad(g)
+    before = r.params(lay)
+    with pytest.raises(NonFiniteGradient):  # adam.cpp:12-13: nothing is updated
+        r.adam_step()
+    np.testing.assert_array_equal(r.params(lay), before)
+    m, v, step = r.adam_state()
+    assert step == 0 and not m.any() and not v.any()
+    bad = sc.mesh.triangles.copy()
+    bad[0, 0] = sc.mesh.V + 5
+    with pytest.raises(CollodiffError):
+        r.self_intersects(sc.mesh.positions, bad)
+    with pytest.raises(CollodiffError):
+        r.closest_points(sc.mesh.positions, bad, np.zeros((1, 3)))
