@@ -269,6 +269,10 @@ void cdr_destroy(cdr_ctx* c) {
     cudaSetDevice(c->device);
     if (c->geo) cdr_destroy(c->geo);
     c->si_pairs.release();
+    free_render_statics(c);
+    free_boundary_statics(c);
+    for (auto& b : c->scr_d) b.release();
+    c->scr_i.release(); c->scr_f.release(); c->scr_flag.release(); c->scr_u64.release();
     if (c->nccl_comm && nccl().ok) nccl().commDestroy(c->nccl_comm);
     cudaStreamSynchronize(c->stream);
     for (auto& e : c->ev) cudaEventDestroy(e);
@@ -530,7 +534,7 @@ int cdr_set_target_f32(cdr_ctx* c, int32_t view, const float* rgb, const float* 
     if (!rgb) throw ApiErr(CDR_ERR_INVALID_ARG, "target rgb is null");
     ViewData& v = c->views[view];
     const size_t np = size_t(v.cam.W) * v.cam.H;
-    static thread_local DBuf<float> stage;
+    DBuf<float>& stage = c->scr_f;
     h2d(stage, rgb, 3 * np, c->stream);
     launch_widen(c, stage.p, int64_t(3 * np), c->target.p + 3 * v.pix_off);
     v.has_target = true;
@@ -592,8 +596,8 @@ int cdr_radiance_at(cdr_ctx* c, int32_t view, int32_t n, const double* xy, doubl
     check_ready(c);
     if (n <= 0) return;
     ensure_prepared(c);
-    static thread_local DBuf<double> dxy, drgb;
-    static thread_local DBuf<int32_t> dtri;
+    DBuf<double>&dxy = c->scr_d[0], &drgb = c->scr_d[1];
+    DBuf<int32_t>& dtri = c->scr_i;
     h2d(dxy, xy, 2 * size_t(n), c->stream);
     drgb.ensure(3 * size_t(n));
     dtri.ensure(n);
@@ -623,7 +627,7 @@ int cdr_view_loss(cdr_ctx* c, int32_t w, int32_t h, const double* rendered, cons
         n_valid = double(w) * h;
     }
     const double scale = lambda / n_valid;
-    static thread_local DBuf<double> dr, dt, dm, da, ds;
+    DBuf<double>&dr = c->scr_d[0], &dt = c->scr_d[1], &dm = c->scr_d[2], &da = c->scr_d[3], &ds = c->scr_d[4];
     h2d(dr, rendered, 3 * np, c->stream);
     h2d(dt, target, 3 * np, c->stream);
     if (masked) h2d(dm, tmask, np, c->stream);
@@ -856,7 +860,7 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
     double terms[6] = {0.0, lap_here ? lambda_lap * lap_sq : 0.0, regv[0], regv[1], regv[2], regv[3]};
     for (int i = 0; i < n; ++i) terms[0] += scales[i] * lacc[slots[i]];
     if (c->nccl_comm) {  // sum the loss terms of all view shards
-        static thread_local DBuf<double> dterm;
+        DBuf<double>& dterm = c->scr_d[0];
         dterm.ensure(6);
         CDR_CUDA_CHECK(cudaMemcpyAsync(dterm.p, terms, sizeof(terms), cudaMemcpyHostToDevice, s));
         nccl_check(nccl().allReduce(dterm.p, dterm.p, 6, kNcclFloat64, kNcclSum, c->nccl_comm, s),
@@ -1091,8 +1095,8 @@ int cdr_closest_points(cdr_ctx* c, const double* positions, int32_t nv, const in
         return;
     }
     cdr_ctx* g = load_geometry(c, positions, nv, triangles, nt);
-    static thread_local DBuf<double> q, pt, di, ba;
-    static thread_local DBuf<int32_t> tr;
+    DBuf<double>&q = g->scr_d[0], &pt = g->scr_d[1], &di = g->scr_d[2], &ba = g->scr_d[3];
+    DBuf<int32_t>& tr = g->scr_i;
     h2d(q, queries, 3 * size_t(nq), g->stream);
     tr.ensure(nq);
     pt.ensure(3 * size_t(nq));

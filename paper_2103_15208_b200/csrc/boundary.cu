@@ -451,15 +451,21 @@ struct BStatics {
     int n_calls = 0;
 };
 
-BStatics& bstatics(cdr_ctx* c) {
-    static thread_local std::vector<std::pair<cdr_ctx*, BStatics*>> reg;
-    for (auto& e : reg)
-        if (e.first == c) return *e.second;
-    reg.push_back({c, new BStatics()});
-    return *reg.back().second;
+BStatics& bstatics(cdr_ctx* c) {  // owned by the context (free_boundary_statics)
+    if (!c->boundary_statics) c->boundary_statics = new BStatics();
+    return *static_cast<BStatics*>(c->boundary_statics);
 }
 
 }  // namespace
+
+void free_boundary_statics(cdr_ctx* c) {
+    auto* st = static_cast<BStatics*>(c->boundary_statics);
+    if (!st) return;
+    st->calls.release();
+    st->pix_off.release();
+    delete st;
+    c->boundary_statics = nullptr;
+}
 
 void set_view_calls(cdr_ctx* c, const int* view_slots, const int* samples, int n_views) {
     BStatics& st = bstatics(c);

@@ -73,6 +73,15 @@ struct cdr_ctx {
     cudaStream_t side = nullptr;  // silhouettes + CDF and the regularisers run here, beside the render
     cudaEvent_t ev_fork = nullptr, ev_sil = nullptr, ev_reg = nullptr;
     cdr_ctx* geo = nullptr;  // geometry-only context of cdr_self_intersects / cdr_evolve (lazy)
+    // Per-context scratch (device memory of this context's GPU): used inside one
+    // synchronous entry point at a time, never across calls.
+    cdr::DBuf<double> scr_d[5];
+    cdr::DBuf<int32_t> scr_i;
+    cdr::DBuf<float> scr_f;
+    cdr::DBuf<int> scr_flag;
+    cdr::DBuf<unsigned long long> scr_u64;
+    void* render_statics = nullptr;    // render.cu (freed by free_render_statics)
+    void* boundary_statics = nullptr;  // boundary.cu (freed by free_boundary_statics)
     uint64_t topo_version = 0;  // bumped by cdr_set_mesh; geo->topo_version = the copy it holds
     // resident optimiser (optimize.cu): AdamState (optimize.hpp:20-28) on the device
     bool adam_ready = false;

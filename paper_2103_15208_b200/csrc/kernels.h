@@ -33,7 +33,9 @@ inline ShadeScene shade_scene(const cdr_ctx* c) {
 // (mesh.cpp:65-95), bbox + t_min (bvh.cpp:92), LBVH (Morton -> radix sort ->
 // Karras hierarchy -> bottom-up fp32 refit).
 void launch_prepare(cdr_ctx* c, double cam_abs_max);
-void launch_bvh(cdr_ctx* c, double cam_abs_max);  // bbox + t_min + LBVH (no normals)
+void launch_bvh(cdr_ctx* c, double cam_abs_max);
+void free_render_statics(cdr_ctx* c);    // render.cu per-context buffers
+void free_boundary_statics(cdr_ctx* c);  // boundary.cu per-context buffers  // bbox + t_min + LBVH (no normals)
 // self_intersects (mesh.cpp:184-214) on the context's mesh and LBVH: returns
 // the number of intersecting pairs (early exit after the first when pairs ==
 // nullptr); pairs (f < g) written up to cap, in no particular order.

@@ -116,7 +116,7 @@ int grid_for(int64_t n) { return int(std::max<int64_t>(1, std::min<int64_t>((n +
 }  // namespace
 
 bool any_nonfinite(cdr_ctx* c, const double* g, int64_t n) {
-    static thread_local DBuf<int> flag;
+    DBuf<int>& flag = c->scr_flag;
     flag.ensure(1);
     CDR_CUDA_CHECK(cudaMemsetAsync(flag.p, 0, sizeof(int), c->stream));
     ++c->launches;
@@ -155,7 +155,7 @@ void launch_adam(cdr_ctx* c, const double* grad, double corr1, double corr2) {
 }
 
 double min_triangle_area(cdr_ctx* c, const double* pos) {
-    static thread_local DBuf<unsigned long long> out;
+    DBuf<unsigned long long>& out = c->scr_u64;
     out.ensure(1);
     CDR_CUDA_CHECK(cudaMemsetAsync(out.p, 0xff, sizeof(unsigned long long), c->stream));
     if (c->T > 0) {
@@ -179,7 +179,7 @@ void launch_candidate(cdr_ctx* c, const double* pos, const double* disp, double 
 }
 
 bool any_nonzero(cdr_ctx* c, const double* d, int64_t n) {
-    static thread_local DBuf<int> flag;
+    DBuf<int>& flag = c->scr_flag;
     flag.ensure(1);
     CDR_CUDA_CHECK(cudaMemsetAsync(flag.p, 0, sizeof(int), c->stream));
     ++c->launches;

@@ -968,13 +968,9 @@ struct RenderStatics {
     DBuf<unsigned char> has_mask;
 };
 
-static RenderStatics& statics(cdr_ctx* c) {
-    // one per context: keyed by address in a small registry
-    static thread_local std::vector<std::pair<cdr_ctx*, RenderStatics*>> reg;
-    for (auto& e : reg)
-        if (e.first == c) return *e.second;
-    reg.push_back({c, new RenderStatics()});
-    return *reg.back().second;
+static RenderStatics& statics(cdr_ctx* c) {  // owned by the context (free_render_statics)
+    if (!c->render_statics) c->render_statics = new RenderStatics();
+    return *static_cast<RenderStatics*>(c->render_statics);
 }
 
 template <int kSPP>
@@ -1009,6 +1005,16 @@ static void launch_trace_kernel(const Params& p, dim3 grid, cdr_ctx* c) {
     else if (p.use_beam) k_trace<true, 0><<<grid, kThreads, 0, c->stream>>>(p);
     else if (p.spp == 16) k_trace<false, 16><<<g16, kTraceThreads16, 0, c->stream>>>(p);
     else k_trace<false, 0><<<grid, kThreads, 0, c->stream>>>(p);
+}
+
+void free_render_statics(cdr_ctx* c) {
+    auto* st = static_cast<RenderStatics*>(c->render_statics);
+    if (!st) return;
+    st->calls.release();
+    st->pix_off.release();
+    st->has_mask.release();
+    delete st;
+    c->render_statics = nullptr;
 }
 
 void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a, bool trace,

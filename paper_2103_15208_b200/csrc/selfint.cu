@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kSiBlock) k_self_intersect(const BNode* __rest
 
 long long launch_self_intersect(cdr_ctx* c, int2* pairs, long long cap) {
     if (c->T < 2) return 0;
-    static thread_local DBuf<unsigned long long> cnt;
+    DBuf<unsigned long long>& cnt = c->scr_u64;
     cnt.ensure(1);
     CDR_CUDA_CHECK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), c->stream));
     ++c->launches;
