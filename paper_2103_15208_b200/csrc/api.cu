@@ -192,11 +192,8 @@ struct NcclUid {
     char internal[128];
 };
 
-NcclApi& nccl() {
-    static NcclApi api;
-    static bool tried = false;
-    if (tried) return api;
-    tried = true;
+NcclApi load_nccl() {
+    NcclApi api;
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
     for (const char* n : names) {
         api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
@@ -210,6 +207,11 @@ NcclApi& nccl() {
     api.commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclCommDestroy"));
     api.getErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(api.h, "ncclGetErrorString"));
     api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy;
+    return api;
+}
+
+NcclApi& nccl() {
+    static NcclApi api = load_nccl();  // loaded once, thread-safe (C++11 static init)
     return api;
 }
 
