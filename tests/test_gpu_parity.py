@@ -362,3 +362,19 @@ def test_odd_image_sizes_exact(wh):
             np.testing.assert_array_equal(mask, mo)
             np.testing.assert_array_equal(rgb, ro)
     _loss_grad_check(sc, 16, 3, param_layout(sc))
+
+
+@pytest.mark.parametrize("knob", ["CDR_NO_BEAM", "CDR_CHUNK_MB", "CDR_NO_SHARED_TOP"])
+def test_alternate_paths_exact(sphere, monkeypatch, knob):
+    """The A/B switches kept in the code (per-ray traversal only; view chunks
+    through lists -> trace -> shade; every tile from the BVH root) stay exact."""
+    monkeypatch.setenv(knob, "1")
+    blob = blob_scene(freq=8, tex=32, views=2, image=48)
+    r, o = _pair(blob)
+    st = RenderSettings(spp=16, seed=4)
+    for v in range(len(blob.cameras)):
+        rgb, mask, hit = r.render(v, st)
+        ro, mo, ho = o.render(v, 16, 4)
+        np.testing.assert_array_equal(hit, ho)
+        np.testing.assert_array_equal(rgb, ro)
+    _loss_grad_check(blob, 16, 4, param_layout(blob))
