@@ -6,6 +6,8 @@
 // include/cdr.h (libcdr.so, sm_100a):
 //
 //   render               render.hpp:67-68       -> cdr_render
+//   radiance_at          render.hpp:61-62       -> cdr_radiance_at (hit_out
+//                        rebuilt on the host from the device's triangle id)
 //   view_rendering_loss  losses.hpp:37-38       -> cdr_view_loss
 //   interior_pass        diff_render.hpp:48-50  -> cdr_interior_pass
 //   boundary_pass        diff_render.hpp:56-59  -> cdr_boundary_pass
@@ -38,6 +40,8 @@
 #include <vector>
 
 #include "cdr.h"
+#include "collodiff/bvh.hpp"
+#include "collodiff/camera.hpp"
 #include "collodiff/diff_render.hpp"
 #include "collodiff/errors.hpp"
 #include "collodiff/laplacian.hpp"
@@ -248,6 +252,34 @@ Image render(const Scene& scene, const SceneContext&, int view, const RenderSett
     d.check(cdr_render(d.ctx, view, &st, reinterpret_cast<double*>(img.pixels.data()), img.mask.data(),
                        hit_cache ? hit_cache->data() : nullptr));
     return img;
+}
+
+// radiance_at (render.hpp:61-62, render.cpp:24-33). The device returns the
+// radiance and the hit triangle; when hit_out is requested the record is
+// rebuilt with the reference's own primary_ray / ray_triangle /
+// make_hit_record on that triangle (the same fp64 arithmetic the device
+// replays, so t and the barycentrics are the device's).
+Vec3 radiance_at(const Scene& scene, const SceneContext& ctx, int view, const Vec2& x,
+                 std::optional<HitRecord>* hit_out) {
+    Device& d = dev();
+    d.scene(scene);
+    const double xy[2] = {x.x, x.y};
+    double rgb[3];
+    int32_t tri = -1;
+    d.check(cdr_radiance_at(d.ctx, view, 1, xy, rgb, &tri));
+    if (hit_out) {
+        if (tri < 0) {
+            *hit_out = std::nullopt;
+        } else {
+            const Ray ray = primary_ray(scene.views[view], x);
+            const auto& f = scene.mesh.triangles[size_t(tri)];
+            const auto& P = scene.mesh.positions;
+            double t = 0, b1 = 0, b2 = 0;
+            ray_triangle(ray.origin, ray.dir, P[size_t(f[0])], P[size_t(f[1])], P[size_t(f[2])], t, b1, b2);
+            *hit_out = make_hit_record(scene.mesh, &ctx.normals, tri, t, b1, b2, ray.origin, ray.dir);
+        }
+    }
+    return Vec3(rgb[0], rgb[1], rgb[2]);
 }
 
 ViewLossResult view_rendering_loss(const Image& rendered, const Image& target, double lambda_rend,

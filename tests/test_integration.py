@@ -1,0 +1,64 @@
+"""Link-level drop-in: the reference's OWN unit
+tests (/root/reference/proj/tests/*.cpp, unmodified, built by
+integration/Makefile against integration/doctest_min/doctest.h) linked twice:
+
+  unit_ref   the reference library alone (CPU)
+  unit_b200  the reference objects with the hot-path symbols weakened, resolved
+             to integration/collodiff_b200.cpp over libcdr.so (B200)
+
+Both must report the same outcome for every test case, and every case that
+routes through the shim (render, radiance_at, extract_silhouettes,
+cotangent_laplacian, point_to_mesh_distance, self_intersects) must pass. The
+binaries are built in the container that has /root/reference and travel to the
+GPU box with the snapshot; the test skips when they are absent.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BUILD = os.path.join(ROOT, "integration", "_build")
+
+# test cases whose code calls a symbol the shim replaces
+SHIM_ROUTED = re.compile(r"^(radiance_at|render|laplacian|point_to_mesh_distance|self_intersects|silhouette)")
+
+
+def _run(binary, timeout=600):
+    p = subprocess.run([binary], capture_output=True, text=True, timeout=timeout)
+    cases = {}
+    for line in p.stdout.splitlines():
+        m = re.match(r"^TEST (PASS|FAIL) (\S+) (.*)$", line)
+        if m:
+            cases[(m.group(2), m.group(3))] = m.group(1)
+    summary = [l for l in p.stdout.splitlines() if l.startswith("SUMMARY")]
+    assert summary, f"{binary} did not finish:\n{p.stdout[-2000:]}\n{p.stderr[-2000:]}"
+    return cases, p.stdout
+
+
+def _need(name):
+    path = os.path.join(BUILD, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not built (make -C integration, needs /root/reference)")
+    return path
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_through_the_shim():
+    ref, _ = _run(_need("unit_ref"))
+    b200, out = _run(_need("unit_b200"))
+    assert set(ref) == set(b200)
+    routed = [k for k in b200 if SHIM_ROUTED.match(k[1])]
+    assert len(routed) >= 20, routed
+    diff = {k: (ref[k], b200[k]) for k in ref if ref[k] != b200[k]}
+    assert not diff, f"outcome differs (ref, b200): {diff}\n{out}"
+    failed_routed = [k for k in routed if b200[k] != "PASS"]
+    assert not failed_routed, f"{failed_routed}\n{out}"
+
+
+@pytest.mark.gpu
+def test_unit_b200_loads_libcdr():
+    path = _need("unit_b200")
+    p = subprocess.run(["ldd", path], capture_output=True, text=True)
+    assert "libcdr.so" in p.stdout and "not found" not in p.stdout, p.stdout
