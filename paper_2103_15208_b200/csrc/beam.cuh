@@ -32,8 +32,15 @@ namespace cdr {
 #define CDR_FRONT_CAP 256
 #endif
 constexpr int kBeamCap = CDR_BEAM_CAP;    // candidates per tile; more -> per-ray traversal
-constexpr int kPixCap = 16;               // candidates per pixel list; more -> scan the tile list
-constexpr int kBigPixCap = 64;            // the same for big tiles (over kBeamCap candidates)
+#ifndef CDR_PIX_CAP
+#define CDR_PIX_CAP 64
+#endif
+#ifndef CDR_BIG_PIX_CAP
+#define CDR_BIG_PIX_CAP 128
+#endif
+constexpr int kPixCap = CDR_PIX_CAP;         // candidates per pixel list; more -> scan the tile list
+constexpr int kBigPixCap = CDR_BIG_PIX_CAP;  // the same for big tiles (over kBeamCap candidates)
+static_assert(kPixCap < 255 && kBigPixCap < 255, "255 marks an overflowed pixel list");
 constexpr int kFrontCap = CDR_FRONT_CAP;  // builder frontier per tile; more -> per-ray traversal
 
 // Candidate record (48 B): three edge functions E_i = A_i x + B_i y + C_i
@@ -113,15 +120,13 @@ __device__ __forceinline__ Hit trace_beam(const BeamCand* __restrict__ cand, int
                                           D3 o, D3 d, double t_min, float px, float py) {
     Hit best{-1, 1e300, 0.0, 0.0};
     for (int k = 0; k < n; ++k) {
-        const float4 e2 = cand[k].e2;
+        // the whole 48-B record in one round trip (the edge functions are
+        // needed unless the bound stops the scan)
+        const float4 e2 = cand[k].e2, e0 = cand[k].e0, e1 = cand[k].e1;
         if (double(e2.y) > best.t) break;  // every remaining candidate is farther
-        const int flags = __float_as_int(e2.w);
-        bool pass = true;
-        if (!(flags & 1)) {
-            const float4 e0 = cand[k].e0, e1 = cand[k].e1;
-            pass = e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
-                   e1.z * px + e1.w * py + e2.x >= 0.0f;
-        }
+        const bool pass = (__float_as_int(e2.w) & 1) ||
+                          (e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
+                           e1.z * px + e1.w * py + e2.x >= 0.0f);
         if (pass) leaf_test(recs, __float_as_int(e2.z), o, d, t_min, best);
     }
     return best;
@@ -134,14 +139,11 @@ __device__ __forceinline__ Hit trace_beam_list(const BeamCand* __restrict__ cand
     Hit best{-1, 1e300, 0.0, 0.0};
     for (int j = 0; j < n; ++j) {
         const int k = idx[j];
-        const float4 e2 = cand[k].e2;
+        const float4 e2 = cand[k].e2, e0 = cand[k].e0, e1 = cand[k].e1;
         if (double(e2.y) > best.t) break;
-        bool pass = true;
-        if (!(__float_as_int(e2.w) & 1)) {
-            const float4 e0 = cand[k].e0, e1 = cand[k].e1;
-            pass = e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
-                   e1.z * px + e1.w * py + e2.x >= 0.0f;
-        }
+        const bool pass = (__float_as_int(e2.w) & 1) ||
+                          (e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
+                           e1.z * px + e1.w * py + e2.x >= 0.0f);
         if (pass) leaf_test(recs, __float_as_int(e2.z), o, d, t_min, best);
     }
     return best;
@@ -194,6 +196,16 @@ __device__ __forceinline__ Hit trace_point(const BeamView& bv, int vi, const Dev
 // edge sample): the same scans as trace_point, stepped in one loop so each
 // thread keeps two independent candidate -> triangle load chains in flight.
 // Per-ray traversal (off-image points, overflowing tiles) runs afterwards.
+#ifdef CDR_TRACE_STATS
+// debug build only: [0] per-ray (off-image / no lists), [1] per-ray (overflow
+// tile), [2] small-tile pixel list, [3] big-tile pixel list, [4] whole small
+// tile scanned, [5] whole big tile scanned, [6] scan steps, [7] empty list
+static __device__ unsigned long long g_probe_stats[8];
+#define CDR_PSTAT(i, v) atomicAdd(&g_probe_stats[i], (unsigned long long)(v))
+#else
+#define CDR_PSTAT(i, v)
+#endif
+
 struct ProbeScan {
     const BeamCand* cand;
     const unsigned char* lst;  // nullptr: scan the whole tile list
@@ -207,15 +219,24 @@ __device__ __forceinline__ void probe_setup(const BeamView& bv, int vi, const De
     s.best = Hit{-1, 1e300, 0.0, 0.0};
     s.mode = 2;
     s.j = 0;
-    if (!bv.valid) return;
+    if (!bv.valid) {
+        CDR_PSTAT(0, 1);
+        return;
+    }
     const double fx = floor(x.x), fy = floor(x.y);
-    if (!(fx >= 0 && fy >= 0 && fx < cam.W && fy < cam.H)) return;
+    if (!(fx >= 0 && fy >= 0 && fx < cam.W && fy < cam.H)) {
+        CDR_PSTAT(0, 1);
+        return;
+    }
     const int px = int(fx), py = int(fy);
     const int tiles_x = (cam.W + bv.TW - 1) / bv.TW;
     const int tx = px / bv.TW, ty = py / bv.TH;
     const size_t tile = size_t(bv.tile_base[vi]) + ty * tiles_x + tx;
     const TileHdr h = bv.hdr[tile];
-    if (h.cnt < 0) return;
+    if (h.cnt < 0) {
+        CDR_PSTAT(1, 1);
+        return;
+    }
     const int q = (py - ty * bv.TH) * bv.TW + (px - tx * bv.TW);
     const size_t li = h.big >= 0 ? size_t(h.big) * bv.P + q : tile * bv.P + q;
     const int cnt = h.big >= 0 ? bv.big_pix_cnt[li] : bv.pix_cnt[li];
@@ -230,6 +251,7 @@ __device__ __forceinline__ void probe_setup(const BeamView& bv, int vi, const De
         s.n = cnt;
     }
     s.mode = s.n > 0 ? 1 : 0;
+    CDR_PSTAT(s.n == 0 ? 7 : (cnt == 255 ? (h.big >= 0 ? 5 : 4) : (h.big >= 0 ? 3 : 2)), 1);
 }
 
 // one candidate of trace_beam / trace_beam_list
@@ -240,17 +262,15 @@ __device__ __forceinline__ void probe_step(ProbeScan& s, const TriRec* __restric
     }
     const int k = s.lst ? int(s.lst[s.j]) : s.j;
     ++s.j;
-    const float4 e2 = s.cand[k].e2;
+    CDR_PSTAT(6, 1);
+    const float4 e2 = s.cand[k].e2, e0 = s.cand[k].e0, e1 = s.cand[k].e1;
     if (double(e2.y) > s.best.t) {  // every remaining candidate is farther
         s.mode = 0;
         return;
     }
-    bool pass = true;
-    if (!(__float_as_int(e2.w) & 1)) {
-        const float4 e0 = s.cand[k].e0, e1 = s.cand[k].e1;
-        pass = e0.x * s.lx + e0.y * s.ly + e0.z >= 0.0f && e0.w * s.lx + e1.x * s.ly + e1.y >= 0.0f &&
-               e1.z * s.lx + e1.w * s.ly + e2.x >= 0.0f;
-    }
+    const bool pass = (__float_as_int(e2.w) & 1) ||
+                      (e0.x * s.lx + e0.y * s.ly + e0.z >= 0.0f && e0.w * s.lx + e1.x * s.ly + e1.y >= 0.0f &&
+                       e1.z * s.lx + e1.w * s.ly + e2.x >= 0.0f);
     if (pass) leaf_test(recs, __float_as_int(e2.z), o, d, t_min, s.best);
 }
 

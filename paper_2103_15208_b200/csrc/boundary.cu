@@ -354,16 +354,14 @@ __global__ void k_bscatter(BParams p) {
 #define CDR_BND_BLOCK 128
 #endif
 constexpr int kBndBlock = CDR_BND_BLOCK;  // probe costs vary per warp: a CTA waits for its slowest
-__global__ void __launch_bounds__(kBndBlock, CDR_BOUNDARY_MIN_BLOCKS * 256 / kBndBlock) k_boundary(BParams p) {
-    const int vi = blockIdx.y;
-    const int lane = threadIdx.x & 31;
-    const DevCamera cam = p.cams[p.calls[vi].slot];
-    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int n_act = p.n_active[vi];
-    if (int64_t(blockIdx.x) * blockDim.x >= n_act) return;  // whole CTA idle (uniform)
+
+// One warp-wide step: sample j (< n_act: active) of view vi, lanes holding
+// consecutive grouped samples. Returns the warp's count of samples with a
+// non-zero contribution (uniform across the warp).
+__device__ __forceinline__ int boundary_samples(const BParams& p, int vi, const DevCamera& cam, int64_t j, bool act,
+                                                int lane) {
     // the RNG pick and lower_bound were done in pass 1: read the grouped result
     BSample b;
-    bool act = j < n_act;
     if (act) {
         const size_t o = size_t(vi) * p.m_stride + j;
         b.si = p.sorted_si[o];
@@ -414,10 +412,7 @@ __global__ void __launch_bounds__(kBndBlock, CDR_BOUNDARY_MIN_BLOCKS * 256 / kBn
             act = false;
         }
     }
-    {
-        int na = __syncthreads_count(act);
-        if (threadIdx.x == 0 && na) atomicAdd(&p.counters->boundary_active, (unsigned long long)na);
-    }
+    const int na = __popc(__ballot_sync(0xffffffffu, act));
     double v[6] = {0, 0, 0, 0, 0, 0};
     if (act) {
         const cdr_segment* sg = b.sg;
@@ -443,6 +438,18 @@ __global__ void __launch_bounds__(kBndBlock, CDR_BOUNDARY_MIN_BLOCKS * 256 / kBn
             if (v[3 + c] != 0) atomicAdd(g + 3 * int64_t(b.sg->v1) + c, v[3 + c]);
         }
     }
+    return na;
+}
+
+__global__ void __launch_bounds__(kBndBlock, CDR_BOUNDARY_MIN_BLOCKS * 256 / kBndBlock) k_boundary(BParams p) {
+    const int vi = blockIdx.y;
+    const int lane = threadIdx.x & 31;
+    const DevCamera cam = p.cams[p.calls[vi].slot];
+    const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int n_act = p.n_active[vi];
+    if (int64_t(blockIdx.x) * blockDim.x >= n_act) return;  // whole CTA idle (uniform)
+    const int na = boundary_samples(p, vi, cam, j, j < n_act, lane);
+    if (lane == 0 && na) atomicAdd(&p.counters->boundary_active, (unsigned long long)na);
 }
 
 struct BStatics {
@@ -585,6 +592,13 @@ extern "C" int cdr_debug_trace_stats_boundary(unsigned long long out[4]) {
     cudaMemcpyFromSymbol(out, cdr::g_trace_stats, sizeof(unsigned long long) * 4);
     unsigned long long z[4] = {0, 0, 0, 0};
     cudaMemcpyToSymbol(cdr::g_trace_stats, z, sizeof(z));
+    return 0;
+}
+
+extern "C" int cdr_debug_probe_stats(unsigned long long out[8]) {
+    cudaMemcpyFromSymbol(out, cdr::g_probe_stats, sizeof(unsigned long long) * 8);
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(cdr::g_probe_stats, z, sizeof(z));
     return 0;
 }
 #endif
