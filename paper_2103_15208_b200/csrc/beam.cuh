@@ -113,6 +113,32 @@ __device__ __forceinline__ bool cand_overlaps_pixel(const BeamCand& c, float x0,
     return true;
 }
 
+// cand_overlaps_pixel for every pixel of a tile of P <= 32 pixels, TW wide:
+// bit q set when pixel (q % TW, q / TW) may be covered. Same arithmetic per
+// pixel as cand_overlaps_pixel, so the same decisions.
+__device__ __forceinline__ unsigned cand_pixel_mask(const BeamCand& c, int TW, int P) {
+    const unsigned all = P >= 32 ? 0xffffffffu : ((1u << P) - 1u);
+    if (__float_as_int(c.e2.w) & 1) return all;
+    const float A[3] = {c.e0.x, c.e0.w, c.e1.z}, B[3] = {c.e0.y, c.e1.x, c.e1.w}, C[3] = {c.e0.z, c.e1.y, c.e2.x};
+    unsigned m = 0;
+    int qx = 0, qy = 0;
+    for (int q = 0; q < P; ++q) {
+        const float x0 = float(qx), y0 = float(qy), x1 = x0 + 1.0f, y1 = y0 + 1.0f;
+        bool in = true;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const float v = A[i] * (A[i] > 0 ? x1 : x0) + B[i] * (B[i] > 0 ? y1 : y0) + C[i];
+            in = in && !(v < 0.0f);
+        }
+        m |= unsigned(in) << q;
+        if (++qx == TW) {
+            qx = 0;
+            ++qy;
+        }
+    }
+    return m;
+}
+
 // Nearest hit of one sample ray using its tile's candidate list (smem or
 // global). Same result as trace(): exact fp64 test, strict t_min < t, ties to
 // the lowest triangle index.

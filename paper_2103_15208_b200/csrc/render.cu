@@ -265,6 +265,33 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
     __syncwarp();  // orders the lanes' pool writes for the per-pixel pass
     // per-pixel lists, in distance order
     const int P = kThreads / p.spp;
+    if (P <= 32) {
+        // lane = candidate: a mask of the tile pixels its triangle may cover
+        // (the same test as cand_overlaps_pixel), then one ballot per pixel
+        // appends the covering candidates in candidate (distance) order
+        unsigned char* lst0 = (big >= 0 ? p.big_pix_list : p.pix_list) + (big >= 0 ? size_t(big) : tile) * P * kPix;
+        int my_cnt = 0;  // list length of pixel q = lane
+        for (int base = 0; base < nl; base += 32) {
+            const int k = base + lane;
+            unsigned mask = 0;
+            if (k < nl) mask = cand_pixel_mask(s_cand[k], p.TW, P);
+            for (int q = 0; q < P; ++q) {
+                const bool on = (mask >> q) & 1u;
+                const unsigned bal = __ballot_sync(0xffffffffu, on);
+                if (!bal) continue;  // warp-uniform
+                const int cq = __shfl_sync(0xffffffffu, my_cnt, q);
+                const int pos = cq + __popc(bal & lt);
+                if (on && pos < kPix) lst0[size_t(q) * kPix + pos] = (unsigned char)k;
+                if (lane == q) my_cnt += __popc(bal);
+            }
+        }
+        if (lane < P) {
+            const size_t li = big >= 0 ? size_t(big) * P + lane : tile * P + lane;
+            (big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li] = (unsigned char)(my_cnt > kPix ? 255 : my_cnt);
+        }
+        if (lane == 0) *hdr = TileHdr{off, nl, big, 0};
+        return true;
+    }
     for (int q = lane; q < P; q += 32) {
         const float qx = float(q % p.TW), qy = float(q / p.TW);
         const size_t li = big >= 0 ? size_t(big) * P + q : tile * P + q;
