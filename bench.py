@@ -292,7 +292,7 @@ def main():
     # ---- roofline of the dominant kernel (fused trace/shade/loss/interior)
     s0 = stats[-1]
     ms_shade = statistics.mean(x["ms_render"] - x["ms_trace"] for x in stats)
-    n_px, n_samp = s0["pixels"], s0["samples"]
+    n_px, n_samp = s0["pixels"], s0["shaded_samples"]  # empty beam tiles read no hit cache
     n_hit, n_adj = s0["hit_samples"], s0["adjoint_samples"]
     algo_bytes = 80 * n_px + 4 * n_samp + 332 * n_hit + 736 * n_adj
     pk, pk_kind = peaks()
@@ -301,7 +301,7 @@ def main():
             "bound": "hbm", "achieved": achieved,
             "peak": pk["hbm_gbs"], "peak_source": pk_kind, "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
             "traffic": None, "algorithmic_bytes_per_launch": algo_bytes,
-            "byte_model": "80*N_px + 4*N_samp + 332*N_hit + 736*N_adj (DESIGN.md §4)",
+            "byte_model": "80*N_px + 4*N_shaded + 332*N_hit + 736*N_adj (DESIGN.md §4)",
             "ms_per_launch": ms_shade, "share_of_step": ms_shade / statistics.mean(ms_steps)}
     traffic_file = os.path.join(ROOT, "profiles", "render_traffic.json")
     if os.path.exists(traffic_file):
@@ -434,7 +434,7 @@ def main():
                 "clocks": clk, "stages_ms": stages,
                 "counters": {k: s0[k] for k in ("pixels", "samples", "hit_samples", "adjoint_samples",
                                                 "boundary_samples", "boundary_active", "segments",
-                                                "beam_fallback_tiles")}}
+                                                "beam_fallback_tiles", "shaded_samples")}}
         print(json.dumps(line), flush=True)
     r.close()
     if dist is not None:

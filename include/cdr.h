@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define CDR_ABI_VERSION 1
+#define CDR_ABI_VERSION 2  /* 2: cdr_stats.shaded_samples appended */
 
 enum {
     CDR_OK = 0,
@@ -130,6 +130,8 @@ typedef struct cdr_stats {
     int64_t kernel_launches;   /* kernels this library launched in the call */
     double ms_trace;           /* primary-visibility kernels (part of ms_render) */
     int64_t beam_fallback_tiles; /* pixel tiles traced per ray (candidate-list overflow) */
+    int64_t shaded_samples;    /* samples through the full shading kernel; the rest lie in
+                                  beam tiles with no candidate triangle (background, no hit read) */
 } cdr_stats;
 
 int cdr_abi_version(void);

@@ -36,6 +36,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -78,6 +79,8 @@ struct Device {
     std::vector<double> buf;
 
     Device() {
+        if (cdr_abi_version() != CDR_ABI_VERSION)  // cdr_stats and friends follow the header's layout
+            throw std::runtime_error("libcdr.so ABI version differs from include/cdr.h: rebuild");
         const char* d = std::getenv("CDR_DEVICE");
         int rc = cdr_create(d ? std::atoi(d) : 0, &ctx);
         if (rc != CDR_OK) raise(rc, "cdr_create failed (no CUDA device?)");

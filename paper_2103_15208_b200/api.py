@@ -92,7 +92,8 @@ class cdr_stats(C.Structure):
                 ("degenerate_skipped", C.c_int32), ("nonfinite", C.c_int32),
                 ("ms_prepare", C.c_double), ("ms_render", C.c_double), ("ms_silhouette", C.c_double),
                 ("ms_boundary", C.c_double), ("ms_finalize", C.c_double), ("ms_total", C.c_double),
-                ("kernel_launches", C.c_int64), ("ms_trace", C.c_double), ("beam_fallback_tiles", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("ms_trace", C.c_double), ("beam_fallback_tiles", C.c_int64),
+                ("shaded_samples", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -108,6 +109,9 @@ _ERRORS = {1: SizeMismatch, 2: NonFiniteGradient, 3: CollodiffError, 4: Collodif
 _lib = None
 
 
+ABI_VERSION = 2  # include/cdr.h CDR_ABI_VERSION
+
+
 def load_library(path: str = LIB_PATH):
     """Load libcdr.so; raises if it was not built (no silent fallback)."""
     global _lib
@@ -116,6 +120,8 @@ def load_library(path: str = LIB_PATH):
     if not os.path.exists(path):
         raise FileNotFoundError(f"{path} missing: run `python -m paper_2103_15208_b200.build`")
     L = C.CDLL(path)
+    if L.cdr_abi_version() != ABI_VERSION:  # the ctypes structs below follow this header version
+        raise RuntimeError(f"{path}: ABI version {L.cdr_abi_version()}, this binding expects {ABI_VERSION}: rebuild")
     L.cdr_last_error.restype = C.c_char_p
     L.cdr_last_error.argtypes = [_vp]
     L.cdr_create.argtypes = [C.c_int, C.POINTER(_vp)]

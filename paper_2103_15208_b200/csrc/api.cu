@@ -886,6 +886,7 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
         stats->adjoint_samples = int64_t(k.adjoint_samples);
         stats->boundary_active = int64_t(k.boundary_active);
         stats->beam_fallback_tiles = int64_t(k.beam_fallback_tiles);
+        stats->shaded_samples = int64_t(k.shaded_samples);
         if (st->boundary_term) {
             std::vector<int32_t> cnt(n), deg(n);
             CDR_CUDA_CHECK(cudaMemcpy(cnt.data(), c->sil_count.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));

@@ -59,6 +59,7 @@ struct Counters {  // device-side work counters (cdr_stats)
     unsigned long long adjoint_samples;
     unsigned long long boundary_active;
     unsigned long long beam_fallback_tiles;  // tiles traced per ray (list overflow)
+    unsigned long long shaded_samples;       // samples through k_render's full path (not an empty beam tile)
     double loss_sum[1];
 };
 

@@ -42,6 +42,7 @@ struct Params {
     uint64_t seed;
     double gamma;
     int use_mask, write_hits;
+    int skip_empty_hits;  // loss calls at spp 16: no hit-cache writes for empty beam tiles (k_render skips them too)
     double* img;
     double* mask;
     double* adj;
@@ -492,6 +493,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kTraceThreads16 : kThreads,
     // records, which the tile's 256 samples share through L1.
     TileHdr th{0, -1, -1, 0};
     if (kBeam) th = p.tile_hdr[vc.tile_base + tile_in_view];
+    if (kBeam && th.cnt == 0 && p.skip_empty_hits) return;  // CTA-uniform: k_render's empty-tile path reads no hits
     if (kBeam && th.cnt >= 0) {
         const size_t tile = size_t(vc.tile_base) + tile_in_view;
         const size_t li = th.big >= 0 ? size_t(th.big) * P + pix : tile * P + pix;
@@ -705,6 +707,25 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
 #ifndef CDR_RENDER_MIN_BLOCKS
 #define CDR_RENDER_MIN_BLOCKS 3
 #endif
+// view_rendering_loss for one (pixel, channel) of the mean radiance: adds the
+// L1 term to loss_part, writes and returns the adjoint (losses.cpp:37-44)
+__device__ __forceinline__ double pixel_loss_adjoint(const Params& p, const ViewCall& vc, size_t qi, int c,
+                                                     double mean, double& loss_part) {
+    const double m = (p.use_mask && p.has_mask[vc.slot]) ? p.target_mask[qi] : 1.0;
+    double a = 0;
+    if (m != 0) {
+        // Φ'(r) = Φ(r) / (γ r) for r in (0, 1); Φ(0) = pow(0, 1/γ) = +0 exactly: skip pow on background
+        const double tr = mean <= 0.0 ? 0.0 : tone_map(mean, p.gamma);
+        const double d = tr - p.target_tone[3 * qi + c];
+        loss_part += m * fabs(d);
+        const double sg = double((d > 0) - (d < 0));
+        const double der = (mean <= 0.0 || mean >= 1.0) ? 0.0 : tr / (p.gamma * mean);
+        a = vc.scale * m * sg * der;
+    }
+    p.adj[3 * qi + c] = a;
+    return a;
+}
+
 template <bool kShade, bool kLoss, bool kInterior, int kSPP>
 __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
                                   kSPP == 16 ? CDR_RENDER_MIN_BLOCKS * kThreads / kRenderThreads16
@@ -732,11 +753,41 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     const size_t pidx = pbase + size_t(y) * W + x;  // arena pixel index
     const D3 org{cam.o[0], cam.o[1], cam.o[2]};
 
+    // Empty beam tile (no candidate at all: k_trace wrote a miss for every
+    // sample): warp 0 writes the 8 pixels' background mean, mask, loss and
+    // adjoint straight away; no hit loads, no staging, no barrier.
+    if (kSPP == 16 && kShade && kLoss && p.use_beam) {
+        const TileHdr th = p.tile_hdr[size_t(vc.tile_base) + (Y0 / 4) * vc.tiles_x + int(blockIdx.x)];
+        if (th.cnt == 0) {
+            if (tid >= 32) return;
+            double loss_part = 0;
+            if (tid < 3 * P) {
+                const int q = tid % P, c = tid / P;
+                const int px = X0 + q % TW, py = Y0 + q / TW;
+                if (px < W && py < H) {
+                    const size_t qi = pbase + size_t(py) * W + px;
+                    double sum = 0;
+                    for (int j = 0; j < kSPP; ++j) sum = sum + p.sc.bg[c];  // render.cpp:48-57, sample order
+                    const double mean = sum / double(kSPP);
+                    p.img[3 * qi + c] = mean;
+                    if (c == 0) p.mask[qi] = 0.0;
+                    pixel_loss_adjoint(p, vc, qi, c, mean, loss_part);
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) loss_part += __shfl_xor_sync(0xffffffffu, loss_part, o);
+            if (tid == 0 && loss_part != 0) atomicAdd(&p.loss_acc[vc.slot], loss_part);
+            return;
+        }
+    }
+
     // ---------------- phase 1: cached triangle -> (t, b1, b2), radiance
     int tri = -1;
     double t = 0, b1 = 0, b2 = 0;
     D3 dir{0, 0, 1};
     if (valid) tri = p.hit[pidx * spp + s];
+#ifdef CDR_EXP_SKIP_MISS  // measurement only (wrong output): cost of all-miss CTAs
+    if (!__syncthreads_or(tri >= 0)) return;
+#endif
     if (tri >= 0) {  // misses need no ray: their radiance is the background
         D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
         dir = primary_dir(cam, ps);
@@ -761,7 +812,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     const int lane = tid & 31, wib = tid >> 5;
     const bool warp_local = (32 % spp) == 0;
     __shared__ double s_wloss[kRT / 32];
-    __shared__ int s_wcnt[kRT / 32][2];
+    __shared__ int s_wcnt[kRT / 32][3];
     if (warp_local) __syncwarp();
     else __syncthreads();
 
@@ -792,22 +843,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
                     p.img[3 * qi + c] = mean;
                     if (c == 0) p.mask[qi] = double(hits) / double(spp);
                 }
-                if (kLoss) {
-                    double m = (p.use_mask && p.has_mask[vc.slot]) ? p.target_mask[qi] : 1.0;
-                    double a = 0;
-                    if (m != 0) {
-                        // losses.cpp:37-44; Φ'(r) = Φ(r) / (γ r) for r in (0, 1)
-                        // Φ(0) = pow(0, 1/γ) = +0 exactly: skip pow on background
-                        double tr = mean <= 0.0 ? 0.0 : tone_map(mean, p.gamma);
-                        double d = tr - p.target_tone[3 * qi + c];
-                        loss_part += m * fabs(d);
-                        double sg = double((d > 0) - (d < 0));
-                        double der = (mean <= 0.0 || mean >= 1.0) ? 0.0 : tr / (p.gamma * mean);
-                        a = vc.scale * m * sg * der;
-                    }
-                    p.adj[3 * qi + c] = a;
-                    s_adj[q][c] = a;
-                }
+                if (kLoss) s_adj[q][c] = pixel_loss_adjoint(p, vc, qi, c, mean, loss_part);
             }
         }
     }
@@ -829,10 +865,12 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
         act = kInterior && valid && tri >= 0 && !(a.x == 0 && a.y == 0 && a.z == 0);
         const int nh = __popc(__ballot_sync(0xffffffffu, valid && tri >= 0));
         const int na = __popc(__ballot_sync(0xffffffffu, act));
+        const int nv = __popc(__ballot_sync(0xffffffffu, valid));
         if (lane == 0) {
             s_wloss[wib] = loss_part;
             s_wcnt[wib][0] = nh;
             s_wcnt[wib][1] = na;
+            s_wcnt[wib][2] = nv;
         }
     }
 
@@ -845,16 +883,18 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
         asm volatile("bar.sync 1, %0;" ::"n"(kRT) : "memory");
         if (lane == 0) {
             double tot = 0;
-            unsigned long long nh = 0, na = 0;
+            unsigned long long nh = 0, na = 0, nv = 0;
             for (int w = 0; w < kRT / 32; ++w) {
                 tot += s_wloss[w];
                 nh += s_wcnt[w][0];
                 na += s_wcnt[w][1];
+                nv += s_wcnt[w][2];
             }
             if (kLoss && tot != 0) atomicAdd(&p.loss_acc[vc.slot], tot);
             if (kShade || kInterior) {
                 if (nh) atomicAdd(&p.counters->hit_samples, nh);
                 if (na) atomicAdd(&p.counters->adjoint_samples, na);
+                if (nv) atomicAdd(&p.counters->shaded_samples, nv);
             }
         }
     } else {
@@ -1125,6 +1165,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     p.no_shared_top = std::getenv("CDR_NO_SHARED_TOP") != nullptr;
     if (const char* e = std::getenv("CDR_BEAM_FAST_CAP")) p.fast_cap = std::max(0, std::min(kBeamCap, std::atoi(e)));
     c->beam_view.valid = 0;
+    p.skip_empty_hits = p.use_beam && loss && a.spp == 16;
     if (c->beam_used_host) c->beam_used_last = *c->beam_used_host;  // previous call has completed
     if (p.use_beam) {
         // candidate pool sized from the previous call's use (overflowing tiles

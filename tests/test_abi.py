@@ -19,7 +19,7 @@ def test_library_builds_and_exports_every_symbol():
     assert declared <= exported, f"missing: {sorted(declared - exported)}"
     assert {s for s in exported if not s.startswith("cdr_")} == set()
     L = api.load_library()
-    assert L.cdr_abi_version() == 1
+    assert L.cdr_abi_version() == 2
 
 
 def test_sm100a_cubin_embedded():
