@@ -307,7 +307,7 @@ def main():
     if os.path.exists(traffic_file):
         try:  # ncu dram bytes per sample of this kernel, scaled to this launch
             tr = json.load(open(traffic_file))
-            roof["traffic"] = tr["dram_bytes_per_sample"] * n_samp
+            roof["traffic"] = tr["dram_bytes_per_sample"] * s0["samples"]
             roof["traffic_source"] = tr.get("source")
         except Exception:
             pass

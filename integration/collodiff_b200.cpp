@@ -194,7 +194,7 @@ struct ShimProfile {
     ~ShimProfile() {
         if (!on) return;
         const char* names[8] = {"total_loss", "  scene+targets upload", "  cdr_total_loss", "  rendered copy",
-                                "self_intersects", "render", "", ""};
+                                "self_intersects", "render", "    Image construction", ""};
         for (int i = 0; i < 8; ++i)
             if (calls[i]) std::fprintf(stderr, "[cdr shim] %-24s %6ld calls %10.2f ms\n", names[i], calls[i], ms[i]);
     }
@@ -542,7 +542,9 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
         res.rendered.reserve(scene.views.size());
         for (int k = 0; k < n; ++k) {
             const Camera& c = scene.views[k];
+            std::optional<ShimTimer> t6(std::in_place, 6);
             Image img(c.width, c.height, true);
+            t6.reset();
             d.check(cdr_get_rendered(d.ctx, k, reinterpret_cast<double*>(img.pixels.data()), img.mask.data()));
             res.rendered.push_back(std::move(img));
         }
