@@ -161,6 +161,20 @@ def test_loss_grad_blob_selfoccluding():
     _loss_grad_check(sc, 4, 2, param_layout(sc, optimize_light=True))
 
 
+def test_loss_grad_spp16_background_empty_tiles():
+    # spp 16: beam tiles with no candidate take k_render's background path
+    # (no hit-cache traffic); a non-zero background exercises its mean and tone
+    # map, 46 x 46 images leave partial edge tiles, masks the masked loss
+    sc = small_scene(freq=5, tex=16, views=2, image=46)
+    sc.background = np.array([0.1, 0.2, 0.3])
+    rng = np.random.default_rng(5)
+    masks = (rng.uniform(size=(2, 46, 46)) > 0.2).astype(np.float64)
+    st = _loss_grad_check(sc, 16, 3, param_layout(sc), use_mask=True, masks=masks)
+    assert 0 < st.shaded_samples < st.samples  # the background path ran
+    st = _loss_grad_check(sc, 16, 5, param_layout(sc))
+    assert 0 < st.shaded_samples < st.samples
+
+
 def test_loss_grad_masks_and_options(sphere):
     rng = np.random.default_rng(3)
     masks = (rng.uniform(size=(3, 40, 40)) > 0.2).astype(np.float64)
