@@ -292,16 +292,22 @@ def main():
     # ---- roofline of the dominant kernel (fused trace/shade/loss/interior)
     s0 = stats[-1]
     ms_shade = statistics.mean(x["ms_render"] - x["ms_trace"] for x in stats)
-    n_px, n_samp = s0["pixels"], s0["shaded_samples"]  # empty beam tiles read no hit cache
+    n_px, n_samp = s0["pixels"], s0["shaded_samples"]  # empty beam tiles touch no hit cache
     n_hit, n_adj = s0["hit_samples"], s0["adjoint_samples"]
-    algo_bytes = 80 * n_px + 4 * n_samp + 332 * n_hit + 736 * n_adj
+    # SURVEY §8(d) per-unit algorithmic bytes (fp32 texels and texel-gradient RMW)
+    algo_bytes = 80 * n_px + 4 * n_samp + 316 * n_hit + 512 * n_adj
+    # the same traffic at this implementation's storage (32-B texel records,
+    # fp64 texel-gradient accumulator): reported beside it, not as `achieved`
+    stored_bytes = 80 * n_px + 4 * n_samp + 332 * n_hit + 736 * n_adj
     pk, pk_kind = peaks()
     achieved = algo_bytes / (ms_shade / 1e3) / 1e9
     roof = {"kernel": "k_render<shade,loss,interior> (fused shading + loss + interior scatter)",
             "bound": "hbm", "achieved": achieved,
             "peak": pk["hbm_gbs"], "peak_source": pk_kind, "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
             "traffic": None, "algorithmic_bytes_per_launch": algo_bytes,
-            "byte_model": "80*N_px + 4*N_shaded + 332*N_hit + 736*N_adj (DESIGN.md §4)",
+            "byte_model": "SURVEY §8(d): 80*N_px + 4*N_shaded + 316*N_hit + 512*N_adj (DESIGN.md §4)",
+            "storage_bytes_per_launch": stored_bytes,
+            "storage_frac": stored_bytes / (ms_shade / 1e3) / 1e9 / pk["hbm_gbs"],
             "ms_per_launch": ms_shade, "share_of_step": ms_shade / statistics.mean(ms_steps)}
     traffic_file = os.path.join(ROOT, "profiles", "render_traffic.json")
     if os.path.exists(traffic_file):
