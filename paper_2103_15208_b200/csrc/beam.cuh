@@ -150,6 +150,7 @@ __device__ __forceinline__ Hit trace_beam(const BeamCand* __restrict__ cand, int
         // needed unless the bound stops the scan)
         const float4 e2 = cand[k].e2, e0 = cand[k].e0, e1 = cand[k].e1;
         if (double(e2.y) > best.t) break;  // every remaining candidate is farther
+        CDR_STAT(3, 1);
         const bool pass = (__float_as_int(e2.w) & 1) ||
                           (e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
                            e1.z * px + e1.w * py + e2.x >= 0.0f);
@@ -167,6 +168,7 @@ __device__ __forceinline__ Hit trace_beam_list(const BeamCand* __restrict__ cand
         const int k = idx[j];
         const float4 e2 = cand[k].e2, e0 = cand[k].e0, e1 = cand[k].e1;
         if (double(e2.y) > best.t) break;
+        CDR_STAT(3, 1);
         const bool pass = (__float_as_int(e2.w) & 1) ||
                           (e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
                            e1.z * px + e1.w * py + e2.x >= 0.0f);
