@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
 // hit cache (the bit-exact output). Kept slim so it runs at high occupancy —
 // traversal is latency-bound, not bandwidth-bound.
 #ifndef CDR_TRACE_MIN_BLOCKS
-#define CDR_TRACE_MIN_BLOCKS 5
+#define CDR_TRACE_MIN_BLOCKS 6  // 12 x 128-thread CTAs per SM: 5 -> 6 after the empty-tile skip (trace 8.03 -> 7.95 ms at cfg2)
 #endif
 // Grids are (tile x, tile y, view call); kSPP = 16 makes the sample/tile
 // geometry compile-time (4x4 pixels x 16 samples), 0 reads it from Params.
