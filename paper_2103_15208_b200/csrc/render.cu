@@ -528,15 +528,23 @@ using RedT = double;
 #endif
 
 // Phase 3 of k_render: the interior adjoint of one sample (diff_render.cpp:78-184).
+// The 4 bilinear weights of the texel scatter, staged per thread in shared
+// memory (transposed: lane-consecutive, conflict-free). The scatter loop
+// indexes them with its loop counter, which put them in local memory, and
+// they live across the position computation and scatter. Staging all ten
+// scatter scalars this way was slower at cfg4: 16 KB per CTA shrinks L1.
+constexpr int kTexState = 4;
+
+template <int kRT>
 __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x, int y, int spp, int tri, double t,
-                                              double b1, double b2, D3 dir, D3 a, bool act) {
+                                              double b1, double b2, D3 dir, D3 a, bool act,
+                                              double (&s_ts)[kTexState][kRT]) {
     a = (spp & (spp - 1)) == 0 ? a * (1.0 / spp) : a / double(spp);  // diff_render.cpp:82 (x/2^n exact as x*2^-n)
 
     // Compute everything the scatter needs first, so the large temporaries
     // (texture sample, BRDF partials, vertex data) are dead before the
     // warp-aggregation loops; only a compact state crosses them.
     int tex0 = 0;           // texel quad key (texel[0] determines all four)
-    double wq[4] = {0, 0, 0, 0};
     double wd0 = 0, ws0 = 0, wr0 = 0;  // d_diffuse/r^2, d_specular/r^2, Σ a L d_rough / r^2
     double aL[3] = {0, 0, 0};
     double lv[3] = {0, 0, 0};          // light gradient (diff_render.cpp:129-131)
@@ -572,7 +580,7 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             const double Lc[3] = {p.sc.L[0], p.sc.L[1], p.sc.L[2]};
             const double ac[3] = {a.x, a.y, a.z};
             tex0 = ts.texel[0];
-            for (int k = 0; k < 4; ++k) wq[k] = ts.w[k];
+            for (int k = 0; k < 4; ++k) s_ts[k][tid] = ts.w[k];
             wd0 = br.d_diffuse * inv_r2;
             ws0 = br.d_specular * inv_r2;
             for (int c = 0; c < 3; ++c) {
@@ -640,35 +648,6 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
     // (+10%: fewer instructions, but a serial load-add chain per lane; this
     // kernel is latency-bound at 6 warps per scheduler, not issue-bound).
     const int lane = tid & 31;
-#ifndef CDR_EXP_NO_TEXEL
-    {
-        // texel scatter through the bilinear weights (diff_render.cpp:110-128)
-        const int key = act ? tex0 : -1 - lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
-        const bool leader = act && (__ffs(peers) - 1) == lane;
-        const int tw = p.sc.tw, th = p.sc.th;
-        const int x0 = tex0 % tw, y0 = tex0 / tw;
-        const int x1 = x0 + 1 == tw ? 0 : x0 + 1, y1 = y0 + 1 == th ? 0 : y0 + 1;
-#pragma unroll 1
-        for (int kq = 0; kq < 4; ++kq) {
-            RedT v[7];
-            const double w = wq[kq];
-            for (int c = 0; c < 3; ++c) {
-                v[c] = RedT(aL[c] * (w * wd0));
-                v[3 + c] = RedT(aL[c] * (w * ws0));
-            }
-            v[6] = RedT(wr0 * w);
-            reduce_peers<7>(0xffffffffu, peers, v);
-            if (leader) {
-                // texel-major accumulator: the 7 values of a texel share 2 sectors
-                const int64_t tx = int64_t((kq < 2 ? y0 : y1)) * tw + ((kq & 1) ? x1 : x0);
-                TexAcc* dst = p.texacc + tx;
-                for (int i = 0; i < 7; ++i)
-                    if (v[i] != 0) atomicAdd(&dst->v[i], TexAccT(v[i]));
-            }
-        }
-    }
-#endif
     if (p.lay_l >= 0) {  // light intensity (diff_render.cpp:129-131)
         for (int o = 16; o > 0; o >>= 1)
             for (int c = 0; c < 3; ++c) lv[c] += __shfl_xor_sync(0xffffffffu, lv[c], o);
@@ -695,6 +674,37 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                 double* dst = p.corner + (size_t(tri) * 3 + j) * 6;
                 for (int i = 0; i < 6; ++i)
                     if (v[i] != 0) atomicAdd(dst + i, double(v[i]));
+            }
+        }
+    }
+#endif
+#ifndef CDR_EXP_NO_TEXEL
+    {
+        // texel scatter through the bilinear weights (diff_render.cpp:110-128)
+        const int key = act ? tex0 : -1 - lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const bool leader = act && (__ffs(peers) - 1) == lane;
+        const int tw = p.sc.tw, th = p.sc.th;
+        const int x0 = tex0 % tw, y0 = tex0 / tw;
+        const int x1 = x0 + 1 == tw ? 0 : x0 + 1, y1 = y0 + 1 == th ? 0 : y0 + 1;
+#pragma unroll 1
+        for (int kq = 0; kq < 4; ++kq) {
+            RedT v[7] = {0, 0, 0, 0, 0, 0, 0};  // lanes without a sample form singleton groups
+            if (act) {
+                const double w = s_ts[kq][tid];
+                for (int c = 0; c < 3; ++c) {
+                    v[c] = RedT(aL[c] * (w * wd0));
+                    v[3 + c] = RedT(aL[c] * (w * ws0));
+                }
+                v[6] = RedT(wr0 * w);
+            }
+            reduce_peers<7>(0xffffffffu, peers, v);
+            if (leader) {
+                // texel-major accumulator: the 7 values of a texel share 2 sectors
+                const int64_t tx = int64_t((kq < 2 ? y0 : y1)) * tw + ((kq & 1) ? x1 : x0);
+                TexAcc* dst = p.texacc + tx;
+                for (int i = 0; i < 7; ++i)
+                    if (v[i] != 0) atomicAdd(&dst->v[i], TexAccT(v[i]));
             }
         }
     }
@@ -735,6 +745,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     __shared__ double s_rad[kRT][3];
     __shared__ double s_adj[kRT][3];  // per pixel (index = pixel in tile)
     __shared__ unsigned char s_hit[kRT];
+    __shared__ double s_ts[kTexState][kRT];  // interior_scatter's texel state
 
     const ViewCall vc = p.calls[blockIdx.z];
     const DevCamera& cam = p.cams[vc.slot];
@@ -875,7 +886,8 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     }
 
     // ---------------- phase 3: interior adjoint scatter
-    if (kInterior && __any_sync(0xffffffffu, act)) interior_scatter(p, tid, x, y, spp, tri, t, b1, b2, dir, a, act);
+    if (kInterior && __any_sync(0xffffffffu, act))
+        interior_scatter<kRT>(p, tid, x, y, spp, tri, t, b1, b2, dir, a, act, s_ts);
 
     // ---------------- publish the CTA's tallies (warp 0 waits for the others)
     __threadfence_block();
