@@ -574,6 +574,20 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             const double inv_len = rcp(n_len);
             D3 n_hat = nt * inv_len;
             double mu = dot(n_hat, -dir);
+            // h = normalize_jacobian(n_tilde) * v_hat (vec.hpp:179-183) and the
+            // vertex-data terms of k1 / k2, now: uvs and normals die here
+            D3 hv;
+            {
+                const D3 n = n_hat, v = -dir;
+                const double sc = inv_len;
+                double J[9] = {(1 - n.x * n.x) * sc, (0 - n.x * n.y) * sc, (0 - n.x * n.z) * sc,
+                               (0 - n.y * n.x) * sc, (1 - n.y * n.y) * sc, (0 - n.y * n.z) * sc,
+                               (0 - n.z * n.x) * sc, (0 - n.z * n.y) * sc, (1 - n.z * n.z) * sc};
+                hv = D3{J[0] * v.x + J[1] * v.y + J[2] * v.z, J[3] * v.x + J[4] * v.y + J[5] * v.z,
+                        J[6] * v.x + J[7] * v.y + J[8] * v.z};
+            }
+            const double du1 = uv1.x - uv0.x, dv1 = uv1.y - uv0.y, du2 = uv2.x - uv0.x, dv2 = uv2.y - uv0.y;
+            const double dn1 = dot(hv, N1) - dot(hv, N0), dn2 = dot(hv, N2) - dot(hv, N0);
             TexSample3 ts = sample_maps(p.sc.tex, p.sc.tw, p.sc.th, uv, true);
             Brdf br = eval_brdf_grad(ts.dv, ts.sv, ts.rv, mu);
             const double inv_r2 = rcp(t * t);
@@ -588,6 +602,24 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                 wr0 += ac[c] * Lc[c] * comp(br.d_rough, c) * inv_r2;
                 lv[c] = ac[c] * comp(br.value, c) * inv_r2;
             }
+            // the intersection-response coefficients (diff_render.cpp:143-160)
+            // now, so the texture sample and BRDF partials die here instead of
+            // living across the vertex loads and the inverse below
+            double cs = 0, cu = 0, cv = 0, cm = 0;
+            {
+                const double m2_r3 = -2.0 * inv_r2 * rcp(t);  // -2 / t^3
+                for (int c = 0; c < 3; ++c) {
+                    double w = ac[c] * Lc[c] * inv_r2;
+                    cs += ac[c] * Lc[c] * (comp(br.value, c) * m2_r3);
+                    double gu = br.d_diffuse * comp(ts.ddu, c) + br.d_specular * comp(ts.sdu, c) +
+                                comp(br.d_rough, c) * ts.rdu;
+                    double gv = br.d_diffuse * comp(ts.ddv, c) + br.d_specular * comp(ts.sdv, c) +
+                                comp(br.d_rough, c) * ts.rdv;
+                    cu += w * gu;
+                    cv += w * gv;
+                    cm += w * comp(br.d_mu, c);
+                }
+            }
             if (mu > 0) {  // diff_render.cpp:133
                 D3 p0 = ld3(p.sc.pos + 3 * va), p1 = ld3(p.sc.pos + 3 * vb), p2 = ld3(p.sc.pos + 3 * vcx);
                 // M = [d, p0-p1, p0-p2] (Mat3::from_columns), inverse rows r0..r2
@@ -596,19 +628,6 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                 double det = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
                              m[2] * (m[3] * m[7] - m[4] * m[6]);
                 if (fabs(det) >= 1e-18) {
-                    double cs = 0, cu = 0, cv = 0, cm = 0;
-                    const double m2_r3 = -2.0 * inv_r2 * rcp(t);  // -2 / t^3
-                    for (int c = 0; c < 3; ++c) {
-                        double w = ac[c] * Lc[c] * inv_r2;
-                        cs += ac[c] * Lc[c] * (comp(br.value, c) * m2_r3);
-                        double gu = br.d_diffuse * comp(ts.ddu, c) + br.d_specular * comp(ts.sdu, c) +
-                                    comp(br.d_rough, c) * ts.rdu;
-                        double gv = br.d_diffuse * comp(ts.ddv, c) + br.d_specular * comp(ts.sdv, c) +
-                                    comp(br.d_rough, c) * ts.rdv;
-                        cu += w * gu;
-                        cv += w * gv;
-                        cm += w * comp(br.d_mu, c);
-                    }
                     if (!isfinite(cs + cu + cv + cm)) {
                         raise_nonfinite(p.err, x, y);
                     } else {
@@ -619,17 +638,8 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                               (m[2] * m[3] - m[0] * m[5]) * inv};
                         D3 r2{(m[3] * m[7] - m[4] * m[6]) * inv, (m[1] * m[6] - m[0] * m[7]) * inv,
                               (m[0] * m[4] - m[1] * m[3]) * inv};
-                        // h = normalize_jacobian(n_tilde) * v_hat (vec.hpp:179-183)
-                        D3 n = n_hat;
-                        D3 v = -dir;
-                        double sc = inv_len;
-                        double J[9] = {(1 - n.x * n.x) * sc, (0 - n.x * n.y) * sc, (0 - n.x * n.z) * sc,
-                                       (0 - n.y * n.x) * sc, (1 - n.y * n.y) * sc, (0 - n.y * n.z) * sc,
-                                       (0 - n.z * n.x) * sc, (0 - n.z * n.y) * sc, (1 - n.z * n.z) * sc};
-                        D3 hv{J[0] * v.x + J[1] * v.y + J[2] * v.z, J[3] * v.x + J[4] * v.y + J[5] * v.z,
-                              J[6] * v.x + J[7] * v.y + J[8] * v.z};
-                        double k1 = cu * (uv1.x - uv0.x) + cv * (uv1.y - uv0.y) + cm * (dot(hv, N1) - dot(hv, N0));
-                        double k2 = cu * (uv2.x - uv0.x) + cv * (uv2.y - uv0.y) + cm * (dot(hv, N2) - dot(hv, N0));
+                        double k1 = cu * du1 + cv * dv1 + cm * dn1;
+                        double k2 = cu * du2 + cv * dv2 + cm * dn2;
                         gc = r0 * cs + r1 * k1 + r2 * k2;
                         hm = hv * cm;
                         pact = true;
