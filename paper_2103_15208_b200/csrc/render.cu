@@ -727,6 +727,9 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
 #ifndef CDR_RENDER_MIN_BLOCKS
 #define CDR_RENDER_MIN_BLOCKS 3
 #endif
+#ifndef CDR_RENDER_CTAS16  // resident CTAs per SM of the spp-16 kernel (its register budget)
+#define CDR_RENDER_CTAS16 (CDR_RENDER_MIN_BLOCKS * kThreads / kRenderThreads16)
+#endif
 // view_rendering_loss for one (pixel, channel) of the mean radiance: adds the
 // L1 term to loss_part, writes and returns the adjoint (losses.cpp:37-44)
 __device__ __forceinline__ double pixel_loss_adjoint(const Params& p, const ViewCall& vc, size_t qi, int c,
@@ -748,7 +751,7 @@ __device__ __forceinline__ double pixel_loss_adjoint(const Params& p, const View
 
 template <bool kShade, bool kLoss, bool kInterior, int kSPP>
 __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
-                                  kSPP == 16 ? CDR_RENDER_MIN_BLOCKS * kThreads / kRenderThreads16
+                                  kSPP == 16 ? CDR_RENDER_CTAS16
                                              : CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
     // spp 16: kRenderThreads16 threads = (kRenderThreads16 / 64) x 4 pixels x 16 samples
     constexpr int kRT = kSPP == 16 ? kRenderThreads16 : kThreads;
