@@ -791,8 +791,9 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
                 if (px < W && py < H) {
                     const size_t qi = pbase + size_t(py) * W + px;
                     double sum = 0;
-                    for (int j = 0; j < kSPP; ++j) sum = sum + p.sc.bg[c];  // render.cpp:48-57, sample order
-                    const double mean = sum / double(kSPP);
+                    constexpr int kS = kSPP > 0 ? kSPP : 1;  // (this path is spp 16 only)
+                    for (int j = 0; j < kS; ++j) sum = sum + p.sc.bg[c];  // render.cpp:48-57, sample order
+                    const double mean = sum / double(kS);
                     p.img[3 * qi + c] = mean;
                     if (c == 0) p.mask[qi] = 0.0;
                     pixel_loss_adjoint(p, vc, qi, c, mean, loss_part);
@@ -1184,7 +1185,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     p.err = c->errinfo.p;
     p.counters = c->counters.p;
 
-    int tiles = ((maxW + p.TW - 1) / p.TW) * ((maxH + p.TH - 1) / p.TH);
+    [[maybe_unused]] int tiles = ((maxW + p.TW - 1) / p.TW) * ((maxH + p.TH - 1) / p.TH);  // CDR_LIST_STRIP
     p.use_beam = trace && c->T > 0 && !std::getenv("CDR_NO_BEAM");
     p.fast_cap = kBeamCap;  // CDR_BEAM_FAST_CAP < kBeamCap pushes tiles to the big pass (tests)
     p.no_shared_top = std::getenv("CDR_NO_SHARED_TOP") != nullptr;
