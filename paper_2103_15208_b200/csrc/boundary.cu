@@ -348,7 +348,7 @@ __global__ void k_bscatter(BParams p) {
 // pass 4: the two radiance probes and the vertex deposit, in segment order so a
 // warp traces neighbouring rays along one silhouette edge (diff_render.cpp:246-277)
 #ifndef CDR_BOUNDARY_MIN_BLOCKS
-#define CDR_BOUNDARY_MIN_BLOCKS 5  // latency-bound probes: occupancy beats the extra spill
+#define CDR_BOUNDARY_MIN_BLOCKS 4  // 8 x 128-thread CTAs / SM, 64 regs: cfg4 boundary 37.7 -> 35.6 ms vs 5, cfg2 equal
 #endif
 #ifndef CDR_BND_BLOCK
 #define CDR_BND_BLOCK 128
