@@ -538,7 +538,7 @@ constexpr int kTexState = 4;
 template <int kRT>
 __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x, int y, int spp, int tri, double t,
                                               double b1, double b2, D3 dir, D3 a, bool act,
-                                              double (&s_ts)[kTexState][kRT]) {
+                                              double (&s_ts)[kTexState][kRT], const double (&s_ray)[5][kRT]) {
     a = (spp & (spp - 1)) == 0 ? a * (1.0 / spp) : a / double(spp);  // diff_render.cpp:82 (x/2^n exact as x*2^-n)
 
     // Compute everything the scatter needs first, so the large temporaries
@@ -623,8 +623,11 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             if (mu > 0) {  // diff_render.cpp:133
                 D3 p0 = ld3(p.sc.pos + 3 * va), p1 = ld3(p.sc.pos + 3 * vb), p2 = ld3(p.sc.pos + 3 * vcx);
                 // M = [d, p0-p1, p0-p2] (Mat3::from_columns), inverse rows r0..r2
-                double m[9] = {dir.x, p0.x - p1.x, p0.x - p2.x, dir.y, p0.y - p1.y, p0.y - p2.y,
-                               dir.z, p0.z - p1.z, p0.z - p2.z};
+                // the ray direction again from shared memory (its registers are
+                // free across the sample / BRDF peak)
+                const double dx = s_ray[0][tid], dy = s_ray[1][tid], dz = s_ray[2][tid];
+                double m[9] = {dx, p0.x - p1.x, p0.x - p2.x, dy, p0.y - p1.y, p0.y - p2.y,
+                               dz, p0.z - p1.z, p0.z - p2.z};
                 double det = m[0] * (m[4] * m[8] - m[5] * m[7]) - m[1] * (m[3] * m[8] - m[5] * m[6]) +
                              m[2] * (m[3] * m[7] - m[4] * m[6]);
                 if (fabs(det) >= 1e-18) {
@@ -674,7 +677,8 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
         const bool leader = pact && (__ffs(peers) - 1) == lane;
 #pragma unroll 1
         for (int j = 0; j < 3; ++j) {
-            const double bj = j == 0 ? b0 : (j == 1 ? b1 : b2);
+            const double rb1 = s_ray[3][tid], rb2 = s_ray[4][tid];
+            const double bj = j == 0 ? 1.0 - rb1 - rb2 : (j == 1 ? rb1 : rb2);  // b0 as computed above
             RedT v[6] = {RedT(gc.x * bj), RedT(gc.y * bj), RedT(gc.z * bj),
                          RedT(hm.x * bj), RedT(hm.y * bj), RedT(hm.z * bj)};
             if (!pact)
@@ -756,9 +760,10 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     // spp 16: kRenderThreads16 threads = (kRenderThreads16 / 64) x 4 pixels x 16 samples
     constexpr int kRT = kSPP == 16 ? kRenderThreads16 : kThreads;
     __shared__ double s_rad[kRT][3];
-    __shared__ double s_adj[kRT][3];  // per pixel (index = pixel in tile)
+    __shared__ double s_adj[kSPP ? kRT / kSPP : kRT][3];  // per pixel of the CTA
     __shared__ unsigned char s_hit[kRT];
     __shared__ double s_ts[kTexState][kRT];  // interior_scatter's texel state
+    __shared__ double s_ray[kInterior ? 5 : 1][kRT];  // dir, b1, b2 of the sample, for the scatter's late uses
 
     const ViewCall vc = p.calls[blockIdx.z];
     const DevCamera& cam = p.cams[vc.slot];
@@ -830,6 +835,13 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
         s_rad[tid][2] = rad.z;
         s_hit[tid] = tri >= 0;
     }
+    if (kInterior) {
+        s_ray[0][tid] = dir.x;
+        s_ray[1][tid] = dir.y;
+        s_ray[2][tid] = dir.z;
+        s_ray[3][tid] = b1;
+        s_ray[4][tid] = b2;
+    }
     // When spp divides 32 a warp holds whole pixels: phase 2 is warp-local and
     // no CTA barrier separates the phases (warps overlap one another's pixel
     // reductions with their scatter); the per-warp tallies meet once, at the
@@ -900,8 +912,9 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     }
 
     // ---------------- phase 3: interior adjoint scatter
-    if (kInterior && __any_sync(0xffffffffu, act))
-        interior_scatter<kRT>(p, tid, x, y, spp, tri, t, b1, b2, dir, a, act, s_ts);
+    if constexpr (kInterior) {
+        if (__any_sync(0xffffffffu, act)) interior_scatter<kRT>(p, tid, x, y, spp, tri, t, b1, b2, dir, a, act, s_ts, s_ray);
+    }
 
     // ---------------- publish the CTA's tallies (warp 0 waits for the others)
     __threadfence_block();
