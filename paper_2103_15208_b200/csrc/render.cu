@@ -139,6 +139,8 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
     if (T == 1) {
         if (lane == 0) s_leaf[0] = 0;
         nl = 1;
+    } else if (T > 1 && init_n < 0) {  // the CTA's union frustum met no node: an empty tile
+        nf = 0;
     } else if (T > 1 && init_n > 0) {  // start below the levels the CTA walked together
         for (int i = lane; i < init_n; i += 32) s_front[0][i] = init_front[i];
         nf = init_n;
@@ -367,7 +369,8 @@ __device__ int shared_top_levels(const Params& p, const DevCamera& cam, int X0, 
             nn += __popc(q0) + __popc(q1);
         }
         __syncwarp();
-        if (leafy || nn > kTopCap || nn == 0) break;  // keep the current level
+        if (!leafy && nn == 0) return -1;  // nothing meets the union frustum: every tile is empty
+        if (leafy || nn > kTopCap) break;  // keep the current level
         nf = nn;
         cur ^= 1;
     }
