@@ -131,8 +131,6 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
     TileHdr* hdr = p.tile_hdr + tile;
     const int X0 = (b % tiles_x) * p.TW, Y0 = (b / tiles_x) * p.TH;
     const int X1 = min(X0 + p.TW, cam.W), Y1 = min(Y0 + p.TH, cam.H);
-    const FrustumPlanes fp = tile_frustum(cam, X0 - 0.01, X1 + 0.01, Y0 - 0.01, Y1 + 0.01);
-    const float of[3] = {float(cam.o[0]), float(cam.o[1]), float(cam.o[2])};
     const int T = p.sc.n_tris;
     int nl = 0, nf = 0, cur = 0;
     bool over = false;
@@ -149,6 +147,14 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
         nf = 1;
     }
     __syncwarp();
+    FrustumPlanes fp;  // only when there is a frontier (empty blocks skip the fp64 set-up)
+    float of[3];
+    if (nf > 0) {
+        fp = tile_frustum(cam, X0 - 0.01, X1 + 0.01, Y0 - 0.01, Y1 + 0.01);
+        of[0] = float(cam.o[0]);
+        of[1] = float(cam.o[1]);
+        of[2] = float(cam.o[2]);
+    }
     while (nf > 0) {
         int nn = 0;
         for (int base = 0; base < nf; base += 32) {
