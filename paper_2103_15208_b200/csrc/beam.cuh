@@ -68,8 +68,11 @@ struct FrustumPlanes {
 // (camera.cpp:29-34: pixel x <-> (q.r)/(q.f) = (2x/W - 1) th aspect, y <-> (q.u)/(q.f) = (1 - 2y/H) th).
 __device__ __forceinline__ FrustumPlanes tile_frustum(const DevCamera& c, double x0, double x1, double y0,
                                                       double y1) {
-    const double s0 = (2.0 * x0 / c.W - 1.0) * c.th * c.aspect, s1 = (2.0 * x1 / c.W - 1.0) * c.th * c.aspect;
-    const double v0 = (1.0 - 2.0 * y0 / c.H) * c.th, v1 = (1.0 - 2.0 * y1 / c.H) * c.th;
+    // culling planes only: one reciprocal per axis (its rounding is far below
+    // the callers' 0.01 px margins and box_outside's slack)
+    const double kx = 2.0 / c.W, ky = 2.0 / c.H;
+    const double s0 = (x0 * kx - 1.0) * c.th * c.aspect, s1 = (x1 * kx - 1.0) * c.th * c.aspect;
+    const double v0 = (1.0 - y0 * ky) * c.th, v1 = (1.0 - y1 * ky) * c.th;
     FrustumPlanes fp;
     for (int k = 0; k < 3; ++k) {
         fp.n[0][k] = float(c.r[k] - s0 * c.f[k]);  // x >= x0

@@ -799,8 +799,8 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
         if (th.cnt == 0) {
             if (tid >= 32) return;
             double loss_part = 0;
-            if (tid < 3 * P) {
-                const int q = tid % P, c = tid / P;
+            for (int item = tid; item < 3 * P; item += 32) {  // (pixel, channel) items
+                const int q = item % P, c = item / P;
                 const int px = X0 + q % TW, py = Y0 + q / TW;
                 if (px < W && py < H) {
                     const size_t qi = pbase + size_t(py) * W + px;
