@@ -472,25 +472,26 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
 #endif
 // Grids are (tile x, tile y, view call); kSPP = 16 makes the sample/tile
 // geometry compile-time (4x4 pixels x 16 samples), 0 reads it from Params.
+#ifndef CDR_TRACE_ITEMS
+#define CDR_TRACE_ITEMS 8  // spp 16: tile columns per CTA (amortises launch: most CTAs of a sparse view are empty tiles)
+#endif
+constexpr int kTraceItems = CDR_TRACE_ITEMS;
+
+// One CTA's worth of k_trace: tile column bx, CTA row by of view call vc.
 template <bool kBeam, int kSPP>
-__global__ void __launch_bounds__(kSPP == 16 ? kTraceThreads16 : kThreads,
-                                  kSPP == 16 ? CDR_TRACE_MIN_BLOCKS * kThreads / kTraceThreads16
-                                             : CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
-    // spp 16: a CTA covers kTraceThreads16 / 64 rows of a 4 x 4 beam tile
+__device__ __forceinline__ void trace_item(const Params& p, const ViewCall& vc, const DevCamera& cam, int bx, int by) {
     constexpr int kCR = kSPP == 16 ? kTraceThreads16 / 64 : 0;  // pixel rows per CTA
-    const ViewCall vc = p.calls[blockIdx.z];
-    const DevCamera cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
     const int tid = threadIdx.x;
     const int spp = kSPP ? kSPP : p.spp;
     const int TW = kSPP == 16 ? 4 : p.TW, TH = kSPP == 16 ? 4 : p.TH;
     const int P = kThreads / spp;  // pixels per beam tile (its pixel lists)
     const int cpix = tid / spp, s = tid - (tid / spp) * spp;  // pixel within the CTA
-    const int ty = kSPP == 16 ? int(blockIdx.y) * kCR / 4 : int(blockIdx.y);
-    if (int(blockIdx.x) >= vc.tiles_x || ty >= vc.tiles_y) return;
-    const int tile_in_view = ty * vc.tiles_x + int(blockIdx.x);
-    const int X0 = int(blockIdx.x) * TW, Y0 = ty * TH;
-    const int pix = kSPP == 16 ? (int(blockIdx.y) * kCR - Y0) * 4 + cpix : cpix;  // pixel within the beam tile
+    const int ty = kSPP == 16 ? by * kCR / 4 : by;
+    if (bx >= vc.tiles_x || ty >= vc.tiles_y) return;
+    const int tile_in_view = ty * vc.tiles_x + bx;
+    const int X0 = bx * TW, Y0 = ty * TH;
+    const int pix = kSPP == 16 ? (by * kCR - Y0) * 4 + cpix : cpix;  // pixel within the beam tile
     const int x = X0 + pix % TW;
     const int y = Y0 + pix / TW;
     if (!(pix < P && x < W && y < H)) return;
@@ -523,6 +524,22 @@ __global__ void __launch_bounds__(kSPP == 16 ? kTraceThreads16 : kThreads,
         h = trace(p.sc_bin, p.sc.recs, p.sc.n_tris, org, dir, p.info->t_min);
     }
     p.hit[pidx * spp + s] = h.tri;
+}
+
+template <bool kBeam, int kSPP>
+__global__ void __launch_bounds__(kSPP == 16 ? kTraceThreads16 : kThreads,
+                                  kSPP == 16 ? CDR_TRACE_MIN_BLOCKS * kThreads / kTraceThreads16
+                                             : CDR_TRACE_MIN_BLOCKS) k_trace(Params p) {
+#ifdef CDR_EXP_TRACE_NOP  // measurement only (wrong output): launch cost of the grid
+    return;
+#endif
+    const ViewCall vc = p.calls[blockIdx.z];
+    const DevCamera cam = p.cams[vc.slot];
+    // spp 16: kTraceItems consecutive tile columns per CTA (no barriers, so an
+    // item's early returns just end that item)
+    constexpr int kItems = kSPP == 16 ? kTraceItems : 1;
+#pragma unroll 1
+    for (int i = 0; i < kItems; ++i) trace_item<kBeam, kSPP>(p, vc, cam, int(blockIdx.x) * kItems + i, int(blockIdx.y));
 }
 
 // Type of the warp partial sums of the scatter. fp64 by default (the whole
@@ -768,6 +785,9 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
                                              : CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
     // spp 16: kRenderThreads16 threads = (kRenderThreads16 / 64) x 4 pixels x 16 samples
     constexpr int kRT = kSPP == 16 ? kRenderThreads16 : kThreads;
+#ifdef CDR_EXP_RENDER_NOP  // measurement only (wrong output): launch cost of the grid
+    if (kLoss) return;
+#endif
     __shared__ double s_rad[kRT][3];
     __shared__ double s_adj[kSPP ? kRT / kSPP : kRT][3];  // per pixel of the CTA
     __shared__ unsigned char s_hit[kRT];
@@ -1115,6 +1135,7 @@ static void launch_render_kernel(const Params& p, dim3 grid, cdr_ctx* c, bool tr
 static void launch_trace_kernel(const Params& p, dim3 grid, cdr_ctx* c) {
     ++c->launches;
     dim3 g16 = grid;
+    g16.x = (grid.x + kTraceItems - 1) / kTraceItems;
     g16.y = grid.y * (kThreads / kTraceThreads16);
     if (p.use_beam && p.spp == 16) k_trace<true, 16><<<g16, kTraceThreads16, 0, c->stream>>>(p);
     else if (p.use_beam) k_trace<true, 0><<<grid, kThreads, 0, c->stream>>>(p);
