@@ -101,6 +101,57 @@ def peaks():
         return PEAKS_FALLBACK, "fallback"
 
 
+class NvmlClockSampler:
+    """SM clock and clock-event reasons during the timed region, polled through
+    NVML from a thread every 5 ms (a timed region of ~100 ms is shorter than an
+    nvidia-smi process takes to start, so that sampler sees one row at best)."""
+
+    def __init__(self, device):
+        import threading
+        import pynvml as nv
+        nv.nvmlInit()
+        self.nv = nv
+        self.h = nv.nvmlDeviceGetHandleByIndex(device)
+        self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        self.rows = []
+        self.halt = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.halt.is_set():
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                  nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+            except Exception:
+                pass
+            self.halt.wait(0.005)
+
+    def stop(self):
+        self.halt.set()
+        self.t.join(timeout=5)
+        nv = self.nv
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["no samples"], "source": "nvml"}
+        sm = [r[0] for r in self.rows]
+        loaded = [x for x in sm if x > 0.5 * self.max_mhz] or sm
+        reasons = sorted({n for _, m in self.rows for n, b in bits.items() if m & b})
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml, 5 ms"}
+
+
+def clock_sampler(device):
+    try:
+        return NvmlClockSampler(device)
+    except Exception:
+        return ClockSampler(device)
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons during the timed region."""
 
@@ -262,7 +313,7 @@ def main():
     for _ in range(args.warmup):
         r.loss_grad(views, st, lay, device_only=True)
     barrier()
-    clocks = ClockSampler(local) if rank == 0 else None
+    clocks = clock_sampler(local) if rank == 0 else None
     evs = []
     stats = []
     for _ in range(args.steps):
