@@ -351,7 +351,7 @@ __global__ void k_bscatter(BParams p) {
 #define CDR_BOUNDARY_MIN_BLOCKS 4  // 8 x 128-thread CTAs / SM, 64 regs: cfg4 boundary 37.7 -> 35.6 ms vs 5, cfg2 equal
 #endif
 #ifndef CDR_BND_BLOCK
-#define CDR_BND_BLOCK 128
+#define CDR_BND_BLOCK 256  // 4 x 256-thread CTAs per SM: boundary cfg2 4.05 -> 3.90 ms vs 128, cfg4 35.6 -> 35.2
 #endif
 constexpr int kBndBlock = CDR_BND_BLOCK;  // probe costs vary per warp: a CTA waits for its slowest
 
