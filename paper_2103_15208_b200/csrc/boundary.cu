@@ -226,7 +226,6 @@ struct BParams {
     int32_t* n_active;   // n_views
     int32_t* key;        // n_views x m_stride : segment of sample i (-1 inactive)
     int32_t* slot;       // n_views x m_stride : rank inside its segment
-    int32_t* order;      // n_views x m_stride : sample indices grouped by segment
     double* s_param;     // n_views x m_stride : s of sample i (pass 1)
     int32_t* sorted_si;  // n_views x m_stride : segment of the j-th grouped sample
     double* sorted_s;    // n_views x m_stride : its s
@@ -331,7 +330,7 @@ __global__ void k_bscan(int32_t* __restrict__ count, const int32_t* __restrict__
     if (threadIdx.x == 0) n_active[vi] = carry;
 }
 
-// pass 3: sample indices grouped by segment
+// pass 3: each sample's segment and position, grouped by (segment, position bucket)
 __global__ void k_bscatter(BParams p) {
     const int vi = blockIdx.y;
     const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -340,7 +339,6 @@ __global__ void k_bscatter(BParams p) {
     int k = p.key[o];
     if (k < 0) return;
     size_t d = size_t(vi) * p.m_stride + p.seg_off[size_t(vi) * p.E * kSBins + k] + p.slot[o];
-    p.order[d] = int32_t(i);
     p.sorted_si[d] = k / kSBins;
     p.sorted_s[d] = p.s_param[o];
 }
@@ -541,7 +539,6 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     c->b_n_active.ensure(n_views);
     c->b_key.ensure(nm);
     c->b_slot.ensure(nm);
-    c->b_order.ensure(nm);
     c->b_s.ensure(nm);
     c->b_sorted_si.ensure(nm);
     c->b_sorted_s.ensure(nm);
@@ -569,7 +566,6 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     p.n_active = c->b_n_active.p;
     p.key = c->b_key.p;
     p.slot = c->b_slot.p;
-    p.order = c->b_order.p;
     p.beam = c->beam_view;
     p.beam.valid = c->beam_view.valid && use_beam;
     p.s_param = c->b_s.p;

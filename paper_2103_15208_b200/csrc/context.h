@@ -156,7 +156,7 @@ struct cdr_ctx {
     cdr::DBuf<double> cdf, total_len;
     cdr::DBuf<int32_t> degenerate;
     // boundary samples binned by segment
-    cdr::DBuf<int32_t> b_seg_count, b_seg_off, b_n_active, b_key, b_slot, b_order, b_sorted_si;
+    cdr::DBuf<int32_t> b_seg_count, b_seg_off, b_n_active, b_key, b_slot, b_sorted_si;
     cdr::DBuf<double> b_s, b_sorted_s;
 
     // gradient + accumulators
