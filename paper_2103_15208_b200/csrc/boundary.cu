@@ -171,7 +171,8 @@ __global__ void k_sil_write(const double* __restrict__ pos, const double* __rest
 // totals[3 vi] = {total_len (acc), usable, extract_total}
 __global__ void __launch_bounds__(32) k_cdf(const cdr_segment* __restrict__ segs, const int32_t* __restrict__ count,
                                             int E, int n_views, double* __restrict__ cdf,
-                                            double* __restrict__ totals, int32_t* __restrict__ degenerate) {
+                                            double* __restrict__ totals, int32_t* __restrict__ degenerate,
+                                            int32_t* __restrict__ guide) {
     const int vi = blockIdx.x, lane = threadIdx.x;
     if (vi >= n_views) return;
     const int n = count[vi];
@@ -193,6 +194,23 @@ __global__ void __launch_bounds__(32) k_cdf(const cdr_segment* __restrict__ segs
         }
         if (i < n) cdf[size_t(vi) * E + i] = mine;
     }
+    // Guide table for the samples' lower_bound: guide[k] = lower_bound(cdf,
+    // acc * k / n) for k = 0..n (n buckets). A pick in bucket g (rounding can
+    // misplace it by one) has its lower_bound in [guide[g-1], guide[g+2]], so
+    // the search there returns the full search's index (boundary_setup).
+    __syncwarp();  // the lanes' cdf stores are visible to the whole warp
+    const double* cv = cdf + size_t(vi) * E;
+    int32_t* gd = guide + size_t(vi) * (E + 1);
+    for (int k = lane; k <= n && n > 0; k += 32) {
+        const double bnd = acc * double(k) / double(n);
+        int lo = 0, hi = n;
+        while (lo < hi) {
+            const int mid = lo + ((hi - lo) >> 1);
+            if (cv[mid] < bnd) lo = mid + 1;
+            else hi = mid;
+        }
+        gd[k] = lo;
+    }
     if (lane == 0) {
         totals[3 * vi] = acc;
         totals[3 * vi + 1] = (n == 0 || ext <= 0 || usable == 0 || acc <= 0) ? 0.0 : 1.0;
@@ -210,6 +228,7 @@ struct BParams {
     const size_t* pix_off;
     const cdr_segment* segs;
     const double* cdf;
+    const int32_t* guide;  // n_views x (E + 1): k_cdf's lower_bound guide
     const double* totals;
     const int32_t* count;
     int E;
@@ -249,7 +268,14 @@ __device__ __forceinline__ bool boundary_setup(const BParams& p, int vi, int64_t
     Rng rng = rng2(p.seed, uint64_t(cam.gid) + 0xb0d1, uint64_t(i));
     double pick = rng.next_double() * total_len;
     const double* cdf = p.cdf + size_t(vi) * p.E;
-    int lo = 0, hi = nseg;  // std::lower_bound
+    int lo = 0, hi = nseg;  // std::lower_bound, narrowed by the guide to a range holding its answer
+    {
+        int g = int(pick * double(nseg) / total_len);
+        g = g < 0 ? 0 : (g > nseg - 1 ? nseg - 1 : g);
+        const int32_t* gd = p.guide + size_t(vi) * (p.E + 1);
+        lo = gd[g > 0 ? g - 1 : 0];
+        hi = gd[g + 2 <= nseg ? g + 2 : nseg];
+    }
     while (lo < hi) {
         int mid = lo + ((hi - lo) >> 1);
         if (cdf[mid] < pick) lo = mid + 1;
@@ -513,8 +539,10 @@ void launch_silhouettes(cdr_ctx* c, int n_views) {
 
 void launch_cdf(cdr_ctx* c, int n_views) {
     if (n_views <= 0) return;
+    c->cdf_guide.ensure(size_t(n_views) * (std::max(1, c->E) + 1));
     { ++c->launches; k_cdf<<<n_views, 32, 0, c->stream>>>(c->segs.p, c->sil_count.p, std::max(1, c->E),
-                                                     n_views, c->cdf.p, c->total_len.p, c->degenerate.p); }
+                                                     n_views, c->cdf.p, c->total_len.p, c->degenerate.p,
+                                                     c->cdf_guide.p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -550,6 +578,7 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     p.pix_off = st.pix_off.p;
     p.segs = c->segs.p;
     p.cdf = c->cdf.p;
+    p.guide = c->cdf_guide.p;
     p.totals = c->total_len.p;
     p.count = c->sil_count.p;
     p.E = E;

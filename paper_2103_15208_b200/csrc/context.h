@@ -154,6 +154,7 @@ struct cdr_ctx {
     cdr::DBuf<int32_t> sil_block_count, sil_block_off, sil_count;
     cdr::DBuf<cdr_segment> segs;
     cdr::DBuf<double> cdf, total_len;
+    cdr::DBuf<int32_t> cdf_guide;  // per view: lower_bound guide over the CDF (k_cdf)
     cdr::DBuf<int32_t> degenerate;
     // boundary samples binned by segment
     cdr::DBuf<int32_t> b_seg_count, b_seg_off, b_n_active, b_key, b_slot, b_sorted_si;
