@@ -2,10 +2,15 @@
 """Benchmark of the B200 differentiable-rendering hot path (one JSON line).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg1..cfg5] [--views K]
 
-Under torchrun (N > 1) every rank drives one GPU: views are sharded (weak
-scaling: each rank owns one cfg2 workload of 50 views with its own global view
-ids), and the gradient is summed by the library's NCCL all-reduce.
+--gpus N > 1 without torchrun's environment re-executes this script under
+`torch.distributed.run --nproc-per-node N` (one rank per GPU; exits non-zero
+when fewer than N devices exist). Under torchrun every rank drives one GPU:
+the config's views are sharded by global view id and the gradient is summed
+by the library's NCCL all-reduce inside cdr_loss_grad. The default config is
+cfg2 (BASELINE configs[1]: 50 views, weak scaling) at N = 1 and cfg3
+(configs[2]: 100 views split over the ranks, strong scaling) at N > 1.
 
 A step = the hot subset of total_loss (losses.cpp:244-297) over the rank's
 views: per-iteration LBVH rebuild + normals, fused trace/shade/loss/interior,
@@ -14,10 +19,13 @@ silhouettes + boundary edge sampling, normal chain, cotangent Laplacian.
           before each step), inputs resident in HBM, gradient left on device.
   e2e   : the same step through the C-ABI with HOST buffers: positions and the
           three texture maps uploaded from pinned memory and the gradient
-          downloaded every step (wall clock around the blocking C-ABI call).
+          downloaded every step (wall clock around the blocking C-ABI call);
+          e2e.with_rendered_images adds total_loss's K rendered images + masks
+          (TotalLossResult::rendered, losses.cpp:259) to the download.
   cpu_baseline : the reference library compiled from its own sources
-          (oracle/_ref; the C oracle port if absent), one cfg2 view per sample,
-          all host threads, rank 0 at N = 1 only.
+          (oracle/_ref; the C oracle port if absent) on the fixed 4-view subset
+          of BASELINE.md §3.4 (global views 0-3), all host threads, rank 0 at
+          N = 1 only.
 """
 from __future__ import annotations
 
@@ -63,18 +71,19 @@ def _env_int(k, d):
         return d
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    p.add_argument("--config", default=None, choices=sorted(CONFIGS),
+                   help="default: cfg2 at one GPU, cfg3 (strong scaling) at N > 1")
     p.add_argument("--views", type=int, default=None, help="override the config's view count")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-iteration", action="store_true", help="skip the resident optimisation-iteration timing")
-    return p.parse_args()
+    return p.parse_args(argv)
 
 
 def build_workload(name, rank, world, n_views=None):
@@ -199,75 +208,122 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline_sample(scene, spp, seed, lay, threads, kind_pref="reference", label="cfg2"):
-    """Reference total_loss on ONE view of the workload (bounded sample)."""
+CPU_SUBSET = 4  # a fixed 4-view subset (global views 0-3)
+
+
+def cpu_baseline_sample(scene, spp, seed, lay, threads, kind_pref="reference", label="cfg2", views=None):
+    """Reference total_loss on a bounded sample: the given camera indices of
+    `scene` (default the first CPU_SUBSET), one total_loss call each."""
     from oracle import pyoracle
     from paper_2103_15208_b200 import scenes as S
-    one = S.Scene(scene.mesh, scene.diffuse, scene.specular, scene.roughness, scene.cameras[:1])
-    tscene = S.perturbed_target_scene(one)
-    kind = "reference"
-    try:
-        if kind_pref != "reference":
-            raise FileNotFoundError
-        ref = pyoracle.RefLib(one)
-        tref = pyoracle.RefLib(tscene)
-        tgt = tref.render(0, spp, seed + 0x7A9, threads=threads)[0][None]
+    views = list(range(min(CPU_SUBSET, len(scene.cameras)))) if views is None else list(views)
+    kind = "reference" if kind_pref == "reference" else "port"
+    dt, samples = 0.0, 0
+    for v in views:
+        one = S.Scene(scene.mesh, scene.diffuse, scene.specular, scene.roughness, [scene.cameras[v]])
+        tscene = S.perturbed_target_scene(one)
+        try:
+            if kind != "reference":
+                raise FileNotFoundError
+            ref = pyoracle.RefLib(one)
+            tgt = pyoracle.RefLib(tscene).render(0, spp, seed + 0x7A9, threads=threads)[0][None]
 
-        def run():
-            return ref.total_loss(tgt, spp, seed, lay, threads=threads)
-    except (FileNotFoundError, OSError):
-        kind = "port"
-        threads = 1
-        orc = pyoracle.Oracle(one)
-        tgt = pyoracle.Oracle(tscene).render(0, spp, seed + 0x7A9)[0][None]
-        st = pyoracle.settings(spp, seed)
+            def run():
+                return ref.total_loss(tgt, spp, seed, lay, threads=threads)
+        except (FileNotFoundError, OSError):
+            kind, threads = "port", 1
+            orc = pyoracle.Oracle(one)
+            tgt = pyoracle.Oracle(tscene).render(0, spp, seed + 0x7A9)[0][None]
+            st = pyoracle.settings(spp, seed)
 
-        def run():
-            return orc.loss_grad(tgt, st, lay)
-    t0 = time.perf_counter()
-    run()
-    dt = time.perf_counter() - t0
-    cam = one.cameras[0]
-    samples = cam.width * cam.height * spp
+            def run():
+                return orc.loss_grad(tgt, st, lay)
+        t0 = time.perf_counter()
+        run()
+        dt += time.perf_counter() - t0
+        cam = one.cameras[0]
+        samples += cam.width * cam.height * spp
+    cam = scene.cameras[views[0]]
     return {"value": samples / dt / 1e6, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"1 {label} view ({cam.width}^2 x {spp} spp, {scene.mesh.T:,} tris, {scene.tex_res[0]}^2 tex) "
-                      f"through total_loss, {dt:.2f} s wall", "seconds": dt}
+            "sample": f"{len(views)} {label} view(s) (cameras {views}; {cam.width}^2 x {spp} spp, "
+                      f"{scene.mesh.T:,} tris, {scene.tex_res[0]}^2 tex), one total_loss each, {dt:.2f} s wall",
+            "seconds": dt, "samples": samples}
 
 
 def run_reference(args, rank, world):
+    """The reference arm: oracle/_ref (the reference compiled from its own
+    sources) on the host cores; each step = total_loss of one view of the
+    4-view subset, cycling through it. Rank 0 only."""
     if rank != 0:
         return 0
     from paper_2103_15208_b200 import api
-    scene, gids, cfg, _ = build_workload(args.config, 0, 1, 1)
+    name = args.config
+    scene, gids, cfg, total = build_workload(name, 0, 1)  # the config's camera set; views 0-3 are sampled
     lay = api.param_layout(scene)
     threads = os.cpu_count() or 1
-    vals = []
+    secs, samples = [], 0
     cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline_sample(scene, cfg["spp"], 1, lay, threads, label=args.config)
+        cb = cpu_baseline_sample(scene, cfg["spp"], 1, lay, threads, label=name,
+                                 views=[i % min(CPU_SUBSET, len(scene.cameras))])
         if i >= args.warmup:
-            vals.append(cb["seconds"])
-    dt = sum(vals)
-    samples = cfg["image"] * cfg["image"] * cfg["spp"] * len(vals)
+            secs.append(cb["seconds"])
+            samples += cb["samples"]
+    dt = sum(secs)
     v = samples / dt / 1e6
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * dt / len(vals), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_text(args.config, cfg, cfg["views"]),
-                       "sample": "1 view per step (bounded CPU sample)",
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / len(secs), "higher_is_better": True,
+            "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_text(name, cfg, CONFIGS[name]["views"]), "name": name,
+                       "sample": f"1 view per step, cycling through the {CPU_SUBSET}-view subset (global views "
+                                 f"0-{CPU_SUBSET - 1}, BASELINE.md §3.4) (bounded CPU sample)",
                        "threads": threads},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cb["cores"], "kind": cb["kind"],
-                             "sample": cb["sample"]},
+                             "sample": f"{len(secs)} steps x 1 view of the {CPU_SUBSET}-view subset through "
+                                       f"total_loss, {dt:.2f} s wall"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def main():
-    args = parse()
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_command(argv, n, port):
+    """torchrun command that re-executes this script with one rank per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+
+
+def relaunch(args, argv):
+    """--gpus N > 1 outside torchrun: check the devices, then run N ranks."""
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+            return 2
+    cmd = launch_command(argv, args.gpus, _free_port())
+    print("bench.py: " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.run(cmd).returncode
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args, argv)
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
     local = _env_int("LOCAL_RANK", 0)
+    if args.config is None:
+        args.config = "cfg2" if world == 1 else "cfg3"
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -291,6 +347,11 @@ def main():
         if dist is not None:
             dist.broadcast_object_list(uid, src=0)
         r.comm_init(uid[0], world, rank)
+        nranks, crank = r.comm_info()
+        print(f"[bench] rank {rank}: NCCL communicator of {nranks} ranks, this rank {crank} on cuda:{local}",
+              file=sys.stderr, flush=True)
+        if nranks != world:
+            raise RuntimeError(f"NCCL communicator has {nranks} ranks, expected {world}")
     # targets: the perturbed scene rendered by the same engine (gradcheck.cpp:49-73)
     from paper_2103_15208_b200 import scenes as S
     tr = api.Renderer(local, S.perturbed_target_scene(scene), view_ids=gids)
@@ -391,7 +452,27 @@ def main():
         h2d = pos_h.nbytes + d_h.nbytes + s_h.nbytes + r_h.nbytes
         d2h = g_h.nbytes + 16
         e2e = {"value": total_samples / float(te.item()) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(te.item()) / args.steps}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(te.item()) / args.steps,
+               "what": "cdr_loss_grad with host buffers: positions + 3 maps up, gradient + loss down"}
+        # the same with total_loss's rendered images and masks (the K Images of
+        # TotalLossResult, losses.cpp:259) downloaded into pinned buffers too
+        npx = sum(c.width * c.height for c in scene.cameras)
+        rgb_h, msk_h = pin(np.zeros(3 * npx)), pin(np.zeros(npx))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r.update_positions(pos_h)
+            r.set_textures(d_h, s_h, r_h)
+            r.loss_grad(views, st, lay, grad=g_h, overwrite=True, rendered_out=rgb_h, mask_out=msk_h)
+        barrier()
+        dt = time.perf_counter() - t0
+        te = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e["with_rendered_images"] = {
+            "value": total_samples / float(te.item()) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h + rgb_h.nbytes + msk_h.nbytes),
+            "ms_per_step": 1e3 * float(te.item()) / args.steps}
 
     # ---- the four mesh/material regularisers of total_loss (losses.cpp:272-292)
     # at the reference's default weights: texture-size work, not per sample, so
@@ -471,10 +552,12 @@ def main():
                      "what": "total_loss (rendering + Laplacian + 4 regularisers, LossWeights defaults) -> "
                              "adam_step + apply -> robust_evolve, resident on the device"}
         if cb is not None:  # the reference's iteration, extrapolated from the bounded sample
-            ref_ms = cb["seconds"] * total_views * 1e3 + (regs or {}).get("cpu_ms", 0.0)
+            per_view_s = cb["seconds"] * (cfg["image"] ** 2 * spp) / cb["samples"]
+            ref_ms = per_view_s * total_views * 1e3 + ((regs or {}).get("cpu_ms") or 0.0)
             iteration["reference_ms_extrapolated"] = ref_ms
-            iteration["reference_basis"] = (f"total_loss of 1 view x {total_views} views ({cb['cores']} threads) "
-                                            "+ the serial regularisers; adam/evolve not included")
+            iteration["reference_basis"] = (f"mean total_loss time per view of the {CPU_SUBSET}-view subset x "
+                                            f"{total_views} views ({cb['cores']} threads) + the serial regularisers; "
+                                            "adam/evolve not included")
 
     if rank == 0:
         stages = {k: statistics.mean(x[k] for x in stats) for k in

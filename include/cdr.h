@@ -180,6 +180,16 @@ int cdr_render(cdr_ctx* ctx, int32_t view, const cdr_settings* settings, double*
 int cdr_radiance_at(cdr_ctx* ctx, int32_t view, int32_t n, const double* xy, double* rgb_out,
                     int32_t* tri_out);
 
+/* The radiance probes of boundary_pass (diff_render.cpp:246-252: radiance_at
+ * at x - n/2 and x + n/2) as the fused loss call traces them: through the
+ * per-pixel candidate lists the LAST cdr_render / cdr_loss_grad /
+ * cdr_total_loss built for `view`, points taken in pairs (xy[2i], xy[2i+1])
+ * exactly like one edge sample's two probes. Same outputs as cdr_radiance_at;
+ * a test hook proving the list path bit-exact against per-ray traversal.
+ * CDR_ERR_INVALID_ARG when the last call built no lists for the view. */
+int cdr_probe_points(cdr_ctx* ctx, int32_t view, int32_t n, const double* xy, double* rgb_out,
+                     int32_t* tri_out);
+
 /* view_rendering_loss (losses.hpp:37-38, losses.cpp:15-49). target_mask may be
  * NULL. adjoint_out is W x H x 3. */
 int cdr_view_loss(cdr_ctx* ctx, int32_t width, int32_t height, const double* rendered,
@@ -319,6 +329,19 @@ int cdr_get_params(cdr_ctx* ctx, const cdr_layout* layout, double* params_out);
  * NCCL (loaded at run time). id is an ncclUniqueId (128 bytes). */
 int cdr_nccl_unique_id(char id_out[128]);
 int cdr_comm_init(cdr_ctx* ctx, const char id[128], int32_t n_ranks, int32_t rank);
+/* One process driving n GPUs (the drop-in shim, CDR_DEVICES): one context per
+ * device, all joined by ncclCommInitAll; context i becomes rank i. Each
+ * context's cdr_loss_grad / cdr_total_loss must then be called concurrently
+ * (one host thread per context), as for ranks in separate processes. */
+int cdr_comm_init_all(cdr_ctx** ctxs, int32_t n);
+/* Ranks and own rank as the attached NCCL communicator reports them
+ * (ncclCommCount / ncclCommUserRank); 1 and 0 without one. */
+int cdr_comm_info(cdr_ctx* ctx, int32_t* n_ranks, int32_t* rank);
+/* View shard of a group summed by the caller instead of NCCL (several
+ * contexts on one device, e.g. testing the sharding on one GPU): only rank 0
+ * adds the once-per-iteration terms (Laplacian, regularisers), as under a
+ * communicator. Not allowed on a context with a communicator. */
+int cdr_set_rank(cdr_ctx* ctx, int32_t rank, int32_t n_ranks);
 
 #ifdef __cplusplus
 }

@@ -866,12 +866,15 @@ int orc_silhouettes(const orc_ctx* c, int32_t view, cdr_segment* out, int32_t ca
 }
 
 /* ---- diff_render.cpp:203-283 boundary_pass ------------------------------ */
+/* boundary_pass with a caller's SilhouetteSet (diff_render.cpp:203-283 takes
+ * the set as an argument); nseg segments, total = its total_length. */
+int orc_boundary_segs(const orc_ctx* c, int32_t view, const double* adjoint, const cdr_segment* segs_in,
+                      int32_t nseg, double tot, int32_t samples, uint64_t seed, int32_t probe,
+                      const cdr_layout* Lay, double* g, int32_t* degenerate);
+
 int orc_boundary(const orc_ctx* c, int32_t view, const double* adjoint, int32_t samples,
                  uint64_t seed, int32_t probe, const cdr_layout* Lay, double* g,
                  int32_t* degenerate) {
-    const orc_scene* s = c->s;
-    const cdr_camera* cam = &s->cams[view];
-    const int gid = view_id(s, view);
     int nseg = 0;
     double tot = 0;
     *degenerate = 0;
@@ -879,6 +882,21 @@ int orc_boundary(const orc_ctx* c, int32_t view, const double* adjoint, int32_t 
     if (nseg == 0 || tot <= 0 || samples <= 0) return 0;
     cdr_segment* segs = (cdr_segment*)malloc(sizeof(cdr_segment) * (size_t)nseg);
     orc_silhouettes(c, view, segs, nseg, &nseg, &tot);
+    int rc = orc_boundary_segs(c, view, adjoint, segs, nseg, tot, samples, seed, probe, Lay, g, degenerate);
+    free(segs);
+    return rc;
+}
+
+int orc_boundary_segs(const orc_ctx* c, int32_t view, const double* adjoint, const cdr_segment* segs_in,
+                      int32_t nseg, double tot, int32_t samples, uint64_t seed, int32_t probe,
+                      const cdr_layout* Lay, double* g, int32_t* degenerate) {
+    const orc_scene* s = c->s;
+    const cdr_camera* cam = &s->cams[view];
+    const int gid = view_id(s, view);
+    *degenerate = 0;
+    if (nseg <= 0 || tot <= 0 || samples <= 0) return 0; /* diff_render.cpp:210-211 */
+    cdr_segment* segs = (cdr_segment*)malloc(sizeof(cdr_segment) * (size_t)nseg);
+    memcpy(segs, segs_in, sizeof(cdr_segment) * (size_t)nseg);
     double* cdf = (double*)malloc(sizeof(double) * (size_t)nseg);
     double acc = 0;
     int usable = 0;

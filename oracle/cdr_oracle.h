@@ -72,6 +72,9 @@ int orc_silhouettes(const orc_ctx* c, int32_t view, cdr_segment* out, int32_t ca
 int orc_boundary(const orc_ctx* c, int32_t view, const double* adjoint, int32_t samples,
                  uint64_t seed, int32_t probe, const cdr_layout* layout, double* grad,
                  int32_t* degenerate);
+int orc_boundary_segs(const orc_ctx* c, int32_t view, const double* adjoint, const cdr_segment* segs,
+                      int32_t nseg, double total_length, int32_t samples, uint64_t seed, int32_t probe,
+                      const cdr_layout* layout, double* grad, int32_t* degenerate);
 int orc_laplacian(const orc_scene* s, int32_t mode, double lambda, double* value, double* grad,
                   int32_t* outer, int32_t* inner, double* vals);
 /* normal_consistency / edge_length / specular_correlation / roughness_tv

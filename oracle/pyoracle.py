@@ -357,10 +357,21 @@ class Oracle:
                                  C.byref(n), C.byref(tot))
         return out, tot.value
 
-    def boundary(self, view, adjoint, samples, seed, lay, probe=0, grad=None):
+    def boundary(self, view, adjoint, samples, seed, lay, probe=0, grad=None, segments=None):
+        """boundary_pass; `segments` (SEGMENT_DTYPE) = a caller's SilhouetteSet,
+        else this view's own extract_silhouettes."""
         g = np.zeros(lay["total"]) if grad is None else grad
         cl = c_layout(lay)
         deg = C.c_int32()
+        if segments is not None:
+            sg = np.ascontiguousarray(segments, dtype=SEGMENT_DTYPE)
+            tot = 0.0
+            for x in sg["length_px"]:  # silhouette.cpp:103
+                tot += float(x)
+            self._chk(self.lib.orc_boundary_segs(C.c_void_p(self.ctx), view, dp(np.ascontiguousarray(adjoint)),
+                                                 sg.ctypes.data_as(C.c_void_p), len(sg), C.c_double(tot), samples,
+                                                 C.c_uint64(seed), probe, C.byref(cl), dp(g), C.byref(deg)))
+            return g, deg.value
         self._chk(self.lib.orc_boundary(C.c_void_p(self.ctx), view, dp(np.ascontiguousarray(adjoint)),
                                         samples, C.c_uint64(seed), probe, C.byref(cl), dp(g), C.byref(deg)))
         return g, deg.value

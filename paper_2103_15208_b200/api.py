@@ -139,6 +139,7 @@ def load_library(path: str = LIB_PATH):
     L.cdr_vertex_normals.argtypes = [_vp, _d]
     L.cdr_render.argtypes = [_vp, C.c_int32, C.POINTER(cdr_settings), _d, _d, _i]
     L.cdr_radiance_at.argtypes = [_vp, C.c_int32, C.c_int32, _d, _d, _i]
+    L.cdr_probe_points.argtypes = [_vp, C.c_int32, C.c_int32, _d, _d, _i]
     L.cdr_view_loss.argtypes = [_vp, C.c_int32, C.c_int32, _d, _d, _d, C.c_double, C.c_double, C.c_int32,
                                 _d, _d]
     L.cdr_interior_pass.argtypes = [_vp, C.c_int32, _d, C.POINTER(cdr_settings), _i, C.c_int64,
@@ -170,6 +171,9 @@ def load_library(path: str = LIB_PATH):
     L.cdr_laplacian_loss.argtypes = [_vp, C.c_int32, C.c_double, _d, _d]
     L.cdr_nccl_unique_id.argtypes = [C.c_char_p]
     L.cdr_comm_init.argtypes = [_vp, C.c_char_p, C.c_int32, C.c_int32]
+    L.cdr_comm_info.argtypes = [_vp, _i, _i]
+    L.cdr_comm_init_all.argtypes = [C.POINTER(_vp), C.c_int32]
+    L.cdr_set_rank.argtypes = [_vp, C.c_int32, C.c_int32]
     L.cdr_device_count.argtypes = [C.POINTER(C.c_int)]
     _lib = L
     return L
@@ -378,6 +382,16 @@ class Renderer:
         self._chk(self.L.cdr_radiance_at(self.h, view, len(xy), _dp(xy), _dp(rgb), _ip(tri)))
         return rgb, tri
 
+    def probe_points(self, view, xy):
+        """The boundary pass's radiance probes through the candidate lists of
+        the last render / loss call (points traced in pairs, as one edge
+        sample's x - n/2 and x + n/2): (rgb n x 3, tri n)."""
+        xy = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
+        rgb = np.zeros((len(xy), 3))
+        tri = np.zeros(len(xy), np.int32)
+        self._chk(self.L.cdr_probe_points(self.h, view, len(xy), _dp(xy), _dp(rgb), _ip(tri)))
+        return rgb, tri
+
     def view_rendering_loss(self, rendered, target, lambda_rend=1.0, gamma=2.2, target_mask=None,
                             use_target_mask=False):
         rendered = np.ascontiguousarray(rendered, dtype=np.float64)
@@ -432,7 +446,7 @@ class Renderer:
 
     def loss_grad(self, views, settings: RenderSettings, layout, lambda_rend=1.0, lambda_lap=0.1,
                   laplacian_mode=0, use_target_mask=False, grad=None, want_rendered=False, device_only=False,
-                  overwrite=False):
+                  overwrite=False, rendered_out=None, mask_out=None):
         """Rendering + Laplacian part of total_loss over `views` (slots). Returns
         (loss[2], grad, stats, rendered). The gradient is added to `grad` (fresh
         zeros by default), or written over it with overwrite=True (the caller's
@@ -444,14 +458,14 @@ class Renderer:
         lay = _clayout(layout)
         loss = np.zeros(2)
         g = None if device_only else (np.zeros(layout["total"]) if grad is None else grad)
-        rend = None
-        if want_rendered:
+        rend = rendered_out
+        if want_rendered and rend is None:
             npx = sum(self.cameras[v].width * self.cameras[v].height for v in views)
             rend = np.zeros(3 * npx)
         stats = cdr_stats()
         self._chk(self.L.cdr_loss_grad(self.h, _ip(views), len(views), C.byref(st), lambda_rend, lambda_lap,
                                        laplacian_mode, int(use_target_mask), C.byref(lay), _dp(loss), _dp(g),
-                                       _dp(rend), None, C.byref(stats)))
+                                       _dp(rend), _dp(mask_out), C.byref(stats)))
         return loss, g, stats, rend
 
     def total_loss(self, targets, settings: RenderSettings, layout, lambda_rend=1.0, lambda_lap=0.1,
@@ -664,6 +678,27 @@ class Renderer:
 
     def comm_init(self, uid: bytes, n_ranks: int, rank: int):
         self._chk(self.L.cdr_comm_init(self.h, C.c_char_p(uid), n_ranks, rank))
+
+    def set_rank(self, rank: int, n_ranks: int):
+        """Shard of a group summed by the caller (no communicator): only rank 0
+        adds the Laplacian and the regularisers."""
+        self._chk(self.L.cdr_set_rank(self.h, rank, n_ranks))
+
+    @staticmethod
+    def comm_init_all(renderers):
+        """One process, one context per device: ncclCommInitAll over them."""
+        L = load_library()
+        arr = (_vp * len(renderers))(*[r.h for r in renderers])
+        rc = L.cdr_comm_init_all(arr, len(renderers))
+        if rc != 0:
+            raise _ERRORS.get(rc, CollodiffError)(L.cdr_last_error(renderers[0].h).decode())
+
+    def comm_info(self):
+        """(ranks, rank) as NCCL's communicator reports them (ncclCommCount /
+        ncclCommUserRank); (1, 0) without a communicator."""
+        n, r = C.c_int32(), C.c_int32()
+        self._chk(self.L.cdr_comm_info(self.h, C.byref(n), C.byref(r)))
+        return n.value, r.value
 
 
 def device_count() -> int:

@@ -184,6 +184,11 @@ struct NcclApi {
     int (*commInitRank)(void**, int, const void* /* by value 128B */, int) = nullptr;
     int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
     int (*commDestroy)(void*) = nullptr;
+    int (*commCount)(void*, int*) = nullptr;
+    int (*commUserRank)(void*, int*) = nullptr;
+    int (*commInitAll)(void**, int, const int*) = nullptr;
+    int (*groupStart)() = nullptr;
+    int (*groupEnd)() = nullptr;
     const char* (*getErrorString)(int) = nullptr;
     bool ok = false;
 };
@@ -206,6 +211,11 @@ NcclApi load_nccl() {
         dlsym(api.h, "ncclAllReduce"));
     api.commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(api.h, "ncclCommDestroy"));
     api.getErrorString = reinterpret_cast<const char* (*)(int)>(dlsym(api.h, "ncclGetErrorString"));
+    api.commCount = reinterpret_cast<int (*)(void*, int*)>(dlsym(api.h, "ncclCommCount"));
+    api.commUserRank = reinterpret_cast<int (*)(void*, int*)>(dlsym(api.h, "ncclCommUserRank"));
+    api.commInitAll = reinterpret_cast<int (*)(void**, int, const int*)>(dlsym(api.h, "ncclCommInitAll"));
+    api.groupStart = reinterpret_cast<int (*)()>(dlsym(api.h, "ncclGroupStart"));
+    api.groupEnd = reinterpret_cast<int (*)()>(dlsym(api.h, "ncclGroupEnd"));
     api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy;
     return api;
 }
@@ -270,40 +280,21 @@ void cdr_destroy(cdr_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->geo) cdr_destroy(c->geo);
-    c->si_pairs.release();
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->side) cudaStreamSynchronize(c->side);
     free_render_statics(c);
     free_boundary_statics(c);
-    for (auto& b : c->scr_d) b.release();
-    c->scr_i.release(); c->scr_f.release(); c->scr_flag.release(); c->scr_u64.release();
     if (c->nccl_comm && nccl().ok) nccl().commDestroy(c->nccl_comm);
-    cudaStreamSynchronize(c->stream);
     for (auto& e : c->ev) cudaEventDestroy(e);
     for (auto& e : c->chunk_ev) cudaEventDestroy(e);
-    // DBufs are released with the process/context; free the big ones explicitly
-    c->pos.release(); c->uv.release(); c->normals.release(); c->accum.release(); c->fnormal.release();
-    c->tris.release(); c->edges.release(); c->vf_start.release(); c->vf_list.release();
-    c->lap_rowptr.release(); c->lap_col.release(); c->lap_edge_slot.release(); c->lap_diag_slot.release();
-    c->lap_val.release(); c->lap_lv.release(); c->lap_grad.release(); c->lap_partial.release();
-    c->info.release(); c->bbox_partial.release(); c->keys.release(); c->keys_alt.release();
-    c->sort_tmp.release(); c->parent_internal.release(); c->parent_leaf.release(); c->refit_flag.release();
-    c->node_box.release(); c->nodes.release(); c->recs.release();
-    c->beam_hdr.release(); c->beam_pool.release(); c->beam_used.release();
-    c->beam_pix_list.release(); c->beam_pix_cnt.release();
-    if (c->beam_used_host) cudaFreeHost(c->beam_used_host); c->tex.release(); c->d_cams.release();
-    c->target.release(); c->target_mask.release(); c->img.release(); c->mask.release(); c->adj.release();
-    c->hit.release(); c->sil_flag.release(); c->sil_block_count.release(); c->sil_block_off.release();
-    c->sil_count.release(); c->segs.release(); c->cdf.release(); c->total_len.release();
-    c->degenerate.release(); c->grad.release(); c->grad_tmp.release(); c->corner_acc.release(); c->tex_acc.release(); c->qvec.release();
-    c->loss_acc.release(); c->errinfo.release(); c->counters.release();
-    if (c->side) {
-        cudaStreamSynchronize(c->side);
-        cudaEventDestroy(c->ev_fork);
-        cudaEventDestroy(c->ev_sil);
-        cudaEventDestroy(c->ev_reg);
-        cudaStreamDestroy(c->side);
-    }
-    cudaStreamDestroy(c->stream);
-    delete c;
+    if (c->beam_used_host) cudaFreeHost(c->beam_used_host);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_sil) cudaEventDestroy(c->ev_sil);
+    if (c->ev_reg) cudaEventDestroy(c->ev_reg);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;  // every DBuf member frees its device allocation (context.h)
 }
 
 const char* cdr_last_error(const cdr_ctx* c) { return c ? c->err.c_str() : "null context"; }
@@ -319,6 +310,9 @@ int cdr_set_mesh(cdr_ctx* c, const double* positions, int32_t nv, const int32_t*
     API_BEGIN(c)
     if (nv < 0 || nt < 0 || (nv > 0 && !positions) || (nt > 0 && !triangles))
         throw ApiErr(CDR_ERR_INVALID_ARG, "bad mesh arguments");
+    // Everything is built and validated in locals first; the context changes
+    // only after every check has passed, so a rejected mesh leaves the
+    // previous one fully usable.
     // build_adjacency validation (mesh.cpp:27-38)
     for (int f = 0; f < nt; ++f) {
         const int32_t* t = triangles + 3 * f;
@@ -329,13 +323,11 @@ int cdr_set_mesh(cdr_ctx* c, const double* positions, int32_t nv, const int32_t*
         if (t[0] == t[1] || t[1] == t[2] || t[0] == t[2])
             throw ApiErr(CDR_ERR_ERROR, "triangle " + std::to_string(f) + " repeats a vertex");
     }
-    c->V = nv;
-    c->T = nt;
-    c->h_tris.assign(triangles, triangles + 3 * size_t(nt));
     // edges: caller's (reference order) or rebuilt with build_adjacency's order
+    std::vector<int32_t> h_edges;
     if (edges) {
         if (ne < 0) throw ApiErr(CDR_ERR_INVALID_ARG, "negative edge count");
-        c->h_edges.assign(edges, edges + 4 * size_t(ne));
+        h_edges.assign(edges, edges + 4 * size_t(ne));
     } else {
         std::vector<std::pair<int64_t, int>> keys;
         keys.reserve(3 * size_t(nt));
@@ -345,7 +337,6 @@ int cdr_set_mesh(cdr_ctx* c, const double* positions, int32_t nv, const int32_t*
                 keys.push_back({int64_t(std::min(a, b)) * nv + std::max(a, b), f});
             }
         std::sort(keys.begin(), keys.end());
-        c->h_edges.clear();
         for (size_t i = 0; i < keys.size();) {
             size_t j = i;
             while (j < keys.size() && keys[j].first == keys[i].first) ++j;
@@ -354,22 +345,21 @@ int cdr_set_mesh(cdr_ctx* c, const double* positions, int32_t nv, const int32_t*
                 throw ApiErr(CDR_ERR_ERROR, "non-manifold edge (" + std::to_string(key / nv) + "," +
                                                 std::to_string(key % nv) + ") with " + std::to_string(j - i) +
                                                 " incident faces");
-            c->h_edges.push_back(int32_t(key / nv));
-            c->h_edges.push_back(int32_t(key % nv));
-            c->h_edges.push_back(keys[i].second);
-            c->h_edges.push_back(j - i > 1 ? keys[i + 1].second : -1);
+            h_edges.push_back(int32_t(key / nv));
+            h_edges.push_back(int32_t(key % nv));
+            h_edges.push_back(keys[i].second);
+            h_edges.push_back(j - i > 1 ? keys[i + 1].second : -1);
             i = j;
         }
     }
-    c->E = int(c->h_edges.size() / 4);
-    ++c->topo_version;
-    c->adam_ready = false;  // a new vertex set: the optimiser state no longer matches
-    cudaStream_t s = c->stream;
-    h2d(c->pos, positions, 3 * size_t(nv), s);
-    c->has_uv = uvs != nullptr;
-    if (uvs) h2d(c->uv, uvs, 2 * size_t(nv), s);
-    h2d(c->tris, triangles, 3 * size_t(nt), s);
-    h2d(c->edges, reinterpret_cast<const int4*>(c->h_edges.data()), size_t(c->E), s);
+    const int ecount = int(h_edges.size() / 4);
+    for (int e = 0; e < ecount; ++e) {  // k_sil_flag reads face normals through f0/f1
+        const int32_t a = h_edges[4 * e], b = h_edges[4 * e + 1], f0 = h_edges[4 * e + 2], f1 = h_edges[4 * e + 3];
+        if (a < 0 || a >= nv || b < 0 || b >= nv)
+            throw ApiErr(CDR_ERR_INVALID_ARG, "edge " + std::to_string(e) + ": vertex out of range");
+        if (f0 < 0 || f0 >= nt || f1 < -1 || f1 >= nt)
+            throw ApiErr(CDR_ERR_INVALID_ARG, "edge " + std::to_string(e) + ": face out of range");
+    }
     // vertex -> (face*3+corner), ascending face (the reference's face-loop order)
     std::vector<int32_t> vstart(size_t(nv) + 1, 0), vlist(3 * size_t(nt));
     for (int f = 0; f < nt; ++f)
@@ -380,18 +370,15 @@ int cdr_set_mesh(cdr_ctx* c, const double* positions, int32_t nv, const int32_t*
         for (int f = 0; f < nt; ++f)
             for (int k = 0; k < 3; ++k) vlist[fill[triangles[3 * f + k]]++] = 3 * f + k;
     }
-    h2d(c->vf_start, vstart.data(), vstart.size(), s);
-    h2d(c->vf_list, vlist.data(), vlist.size(), s);
     // Laplacian CSR pattern: row i = sorted {neighbours} ∪ {i}
     std::vector<std::vector<int32_t>> nb(nv);
-    for (int e = 0; e < c->E; ++e) {
-        int a = c->h_edges[4 * e], b = c->h_edges[4 * e + 1];
-        if (a < 0 || a >= nv || b < 0 || b >= nv) throw ApiErr(CDR_ERR_INVALID_ARG, "edge vertex out of range");
+    for (int e = 0; e < ecount; ++e) {
+        int a = h_edges[4 * e], b = h_edges[4 * e + 1];
         nb[a].push_back(b);
         nb[b].push_back(a);
     }
     std::vector<int32_t> rowptr(size_t(nv) + 1, 0), col, dslot(nv);
-    col.reserve(size_t(nv) + 2 * size_t(c->E));
+    col.reserve(size_t(nv) + 2 * size_t(ecount));
     for (int i = 0; i < nv; ++i) {
         nb[i].push_back(i);
         std::sort(nb[i].begin(), nb[i].end());
@@ -401,25 +388,50 @@ int cdr_set_mesh(cdr_ctx* c, const double* positions, int32_t nv, const int32_t*
         }
         rowptr[i + 1] = int32_t(col.size());
     }
-    std::vector<int2> eslot(c->E);
-    for (int e = 0; e < c->E; ++e) {
-        int a = c->h_edges[4 * e], b = c->h_edges[4 * e + 1];
+    std::vector<int2> eslot(ecount);
+    for (int e = 0; e < ecount; ++e) {
+        int a = h_edges[4 * e], b = h_edges[4 * e + 1];
         auto find = [&](int row, int cc) {
             auto it = std::lower_bound(col.begin() + rowptr[row], col.begin() + rowptr[row + 1], cc);
             return int32_t(it - col.begin());
         };
         eslot[e] = make_int2(find(a, b), find(b, a));
     }
-    h2d(c->lap_rowptr, rowptr.data(), rowptr.size(), s);
-    h2d(c->lap_col, col.data(), col.size(), s);
-    h2d(c->lap_diag_slot, dslot.data(), dslot.size(), s);
-    h2d(c->lap_edge_slot, eslot.data(), eslot.size(), s);
-    c->lap_val.ensure(std::max<size_t>(1, col.size()));
-    c->normals.ensure(3 * size_t(std::max(1, nv)));
-    c->accum.ensure(3 * size_t(std::max(1, nv)));
-    c->fnormal.ensure(3 * size_t(std::max(1, nt)));
+    // commit: host state, then the device copies (a failed upload leaves an
+    // empty mesh rather than a mix of old buffers and new sizes)
+    c->V = nv;
+    c->T = nt;
+    c->E = ecount;
+    c->h_tris.assign(triangles, triangles + 3 * size_t(nt));
+    c->h_edges.swap(h_edges);
+    ++c->topo_version;
+    c->adam_ready = false;  // a new vertex set: the optimiser state no longer matches
     c->geometry_dirty = true;
-    sync(c);
+    c->beam_view.valid = false;
+    try {
+        cudaStream_t s = c->stream;
+        h2d(c->pos, positions, 3 * size_t(nv), s);
+        c->has_uv = uvs != nullptr;
+        if (uvs) h2d(c->uv, uvs, 2 * size_t(nv), s);
+        h2d(c->tris, triangles, 3 * size_t(nt), s);
+        h2d(c->edges, reinterpret_cast<const int4*>(c->h_edges.data()), size_t(c->E), s);
+        h2d(c->vf_start, vstart.data(), vstart.size(), s);
+        h2d(c->vf_list, vlist.data(), vlist.size(), s);
+        h2d(c->lap_rowptr, rowptr.data(), rowptr.size(), s);
+        h2d(c->lap_col, col.data(), col.size(), s);
+        h2d(c->lap_diag_slot, dslot.data(), dslot.size(), s);
+        h2d(c->lap_edge_slot, eslot.data(), eslot.size(), s);
+        c->lap_val.ensure(std::max<size_t>(1, col.size()));
+        c->normals.ensure(3 * size_t(std::max(1, nv)));
+        c->accum.ensure(3 * size_t(std::max(1, nv)));
+        c->fnormal.ensure(3 * size_t(std::max(1, nt)));
+        sync(c);
+    } catch (...) {
+        c->V = c->T = c->E = 0;
+        c->h_tris.clear();
+        c->h_edges.clear();
+        throw;
+    }
     API_END
 }
 
@@ -610,6 +622,27 @@ int cdr_radiance_at(cdr_ctx* c, int32_t view, int32_t n, const double* xy, doubl
     API_END
 }
 
+int cdr_probe_points(cdr_ctx* c, int32_t view, int32_t n, const double* xy, double* rgb, int32_t* tri) {
+    API_BEGIN(c)
+    check_view(c, view);
+    check_ready(c);
+    if (n < 0 || (n > 0 && !xy)) throw ApiErr(CDR_ERR_INVALID_ARG, "bad probe points");
+    if (n == 0) return;
+    const auto it = std::find(c->beam_slots.begin(), c->beam_slots.end(), view);
+    if (!c->beam_view.valid || it == c->beam_slots.end())
+        throw ApiErr(CDR_ERR_INVALID_ARG, "the last render call built no candidate lists for this view");
+    DBuf<double>&dxy = c->scr_d[0], &drgb = c->scr_d[1];
+    DBuf<int32_t>& dtri = c->scr_i;
+    h2d(dxy, xy, 2 * size_t(n), c->stream);
+    drgb.ensure(3 * size_t(n));
+    dtri.ensure(n);
+    launch_probe_points(c, int(it - c->beam_slots.begin()), n, dxy.p, drgb.p, dtri.p);
+    if (rgb) CDR_CUDA_CHECK(cudaMemcpyAsync(rgb, drgb.p, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c->stream));
+    if (tri) CDR_CUDA_CHECK(cudaMemcpyAsync(tri, dtri.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    sync(c);
+    API_END
+}
+
 int cdr_view_loss(cdr_ctx* c, int32_t w, int32_t h, const double* rendered, const double* target,
                   const double* tmask, double lambda, double gamma, int32_t use_mask, double* value,
                   double* adjoint) {
@@ -716,12 +749,15 @@ int cdr_boundary_pass(cdr_ctx* c, int32_t view, const double* adjoint, const cdr
     int slot = view;
     int m = samples;
     if (segments) {
-        if (nseg > std::max(1, c->E)) {
-            // caller-provided sets may exceed the per-view capacity of E
-            c->segs.ensure(size_t(nseg));
-            c->cdf.ensure(size_t(nseg));
-        }
-        set_view_calls(c, &slot, &m, 1);
+        if (nseg < 0) throw ApiErr(CDR_ERR_INVALID_ARG, "negative segment count");
+        for (int32_t i = 0; i < nseg; ++i)  // the deposits index the position gradient by v0/v1
+            if (segments[i].v0 < 0 || segments[i].v0 >= c->V || segments[i].v1 < 0 || segments[i].v1 >= c->V)
+                throw ApiErr(CDR_ERR_INVALID_ARG, "silhouette segment " + std::to_string(i) +
+                                                      " references a vertex out of range (stale set?)");
+        // a caller-provided set may hold more segments than the mesh has
+        // edges: every per-view array (segments, CDF, guide, bins) is sized
+        // and strided by max(E, nseg)
+        set_view_calls(c, &slot, &m, 1, nseg);
         if (nseg > 0)
             CDR_CUDA_CHECK(cudaMemcpyAsync(c->segs.p, segments, sizeof(cdr_segment) * nseg, cudaMemcpyHostToDevice,
                                            c->stream));
@@ -1335,6 +1371,54 @@ int cdr_comm_init(cdr_ctx* c, const char id[128], int32_t n_ranks, int32_t rank)
     c->nccl_comm = comm;
     c->n_ranks = n_ranks;
     c->rank = rank;
+    API_END
+}
+
+int cdr_comm_info(cdr_ctx* c, int32_t* n_ranks, int32_t* rank) {
+    API_BEGIN(c)
+    int n = 1, r = 0;
+    if (c->nccl_comm) {
+        NcclApi& api = nccl();
+        if (!api.commCount || !api.commUserRank) throw ApiErr(CDR_ERR_ERROR, "ncclCommCount not available");
+        nccl_check(api.commCount(c->nccl_comm, &n), "ncclCommCount");
+        nccl_check(api.commUserRank(c->nccl_comm, &r), "ncclCommUserRank");
+    }
+    if (n_ranks) *n_ranks = n;
+    if (rank) *rank = r;
+    API_END
+}
+
+int cdr_comm_init_all(cdr_ctx** ctxs, int32_t n) {
+    if (!ctxs || n < 1) return CDR_ERR_INVALID_ARG;
+    for (int i = 0; i < n; ++i)
+        if (!ctxs[i]) return CDR_ERR_INVALID_ARG;
+    return handle(ctxs[0], [&]() {
+        NcclApi& api = nccl();
+        if (!api.ok || !api.commInitAll) throw ApiErr(CDR_ERR_ERROR, "NCCL (libnccl.so.2) not loadable");
+        std::vector<int> devs(n);
+        for (int i = 0; i < n; ++i) {
+            devs[i] = ctxs[i]->device;
+            for (int j = 0; j < i; ++j)
+                if (devs[j] == devs[i])
+                    throw ApiErr(CDR_ERR_INVALID_ARG, "one NCCL rank per device: contexts share device " +
+                                                          std::to_string(devs[i]));
+        }
+        std::vector<void*> comms(n, nullptr);
+        nccl_check(api.commInitAll(comms.data(), n, devs.data()), "ncclCommInitAll");
+        for (int i = 0; i < n; ++i) {
+            ctxs[i]->nccl_comm = comms[i];
+            ctxs[i]->n_ranks = n;
+            ctxs[i]->rank = i;
+        }
+    });
+}
+
+int cdr_set_rank(cdr_ctx* c, int32_t rank, int32_t n_ranks) {
+    API_BEGIN(c)
+    if (c->nccl_comm) throw ApiErr(CDR_ERR_INVALID_ARG, "the context has a communicator: its rank is NCCL's");
+    if (n_ranks < 1 || rank < 0 || rank >= n_ranks) throw ApiErr(CDR_ERR_INVALID_ARG, "bad rank");
+    c->rank = rank;
+    c->n_ranks = n_ranks;
     API_END
 }
 

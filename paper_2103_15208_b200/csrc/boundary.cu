@@ -146,7 +146,7 @@ __global__ void k_sil_scan(const int32_t* __restrict__ block_count, int nb,
 __global__ void k_sil_write(const double* __restrict__ pos, const double* __restrict__ fn,
                             const int4* __restrict__ edges, int E, const DevCamera* __restrict__ cams,
                             const SilCall* __restrict__ calls, const unsigned char* __restrict__ flags,
-                            const int32_t* __restrict__ block_off, int nb,
+                            const int32_t* __restrict__ block_off, int nb, int stride,
                             cdr_segment* __restrict__ segs) {
     const int vi = blockIdx.y;
     const DevCamera& cam = cams[calls[vi].slot];
@@ -160,7 +160,7 @@ __global__ void k_sil_write(const double* __restrict__ pos, const double* __rest
     int off = block_off[size_t(vi) * nb + blockIdx.x];
     for (int k = 0; k < w; ++k) off += warp_tot[k];
     off += __popc(bal & ((1u << lane) - 1u));
-    if (f) make_segment(pos, fn, edges[i], cam, &segs[size_t(vi) * E + off]);
+    if (f) make_segment(pos, fn, edges[i], cam, &segs[size_t(vi) * stride + off]);
 }
 
 // Running CDF in segment order (diff_render.cpp:213-228), one warp per view:
@@ -476,6 +476,41 @@ __global__ void __launch_bounds__(kBndBlock, CDR_BOUNDARY_MIN_BLOCKS * 256 / kBn
     if (lane == 0 && na) atomicAdd(&p.counters->boundary_active, (unsigned long long)na);
 }
 
+// cdr_probe_points: point pairs (2i, 2i+1) through trace_points2, the odd last
+// point through trace_point, then shade_hit / background as the probes do.
+__global__ void k_probe_points(ShadeScene sc, const SceneInfo* __restrict__ info, DevCamera cam, BeamView bv,
+                               int vi, int n, const double* __restrict__ xy, double* __restrict__ rgb,
+                               int32_t* __restrict__ tri) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int a = 2 * i, b = 2 * i + 1;
+    if (a >= n) return;
+    const double t_min = info->t_min;
+    const D2 xa{xy[2 * a], xy[2 * a + 1]};
+    const D3 da = primary_dir(cam, xa);
+    Hit ha, hb;
+    D3 db{0, 0, 0};
+    if (b < n) {
+        const D2 xb{xy[2 * b], xy[2 * b + 1]};
+        db = primary_dir(cam, xb);
+        trace_points2(bv, vi, cam, sc.nodes, sc.recs, sc.n_tris, xa, da, xb, db, t_min, ha, hb);
+    } else {
+        ha = trace_point(bv, vi, cam, sc.nodes, sc.recs, sc.n_tris, xa, da, t_min);
+    }
+    const D3 bg{sc.bg[0], sc.bg[1], sc.bg[2]};
+    for (int k = 0; k < 2; ++k) {
+        const int j = k == 0 ? a : b;
+        if (j >= n) break;
+        const Hit& h = k == 0 ? ha : hb;
+        if (tri) tri[j] = h.tri;
+        if (rgb) {
+            const D3 r = h.tri >= 0 ? shade_hit(sc, h, k == 0 ? da : db) : bg;
+            rgb[3 * j] = r.x;
+            rgb[3 * j + 1] = r.y;
+            rgb[3 * j + 2] = r.z;
+        }
+    }
+}
+
 struct BStatics {
     DBuf<SilCall> calls;
     DBuf<size_t> pix_off;
@@ -498,7 +533,7 @@ void free_boundary_statics(cdr_ctx* c) {
     c->boundary_statics = nullptr;
 }
 
-void set_view_calls(cdr_ctx* c, const int* view_slots, const int* samples, int n_views) {
+void set_view_calls(cdr_ctx* c, const int* view_slots, const int* samples, int n_views, int min_stride) {
     BStatics& st = bstatics(c);
     std::vector<SilCall> calls(n_views);
     for (int i = 0; i < n_views; ++i) calls[i] = SilCall{view_slots[i], samples ? samples[i] : 0};
@@ -506,7 +541,10 @@ void set_view_calls(cdr_ctx* c, const int* view_slots, const int* samples, int n
     st.n_calls = n_views;
     CDR_CUDA_CHECK(cudaMemcpyAsync(st.calls.p, calls.data(), sizeof(SilCall) * n_views,
                                    cudaMemcpyHostToDevice, c->stream));
-    const int E = std::max(1, c->E);
+    // per-view stride of the segment/CDF/bin arrays: E, or more for a
+    // caller-supplied silhouette set (cdr_boundary_pass) larger than E
+    const int E = std::max(std::max(1, c->E), min_stride);
+    c->seg_stride = E;
     c->segs.ensure(size_t(std::max(1, n_views)) * E);
     c->cdf.ensure(size_t(std::max(1, n_views)) * E);
     c->sil_count.ensure(std::max(1, n_views));
@@ -533,14 +571,14 @@ void launch_silhouettes(cdr_ctx* c, int n_views) {
                                                 c->sil_count.p); }
     { ++c->launches; k_sil_write<<<grid, kBlock, 0, c->stream>>>(c->pos.p, c->fnormal.p, c->edges.p, c->E, c->d_cams.p,
                                                 st.calls.p, c->sil_flag.p, c->sil_block_off.p, nb,
-                                                c->segs.p); }
+                                                c->seg_stride, c->segs.p); }
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_cdf(cdr_ctx* c, int n_views) {
     if (n_views <= 0) return;
-    c->cdf_guide.ensure(size_t(n_views) * (std::max(1, c->E) + 1));
-    { ++c->launches; k_cdf<<<n_views, 32, 0, c->stream>>>(c->segs.p, c->sil_count.p, std::max(1, c->E),
+    c->cdf_guide.ensure(size_t(n_views) * (size_t(c->seg_stride) + 1));
+    { ++c->launches; k_cdf<<<n_views, 32, 0, c->stream>>>(c->segs.p, c->sil_count.p, c->seg_stride,
                                                      n_views, c->cdf.p, c->total_len.p, c->degenerate.p,
                                                      c->cdf_guide.p); }
     CDR_CUDA_CHECK(cudaGetLastError());
@@ -556,7 +594,7 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     st.pix_off.ensure(nslots);
     CDR_CUDA_CHECK(cudaMemcpyAsync(st.pix_off.p, offs.data(), sizeof(size_t) * nslots,
                                    cudaMemcpyHostToDevice, c->stream));
-    const int E = std::max(1, c->E);
+    const int E = c->seg_stride;  // set_view_calls
     const size_t nm = size_t(n_views) * samples;
     const size_t nbins = size_t(n_views) * E * kSBins;
     if (c->b_seg_count.n < nbins) {  // zeroed once; k_bscan re-zeroes what it consumed
@@ -606,6 +644,16 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     { ++c->launches; k_bscatter<<<grid, kBlock, 0, c->stream>>>(p); }
     dim3 bgrid((samples + kBndBlock - 1) / kBndBlock, n_views);
     { ++c->launches; k_boundary<<<bgrid, kBndBlock, 0, c->stream>>>(p); }
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_probe_points(cdr_ctx* c, int vi, int n, const double* xy, double* rgb, int32_t* tri) {
+    if (n <= 0) return;
+    const int pairs = (n + 1) / 2;
+    const DevCamera cam = c->views[c->beam_slots[vi]].cam;
+    ++c->launches;
+    k_probe_points<<<(pairs + 127) / 128, 128, 0, c->stream>>>(shade_scene(c), c->info.p, cam, c->beam_view, vi, n,
+                                                               xy, rgb, tri);
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 

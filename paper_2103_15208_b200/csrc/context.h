@@ -20,11 +20,22 @@ struct SceneInfo {        // device-resident, rewritten by prepare()
     double pad;           // absolute box padding for the fp32 traversal
 };
 
-// Device buffer with grow-only capacity.
+// Device buffer with grow-only capacity. Owns its allocation: freed on
+// destruction (cdr_destroy deletes the context with its device current), so a
+// destroyed context returns all of its device memory. Move-only.
 template <typename T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
     void ensure(size_t count) {
         if (count <= n) return;
         if (p) cudaFree(p);
@@ -127,6 +138,7 @@ struct cdr_ctx {
     cdr::DBuf<int> beam_big_count;
     cdr::DBuf<unsigned char> beam_big_pix_list, beam_big_pix_cnt;      // per view index of the last render call
     cdr::BeamView beam_view{};          // lists of the last render call (valid flag)
+    std::vector<int> beam_slots;        // view slots of that call, in call order (beam_view's view index)
     int* beam_used_host = nullptr;   // pinned; previous call's pool use
     int beam_used_last = 0;
     double t_min_host = 1e-8;
@@ -152,6 +164,7 @@ struct cdr_ctx {
     // silhouettes (per view slot capacity E)
     cdr::DBuf<unsigned char> sil_flag;
     cdr::DBuf<int32_t> sil_block_count, sil_block_off, sil_count;
+    int seg_stride = 1;  // per-view stride of segs/cdf/cdf_guide/bin arrays (set_view_calls)
     cdr::DBuf<cdr_segment> segs;
     cdr::DBuf<double> cdf, total_len;
     cdr::DBuf<int32_t> cdf_guide;  // per view: lower_bound guide over the CDF (k_cdf)

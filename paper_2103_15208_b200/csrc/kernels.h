@@ -78,13 +78,19 @@ float render_trace_ms(cdr_ctx* c);
 // boundary.cu — extract_silhouettes (silhouette.cpp:55-106), the CDF of
 // boundary_pass (diff_render.cpp:213-228) and its edge samples (:230-278).
 // view list of the next silhouette/CDF/boundary launches; samples[i] = M per view
-void set_view_calls(cdr_ctx* c, const int* view_slots, const int* samples, int n_views);
+// min_stride: per-view capacity of the segment arrays when a caller supplies
+// more segments than the mesh has edges (cdr_boundary_pass)
+void set_view_calls(cdr_ctx* c, const int* view_slots, const int* samples, int n_views, int min_stride = 0);
 void launch_silhouettes(cdr_ctx* c, int n_views);
 void launch_cdf(cdr_ctx* c, int n_views);
 // use_beam: probes may use the candidate lists the preceding render call built
 // for the same view list (cdr_loss_grad); otherwise per-ray traversal
 void launch_boundary(cdr_ctx* c, int n_views, int max_samples, uint64_t seed, int probe,
                      int64_t lay_pos, bool use_beam = false);
+// The boundary probes' visibility on its own (cdr_probe_points): n points of
+// the view at index vi of the last render call, traced in pairs through that
+// call's candidate lists exactly as k_boundary traces x -/+ n/2 (rgb nullable).
+void launch_probe_points(cdr_ctx* c, int vi, int n, const double* xy, double* rgb, int32_t* tri);
 
 // finalize.cu — position gradient assembly: per-corner interior sums, the
 // one-ring normal chain (diff_render.cpp:174-184) restated as q_v x d_{f,w},

@@ -1273,6 +1273,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
                                        cudaMemcpyHostToDevice, c->stream));
         c->beam_view = BeamView{p.tile_hdr,     p.pool, p.pix_list, p.pix_cnt, p.big_pix_list, p.big_pix_cnt,
                                 c->beam_tile_base.p, TW,   TH,         P,         1};
+        c->beam_slots.assign(view_slots, view_slots + n_views);
     }
     // Views can go through lists -> trace -> shade in chunks whose hit cache
     // (4 B per sample) fits in L2, so the shading kernel's first load hits L2.
