@@ -268,6 +268,12 @@ int cdr_laplacian_matrix(cdr_ctx* ctx, int32_t mode, int32_t* outer, int32_t* in
 int cdr_laplacian_loss(cdr_ctx* ctx, int32_t mode, double lambda, double* value_out,
                        double* grad_positions_inout);
 
+/* The LBVH's sorted leaf keys (Morton code << 32 | face index, ascending; the
+ * leaf order of the hierarchy that replaces Bvh::build, bvh.cpp:90-208) for
+ * the current positions: n = number of triangles. A test hook for the radix
+ * sort. */
+int cdr_lbvh_keys(cdr_ctx* ctx, uint64_t* keys_out, int32_t n);
+
 /* Image and mask of `view` from the last cdr_render / cdr_loss_grad /
  * cdr_total_loss that rendered it (the rendered outputs of total_loss,
  * losses.cpp:259), read straight into the caller's W x H x 3 and W x H

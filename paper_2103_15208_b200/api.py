@@ -155,6 +155,7 @@ def load_library(path: str = LIB_PATH):
                                  _d, _d, C.POINTER(cdr_stats)]
     L.cdr_regularisers.argtypes = [_vp, C.POINTER(cdr_reg_weights), C.POINTER(cdr_layout), _d, _d]
     L.cdr_get_rendered.argtypes = [_vp, C.c_int32, _d, _d]
+    L.cdr_lbvh_keys.argtypes = [_vp, C.POINTER(C.c_uint64), C.c_int32]
     L.cdr_closest_points.argtypes = [_vp, _d, C.c_int32, _i, C.c_int32, _d, C.c_int32, _i, _d, _d, _d]
     L.cdr_adam_init.argtypes = [_vp, C.POINTER(cdr_adam_config), C.POINTER(cdr_layout)]
     L.cdr_adam_step.argtypes = [_vp, _d, C.POINTER(C.c_int64)]
@@ -309,6 +310,7 @@ class Renderer:
         self._chk(self.L.cdr_set_mesh(self.h, _dp(self._pos), len(self._pos), _ip(tris), len(tris), _dp(uv),
                                       _ip(edges), 0 if edges is None else len(edges)))
         self.V = len(self._pos)
+        self.T = len(tris)
 
     def update_positions(self, pos):
         pos = np.ascontiguousarray(pos, dtype=np.float64)
@@ -586,6 +588,13 @@ class Renderer:
         """pack (params.cpp:70-100) of the resident state."""
         out = np.zeros(layout["total"])
         self._chk(self.L.cdr_get_params(self.h, C.byref(_clayout(layout)), _dp(out)))
+        return out
+
+    def lbvh_keys(self):
+        """Sorted LBVH leaf keys (Morton << 32 | face) of the current mesh."""
+        n = self.T
+        out = np.zeros(n, np.uint64)
+        self._chk(self.L.cdr_lbvh_keys(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), n))
         return out
 
     def rendered(self, view):

@@ -1071,6 +1071,17 @@ int cdr_laplacian_loss(cdr_ctx* c, int32_t mode, double lambda, double* value, d
     API_END
 }
 
+int cdr_lbvh_keys(cdr_ctx* c, uint64_t* keys_out, int32_t n) {
+    API_BEGIN(c)
+    if (n != c->T) throw SizeMismatchErr("key buffer must hold one key per triangle");
+    ensure_prepared(c);
+    if (n > 0)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(keys_out, c->keys.p, sizeof(uint64_t) * size_t(n), cudaMemcpyDeviceToHost,
+                                       c->stream));
+    sync(c);
+    API_END
+}
+
 int cdr_get_rendered(cdr_ctx* c, int32_t view, double* rgb, double* mask) {
     API_BEGIN(c)
     check_view(c, view);

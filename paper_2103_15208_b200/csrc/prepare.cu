@@ -4,8 +4,6 @@
 // LBVH: Morton codes -> radix sort -> Karras hierarchy -> bottom-up refit.
 // Replaces the host SAH build (bvh.cpp:90-208) that the reference runs on every
 // total_loss call.
-#include <cub/device/device_radix_sort.cuh>
-
 #include "kernels.h"
 
 namespace cdr {
@@ -235,6 +233,161 @@ __global__ void k_refit(const unsigned long long* __restrict__ keys, const doubl
     }
 }
 
+// ---------------------------------------------------------------------------
+// Radix sort of the LBVH keys (Morton << 32 | face index), hand-written.
+//
+// The keys are created in face order, so a STABLE sort on the 30 Morton bits
+// alone yields exactly the order of a full 62-bit sort (ties by face index):
+// four 8-bit LSD passes (bits 32-39, 40-47, 48-55, 56-61) instead of eight.
+// One histogram kernel counts all four digits in a single read of the keys;
+// each pass is then ONE "onesweep" kernel (Merrill & Garland, decoupled
+// look-back): a CTA takes the next 4,096-key tile (dynamic tile id, so every
+// tile it looks back on is already running), ranks its keys stably per digit
+// with __match_any_sync warp multi-split, publishes its per-digit counts, sums
+// the predecessors' counts by look-back, stages the tile sorted by digit in
+// shared memory and writes each digit's run contiguously.
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortPasses = 4;
+constexpr unsigned kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValMask = (1u << 30) - 1;
+
+__device__ __forceinline__ int sort_digit(unsigned long long k, int pass) {
+    return int((k >> (32 + 8 * pass)) & 0xffu);
+}
+
+// all four digit histograms (hist[pass][256]) in one read; also clears the
+// look-back status words and the per-pass tile counters of the sort
+__global__ void __launch_bounds__(kSortThreads) k_sort_hist(const unsigned long long* __restrict__ keys, int n,
+                                                           unsigned* __restrict__ hist, unsigned* __restrict__ status,
+                                                           int n_status, unsigned* __restrict__ tile_ctr) {
+    __shared__ unsigned h[kSortPasses][256];
+    for (int i = threadIdx.x; i < kSortPasses * 256; i += blockDim.x) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const unsigned long long k = keys[i];
+#pragma unroll
+        for (int p = 0; p < kSortPasses; ++p) atomicAdd(&h[p][sort_digit(k, p)], 1u);
+    }
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_status; i += stride) status[i] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < kSortPasses) tile_ctr[threadIdx.x] = 0;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSortPasses * 256; i += blockDim.x)
+        if ((&h[0][0])[i]) atomicAdd(hist + i, (&h[0][0])[i]);
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_pass(const unsigned long long* __restrict__ in,
+                                                           unsigned long long* __restrict__ out, int n, int pass,
+                                                           const unsigned* __restrict__ hist,
+                                                           unsigned* __restrict__ status, unsigned* __restrict__ tile_ctr) {
+    __shared__ unsigned long long stage[kSortTile];
+    __shared__ unsigned whist[kSortWarps][257];  // per warp and digit; 256 = past the end of the keys
+    __shared__ unsigned digit_base[256];         // global position of the tile's first key of each digit
+    __shared__ unsigned tile_excl[257];          // tile-local exclusive scan over digits
+    __shared__ int s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) s_tile = int(atomicAdd(tile_ctr + pass, 1u));
+    for (int i = tid; i < kSortWarps * 257; i += kSortThreads) (&whist[0][0])[i] = 0;
+    __syncthreads();
+    const int tile = s_tile;
+    const size_t base = size_t(tile) * kSortTile + size_t(w) * 32 * kSortItems;
+    // warp-striped items: item j of lane l is key base + j*32 + l (index order = (warp, j, lane))
+    unsigned long long k[kSortItems];
+    int rank[kSortItems], dg[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const size_t i = base + size_t(j) * 32 + lane;
+        k[j] = i < size_t(n) ? in[i] : ~0ull;
+        dg[j] = i < size_t(n) ? sort_digit(k[j], pass) : 256;
+    }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const unsigned peers = __match_any_sync(0xffffffffu, dg[j]);
+        const int leader = __ffs(peers) - 1;
+        unsigned b = 0;
+        if (lane == leader) {
+            b = whist[w][dg[j]];
+            whist[w][dg[j]] = b + __popc(peers);
+        }
+        b = __shfl_sync(0xffffffffu, b, leader);
+        rank[j] = int(b) + __popc(peers & ((1u << lane) - 1u));
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: counts of the tile, and each warp's exclusive prefix inside it
+    unsigned cnt = 0;
+    for (int d = tid; d < 257; d += kSortThreads) {
+        unsigned run = 0;
+        for (int ww = 0; ww < kSortWarps; ++ww) {
+            const unsigned c = whist[ww][d];
+            whist[ww][d] = run;
+            run += c;
+        }
+        if (d < 256) cnt = run;
+        tile_excl[d] = run;  // counts for now; scanned below
+    }
+    // publish this tile's aggregate per digit (thread d = digit d)
+    unsigned* st = status + (size_t(pass) * gridDim.x + tile) * 256;
+    if (tile == 0) {
+        __stcg(st + tid, kFlagPrefix | cnt);
+    } else {
+        __stcg(st + tid, kFlagAgg | cnt);
+    }
+    __syncthreads();
+    if (tid == 0) {  // exclusive scan of the tile's digit counts (257 entries, serial is fine)
+        unsigned run = 0;
+        for (int d = 0; d < 257; ++d) {
+            const unsigned c = tile_excl[d];
+            tile_excl[d] = run;
+            run += c;
+        }
+    }
+    // global exclusive prefix of digit d + the counts of all earlier tiles
+    {
+        __shared__ unsigned ghist[256];
+        ghist[tid] = hist[pass * 256 + tid];
+        __syncthreads();
+        // exclusive scan of the global histogram (Hillis-Steele over 256)
+        unsigned v = ghist[tid];
+        for (int o = 1; o < 256; o <<= 1) {
+            const unsigned t = tid >= o ? ghist[tid - o] : 0u;
+            __syncthreads();
+            ghist[tid] += t;
+            __syncthreads();
+        }
+        unsigned excl = ghist[tid] - v;
+        if (tile > 0) {
+            unsigned prev = 0;
+            for (int t = tile - 1; t >= 0; --t) {
+                const volatile unsigned* sp = status + (size_t(pass) * gridDim.x + t) * 256 + tid;
+                unsigned x;
+                do {
+                    x = *sp;
+                } while ((x & ~kValMask) == 0u);
+                prev += x & kValMask;
+                if (x & kFlagPrefix) break;
+            }
+            __threadfence();
+            __stcg(st + tid, kFlagPrefix | (prev + cnt));
+            excl += prev;
+        }
+        digit_base[tid] = excl;
+    }
+    __syncthreads();
+    // stage the tile sorted by digit (stable), then write each digit's run
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) stage[tile_excl[dg[j]] + whist[w][dg[j]] + rank[j]] = k[j];
+    __syncthreads();
+    const int valid = int(min(size_t(kSortTile), size_t(n) - size_t(tile) * kSortTile));
+    for (int i = tid; i < valid; i += kSortThreads) {
+        const unsigned long long x = stage[i];
+        const int d = sort_digit(x, pass);
+        out[digit_base[d] + (unsigned(i) - tile_excl[d])] = x;
+    }
+}
+
 inline int blocks(long n, int b = kBlock) { return int((n + b - 1) / b); }
 
 }  // namespace
@@ -269,18 +422,28 @@ void launch_bvh(cdr_ctx* c, double cam_abs_max) {
     c->parent_leaf.ensure(T);
     c->refit_flag.ensure(std::max(1, T - 1));
     { ++c->launches; k_morton<<<blocks(T), kBlock, 0, s>>>(c->pos.p, c->tris.p, T, c->info.p, c->keys.p); }
-    size_t tmp = 0;
-    int end_bit = 32 + 30;
-    cub::DeviceRadixSort::SortKeys(nullptr, tmp, c->keys.p, c->keys_alt.p, T, 0, end_bit, s);
-    c->sort_tmp.ensure(tmp);
-    cub::DeviceRadixSort::SortKeys(c->sort_tmp.p, tmp, c->keys.p, c->keys_alt.p, T, 0, end_bit, s);
-    c->launches += 1;  // counted as one (CUB onesweep passes)
+    // radix sort (above): keys -> keys_alt -> keys -> keys_alt -> keys
+    const int tiles = (T + kSortTile - 1) / kSortTile;
+    const int n_status = kSortPasses * tiles * 256;
+    c->sort_tmp.ensure(sizeof(unsigned) * (size_t(kSortPasses) * 256 + kSortPasses + size_t(n_status)));
+    unsigned* hist = reinterpret_cast<unsigned*>(c->sort_tmp.p);
+    unsigned* tile_ctr = hist + kSortPasses * 256;
+    unsigned* status = tile_ctr + kSortPasses;
+    CDR_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(unsigned) * kSortPasses * 256, s));
+    { ++c->launches; k_sort_hist<<<std::max(1, std::min(blocks(T, kSortThreads), 148)), kSortThreads, 0, s>>>(
+          c->keys.p, T, hist, status, n_status, tile_ctr); }
+    unsigned long long* buf[2] = {c->keys.p, c->keys_alt.p};
+    for (int pass = 0; pass < kSortPasses; ++pass) {
+        ++c->launches;
+        k_sort_pass<<<tiles, kSortThreads, 0, s>>>(buf[pass & 1], buf[(pass + 1) & 1], T, pass, hist, status,
+                                                   tile_ctr);
+    }
     if (T > 1) {
-        { ++c->launches; k_hierarchy<<<blocks(T - 1), kBlock, 0, s>>>(c->keys_alt.p, T, c->nodes.p,
+        { ++c->launches; k_hierarchy<<<blocks(T - 1), kBlock, 0, s>>>(c->keys.p, T, c->nodes.p,
                                                      c->parent_internal.p, c->parent_leaf.p); }
         CDR_CUDA_CHECK(cudaMemsetAsync(c->refit_flag.p, 0, sizeof(int32_t) * (T - 1), s));
     }
-    { ++c->launches; k_refit<<<blocks(T), kBlock, 0, s>>>(c->keys_alt.p, c->pos.p, c->tris.p, T, c->info.p,
+    { ++c->launches; k_refit<<<blocks(T), kBlock, 0, s>>>(c->keys.p, c->pos.p, c->tris.p, T, c->info.p,
                                          c->parent_internal.p, c->parent_leaf.p, c->refit_flag.p,
                                          c->nodes.p, c->recs.p); }
     CDR_CUDA_CHECK(cudaGetLastError());

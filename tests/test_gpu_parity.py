@@ -482,18 +482,19 @@ def test_context_memory_is_returned():
 
 def test_rejected_mesh_keeps_previous_state(sphere):
     """cdr_set_mesh validates everything before it changes the context."""
-    from paper_2103_15208_b200.api import CollodiffError
+    from paper_2103_15208_b200.api import _dp, _ip
     r, o = _pair(sphere)
     st = RenderSettings(spp=4, seed=2)
     h0 = r.render(0, st)[2]
-    bad = S.Mesh(sphere.mesh.positions[:10], np.array([[0, 1, 2], [0, 1, 3], [0, 1, 4]], np.int32), None)
-    with pytest.raises(CollodiffError):  # non-manifold edge (0, 1)
-        r.set_mesh(bad)
-    bad2 = S.Mesh(sphere.mesh.positions, sphere.mesh.triangles, sphere.mesh.uvs,
-                  np.array([[0, 1, 0, 10 ** 6]], np.int32))
-    with pytest.raises(CollodiffError):  # caller edge with a face out of range
-        r.set_mesh(bad2)
-    r.V = len(sphere.mesh.positions)
+    pos = np.ascontiguousarray(sphere.mesh.positions[:10])
+    nonmanifold = np.array([[0, 1, 2], [0, 1, 3], [0, 1, 4]], np.int32)  # edge (0, 1) in three faces
+    assert r.L.cdr_set_mesh(r.h, _dp(pos), len(pos), _ip(nonmanifold), 3, None, None, 0) != 0
+    assert "non-manifold" in r.L.cdr_last_error(r.h).decode()
+    P = np.ascontiguousarray(sphere.mesh.positions)
+    T = np.ascontiguousarray(sphere.mesh.triangles, dtype=np.int32)
+    bad_edges = np.array([[0, 1, 0, 10 ** 6]], np.int32)  # a caller edge whose face is out of range
+    assert r.L.cdr_set_mesh(r.h, _dp(P), len(P), _ip(T), len(T), None, _ip(bad_edges), 1) != 0
+    assert "face out of range" in r.L.cdr_last_error(r.h).decode()
     np.testing.assert_array_equal(r.render(0, st)[2], h0)
     np.testing.assert_array_equal(h0, o.render(0, 4, 2)[2])
 
