@@ -6,6 +6,7 @@
 // render.cu, boundary.cu and finalize.cu. There is no CPU fallback: without a
 // CUDA device every call fails with CDR_ERR_NO_DEVICE / CDR_ERR_CUDA.
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: stage ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <cmath>
@@ -14,6 +15,7 @@
 #include <map>
 #include <memory>
 #include <new>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -779,6 +781,14 @@ int cdr_boundary_pass(cdr_ctx* c, int32_t view, const double* adjoint, const cdr
     API_END
 }
 
+// NVTX range of one pipeline stage (host launch time; ncu --nvtx filters on it).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 // Scope in which the context's launchers target its side stream.
 struct OnSideStream {
     cdr_ctx* c;
@@ -811,9 +821,11 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
         samples[i] = st->boundary_samples > 0 ? st->boundary_samples : v.cam.W * v.cam.H;
         max_samples = std::max(max_samples, samples[i]);
     }
+    NvtxRange whole("cdr.total_loss");
     cudaStream_t s = c->stream;
     auto& ev = c->ev;
     c->launches = 0;
+    std::optional<NvtxRange> stage(std::in_place, "cdr.prepare (normals, LBVH)");
     CDR_CUDA_CHECK(cudaEventRecord(ev[0], s));
     zero_grad(c, lay->total);  // fresh GradVector (losses.cpp:250)
     reset_flags(c);
@@ -825,6 +837,7 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
         c->target_tone_gamma = st->gamma;
     }
     CDR_CUDA_CHECK(cudaEventRecord(ev[1], s));
+    stage.emplace("cdr.silhouettes+cdf+regularisers (side stream)");
     // Side stream: silhouettes + CDF (they need only the prepared geometry) and
     // the regularisers (mesh + maps, into their own gradient buffer) run
     // beside the render; the main stream joins them where their results are used.
@@ -852,19 +865,23 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
     }
     RenderArgs a = render_args(c, st, lay);
     a.use_mask = use_mask;
+    stage.emplace("cdr.render (lists, trace, shade+loss+interior)");
     launch_render(c, slots.data(), n, a, true, true, true, scales.data(), ev[7]);
     CDR_CUDA_CHECK(cudaEventRecord(ev[2], s));
     CDR_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_sil, 0));  // segments + CDF for the boundary pass
     CDR_CUDA_CHECK(cudaEventRecord(ev[3], s));
+    stage.emplace("cdr.boundary");
     if (st->boundary_term)  // the render above built candidate lists for exactly these views
         launch_boundary(c, n, max_samples, st->seed, CDR_PROBE_RADIANCE, lay->positions, /*use_beam=*/true);
     CDR_CUDA_CHECK(cudaEventRecord(ev[4], s));
+    stage.emplace("cdr.finalize (texel flush, normal chain, Laplacian)");
     launch_texel_flush(c, lay->diffuse, lay->specular, lay->roughness);
     launch_finalize_positions(c, lay->positions);
     if (lap_here) launch_laplacian(c, lap_mode, lambda_lap, c->grad.p + lay->positions);
     CDR_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_reg, 0));  // the regularisers' gradient and values
     if (reg_here) launch_axpy(c, c->grad.p, c->reg_grad.p, lay->total);  // grad += reg_grad
     CDR_CUDA_CHECK(cudaEventRecord(ev[5], s));
+    stage.emplace("cdr.allreduce + download");
     if (c->nccl_comm)
         nccl_check(nccl().allReduce(c->grad.p, c->grad.p, size_t(lay->total), kNcclFloat64, kNcclSum, c->nccl_comm, s),
                    "ncclAllReduce(grad)");

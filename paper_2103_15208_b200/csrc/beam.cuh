@@ -54,11 +54,28 @@ struct __align__(16) BeamCand {
 };
 
 struct TileHdr {
-    int off;  // first candidate in the pool
-    int cnt;  // candidates, or -1: overflow (per-ray traversal)
+    int off;  // first candidate in the pool; split tiles: index of their 4 quadrant lists
+    int cnt;  // candidates, or -1: overflow (per-ray traversal), -2: split into quadrants
     int big;  // index of the tile's kBigPixCap pixel lists, -1: the kPixCap ones
     int pad;
 };
+
+// A tile whose big-pass list overflows (> 255 candidates: silhouette-dense
+// tiles of thin geometry) is split into its four pixel quadrants, each with
+// its own candidate list (off, cnt; cnt -1: that quadrant traverses per ray).
+// The pixel lists of all four stay in the tile's big slot (pixel q's list
+// indexes its own quadrant's candidates), and the edge functions stay relative
+// to the tile origin, so a consumer only swaps the (off, cnt) it scans.
+__device__ __forceinline__ int tile_quadrant(int q, int TW, int TH) {
+    return (q / TW >= TH / 2 ? 2 : 0) + (q % TW >= TW / 2 ? 1 : 0);
+}
+
+// (first candidate, count) of the list pixel q of tile header h scans.
+__device__ __forceinline__ int2 pixel_tile_list(const TileHdr& h, const int2* __restrict__ split, int q, int TW,
+                                                int TH) {
+    if (h.cnt != -2) return make_int2(h.off, h.cnt);
+    return split[4 * h.off + tile_quadrant(q, TW, TH)];
+}
 
 struct FrustumPlanes {
     float n[5][3];  // inward normals through the camera origin
@@ -190,6 +207,7 @@ struct BeamView {
     const unsigned char* big_pix_list;
     const unsigned char* big_pix_cnt;
     const int* tile_base;  // per view index of the call
+    const int2* split;     // quadrant lists of split tiles (4 per split tile)
     int TW, TH, P;
     int valid;
 };
@@ -208,15 +226,16 @@ __device__ __forceinline__ Hit trace_point(const BeamView& bv, int vi, const Dev
             const int tx = px / bv.TW, ty = py / bv.TH;
             const size_t tile = size_t(bv.tile_base[vi]) + ty * tiles_x + tx;
             const TileHdr h = bv.hdr[tile];
-            if (h.cnt >= 0) {
-                const int q = (py - ty * bv.TH) * bv.TW + (px - tx * bv.TW);
+            const int q = (py - ty * bv.TH) * bv.TW + (px - tx * bv.TW);
+            const int2 tl = pixel_tile_list(h, bv.split, q, bv.TW, bv.TH);
+            if (tl.y >= 0) {
                 const size_t li = h.big >= 0 ? size_t(h.big) * bv.P + q : tile * bv.P + q;
                 const int cnt = h.big >= 0 ? bv.big_pix_cnt[li] : bv.pix_cnt[li];
                 const unsigned char* lst = h.big >= 0 ? bv.big_pix_list + li * kBigPixCap : bv.pix_list + li * kPixCap;
                 const float lx = float(x.x - tx * bv.TW), ly = float(x.y - ty * bv.TH);
                 if (cnt == 0) return Hit{-1, 1e300, 0.0, 0.0};
-                if (cnt == 255) return trace_beam(bv.pool + h.off, h.cnt, recs, o, d, t_min, lx, ly);
-                return trace_beam_list(bv.pool + h.off, lst, cnt, recs, o, d, t_min, lx, ly);
+                if (cnt == 255) return trace_beam(bv.pool + tl.x, tl.y, recs, o, d, t_min, lx, ly);
+                return trace_beam_list(bv.pool + tl.x, lst, cnt, recs, o, d, t_min, lx, ly);
             }
         }
     }
@@ -264,19 +283,20 @@ __device__ __forceinline__ void probe_setup(const BeamView& bv, int vi, const De
     const int tx = px / bv.TW, ty = py / bv.TH;
     const size_t tile = size_t(bv.tile_base[vi]) + ty * tiles_x + tx;
     const TileHdr h = bv.hdr[tile];
-    if (h.cnt < 0) {
+    const int q = (py - ty * bv.TH) * bv.TW + (px - tx * bv.TW);
+    const int2 tl = pixel_tile_list(h, bv.split, q, bv.TW, bv.TH);
+    if (tl.y < 0) {
         CDR_PSTAT(1, 1);
         return;
     }
-    const int q = (py - ty * bv.TH) * bv.TW + (px - tx * bv.TW);
     const size_t li = h.big >= 0 ? size_t(h.big) * bv.P + q : tile * bv.P + q;
     const int cnt = h.big >= 0 ? bv.big_pix_cnt[li] : bv.pix_cnt[li];
-    s.cand = bv.pool + h.off;
+    s.cand = bv.pool + tl.x;
     s.lx = float(x.x - tx * bv.TW);
     s.ly = float(x.y - ty * bv.TH);
     if (cnt == 255) {
         s.lst = nullptr;
-        s.n = h.cnt;
+        s.n = tl.y;
     } else {
         s.lst = h.big >= 0 ? bv.big_pix_list + li * kBigPixCap : bv.pix_list + li * kPixCap;
         s.n = cnt;

@@ -135,7 +135,9 @@ struct cdr_ctx {
     cdr::DBuf<unsigned char> beam_pix_list, beam_pix_cnt;
     cdr::DBuf<int> beam_tile_base;
     cdr::DBuf<int2> beam_big_queue;  // tiles rebuilt with the big candidate cap
-    cdr::DBuf<int> beam_big_count;
+    cdr::DBuf<int> beam_big_count;   // [0] big queue, [1] split queue
+    cdr::DBuf<int> beam_split_queue;  // big-queue index of each split tile
+    cdr::DBuf<int2> beam_split_hdr;   // 4 quadrant lists per split tile
     cdr::DBuf<unsigned char> beam_big_pix_list, beam_big_pix_cnt;      // per view index of the last render call
     cdr::BeamView beam_view{};          // lists of the last render call (valid flag)
     std::vector<int> beam_slots;        // view slots of that call, in call order (beam_view's view index)

@@ -79,15 +79,34 @@ __global__ void k_bbox_partial(const double* __restrict__ pos, int V, double* __
     if (threadIdx.x < 6) part[6 * blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
 }
 
-__global__ void k_bbox_final(const double* __restrict__ part, int nb, int T, double cam_abs_max,
-                             SceneInfo* __restrict__ info) {
-    if (threadIdx.x != 0) return;
+// min / max are exact in any order: one CTA folds the per-block partials
+__global__ void __launch_bounds__(kBlock) k_bbox_final(const double* __restrict__ part, int nb, int T,
+                                                      double cam_abs_max, SceneInfo* __restrict__ info) {
+    __shared__ double s[6][kBlock];
     double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-    for (int b = 0; b < nb; ++b)
+    for (int b = threadIdx.x; b < nb; b += kBlock)
         for (int k = 0; k < 3; ++k) {
             lo[k] = fmin(lo[k], part[6 * b + k]);
             hi[k] = fmax(hi[k], part[6 * b + 3 + k]);
         }
+    for (int k = 0; k < 3; ++k) {
+        s[k][threadIdx.x] = lo[k];
+        s[3 + k][threadIdx.x] = hi[k];
+    }
+    __syncthreads();
+    for (int st = kBlock / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st)
+            for (int k = 0; k < 3; ++k) {
+                s[k][threadIdx.x] = fmin(s[k][threadIdx.x], s[k][threadIdx.x + st]);
+                s[3 + k][threadIdx.x] = fmax(s[3 + k][threadIdx.x], s[3 + k][threadIdx.x + st]);
+            }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = s[k][0];
+        hi[k] = s[3 + k][0];
+    }
     SceneInfo si;
     double mag = cam_abs_max;
     for (int k = 0; k < 3; ++k) {
@@ -326,55 +345,51 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const unsigned long 
             run += c;
         }
         if (d < 256) cnt = run;
-        tile_excl[d] = run;  // counts for now; scanned below
     }
     // publish this tile's aggregate per digit (thread d = digit d)
     unsigned* st = status + (size_t(pass) * gridDim.x + tile) * 256;
-    if (tile == 0) {
-        __stcg(st + tid, kFlagPrefix | cnt);
-    } else {
-        __stcg(st + tid, kFlagAgg | cnt);
+    __stcg(st + tid, (tile == 0 ? kFlagPrefix : kFlagAgg) | cnt);
+    // exclusive scans over the 256 digits, both at once: the tile's counts
+    // (tile-local run starts) and the global histogram (run starts in `out`)
+    __shared__ unsigned wsum[2][kSortWarps];
+    unsigned a = cnt, g = hist[pass * 256 + tid];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned ta = __shfl_up_sync(0xffffffffu, a, o), tg = __shfl_up_sync(0xffffffffu, g, o);
+        if (lane >= o) {
+            a += ta;
+            g += tg;
+        }
+    }
+    if (lane == 31) {
+        wsum[0][w] = a;
+        wsum[1][w] = g;
     }
     __syncthreads();
-    if (tid == 0) {  // exclusive scan of the tile's digit counts (257 entries, serial is fine)
-        unsigned run = 0;
-        for (int d = 0; d < 257; ++d) {
-            const unsigned c = tile_excl[d];
-            tile_excl[d] = run;
-            run += c;
-        }
+    unsigned pa = 0, pg = 0;
+    for (int ww = 0; ww < w; ++ww) {
+        pa += wsum[0][ww];
+        pg += wsum[1][ww];
     }
-    // global exclusive prefix of digit d + the counts of all earlier tiles
-    {
-        __shared__ unsigned ghist[256];
-        ghist[tid] = hist[pass * 256 + tid];
-        __syncthreads();
-        // exclusive scan of the global histogram (Hillis-Steele over 256)
-        unsigned v = ghist[tid];
-        for (int o = 1; o < 256; o <<= 1) {
-            const unsigned t = tid >= o ? ghist[tid - o] : 0u;
-            __syncthreads();
-            ghist[tid] += t;
-            __syncthreads();
+    tile_excl[tid] = pa + a - cnt;
+    if (tid == 255) tile_excl[256] = pa + a;  // the past-the-end keys stage after every valid one
+    unsigned excl = pg + g - hist[pass * 256 + tid];
+    // + the counts of all earlier tiles (decoupled look-back)
+    if (tile > 0) {
+        unsigned prev = 0;
+        for (int t = tile - 1; t >= 0; --t) {
+            const volatile unsigned* sp = status + (size_t(pass) * gridDim.x + t) * 256 + tid;
+            unsigned x;
+            do {
+                x = *sp;
+            } while ((x & ~kValMask) == 0u);
+            prev += x & kValMask;
+            if (x & kFlagPrefix) break;
         }
-        unsigned excl = ghist[tid] - v;
-        if (tile > 0) {
-            unsigned prev = 0;
-            for (int t = tile - 1; t >= 0; --t) {
-                const volatile unsigned* sp = status + (size_t(pass) * gridDim.x + t) * 256 + tid;
-                unsigned x;
-                do {
-                    x = *sp;
-                } while ((x & ~kValMask) == 0u);
-                prev += x & kValMask;
-                if (x & kFlagPrefix) break;
-            }
-            __threadfence();
-            __stcg(st + tid, kFlagPrefix | (prev + cnt));
-            excl += prev;
-        }
-        digit_base[tid] = excl;
+        __stcg(st + tid, kFlagPrefix | (prev + cnt));
+        excl += prev;
     }
+    digit_base[tid] = excl;
     __syncthreads();
     // stage the tile sorted by digit (stable), then write each digit's run
 #pragma unroll
@@ -411,7 +426,7 @@ void launch_bvh(cdr_ctx* c, double cam_abs_max) {
     int nb = std::max(1, std::min(blocks(V), 1184));
     c->bbox_partial.ensure(size_t(nb) * 6);
     { ++c->launches; k_bbox_partial<<<nb, kBlock, 0, s>>>(c->pos.p, V, c->bbox_partial.p); }
-    { ++c->launches; k_bbox_final<<<1, 32, 0, s>>>(c->bbox_partial.p, nb, T, cam_abs_max, c->info.p); }
+    { ++c->launches; k_bbox_final<<<1, kBlock, 0, s>>>(c->bbox_partial.p, nb, T, cam_abs_max, c->info.p); }
     if (T == 0) return;
 
     c->keys.ensure(T);

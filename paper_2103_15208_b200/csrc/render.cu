@@ -69,10 +69,15 @@ struct Params {
     unsigned char* big_pix_cnt;
     int use_beam;
     int fast_cap;     // candidate cap of the fast pass (kBeamCap; lower only to test the big pass)
+    int big_list_cap;  // the same for the big pass (kBigCap; lower only to test the split pass)
     int no_shared_top;  // 1: every tile walks the BVH from the root (A/B and tests)
     int2* big_queue;  // (call, tile) of the tiles over kBeamCap candidates
     int* big_count;
     int big_cap;
+    int* split_queue;  // big-queue index of the tiles over kBigCap candidates (split into quadrants)
+    int* split_count;
+    int split_cap;
+    int2* split_hdr;  // per split tile: 4 quadrant lists (first candidate, count; -1 = per ray)
 };
 
 constexpr int kThreads = 256;
@@ -121,16 +126,25 @@ __device__ void warp_bitonic_sort(unsigned long long* key, int n, int lane) {
         }
 }
 
+// sub_out != nullptr: the list of one quadrant of a split tile — pixels
+// [sx0, sx0 + sw) x [sy0, sy0 + sh) of the tile (tile coordinates), its
+// (first candidate, count) written to *sub_out instead of the tile header.
 template <int kCap, int kFront, int kPix>
 __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCamera& cam, int b, int lane,
                                 int (*s_front)[kFront], int* s_leaf, float* s_d, unsigned long long* s_key,
-                                int big, const int* init_front = nullptr, int init_n = 0) {
+                                int big, const int* init_front = nullptr, int init_n = 0, int sx0 = 0, int sy0 = 0,
+                                int sw = 1 << 20, int sh = 1 << 20, int2* sub_out = nullptr, int cap = -1) {
     const int tiles_x = vc.tiles_x;
     const unsigned lt = (1u << lane) - 1u;
     const size_t tile = size_t(vc.tile_base) + b;
     TileHdr* hdr = p.tile_hdr + tile;
     const int X0 = (b % tiles_x) * p.TW, Y0 = (b / tiles_x) * p.TH;
-    const int X1 = min(X0 + p.TW, cam.W), Y1 = min(Y0 + p.TH, cam.H);
+    const int X1 = min(X0 + sx0 + sw, min(X0 + p.TW, cam.W)), Y1 = min(Y0 + sy0 + sh, min(Y0 + p.TH, cam.H));
+    const int RX0 = X0 + sx0, RY0 = Y0 + sy0;  // the rectangle the frustum encloses
+    if (RX0 >= X1 || RY0 >= Y1) {  // a quadrant wholly outside the image: no pixel asks for it
+        if (lane == 0 && sub_out) *sub_out = make_int2(0, 0);
+        return true;
+    }
     const int T = p.sc.n_tris;
     int nl = 0, nf = 0, cur = 0;
     bool over = false;
@@ -150,7 +164,7 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
     FrustumPlanes fp;  // only when there is a frontier (empty blocks skip the fp64 set-up)
     float of[3];
     if (nf > 0) {
-        fp = tile_frustum(cam, X0 - 0.01, X1 + 0.01, Y0 - 0.01, Y1 + 0.01);
+        fp = tile_frustum(cam, RX0 - 0.01, X1 + 0.01, RY0 - 0.01, Y1 + 0.01);
         of[0] = float(cam.o[0]);
         of[1] = float(cam.o[1]);
         of[2] = float(cam.o[2]);
@@ -184,7 +198,7 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
             nn += __popc(q0) + __popc(q1);
         }
         __syncwarp();
-        if (nl > (kCap == kBeamCap ? p.fast_cap : kCap) || nn > kFront) {
+        if (nl > (cap >= 0 ? cap : kCap) || nn > kFront) {
             over = true;
             break;
         }
@@ -215,7 +229,8 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
     off = __shfl_sync(0xffffffffu, off, 0);
     if (off + nl > p.pool_cap) {
         if (lane == 0) {
-            *hdr = TileHdr{0, -1, -1, 0};
+            if (sub_out) *sub_out = make_int2(0, -1);
+            else *hdr = TileHdr{0, -1, -1, 0};
             atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
         }
         return true;  // pool full: per-ray traversal
@@ -272,18 +287,23 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
         s_cand[rank] = bc;
     }
     __syncwarp();  // orders the lanes' pool writes for the per-pixel pass
-    // per-pixel lists, in distance order
+    // per-pixel lists, in distance order (only the rectangle's pixels)
     const int P = kThreads / p.spp;
+    auto in_rect = [&](int q) {
+        const int qx = q % p.TW - sx0, qy = q / p.TW - sy0;
+        return qx >= 0 && qx < sw && qy >= 0 && qy < sh;
+    };
     if (P <= 32) {
         // lane = candidate: a mask of the tile pixels its triangle may cover
         // (the same test as cand_overlaps_pixel), then one ballot per pixel
         // appends the covering candidates in candidate (distance) order
         unsigned char* lst0 = (big >= 0 ? p.big_pix_list : p.pix_list) + (big >= 0 ? size_t(big) : tile) * P * kPix;
         int my_cnt = 0;  // list length of pixel q = lane
+        const unsigned rmask = __ballot_sync(0xffffffffu, lane < P && in_rect(lane));
         for (int base = 0; base < nl; base += 32) {
             const int k = base + lane;
             unsigned mask = 0;
-            if (k < nl) mask = cand_pixel_mask(s_cand[k], p.TW, P);
+            if (k < nl) mask = cand_pixel_mask(s_cand[k], p.TW, P) & rmask;
             for (int q = 0; q < P; ++q) {
                 const bool on = (mask >> q) & 1u;
                 const unsigned bal = __ballot_sync(0xffffffffu, on);
@@ -294,14 +314,18 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
                 if (lane == q) my_cnt += __popc(bal);
             }
         }
-        if (lane < P) {
+        if (lane < P && ((rmask >> lane) & 1u)) {
             const size_t li = big >= 0 ? size_t(big) * P + lane : tile * P + lane;
             (big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li] = (unsigned char)(my_cnt > kPix ? 255 : my_cnt);
         }
-        if (lane == 0) *hdr = TileHdr{off, nl, big, 0};
+        if (lane == 0) {
+            if (sub_out) *sub_out = make_int2(off, nl);
+            else *hdr = TileHdr{off, nl, big, 0};
+        }
         return true;
     }
     for (int q = lane; q < P; q += 32) {
+        if (!in_rect(q)) continue;
         const float qx = float(q % p.TW), qy = float(q / p.TW);
         const size_t li = big >= 0 ? size_t(big) * P + q : tile * P + q;
         unsigned char* lst = (big >= 0 ? p.big_pix_list : p.pix_list) + li * kPix;
@@ -313,7 +337,10 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
             }
         (big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li] = (unsigned char)(cnt > kPix ? 255 : cnt);
     }
-    if (lane == 0) *hdr = TileHdr{off, nl, big, 0};
+    if (lane == 0) {
+        if (sub_out) *sub_out = make_int2(off, nl);
+        else *hdr = TileHdr{off, nl, big, 0};
+    }
     return true;
 }
 
@@ -432,7 +459,8 @@ __global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_l
     if (b > b1) return;  // warp-uniform (after the only barrier)
 #endif
     if (build_tile_list<kBeamCap, kFrontCap, kPixCap>(p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], nullptr,
-                                                       -1, share ? s_top : nullptr, share ? s_ntop : 0))
+                                                       -1, share ? s_top : nullptr, share ? s_ntop : 0, 0, 0, 1 << 20,
+                                                       1 << 20, nullptr, p.fast_cap))
         return;
     if (lane == 0) {
         p.tile_hdr[size_t(vc.tile_base) + b] = TileHdr{0, -1, -1, 0};
@@ -457,9 +485,46 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
         const ViewCall vc = p.calls[e.x];
         const DevCamera& cam = p.cams[vc.slot];
         if (!build_tile_list<kBigCap, kBigFront, kBigPixCap>(p, vc, cam, e.y, lane, s_front[w], s_leaf[w], s_d[w],
-                                                             reinterpret_cast<unsigned long long*>(s_front[w]), i) &&
-            lane == 0)
+                                                             reinterpret_cast<unsigned long long*>(s_front[w]), i,
+                                                             nullptr, 0, 0, 0, 1 << 20, 1 << 20, nullptr,
+                                                             p.big_list_cap) &&
+            lane == 0) {
+            const int j = atomicAdd(p.split_count, 1);  // split into quadrants (k_tile_lists_split)
+            if (j < p.split_cap) p.split_queue[j] = i;
+            else atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+        }
+        __syncwarp();
+    }
+}
+
+// Split pass: the tiles still over kBigCap candidates, one warp per
+// (tile, quadrant); the quadrants share the tile's big pixel-list slot. A
+// quadrant that still overflows is traced per ray (beam_fallback_tiles counts
+// such quadrants).
+__global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_split(Params p) {
+    __shared__ __align__(8) int s_front[kBigWarps][2][kBigFront];
+    __shared__ int s_leaf[kBigWarps][kBigCap];
+    __shared__ float s_d[kBigWarps][kBigCap];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = min(*p.split_count, p.split_cap);
+    const int hw = p.TW / 2, hh = p.TH / 2;
+    for (int it = blockIdx.x * kBigWarps + w; it < 4 * n; it += gridDim.x * kBigWarps) {
+        const int j = it >> 2, qd = it & 3;  // quadrant bits as tile_quadrant (beam.cuh)
+        const int i = p.split_queue[j];
+        const int2 e = p.big_queue[i];
+        const ViewCall vc = p.calls[e.x];
+        const DevCamera& cam = p.cams[vc.slot];
+        const int sx0 = (qd & 1) ? hw : 0, sw = (qd & 1) ? p.TW - hw : hw;
+        const int sy0 = (qd & 2) ? hh : 0, sh = (qd & 2) ? p.TH - hh : hh;
+        int2* out = p.split_hdr + 4 * j + qd;
+        if (!build_tile_list<kBigCap, kBigFront, kBigPixCap>(p, vc, cam, e.y, lane, s_front[w], s_leaf[w], s_d[w],
+                                                             reinterpret_cast<unsigned long long*>(s_front[w]), i,
+                                                             nullptr, 0, sx0, sy0, sw, sh, out) &&
+            lane == 0) {
+            *out = make_int2(0, -1);
             atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+        }
+        if (qd == 0 && lane == 0) p.tile_hdr[size_t(vc.tile_base) + e.y] = TileHdr{j, -2, i, 0};
         __syncwarp();
     }
 }
@@ -504,7 +569,8 @@ __device__ __forceinline__ void trace_item(const Params& p, const ViewCall& vc, 
     TileHdr th{0, -1, -1, 0};
     if (kBeam) th = p.tile_hdr[vc.tile_base + tile_in_view];
     if (kBeam && th.cnt == 0 && p.skip_empty_hits) return;  // CTA-uniform: k_render's empty-tile path reads no hits
-    if (kBeam && th.cnt >= 0) {
+    const int2 tl = kBeam ? pixel_tile_list(th, p.split_hdr, pix, TW, TH) : make_int2(0, -1);
+    if (kBeam && tl.y >= 0) {
         const size_t tile = size_t(vc.tile_base) + tile_in_view;
         const size_t li = th.big >= 0 ? size_t(th.big) * P + pix : tile * P + pix;
         const int cnt = (th.big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li];
@@ -512,8 +578,8 @@ __device__ __forceinline__ void trace_item(const Params& p, const ViewCall& vc, 
             D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
             D3 dir = primary_dir(cam, ps);
             const float fx = float(ps.x - X0), fy = float(ps.y - Y0);
-            const BeamCand* cands = p.pool + th.off;
-            h = cnt == 255 ? trace_beam(cands, th.cnt, p.sc.recs, org, dir, p.info->t_min, fx, fy)
+            const BeamCand* cands = p.pool + tl.x;
+            h = cnt == 255 ? trace_beam(cands, tl.y, p.sc.recs, org, dir, p.info->t_min, fx, fy)
                            : trace_beam_list(cands,
                                              (th.big >= 0 ? p.big_pix_list + li * kBigPixCap : p.pix_list + li * kPixCap),
                                              cnt, p.sc.recs, org, dir, p.info->t_min, fx, fy);
@@ -1233,6 +1299,8 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     p.fast_cap = kBeamCap;  // CDR_BEAM_FAST_CAP < kBeamCap pushes tiles to the big pass (tests)
     p.no_shared_top = std::getenv("CDR_NO_SHARED_TOP") != nullptr;
     if (const char* e = std::getenv("CDR_BEAM_FAST_CAP")) p.fast_cap = std::max(0, std::min(kBeamCap, std::atoi(e)));
+    p.big_list_cap = kBigCap;  // CDR_BEAM_BIG_CAP < kBigCap pushes big tiles to the split pass (tests)
+    if (const char* e = std::getenv("CDR_BEAM_BIG_CAP")) p.big_list_cap = std::max(0, std::min(kBigCap, std::atoi(e)));
     c->beam_view.valid = 0;
     p.skip_empty_hits = p.use_beam && loss && a.spp == 16;
     if (c->beam_used_host) c->beam_used_last = *c->beam_used_host;  // previous call has completed
@@ -1257,7 +1325,14 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         // fit k_trace's staging buffer (P <= 64, spp >= 4)
         const int big_cap = P * kBigPixCap <= kThreads * kPixCap ? std::max(64, tile_total / 16) : 0;
         c->beam_big_queue.ensure(std::max(1, big_cap));
-        c->beam_big_count.ensure(1);
+        c->beam_big_count.ensure(2);  // big queue, split queue
+        const int split_cap = big_cap > 0 ? std::max(64, big_cap / 8) : 0;
+        c->beam_split_queue.ensure(std::max(1, split_cap));
+        c->beam_split_hdr.ensure(std::max<size_t>(4, 4 * size_t(split_cap)));
+        p.split_queue = c->beam_split_queue.p;
+        p.split_count = c->beam_big_count.p + 1;
+        p.split_cap = split_cap;
+        p.split_hdr = c->beam_split_hdr.p;
         c->beam_big_pix_list.ensure(std::max<size_t>(16, size_t(big_cap) * P * kBigPixCap));
         c->beam_big_pix_cnt.ensure(std::max<size_t>(1, size_t(big_cap) * P));
         p.big_queue = c->beam_big_queue.p;
@@ -1271,8 +1346,8 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         c->beam_tile_base.ensure(n_views);
         CDR_CUDA_CHECK(cudaMemcpyAsync(c->beam_tile_base.p, bases.data(), sizeof(int) * n_views,
                                        cudaMemcpyHostToDevice, c->stream));
-        c->beam_view = BeamView{p.tile_hdr,     p.pool, p.pix_list, p.pix_cnt, p.big_pix_list, p.big_pix_cnt,
-                                c->beam_tile_base.p, TW,   TH,         P,         1};
+        c->beam_view = BeamView{p.tile_hdr,          p.pool,      p.pix_list, p.pix_cnt, p.big_pix_list, p.big_pix_cnt,
+                                c->beam_tile_base.p, p.split_hdr, TW,         TH,        P,              1};
         c->beam_slots.assign(view_slots, view_slots + n_views);
     }
     // Views can go through lists -> trace -> shade in chunks whose hit cache
@@ -1306,11 +1381,15 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
 #else
             dim3 lgrid((tiles + kListWarps - 1) / kListWarps, nv);
 #endif
-            CDR_CUDA_CHECK(cudaMemsetAsync(pc.big_count, 0, sizeof(int), c->stream));
+            CDR_CUDA_CHECK(cudaMemsetAsync(pc.big_count, 0, 2 * sizeof(int), c->stream));
             ++c->launches;
             k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(pc);
             ++c->launches;
             k_tile_lists_big<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
+            if (!std::getenv("CDR_NO_SPLIT")) {
+                ++c->launches;
+                k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
+            }
         }
         if (trace) launch_trace_kernel(pc, grid, c);
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k + 1], c->stream));

@@ -344,12 +344,16 @@ def test_fp32_targets_equal_widened_fp64(sphere):
     assert rel_l2(out[0][1], out[1][1]) <= 1e-12
 
 
-@pytest.mark.parametrize("fast_cap", ["0", "3"])
-def test_big_tile_lists_exact(sphere, monkeypatch, fast_cap):
+@pytest.mark.parametrize("fast_cap,big_cap", [("0", None), ("3", None), ("3", "8"), ("0", "0")])
+def test_big_tile_lists_exact(sphere, monkeypatch, fast_cap, big_cap):
     """Tiles over the fast pass's candidate cap are rebuilt by the big pass
-    (255 candidates, 64-entry pixel lists). Forcing (almost) every tile there
-    must leave hit caches and images bit-exact and gradients in tolerance."""
+    (255 candidates, 128-entry pixel lists); tiles over that are split into
+    quadrant lists (k_tile_lists_split). Forcing (almost) every tile through
+    those passes must leave hit caches and images bit-exact and gradients in
+    tolerance."""
     monkeypatch.setenv("CDR_BEAM_FAST_CAP", fast_cap)
+    if big_cap is not None:
+        monkeypatch.setenv("CDR_BEAM_BIG_CAP", big_cap)
     blob = blob_scene(freq=8, tex=32, views=2, image=48)
     for sc in (sphere, blob):
         r, o = _pair(sc)
@@ -387,7 +391,7 @@ def test_odd_image_sizes_exact(wh):
     _loss_grad_check(sc, 16, 3, param_layout(sc))
 
 
-@pytest.mark.parametrize("knob", ["CDR_NO_BEAM", "CDR_CHUNK_MB", "CDR_NO_SHARED_TOP"])
+@pytest.mark.parametrize("knob", ["CDR_NO_BEAM", "CDR_CHUNK_MB", "CDR_NO_SHARED_TOP", "CDR_NO_SPLIT"])
 def test_alternate_paths_exact(sphere, monkeypatch, knob):
     """The A/B switches kept in the code (per-ray traversal only; view chunks
     through lists -> trace -> shade; every tile from the BVH root) stay exact."""
@@ -421,7 +425,7 @@ def _silhouette_probe_points(o, v, rng, per_seg=8):
 
 
 @pytest.mark.parametrize("spp", [4, 16])
-@pytest.mark.parametrize("fast_cap", [None, "0"])
+@pytest.mark.parametrize("fast_cap", [None, "0", "split"])
 def test_probe_points_through_lists_bit_exact(monkeypatch, spp, fast_cap):
     """The boundary probes of the fused loss call trace through the per-pixel
     candidate lists (trace_points2, beam.cuh), not per-ray traversal. After a
@@ -429,7 +433,10 @@ def test_probe_points_through_lists_bit_exact(monkeypatch, spp, fast_cap):
     that same path, must hit exactly the oracle's triangles and return its
     radiance. fast_cap "0" sends every tile through the big-list pass (and its
     overflow to per-ray traversal)."""
-    if fast_cap is not None:
+    if fast_cap == "split":  # every tile through the big pass, most of them split into quadrants
+        monkeypatch.setenv("CDR_BEAM_FAST_CAP", "0")
+        monkeypatch.setenv("CDR_BEAM_BIG_CAP", "6")
+    elif fast_cap is not None:
         monkeypatch.setenv("CDR_BEAM_FAST_CAP", fast_cap)
     sc = blob_scene(freq=8, tex=16, views=2, image=64)
     r, o = _pair(sc)
