@@ -27,10 +27,23 @@
 // host code — run_coarse_to_fine, cmd_gradcheck, cmd_render, ... — resolves
 // to these definitions. Status codes become the reference's exceptions.
 //
-// Device selection: env CDR_DEVICE (default 0). Env CDR_SKIP_RENDERED=1 makes
-// total_loss leave TotalLossResult::rendered empty (run_coarse_to_fine does
-// not read it; it costs a K-image download per iteration).
+// Device selection: env CDR_DEVICE (default 0) for every entry point. Env
+// CDR_DEVICES="0,1,...,7" makes total_loss — the per-iteration call of
+// run_coarse_to_fine — fan out over one context per listed GPU, each on its own
+// host thread with a contiguous block of the views (global view ids as RNG
+// keys, so results do not depend on the split); distinct devices are joined by
+// one ncclCommInitAll communicator and the library all-reduces the gradient
+// and loss terms. Listing one device several times ("0,0") runs the same
+// sharding with several contexts on that GPU and sums their results on the
+// host (SURVEY §4's fake multi-GPU mode: tests the sharding on one GPU). Env
+// CDR_SKIP_RENDERED=1 makes total_loss leave TotalLossResult::rendered empty
+// (run_coarse_to_fine does not read it; it costs a K-image download per
+// iteration).
+#include <algorithm>
+#include <array>
 #include <chrono>
+#include <exception>
+#include <optional>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -38,6 +51,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "cdr.h"
@@ -69,7 +83,7 @@ uint64_t fnv1a(const void* p, size_t n, uint64_t h = 1469598103934665603ULL) {
     return h;
 }
 
-// One GPU context per process, with the mesh topology and targets cached.
+// One GPU context, with the mesh topology, views and targets cached.
 struct Device {
     cdr_ctx* ctx = nullptr;
     uint64_t topo_key = 0;
@@ -78,12 +92,11 @@ struct Device {
     std::vector<int32_t> tris, edges;
     std::vector<double> buf;
 
-    Device() {
+    explicit Device(int device) {
         if (cdr_abi_version() != CDR_ABI_VERSION)  // cdr_stats and friends follow the header's layout
             throw std::runtime_error("libcdr.so ABI version differs from include/cdr.h: rebuild");
-        const char* d = std::getenv("CDR_DEVICE");
-        int rc = cdr_create(d ? std::atoi(d) : 0, &ctx);
-        if (rc != CDR_OK) raise(rc, "cdr_create failed (no CUDA device?)");
+        int rc = cdr_create(device, &ctx);
+        if (rc != CDR_OK) raise(rc, "cdr_create failed (no CUDA device " + std::to_string(device) + "?)");
     }
     void check(int rc) {
         if (rc != CDR_OK) raise(rc, cdr_last_error(ctx));
@@ -95,6 +108,8 @@ struct Device {
         for (int f = 0; f < m.triangle_count(); ++f)
             for (int k = 0; k < 3; ++k) tris[3 * size_t(f) + k] = m.triangles[f][k];
         uint64_t key = fnv1a(tris.data(), tris.size() * 4, uint64_t(m.vertex_count()) * 0x9e3779b97f4a7c15ULL);
+        if (!m.uvs.empty()) key = fnv1a(m.uvs.data(), m.uvs.size() * sizeof(m.uvs[0]), key);  // new UVs re-upload
+        if (m.has_adjacency) key = fnv1a(m.edges.data(), m.edges.size() * sizeof(m.edges[0]), key);
         buf.resize(size_t(m.vertex_count()) * 3);
         for (int v = 0; v < m.vertex_count(); ++v) {
             buf[3 * size_t(v)] = m.positions[v].x;
@@ -129,7 +144,8 @@ struct Device {
         }
     }
 
-    void scene(const Scene& s) {
+    // gids: global view ids of s.views' shard (nullptr: all views, ids 0..K-1)
+    void scene(const Scene& s, const std::vector<int32_t>* gids = nullptr) {
         mesh(s.mesh);
         const MaterialMaps& mp = s.maps;
         if (mp.diffuse.width != mp.roughness.width || mp.specular.width != mp.roughness.width ||
@@ -140,14 +156,15 @@ struct Device {
         double L[3] = {s.light.intensity.x, s.light.intensity.y, s.light.intensity.z};
         double B[3] = {s.background.x, s.background.y, s.background.z};
         check(cdr_set_light(ctx, L, B));
-        views(s.views);
+        views(s.views, gids);
     }
 
-    void views(const std::vector<Camera>& cams) {
-        std::vector<cdr_camera> cc(cams.size());
+    void views(const std::vector<Camera>& cams, const std::vector<int32_t>* gids = nullptr) {
+        const size_t n = gids ? gids->size() : cams.size();
+        std::vector<cdr_camera> cc(n);
         std::memset(cc.data(), 0, sizeof(cdr_camera) * cc.size());  // hashed below: no padding garbage
-        for (size_t i = 0; i < cams.size(); ++i) {
-            const Camera& c = cams[i];
+        for (size_t i = 0; i < n; ++i) {
+            const Camera& c = cams[gids ? size_t((*gids)[i]) : i];
             const Vec3* src[4] = {&c.origin, &c.right, &c.up, &c.forward};
             double* dst[4] = {cc[i].origin, cc[i].right, cc[i].up, cc[i].forward};
             for (int k = 0; k < 4; ++k) {
@@ -161,29 +178,46 @@ struct Device {
         }
         // the cameras rarely change across iterations: re-sending them would
         // reset the per-view slots and force every target to be re-uploaded
-        const uint64_t key = fnv1a(cc.data(), sizeof(cdr_camera) * cc.size(), 0xca3e + cc.size());
+        uint64_t key = fnv1a(cc.data(), sizeof(cdr_camera) * cc.size(), 0xca3e + cc.size());
+        if (gids) key = fnv1a(gids->data(), sizeof(int32_t) * gids->size(), key);
         if (key == view_key && view_key != 0) return;
-        check(cdr_set_views(ctx, cc.data(), nullptr, int32_t(cc.size())));
+        check(cdr_set_views(ctx, cc.data(), gids ? gids->data() : nullptr, int32_t(cc.size())));
         view_key = key;
         target_key = 0;  // set_views resets the per-view slots
     }
 
-    void targets(const std::vector<Image>& tg) {
-        uint64_t key = 0x51ed;
-        for (const auto& t : tg) {  // identity + a sparse content probe
-            key = fnv1a(&t.pixels, sizeof(void*), key);
-            size_t n = t.pixels.size();
-            for (size_t i = 0; i < n; i += 1 + n / 64) key = fnv1a(&t.pixels[i], sizeof(Vec3), key);
+    // Targets of the views (or of the shard gids): uploaded when their full
+    // contents (pixels and mask) change. Hashing every byte costs far less
+    // than the upload it avoids, and an in-place edit or a new image at a
+    // reused address can never leave a stale target on the device.
+    void targets(const std::vector<Image>& tg, const std::vector<int32_t>* gids = nullptr) {
+        static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be 3 packed doubles");
+        const size_t n = gids ? gids->size() : tg.size();
+        uint64_t key = 0x51ed + n;
+        for (size_t i = 0; i < n; ++i) {
+            const Image& t = tg[gids ? size_t((*gids)[i]) : i];
+            key = fnv1a(t.pixels.data(), t.pixels.size() * sizeof(Vec3), key);
+            key = fnv1a(t.mask.data(), t.mask.size() * sizeof(double), key ^ t.mask.size());
         }
-        if (key == target_key) return;
-        for (size_t k = 0; k < tg.size(); ++k) {
-            const Image& t = tg[k];
-            static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be 3 packed doubles");
+        if (key == target_key && target_key != 0) return;
+        for (size_t k = 0; k < n; ++k) {
+            const Image& t = tg[gids ? size_t((*gids)[k]) : k];
             check(cdr_set_target(ctx, int32_t(k), reinterpret_cast<const double*>(t.pixels.data()),
                                  t.has_mask() ? t.mask.data() : nullptr));
         }
         target_key = key;
     }
+};
+
+int env_device() {
+    const char* d = std::getenv("CDR_DEVICE");
+    return d ? std::atoi(d) : 0;
+}
+
+// The contexts total_loss fans out over (CDR_DEVICES); the first is dev().
+struct Group {
+    std::vector<Device*> devs;
+    bool nccl = false;  // distinct devices joined by ncclCommInitAll; else summed on the host
 };
 
 // CDR_SHIM_PROFILE=1: wall time per shim entry point, printed at exit
@@ -216,8 +250,50 @@ struct ShimTimer {
 };
 
 Device& dev() {
-    static Device d;
+    static Device d(env_device());
     return d;
+}
+
+Group& group() {
+    static Group g = [] {
+        Group g;
+        g.devs.push_back(&dev());
+        const char* env = std::getenv("CDR_DEVICES");
+        if (!env || !*env) return g;
+        std::vector<int> ids;
+        for (const char* p = env; *p;) {
+            char* end = nullptr;
+            long v = std::strtol(p, &end, 10);
+            if (end == p) throw Error("cdr: CDR_DEVICES must be a comma-separated device list, got \"" +
+                                      std::string(env) + "\"");
+            ids.push_back(int(v));
+            p = *end == ',' ? end + 1 : end;
+        }
+        if (ids.empty()) return g;
+        int count = 0;
+        cdr_device_count(&count);
+        for (int id : ids)
+            if (id < 0 || id >= count)
+                throw Error("cdr: CDR_DEVICES lists device " + std::to_string(id) + " but " + std::to_string(count) +
+                            " are visible");
+        g.devs.clear();
+        for (size_t k = 0; k < ids.size(); ++k)
+            g.devs.push_back(k == 0 && ids[0] == env_device() ? &dev() : new Device(ids[k]));  // leaked with the process
+        std::vector<int> sorted = ids;
+        std::sort(sorted.begin(), sorted.end());
+        g.nccl = g.devs.size() > 1 && std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+        if (g.nccl) {
+            std::vector<cdr_ctx*> ctxs;
+            for (Device* d : g.devs) ctxs.push_back(d->ctx);
+            const int rc = cdr_comm_init_all(ctxs.data(), int32_t(ctxs.size()));
+            if (rc != CDR_OK) raise(rc, std::string("ncclCommInitAll: ") + cdr_last_error(ctxs[0]));
+        } else {
+            for (size_t k = 0; k < g.devs.size(); ++k)
+                g.devs[k]->check(cdr_set_rank(g.devs[k]->ctx, int32_t(k), int32_t(g.devs.size())));
+        }
+        return g;
+    }();
+    return g;
 }
 
 cdr_settings settings_of(const RenderSettings& s) {
@@ -506,46 +582,90 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
     if (targets.size() != scene.views.size()) throw SizeMismatch("target count does not match views");
     ShimTimer timer(0);
     TotalLossResult res{LossBreakdown{}, GradVector(layout), {}};
-    Device& d = dev();
-    {
-        ShimTimer t(1);
-        d.scene(scene);
-        d.targets(targets);
-    }
-    const int n = int(scene.views.size());
-    std::vector<int32_t> views(n);
-    for (int k = 0; k < n; ++k) views[k] = k;
+    Group& g = group();
+    const int K = int(scene.views.size());
+    const int N = std::max(1, std::min<int>(int(g.devs.size()), K));  // ranks with at least one view
+    // contiguous blocks of ceil(K / N) global view ids (shard.py: shard_views)
+    const int per = (K + N - 1) / N;
+    std::vector<std::vector<int32_t>> gids(g.devs.size());
+    for (int k = 0; k < N; ++k)
+        for (int v = k * per; v < std::min(K, (k + 1) * per); ++v) gids[k].push_back(v);
     cdr_settings st = settings_of(options.render);
     st.flags |= CDR_FLAG_GRAD_OVERWRITE;  // res.grad is the fresh GradVector (losses.cpp:250)
     cdr_layout lay = layout_of(*layout);
-    const bool want_rendered = !std::getenv("CDR_SKIP_RENDERED");
     const cdr_reg_weights reg{weights.normal, weights.edge, weights.spec, weights.roug, weights.sigma1,
                               weights.sigma2};
-    double bd[7] = {0, 0, 0, 0, 0, 0, 0};
-    {
-        ShimTimer t2(2);
-        d.check(cdr_total_loss(d.ctx, views.data(), n, &st, weights.rend, weights.lap, &reg,
-                               options.laplacian_mode == LaplacianMode::Uniform ? CDR_LAPLACIAN_UNIFORM
-                                                                                 : CDR_LAPLACIAN_COTANGENT,
-                               options.use_target_masks ? 1 : 0, &lay, bd, res.grad.values.data(), nullptr,
-                               nullptr, nullptr));
+    const int32_t lap_mode = options.laplacian_mode == LaplacianMode::Uniform ? CDR_LAPLACIAN_UNIFORM
+                                                                               : CDR_LAPLACIAN_COTANGENT;
+    const bool single = g.devs.size() == 1;
+    std::vector<std::array<double, 7>> bd(g.devs.size(), std::array<double, 7>{});
+    std::vector<std::vector<double>> part(single || g.nccl ? 0 : g.devs.size());
+    std::vector<std::exception_ptr> err(g.devs.size());
+    auto run = [&](size_t k) {
+        try {
+            Device& d = *g.devs[k];
+            {
+                ShimTimer t(1);
+                d.scene(scene, single ? nullptr : &gids[k]);
+                d.targets(targets, single ? nullptr : &gids[k]);
+            }
+            const int n = int(single ? K : gids[k].size());
+            std::vector<int32_t> slots(n);
+            for (int i = 0; i < n; ++i) slots[i] = i;
+            // rank 0 receives the (all-reduced) gradient; the other NCCL ranks
+            // keep theirs on the device; host-summed ranks return their part
+            double* gout = nullptr;
+            if (k == 0 && (single || g.nccl)) gout = res.grad.values.data();
+            else if (!g.nccl) {
+                part[k].assign(res.grad.values.size(), 0.0);
+                gout = part[k].data();
+            }
+            ShimTimer t2(2);
+            d.check(cdr_total_loss(d.ctx, slots.data(), n, &st, weights.rend, weights.lap, &reg, lap_mode,
+                                   options.use_target_masks ? 1 : 0, &lay, bd[k].data(), gout, nullptr, nullptr,
+                                   nullptr));
+        } catch (...) {
+            err[k] = std::current_exception();
+        }
+    };
+    if (single) {
+        run(0);
+    } else {  // one host thread per context: NCCL ranks must enter the all-reduce together
+        std::vector<std::thread> th;
+        for (size_t k = 0; k < g.devs.size(); ++k) th.emplace_back(run, k);
+        for (auto& t : th) t.join();
     }
-    res.breakdown.total = bd[0];
-    res.breakdown.rend = bd[1];
-    res.breakdown.lap = bd[2];
-    res.breakdown.normal = bd[3];
-    res.breakdown.edge = bd[4];
-    res.breakdown.spec = bd[5];
-    res.breakdown.roug = bd[6];
-    if (want_rendered) {  // straight from the device arena into the returned images
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+    double t[7] = {bd[0][0], bd[0][1], bd[0][2], bd[0][3], bd[0][4], bd[0][5], bd[0][6]};
+    if (!single && !g.nccl) {  // host sum of the shards, in rank order (rank 0 holds the once-only terms)
+        std::vector<double>& out = res.grad.values;
+        out = part[0];
+        for (size_t k = 1; k < part.size(); ++k) {
+            for (size_t i = 0; i < out.size(); ++i) out[i] += part[k][i];
+            for (int j = 1; j < 7; ++j) t[j] += bd[k][j];
+        }
+        t[0] = t[1] + t[2] + t[3] + t[4] + t[5] + t[6];  // losses.cpp:294-295
+    }
+    res.breakdown.total = t[0];
+    res.breakdown.rend = t[1];
+    res.breakdown.lap = t[2];
+    res.breakdown.normal = t[3];
+    res.breakdown.edge = t[4];
+    res.breakdown.spec = t[5];
+    res.breakdown.roug = t[6];
+    if (!std::getenv("CDR_SKIP_RENDERED")) {  // straight from the device arenas into the returned images
         ShimTimer t3(3);
         res.rendered.reserve(scene.views.size());
-        for (int k = 0; k < n; ++k) {
-            const Camera& c = scene.views[k];
+        for (int v = 0; v < K; ++v) {
+            const size_t k = single ? 0 : size_t(v / per);
+            const int slot = single ? v : v - int(k) * per;
+            const Camera& c = scene.views[v];
             std::optional<ShimTimer> t6(std::in_place, 6);
             Image img(c.width, c.height, true);
             t6.reset();
-            d.check(cdr_get_rendered(d.ctx, k, reinterpret_cast<double*>(img.pixels.data()), img.mask.data()));
+            Device& d = *g.devs[k];
+            d.check(cdr_get_rendered(d.ctx, slot, reinterpret_cast<double*>(img.pixels.data()), img.mask.data()));
             res.rendered.push_back(std::move(img));
         }
     }

@@ -60,6 +60,12 @@ int main(int argc, char** argv) {
     auto t0 = clk::now();
     TotalLossResult tl = total_loss(init, targets, w, opt, layout);
     double t_loss = secs(t0, clk::now());
+    if (const char* dump = std::getenv("CDR_DEMO_DUMP")) {  // the first gradient, raw fp64 (tests)
+        if (FILE* f = std::fopen(dump, "wb")) {
+            std::fwrite(tl.grad.values.data(), sizeof(double), tl.grad.values.size(), f);
+            std::fclose(f);
+        }
+    }
 
     StagePlan plan;
     for (int si = 0; si < stages; ++si) {
@@ -89,9 +95,9 @@ int main(int argc, char** argv) {
     for (double s : it_s) mean += s;
     mean /= std::max<size_t>(1, it_s.size());
     std::printf("{\"tris\": %d, \"views\": %d, \"image\": %d, \"spp\": %d, \"threads\": %d, "
-                "\"ms_per_iteration\": %.3f, \"ms_total_loss\": %.3f, \"loss0\": %.9g, \"rend0\": %.9g, "
-                "\"lap0\": %.9g, \"normal0\": %.9g, \"edge0\": %.9g, \"spec0\": %.9g, \"roug0\": %.9g, "
-                "\"loss_last\": %.9g, \"iterations\": %zu, \"stages\": %d, \"tris_final\": %d, "
+                "\"ms_per_iteration\": %.3f, \"ms_total_loss\": %.3f, \"loss0\": %.17g, \"rend0\": %.17g, "
+                "\"lap0\": %.17g, \"normal0\": %.17g, \"edge0\": %.17g, \"spec0\": %.17g, \"roug0\": %.17g, "
+                "\"loss_last\": %.17g, \"iterations\": %zu, \"stages\": %d, \"tris_final\": %d, "
                 "\"p2m_last\": %.12g, \"safety_ok\": %d}\n",
                 gt.mesh.triangle_count(), views, image, spp, threads, 1e3 * mean, 1e3 * t_loss,
                 tl.breakdown.total, tl.breakdown.rend, tl.breakdown.lap, tl.breakdown.normal, tl.breakdown.edge,

@@ -1326,7 +1326,8 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         const int big_cap = P * kBigPixCap <= kThreads * kPixCap ? std::max(64, tile_total / 16) : 0;
         c->beam_big_queue.ensure(std::max(1, big_cap));
         c->beam_big_count.ensure(2);  // big queue, split queue
-        const int split_cap = big_cap > 0 ? std::max(64, big_cap / 8) : 0;
+        // CDR_NO_SPLIT (A/B): no split pass, its tiles traced per ray (and counted so)
+        const int split_cap = big_cap > 0 && !std::getenv("CDR_NO_SPLIT") ? std::max(64, big_cap / 8) : 0;
         c->beam_split_queue.ensure(std::max(1, split_cap));
         c->beam_split_hdr.ensure(std::max<size_t>(4, 4 * size_t(split_cap)));
         p.split_queue = c->beam_split_queue.p;
@@ -1386,7 +1387,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(pc);
             ++c->launches;
             k_tile_lists_big<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
-            if (!std::getenv("CDR_NO_SPLIT")) {
+            if (p.split_cap > 0) {
                 ++c->launches;
                 k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
             }

@@ -93,3 +93,54 @@ def test_drop_in_demo_matches_reference():
     # between the reference's own thread counts, whose merge order differs)
     assert b200["loss_last"] == pytest.approx(ref["loss_last"], rel=1e-2)
     assert b200["tris_final"] == ref["tris_final"]
+
+
+@pytest.mark.gpu
+def test_drop_in_demo_coarse_to_fine_stages():
+    """Three coarse-to-fine stages through the unmodified run_coarse_to_fine:
+    a remesh at every stage change (coarse_to_fine.cpp:128-158), so the shim
+    sees a new topology — cdr_set_mesh with new vertex/face/edge counts, a new
+    ParamLayout and a rebuilt LBVH, Laplacian CSR and normal-Jacobian tables —
+    and the next total_loss runs on it. The texture resolution is held fixed:
+    the reference's own carry_texture_moments throws on a resolution-doubling
+    plan ("moment upsample size mismatch")."""
+    args = "2 64 4 2 3 32 8 3"  # views image spp iters subdiv tex threads stages
+    ref = _demo(_need("demo_ref"), args)
+    b200 = _demo(_need("demo_b200"), args)
+    assert ref["stages"] == b200["stages"] == 3
+    assert b200["iterations"] == ref["iterations"] == 6
+    for k in ("lap0", "edge0", "normal0"):
+        assert b200[k] == pytest.approx(ref[k], rel=1e-12, abs=1e-300), k
+    for k in ("loss0", "rend0", "spec0", "roug0"):
+        assert b200[k] == pytest.approx(ref[k], rel=1e-6, abs=1e-12), k
+    # remeshed twice: the final topology follows the same remesh decisions
+    assert b200["tris_final"] == pytest.approx(ref["tris_final"], rel=0.02)
+    assert b200["loss_last"] == pytest.approx(ref["loss_last"], rel=5e-2)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", ["0,0", "0,0,0"])
+def test_shim_total_loss_sharded_over_contexts(tmp_path, devices):
+    """CDR_DEVICES fan-out of the shim's total_loss: the views split into
+    contiguous blocks over several contexts (here all on GPU 0: summed on the
+    host; distinct GPUs use ncclCommInitAll), global view ids as RNG keys.
+    The first total_loss of the drop-in demo must equal the one-context
+    result: loss terms and gradient within 1e-12 (fp64 sum order only)."""
+    import numpy as np
+    binary = _need("demo_b200")
+    args = "5 64 4 1 3 32"  # 5 views: uneven shards (3+2, 2+2+1)
+    out = {}
+    for name, env in (("one", {}), ("many", {"CDR_DEVICES": devices})):
+        dump = tmp_path / f"{name}.bin"
+        e = dict(os.environ, CDR_DEMO_DUMP=str(dump), **env)
+        e.pop("CDR_DEVICES", None) if name == "one" else None
+        p = subprocess.run([binary, *args.split()], capture_output=True, text=True, timeout=600, env=e,
+                           cwd=os.path.dirname(binary))
+        assert p.returncode == 0, p.stderr[-2000:]
+        import json
+        out[name] = (json.loads(p.stdout.strip().splitlines()[-1]), np.fromfile(dump, dtype=np.float64))
+    (a, ga), (b, gb) = out["one"], out["many"]
+    for k in ("loss0", "rend0", "lap0", "normal0", "edge0", "spec0", "roug0"):
+        assert b[k] == pytest.approx(a[k], rel=1e-12, abs=1e-300), k
+    assert len(ga) == len(gb) and np.linalg.norm(ga) > 0
+    assert np.linalg.norm(ga - gb) <= 1e-12 * np.linalg.norm(ga)
