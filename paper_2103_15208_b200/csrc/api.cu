@@ -889,7 +889,8 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
     std::vector<double> lacc(c->views.size());
     double lap_sq = 0;
     CDR_CUDA_CHECK(cudaMemcpyAsync(lacc.data(), c->loss_acc.p, sizeof(double) * lacc.size(), cudaMemcpyDeviceToHost, s));
-    CDR_CUDA_CHECK(cudaMemcpyAsync(&lap_sq, c->lap_partial.p, sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (lap_here)  // ranks > 0 never run the Laplacian (its buffers may not exist)
+        CDR_CUDA_CHECK(cudaMemcpyAsync(&lap_sq, c->lap_partial.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     double regv[4] = {0, 0, 0, 0};
     CDR_CUDA_CHECK(cudaMemcpyAsync(regv, c->reg_vals.p, sizeof(regv), cudaMemcpyDeviceToHost, s));
     if (grad && (st->flags & CDR_FLAG_GRAD_OVERWRITE))

@@ -86,3 +86,39 @@ def test_cfg1_full():
 def test_nccl_single_rank_allreduce_path():
     sc = S.make_scene(S.blob(6), 16, 2, 32)
     _compare(sc, 4, 2, nccl=True)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rank_shards_sum_to_single_context(world):
+    """The library's multi-rank path on one GPU: `world` contexts, each a
+    contiguous block of the views with their GLOBAL ids (shard.py) and its rank
+    set (cdr_set_rank: only rank 0 adds the Laplacian and the regularisers), the
+    per-rank gradients and loss terms summed on the host — as the NCCL
+    all-reduce sums them across GPUs. Must equal one context over all views."""
+    from paper_2103_15208_b200.api import LossWeights
+    from paper_2103_15208_b200.shard import shard_views
+    sc = S.make_scene(S.blob(8), 32, 5, 48)
+    spp, seed = 4, 3
+    tgt = S.perturbed_target_scene(sc)
+    to = Oracle(tgt)
+    targets = np.stack([to.render(v, spp, seed + 0x7A9)[0] for v in range(len(sc.cameras))])
+    lay = layout_for(sc)
+    st = RenderSettings(spp=spp, seed=seed)
+    lw = LossWeights()
+    one = Renderer(0, sc)
+    bd1, g1, _ = one.total_loss(list(targets), st, lay, weights=lw)
+    terms = np.zeros(6)
+    g = np.zeros_like(g1)
+    for rank in range(world):
+        gids = shard_views(len(sc.cameras), world, rank)
+        part = S.Scene(sc.mesh, sc.diffuse, sc.specular, sc.roughness, [sc.cameras[i] for i in gids])
+        r = Renderer(0, part, view_ids=gids)
+        r.set_rank(rank, world)
+        bd, gr, _ = r.total_loss(list(targets[gids]), st, lay, weights=lw)
+        terms += [bd[k] for k in ("rend", "lap", "normal", "edge", "spec", "roug")]
+        g += gr
+        if rank > 0:
+            assert bd["lap"] == 0 and bd["normal"] == 0 and bd["spec"] == 0
+    for i, k in enumerate(("rend", "lap", "normal", "edge", "spec", "roug")):
+        assert terms[i] == pytest.approx(bd1[k], rel=1e-12, abs=1e-300), k
+    assert rel_l2(g, g1) <= 1e-12
