@@ -135,6 +135,10 @@ typedef struct cdr_stats {
 } cdr_stats;
 
 int cdr_abi_version(void);
+/* How the library was built: CDR_BUILD_CHECKED = device-side bounds checks on
+ * (the test build that stands in for compute-sanitizer). */
+#define CDR_BUILD_CHECKED 1
+int cdr_build_flags(void);
 int cdr_device_count(int* count);
 
 int cdr_create(int device, cdr_ctx** out);

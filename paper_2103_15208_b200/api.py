@@ -122,6 +122,7 @@ def load_library(path: str = LIB_PATH):
     L = C.CDLL(path)
     if L.cdr_abi_version() != ABI_VERSION:  # the ctypes structs below follow this header version
         raise RuntimeError(f"{path}: ABI version {L.cdr_abi_version()}, this binding expects {ABI_VERSION}: rebuild")
+    L.cdr_build_flags.restype = C.c_int
     L.cdr_last_error.restype = C.c_char_p
     L.cdr_last_error.argtypes = [_vp]
     L.cdr_create.argtypes = [C.c_int, C.POINTER(_vp)]

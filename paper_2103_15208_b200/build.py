@@ -80,5 +80,17 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     return lib
 
 
+CHECKED_LIB = os.path.join(OUT_DIR, "checked", "libcdr.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The same library with the device-side bounds checks on (-DCDR_CHECKED,
+    CDR_DCHECK in common.cuh): the GPU suite runs against it too
+    (tests/test_checked_build.py) in place of compute-sanitizer, which the GPU
+    pool does not offer."""
+    os.makedirs(os.path.dirname(CHECKED_LIB), exist_ok=True)
+    return build(force=force, out=CHECKED_LIB, defines=("CDR_CHECKED",))
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

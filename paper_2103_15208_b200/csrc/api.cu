@@ -244,6 +244,14 @@ extern "C" {
 
 int cdr_abi_version(void) { return CDR_ABI_VERSION; }
 
+int cdr_build_flags(void) {
+#ifdef CDR_CHECKED
+    return CDR_BUILD_CHECKED;
+#else
+    return 0;
+#endif
+}
+
 int cdr_device_count(int* count) {
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);

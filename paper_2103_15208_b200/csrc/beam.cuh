@@ -186,6 +186,7 @@ __device__ __forceinline__ Hit trace_beam_list(const BeamCand* __restrict__ cand
     Hit best{-1, 1e300, 0.0, 0.0};
     for (int j = 0; j < n; ++j) {
         const int k = idx[j];
+        CDR_DCHECK(k < 255);
         const float4 e2 = cand[k].e2, e0 = cand[k].e0, e1 = cand[k].e1;
         if (double(e2.y) > best.t) break;
         CDR_STAT(3, 1);

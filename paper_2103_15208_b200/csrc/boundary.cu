@@ -282,6 +282,7 @@ __device__ __forceinline__ bool boundary_setup(const BParams& p, int vi, int64_t
         else hi = mid;
     }
     b.si = lo < nseg - 1 ? lo : nseg - 1;
+    CDR_DCHECK(b.si >= 0 && b.si < nseg && nseg <= p.E);
     b.sg = p.segs + size_t(vi) * p.E + b.si;
     if (b.sg->length_px < 1e-12) return false;
     b.s = rng.next_double();
@@ -390,6 +391,7 @@ __device__ __forceinline__ int boundary_samples(const BParams& p, int vi, const 
         const size_t o = size_t(vi) * p.m_stride + j;
         b.si = p.sorted_si[o];
         b.s = p.sorted_s[o];
+        CDR_DCHECK(b.si >= 0 && b.si < p.count[vi]);
         b.sg = p.segs + size_t(vi) * p.E + b.si;
         const cdr_segment* sg = b.sg;
         b.xq = D2{sg->q0[0] + (sg->q1[0] - sg->q0[0]) * b.s, sg->q0[1] + (sg->q1[1] - sg->q0[1]) * b.s};

@@ -143,7 +143,13 @@ __device__ __forceinline__ Hit trace(const BNode* __restrict__ nodes,
         if (h0 && h1) {
             int nearc = t0 <= t1 ? k.x : k.y;
             int farc = t0 <= t1 ? k.y : k.x;
-            if (sp < 64) stack[sp++] = farc;
+            // Depth bound: a Karras node splits its key range at a strictly lower
+            // bit than its parent, and keys have 62 bits (30 Morton + 32 index),
+            // so a root-to-leaf path holds <= 62 internal nodes and the stack
+            // (one entry per internal node on the path) never exceeds 62 < 64.
+            // An overflow would mean a corrupt hierarchy: fail loudly.
+            if (sp >= 64) __trap();
+            stack[sp++] = farc;
             node = nearc;
         } else if (h0) {
             node = k.x;

@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(kCpBlock) k_closest(const BNode* __restrict__ 
                 if (far(dd[j])) continue;
                 if (ch[j] < 0) {
                     leaf(~ch[j]);
-                } else if (sp < 64) {
+                } else {
+                    // <= one entry per level of the path plus the sibling just
+                    // pushed: <= 63 by the LBVH depth bound (bvh.cuh trace)
+                    if (sp >= 64) __trap();
                     stack[sp] = ch[j];
                     sd[sp++] = dd[j];
                 }

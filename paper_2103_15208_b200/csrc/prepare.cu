@@ -393,12 +393,16 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const unsigned long 
     __syncthreads();
     // stage the tile sorted by digit (stable), then write each digit's run
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) stage[tile_excl[dg[j]] + whist[w][dg[j]] + rank[j]] = k[j];
+    for (int j = 0; j < kSortItems; ++j) {
+        CDR_DCHECK(tile_excl[dg[j]] + whist[w][dg[j]] + rank[j] < unsigned(kSortTile));
+        stage[tile_excl[dg[j]] + whist[w][dg[j]] + rank[j]] = k[j];
+    }
     __syncthreads();
     const int valid = int(min(size_t(kSortTile), size_t(n) - size_t(tile) * kSortTile));
     for (int i = tid; i < valid; i += kSortThreads) {
         const unsigned long long x = stage[i];
         const int d = sort_digit(x, pass);
+        CDR_DCHECK(digit_base[d] + (unsigned(i) - tile_excl[d]) < unsigned(n));
         out[digit_base[d] + (unsigned(i) - tile_excl[d])] = x;
     }
 }

@@ -910,6 +910,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     double t = 0, b1 = 0, b2 = 0;
     D3 dir{0, 0, 1};
     if (valid) tri = p.hit[pidx * spp + s];
+    CDR_DCHECK(tri >= -1 && tri < p.sc.n_tris);
 #ifdef CDR_EXP_SKIP_MISS  // measurement only (wrong output): cost of all-miss CTAs
     if (!__syncthreads_or(tri >= 0)) return;
 #endif

@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(kSiBlock) k_self_intersect(const BNode* __rest
             h1 = false;
         }
         if (h0 && h1) {
+            if (sp >= 64) __trap();  // LBVH depth bound (bvh.cuh trace): never taken
             stack[sp++] = k.y;
             node = k.x;
         } else if (h0) {
