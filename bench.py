@@ -421,14 +421,32 @@ def main(argv=None):
             "storage_bytes_per_launch": stored_bytes,
             "storage_frac": stored_bytes / (ms_shade / 1e3) / 1e9 / pk["hbm_gbs"],
             "ms_per_launch": ms_shade, "share_of_step": ms_shade / statistics.mean(ms_steps)}
-    traffic_file = os.path.join(ROOT, "profiles", "render_traffic.json")
-    if os.path.exists(traffic_file):
-        try:  # ncu dram bytes per sample of this kernel, scaled to this launch
-            tr = json.load(open(traffic_file))
-            roof["traffic"] = tr["dram_bytes_per_sample"] * s0["samples"]
-            roof["traffic_source"] = tr.get("source")
-        except Exception:
-            pass
+    # DRAM traffic of the same kernel at THIS config, from the committed ncu
+    # capture of one iteration (profiles/profile_step.py, profiles/r2/per_kernel_<cfg>.json);
+    # configs without a capture report null rather than a scaled figure
+    traffic_file = os.path.join(ROOT, "profiles", "r2", f"per_kernel_{args.config}.json")
+    roof["traffic"] = None
+    roof["traffic_source"] = f"no ncu capture of {args.config}"
+    if os.path.exists(traffic_file) and args.views is None and world == 1:
+        try:
+            kern = json.load(open(traffic_file))["kernels"]
+            kr = next(v for k, v in kern.items() if k.startswith("k_render<1, 1, 1"))
+            roof["traffic"] = 1e6 * (kr["dram_read_MB"] + kr["dram_write_MB"])
+            roof["traffic_source"] = (f"ncu dram__bytes_read.sum + dram__bytes_write.sum of k_render<1,1,1,16> at "
+                                      f"{args.config}, {os.path.relpath(traffic_file, ROOT)}")
+        except Exception as e:  # noqa: BLE001
+            roof["traffic_source"] = f"unreadable capture: {e}"
+
+    # traversal throughput (latency-bound, reported as Mrays/s):
+    # primary rays = samples of non-empty beam tiles (k_tile_lists + k_trace),
+    # boundary probe rays = 2 per active edge sample (k_bsample..k_boundary)
+    ms_trace = statistics.mean(x["ms_trace"] for x in stats)
+    ms_bnd = statistics.mean(x["ms_boundary"] for x in stats)
+    traversal = {"primary_Mrays_per_s": s0["shaded_samples"] / (ms_trace / 1e3) / 1e6,
+                 "primary_rays": s0["shaded_samples"], "ms_visibility": ms_trace,
+                 "probe_Mrays_per_s": 2 * s0["boundary_active"] / (ms_bnd / 1e3) / 1e6,
+                 "probe_rays": 2 * s0["boundary_active"], "ms_boundary": ms_bnd,
+                 "note": "per rank; visibility = candidate lists + trace; boundary = sampling + probes + deposits"}
 
     # ---- e2e: host buffers through the C-ABI
     e2e = None
@@ -570,6 +588,7 @@ def main(argv=None):
                            "samples_per_step": samples_all, "parallelism": f"views sharded x{world}",
                            "l2": "flushed (256 MB write) before every timed step; step working set ~2 GB"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "regularisers": regs, "iteration": iteration,
+                "traversal": traversal,
                 "gpu_launches": int(sum(x["kernel_launches"] for x in stats)),
                 "clocks": clk, "stages_ms": stages,
                 "counters": {k: s0[k] for k in ("pixels", "samples", "hit_samples", "adjoint_samples",

@@ -41,6 +41,7 @@ constexpr int kBeamCap = CDR_BEAM_CAP;    // candidates per tile; more -> per-ra
 constexpr int kPixCap = CDR_PIX_CAP;         // candidates per pixel list; more -> scan the tile list
 constexpr int kBigPixCap = CDR_BIG_PIX_CAP;  // the same for big tiles (over kBeamCap candidates)
 static_assert(kPixCap < 255 && kBigPixCap < 255, "255 marks an overflowed pixel list");
+static_assert(kPixCap % 4 == 0 && kBigPixCap % 4 == 0, "lists are read four entries per 32-bit load");
 constexpr int kFrontCap = CDR_FRONT_CAP;  // builder frontier per tile; more -> per-ray traversal
 
 // Candidate record (48 B): three edge functions E_i = A_i x + B_i y + C_i
@@ -184,8 +185,10 @@ __device__ __forceinline__ Hit trace_beam_list(const BeamCand* __restrict__ cand
                                                int n, const TriRec* __restrict__ recs, D3 o, D3 d, double t_min,
                                                float px, float py) {
     Hit best{-1, 1e300, 0.0, 0.0};
+    unsigned iw = 0;  // four list entries per load (lists are 4-byte aligned, kPix % 4 == 0)
     for (int j = 0; j < n; ++j) {
-        const int k = idx[j];
+        if ((j & 3) == 0) iw = __ldg(reinterpret_cast<const unsigned*>(idx + j));
+        const int k = int((iw >> (8 * (j & 3))) & 0xffu);
         CDR_DCHECK(k < 255);
         const float4 e2 = cand[k].e2, e0 = cand[k].e0, e1 = cand[k].e1;
         if (double(e2.y) > best.t) break;
@@ -260,6 +263,7 @@ static __device__ unsigned long long g_probe_stats[8];
 struct ProbeScan {
     const BeamCand* cand;
     const unsigned char* lst;  // nullptr: scan the whole tile list
+    unsigned iw;               // the current 4-entry word of lst
     int n, j;
     float lx, ly;
     int mode;  // 0 done, 1 scanning, 2 per-ray traversal
@@ -312,7 +316,11 @@ __device__ __forceinline__ void probe_step(ProbeScan& s, const TriRec* __restric
         s.mode = 0;
         return;
     }
-    const int k = s.lst ? int(s.lst[s.j]) : s.j;
+    int k = s.j;
+    if (s.lst) {  // four list entries per load: no dependent byte load on most steps
+        if ((s.j & 3) == 0) s.iw = __ldg(reinterpret_cast<const unsigned*>(s.lst + s.j));
+        k = int((s.iw >> (8 * (s.j & 3))) & 0xffu);
+    }
     ++s.j;
     CDR_PSTAT(6, 1);
     const float4 e2 = s.cand[k].e2, e0 = s.cand[k].e0, e1 = s.cand[k].e1;

@@ -324,35 +324,55 @@ __global__ void __launch_bounds__(kBlock) k_bsample(BParams p) {
     }
 }
 
-// pass 2 (one CTA per view): exclusive scan of the per-bin counts
-__global__ void k_bscan(int32_t* __restrict__ count, const int32_t* __restrict__ nseg, int E,
-                        int32_t* __restrict__ off, int32_t* __restrict__ n_active) {
+// pass 2 (one CTA per view): exclusive scan of the per-bin counts. Chunks of
+// 4,096 bins: four consecutive bins per thread, a warp-shuffle scan of the
+// thread sums, one more over the 32 warp totals (two barriers per chunk).
+__global__ void __launch_bounds__(1024) k_bscan(int32_t* __restrict__ count, const int32_t* __restrict__ nseg, int E,
+                                                int32_t* __restrict__ off, int32_t* __restrict__ n_active) {
     const int vi = blockIdx.x;
     const int n = nseg[vi] * kSBins;
-    E *= kSBins;  // per-view stride of the bin arrays
-    __shared__ int32_t sh[1024];
-    __shared__ int32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < n; base += 1024) {
-        int i = base + threadIdx.x;
-        int v = 0;
-        if (i < n) {
-            v = count[size_t(vi) * E + i];
-            count[size_t(vi) * E + i] = 0;  // counters are left zeroed for the next call
+    const size_t vb = size_t(vi) * size_t(E) * kSBins;  // per-view stride of the bin arrays
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ int32_t wsum[32];
+    int carry = 0;
+    for (int base = 0; base < n; base += 4 * 1024) {
+        const int i0 = base + 4 * int(threadIdx.x);
+        int v[4];
+        int tsum = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k;
+            v[k] = i < n ? count[vb + i] : 0;
+            if (i < n) count[vb + i] = 0;  // counters are left zeroed for the next call
+            tsum += v[k];
         }
-        sh[threadIdx.x] = v;
-        __syncthreads();
-        for (int o = 1; o < 1024; o <<= 1) {
-            int t = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
-            __syncthreads();
-            sh[threadIdx.x] += t;
-            __syncthreads();
+        int x = tsum;  // inclusive scan of the thread sums within the warp
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        if (i < n) off[size_t(vi) * E + i] = carry + sh[threadIdx.x] - v;
+        if (lane == 31) wsum[w] = x;
         __syncthreads();
-        if (threadIdx.x == 1023) carry += sh[1023];
+        if (w == 0) {
+            int t = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            wsum[lane] = t;
+        }
         __syncthreads();
+        int e = carry + (w > 0 ? wsum[w - 1] : 0) + x - tsum;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int i = i0 + k;
+            if (i < n) off[vb + i] = e;
+            e += v[k];
+        }
+        carry += wsum[31];
+        __syncthreads();  // wsum is rewritten by the next chunk
     }
     if (threadIdx.x == 0) n_active[vi] = carry;
 }
