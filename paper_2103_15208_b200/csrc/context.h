@@ -139,6 +139,10 @@ struct cdr_ctx {
     cdr::DBuf<int> beam_split_queue;  // big-queue index of each split tile
     cdr::DBuf<int2> beam_split_hdr;   // 4 quadrant lists per split tile
     cdr::DBuf<unsigned char> beam_big_pix_list, beam_big_pix_cnt;      // per view index of the last render call
+    cdr::DBuf<int2> tile_queue;         // non-empty tiles (call, tile) of a queue-mode loss call
+    cdr::DBuf<int> tile_queue_count;
+    int* tile_queue_host = nullptr;     // pinned: its length, read back during k_trace
+    cudaEvent_t tile_queue_ev = nullptr;
     cdr::BeamView beam_view{};          // lists of the last render call (valid flag)
     std::vector<int> beam_slots;        // view slots of that call, in call order (beam_view's view index)
     int* beam_used_host = nullptr;   // pinned; previous call's pool use

@@ -78,6 +78,12 @@ struct Params {
     int* split_count;
     int split_cap;
     int2* split_hdr;  // per split tile: 4 quadrant lists (first candidate, count; -1 = per ray)
+    // tile queue (loss calls at spp 16): k_tile_lists appends every non-empty
+    // tile (call, tile); k_render then runs over the queue only and
+    // k_background writes the empty tiles' pixels
+    int2* tile_queue;
+    int* tile_queue_count;
+    int queue_mode;  // k_render: CTAs from tile_queue instead of the full tile grid
 };
 
 constexpr int kThreads = 256;
@@ -458,10 +464,14 @@ __global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_l
     const int b = b0 + w;
     if (b > b1) return;  // warp-uniform (after the only barrier)
 #endif
-    if (build_tile_list<kBeamCap, kFrontCap, kPixCap>(p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], nullptr,
-                                                       -1, share ? s_top : nullptr, share ? s_ntop : 0, 0, 0, 1 << 20,
-                                                       1 << 20, nullptr, p.fast_cap))
-        return;
+    const bool fits = build_tile_list<kBeamCap, kFrontCap, kPixCap>(
+        p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], nullptr, -1, share ? s_top : nullptr,
+        share ? s_ntop : 0, 0, 0, 1 << 20, 1 << 20, nullptr, p.fast_cap);
+    if (lane == 0 && p.tile_queue) {  // every tile that can be hit (lane 0 wrote the header)
+        if (!fits || p.tile_hdr[size_t(vc.tile_base) + b].cnt != 0)
+            p.tile_queue[atomicAdd(p.tile_queue_count, 1)] = make_int2(int(blockIdx.y), b);
+    }
+    if (fits) return;
     if (lane == 0) {
         p.tile_hdr[size_t(vc.tile_base) + b] = TileHdr{0, -1, -1, 0};
         const int i = atomicAdd(p.big_count, 1);
@@ -845,6 +855,42 @@ __device__ __forceinline__ double pixel_loss_adjoint(const Params& p, const View
     return a;
 }
 
+// The pixels of empty beam tiles in a queue-mode loss call (spp 16): no
+// triangle can cover them, so every sample misses (k_trace wrote no hits) and
+// the pixel is the background mean, mask 0, with its loss and adjoint — the
+// same arithmetic as k_render's empty-tile path, streamed one thread per pixel.
+__global__ void __launch_bounds__(256) k_background(Params p) {
+    const ViewCall vc = p.calls[blockIdx.y];
+    const DevCamera& cam = p.cams[vc.slot];
+    const int W = cam.W, H = cam.H;
+    const int i = int(blockIdx.x) * 256 + int(threadIdx.x);
+    double loss_part = 0;
+    if (i < W * H) {
+        const int x = i % W, y = i / W;
+        const TileHdr th = p.tile_hdr[size_t(vc.tile_base) + (y / 4) * vc.tiles_x + x / 4];
+        if (th.cnt == 0) {
+            const size_t qi = p.pix_off[vc.slot] + size_t(i);
+            for (int c = 0; c < 3; ++c) {
+                double sum = 0;
+                for (int j = 0; j < 16; ++j) sum = sum + p.sc.bg[c];  // render.cpp:48-57, sample order
+                const double mean = sum / 16.0;
+                p.img[3 * qi + c] = mean;
+                pixel_loss_adjoint(p, vc, qi, c, mean, loss_part);
+            }
+            p.mask[qi] = 0.0;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) loss_part += __shfl_xor_sync(0xffffffffu, loss_part, o);
+    __shared__ double s_l[8];
+    if ((threadIdx.x & 31) == 0) s_l[threadIdx.x >> 5] = loss_part;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0;
+        for (int w = 0; w < 8; ++w) tot += s_l[w];
+        if (tot != 0) atomicAdd(&p.loss_acc[vc.slot], tot);
+    }
+}
+
 template <bool kShade, bool kLoss, bool kInterior, int kSPP>
 __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
                                   kSPP == 16 ? CDR_RENDER_CTAS16
@@ -860,16 +906,26 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     __shared__ double s_ts[kTexState][kRT];  // interior_scatter's texel state
     __shared__ double s_ray[kInterior ? 5 : 1][kRT];  // dir, b1, b2 of the sample, for the scatter's late uses
 
-    const ViewCall vc = p.calls[blockIdx.z];
+    constexpr bool kQueue = kSPP == 16 && kShade && kLoss;  // may run over the tile queue
+    int cx = int(blockIdx.x), cy = int(blockIdx.y), cz = int(blockIdx.z);
+    if (kQueue && p.queue_mode) {  // CTA = (non-empty tile, pixel-row group) from k_tile_lists' queue
+        constexpr int kCPT = 4 / (kRT / 64);  // CTAs per 4 x 4 tile
+        const int2 e = p.tile_queue[int(blockIdx.x) / kCPT];
+        cz = e.x;
+        const int tiles_x = p.calls[cz].tiles_x;
+        cx = e.y % tiles_x;
+        cy = (e.y / tiles_x) * kCPT + int(blockIdx.x) % kCPT;
+    }
+    const ViewCall vc = p.calls[cz];
     const DevCamera& cam = p.cams[vc.slot];
     const int W = cam.W, H = cam.H;
     const int tid = threadIdx.x;
     const int spp = kSPP ? kSPP : p.spp;
     const int TW = kSPP == 16 ? 4 : p.TW, TH = kSPP == 16 ? kRT / 64 : p.TH;
-    if (int(blockIdx.x) * TW >= W || int(blockIdx.y) * TH >= H) return;  // uniform per CTA
+    if (cx * TW >= W || cy * TH >= H) return;  // uniform per CTA
     const int P = kRT / spp;
     const int pix = tid / spp, s = tid - (tid / spp) * spp;
-    const int X0 = int(blockIdx.x) * TW, Y0 = int(blockIdx.y) * TH;
+    const int X0 = cx * TW, Y0 = cy * TH;
     const int x = X0 + pix % TW;
     const int y = Y0 + pix / TW;
     const bool valid = pix < P && x < W && y < H;
@@ -880,9 +936,12 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     // Empty beam tile (no candidate at all: k_trace wrote a miss for every
     // sample): warp 0 writes the 8 pixels' background mean, mask, loss and
     // adjoint straight away; no hit loads, no staging, no barrier.
-    if (kSPP == 16 && kShade && kLoss && p.use_beam) {
-        const TileHdr th = p.tile_hdr[size_t(vc.tile_base) + (Y0 / 4) * vc.tiles_x + int(blockIdx.x)];
+    if (kSPP == 16 && kShade && kLoss && p.use_beam && !p.queue_mode) {
+        const TileHdr th = p.tile_hdr[size_t(vc.tile_base) + (Y0 / 4) * vc.tiles_x + cx];
         if (th.cnt == 0) {
+#ifdef CDR_EXP_EMPTY_RETURN  // measurement only (wrong output): cost of the empty-tile path
+            return;
+#endif
             if (tid >= 32) return;
             double loss_part = 0;
             for (int item = tid; item < 3 * P; item += 32) {  // (pixel, channel) items
@@ -1363,6 +1422,22 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     if (trace && chunk_bytes > 0) chunk = int(std::max<size_t>(1, std::min<size_t>(n_views, chunk_bytes / per_view)));
     const int n_chunks = (n_views + chunk - 1) / chunk;
     const bool timed = after_trace != nullptr;
+    // Tile queue (loss calls at spp 16, one chunk): the shading kernel runs
+    // over the non-empty tiles only, the empty tiles' pixels go through
+    // k_background. The queue length is read back while k_trace runs (the
+    // host waits on a copy issued right after the list builders), so the
+    // shading grid is exact and the GPU does not idle. Cuts the launch and
+    // prologue of ~2/3 (cfg2) to ~9/10 (cfg4) of the shading CTAs.
+    const bool queue = p.skip_empty_hits && n_chunks == 1 && !std::getenv("CDR_NO_QUEUE");
+    if (queue) {
+        c->tile_queue.ensure(std::max(1, tile_total));
+        c->tile_queue_count.ensure(1);
+        if (!c->tile_queue_host) CDR_CUDA_CHECK(cudaHostAlloc(&c->tile_queue_host, sizeof(int), cudaHostAllocDefault));
+        if (!c->tile_queue_ev) CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->tile_queue_ev, cudaEventDisableTiming));
+        p.tile_queue = c->tile_queue.p;
+        p.tile_queue_count = c->tile_queue_count.p;
+        CDR_CUDA_CHECK(cudaMemsetAsync(p.tile_queue_count, 0, sizeof(int), c->stream));
+    }
     if (timed) {
         while (c->chunk_ev.size() < size_t(2 * n_chunks + 1)) {
             cudaEvent_t e;
@@ -1393,9 +1468,27 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
                 k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
             }
         }
+        if (queue) {
+            CDR_CUDA_CHECK(cudaMemcpyAsync(c->tile_queue_host, p.tile_queue_count, sizeof(int), cudaMemcpyDeviceToHost,
+                                           c->stream));
+            CDR_CUDA_CHECK(cudaEventRecord(c->tile_queue_ev, c->stream));
+        }
         if (trace) launch_trace_kernel(pc, grid, c);
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k + 1], c->stream));
-        launch_render_kernel(pc, grid, c, trace, loss, interior);
+        if (queue) {
+            CDR_CUDA_CHECK(cudaEventSynchronize(c->tile_queue_ev));
+            const int nq = *c->tile_queue_host;
+            pc.queue_mode = 1;
+            constexpr int kCPT = 4 / (kRenderThreads16 / 64);
+            if (nq > 0) {
+                ++c->launches;
+                launch_render_kernel_t<16>(pc, dim3(unsigned(nq) * kCPT, 1, 1), c, trace, loss, interior);
+            }
+            ++c->launches;
+            k_background<<<dim3((maxW * maxH + 255) / 256, nv), 256, 0, c->stream>>>(pc);
+        } else {
+            launch_render_kernel(pc, grid, c, trace, loss, interior);
+        }
     }
     if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * n_chunks], c->stream));
     if (p.use_beam) {
