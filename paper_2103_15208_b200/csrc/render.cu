@@ -609,25 +609,11 @@ __global__ void __launch_bounds__(kSPP == 16 ? kTraceThreads16 : kThreads,
 #ifdef CDR_EXP_TRACE_NOP  // measurement only (wrong output): launch cost of the grid
     return;
 #endif
+    const ViewCall vc = p.calls[blockIdx.z];
+    const DevCamera cam = p.cams[vc.slot];
     // spp 16: kTraceItems consecutive tile columns per CTA (no barriers, so an
     // item's early returns just end that item)
     constexpr int kItems = kSPP == 16 ? kTraceItems : 1;
-    if (kBeam && kSPP == 16 && p.queue_mode) {  // items = (queued non-empty tile, CTA row group)
-        constexpr int kCPT = 4 / (kTraceThreads16 / 64);
-        const int nq = *p.tile_queue_count;
-#pragma unroll 1
-        for (int i = 0; i < kItems; ++i) {
-            const int it = int(blockIdx.x) * kItems + i;
-            if (it >= nq * kCPT) return;
-            const int2 e = p.tile_queue[it / kCPT];
-            const ViewCall vc = p.calls[e.x];
-            const DevCamera cam = p.cams[vc.slot];
-            trace_item<kBeam, kSPP>(p, vc, cam, e.y % vc.tiles_x, (e.y / vc.tiles_x) * kCPT + it % kCPT);
-        }
-        return;
-    }
-    const ViewCall vc = p.calls[blockIdx.z];
-    const DevCamera cam = p.cams[vc.slot];
 #pragma unroll 1
     for (int i = 0; i < kItems; ++i) trace_item<kBeam, kSPP>(p, vc, cam, int(blockIdx.x) * kItems + i, int(blockIdx.y));
 }
@@ -1487,25 +1473,11 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
                                            c->stream));
             CDR_CUDA_CHECK(cudaEventRecord(c->tile_queue_ev, c->stream));
         }
-        int nq = 0;
-        if (queue && trace && !std::getenv("CDR_NO_TRACE_QUEUE")) {  // k_trace over the queue too
-            CDR_CUDA_CHECK(cudaEventSynchronize(c->tile_queue_ev));
-            nq = *c->tile_queue_host;
-            Params pt = pc;
-            pt.queue_mode = 1;
-            constexpr int kCPT = 4 / (kTraceThreads16 / 64);
-            if (nq > 0) {
-                ++c->launches;
-                k_trace<true, 16><<<(unsigned(nq) * kCPT + kTraceItems - 1) / kTraceItems, kTraceThreads16, 0,
-                                    c->stream>>>(pt);
-            }
-        } else if (trace) {
-            launch_trace_kernel(pc, grid, c);
-        }
+        if (trace) launch_trace_kernel(pc, grid, c);
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k + 1], c->stream));
         if (queue) {
             CDR_CUDA_CHECK(cudaEventSynchronize(c->tile_queue_ev));
-            nq = *c->tile_queue_host;
+            const int nq = *c->tile_queue_host;
             pc.queue_mode = 1;
             constexpr int kCPT = 4 / (kRenderThreads16 / 64);
             if (nq > 0) {
