@@ -21,6 +21,8 @@
 // Tiles with more than kBeamCap candidates fall back to per-ray traversal.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "bvh.cuh"
 
 namespace cdr {
@@ -44,15 +46,39 @@ static_assert(kPixCap < 255 && kBigPixCap < 255, "255 marks an overflowed pixel 
 static_assert(kPixCap % 4 == 0 && kBigPixCap % 4 == 0, "lists are read four entries per 32-bit load");
 constexpr int kFrontCap = CDR_FRONT_CAP;  // builder frontier per tile; more -> per-ray traversal
 
-// Candidate record (48 B): three edge functions E_i = A_i x + B_i y + C_i
-// (pixel coordinates relative to the tile origin, margin folded into C_i;
-// E_i >= 0 for all i -> possible hit), the distance bound, the leaf index and
-// flags (bit 0: always run the exact test).
+// Candidate record, 32 B = one sector (the list scans are L1-bandwidth bound:
+// 48-B records measured the boundary probes at 72 % L1 throughput): the
+// distance bound, the leaf index with the "always run the exact test" flag in
+// bit 31, and three edge functions E_i = A_i x + B_i y + C_i in pixels
+// relative to the tile origin, normalised by the edge length (|A|, |B| <= 1),
+// E_i >= 0 for all i -> possible hit. A and B are stored as fp16; C (fp32,
+// rounded up) carries the 0.01 px margin plus the fp16 rounding error of A and
+// B over the tile (|dA| TW + |dB| TH), so the test stays conservative.
 struct __align__(16) BeamCand {
-    float4 e0;  // A0 B0 C0 A1
-    float4 e1;  // B1 C1 A2 B2
-    float4 e2;  // C2 dmin leaf flags
+    float4 a;  // dmin, leaf | flag << 31, half2 (A0, B0), half2 (A1, B1)
+    float4 b;  // half2 (A2, B2), C0, C1, C2
 };
+
+__device__ __forceinline__ float2 cand_ab(float f) {
+    const unsigned u = __float_as_uint(f);
+    return make_float2(__half2float(__ushort_as_half((unsigned short)(u & 0xffffu))),
+                       __half2float(__ushort_as_half((unsigned short)(u >> 16))));
+}
+__device__ __forceinline__ bool cand_always(const float4& a) { return __float_as_int(a.y) < 0; }
+__device__ __forceinline__ int cand_leaf(const float4& a) { return __float_as_int(a.y) & 0x7fffffff; }
+// edge coefficients A[3], B[3], C[3] of a record
+__device__ __forceinline__ void cand_edges(const float4& a, const float4& b, float A[3], float B[3], float C[3]) {
+    const float2 e0 = cand_ab(a.z), e1 = cand_ab(a.w), e2 = cand_ab(b.x);
+    A[0] = e0.x; B[0] = e0.y; C[0] = b.y;
+    A[1] = e1.x; B[1] = e1.y; C[1] = b.z;
+    A[2] = e2.x; B[2] = e2.y; C[2] = b.w;
+}
+// the 2D test at tile-relative point (x, y)
+__device__ __forceinline__ bool cand_covers(const float4& a, const float4& b, float x, float y) {
+    if (cand_always(a)) return true;
+    const float2 e0 = cand_ab(a.z), e1 = cand_ab(a.w), e2 = cand_ab(b.x);
+    return e0.x * x + e0.y * y + b.y >= 0.0f && e1.x * x + e1.y * y + b.z >= 0.0f && e2.x * x + e2.y * y + b.w >= 0.0f;
+}
 
 struct TileHdr {
     int off;  // first candidate in the pool; split tiles: index of their 4 quadrant lists
@@ -123,9 +149,10 @@ __device__ __forceinline__ bool box_outside(const FrustumPlanes& fp, const float
 // pixel rectangle [x0,x0+1]x[y0,y0+1] (tile-relative): false only if one edge
 // function is negative on all four corners.
 __device__ __forceinline__ bool cand_overlaps_pixel(const BeamCand& c, float x0, float y0) {
-    if (__float_as_int(c.e2.w) & 1) return true;
+    if (cand_always(c.a)) return true;
     const float x1 = x0 + 1.0f, y1 = y0 + 1.0f;
-    const float A[3] = {c.e0.x, c.e0.w, c.e1.z}, B[3] = {c.e0.y, c.e1.x, c.e1.w}, C[3] = {c.e0.z, c.e1.y, c.e2.x};
+    float A[3], B[3], C[3];
+    cand_edges(c.a, c.b, A, B, C);
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
         const float m = A[i] * (A[i] > 0 ? x1 : x0) + B[i] * (B[i] > 0 ? y1 : y0) + C[i];
@@ -139,8 +166,9 @@ __device__ __forceinline__ bool cand_overlaps_pixel(const BeamCand& c, float x0,
 // pixel as cand_overlaps_pixel, so the same decisions.
 __device__ __forceinline__ unsigned cand_pixel_mask(const BeamCand& c, int TW, int P) {
     const unsigned all = P >= 32 ? 0xffffffffu : ((1u << P) - 1u);
-    if (__float_as_int(c.e2.w) & 1) return all;
-    const float A[3] = {c.e0.x, c.e0.w, c.e1.z}, B[3] = {c.e0.y, c.e1.x, c.e1.w}, C[3] = {c.e0.z, c.e1.y, c.e2.x};
+    if (cand_always(c.a)) return all;
+    float A[3], B[3], C[3];
+    cand_edges(c.a, c.b, A, B, C);
     unsigned m = 0;
     int qx = 0, qy = 0;
     for (int q = 0; q < P; ++q) {
@@ -167,15 +195,12 @@ __device__ __forceinline__ Hit trace_beam(const BeamCand* __restrict__ cand, int
                                           D3 o, D3 d, double t_min, float px, float py) {
     Hit best{-1, 1e300, 0.0, 0.0};
     for (int k = 0; k < n; ++k) {
-        // the whole 48-B record in one round trip (the edge functions are
+        // the whole 32-B record in one round trip (the edge functions are
         // needed unless the bound stops the scan)
-        const float4 e2 = cand[k].e2, e0 = cand[k].e0, e1 = cand[k].e1;
-        if (double(e2.y) > best.t) break;  // every remaining candidate is farther
+        const float4 ra = cand[k].a, rb = cand[k].b;
+        if (double(ra.x) > best.t) break;  // every remaining candidate is farther
         CDR_STAT(3, 1);
-        const bool pass = (__float_as_int(e2.w) & 1) ||
-                          (e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
-                           e1.z * px + e1.w * py + e2.x >= 0.0f);
-        if (pass) leaf_test(recs, __float_as_int(e2.z), o, d, t_min, best);
+        if (cand_covers(ra, rb, px, py)) leaf_test(recs, cand_leaf(ra), o, d, t_min, best);
     }
     return best;
 }
@@ -190,13 +215,10 @@ __device__ __forceinline__ Hit trace_beam_list(const BeamCand* __restrict__ cand
         if ((j & 3) == 0) iw = __ldg(reinterpret_cast<const unsigned*>(idx + j));
         const int k = int((iw >> (8 * (j & 3))) & 0xffu);
         CDR_DCHECK(k < 255);
-        const float4 e2 = cand[k].e2, e0 = cand[k].e0, e1 = cand[k].e1;
-        if (double(e2.y) > best.t) break;
+        const float4 ra = cand[k].a, rb = cand[k].b;
+        if (double(ra.x) > best.t) break;
         CDR_STAT(3, 1);
-        const bool pass = (__float_as_int(e2.w) & 1) ||
-                          (e0.x * px + e0.y * py + e0.z >= 0.0f && e0.w * px + e1.x * py + e1.y >= 0.0f &&
-                           e1.z * px + e1.w * py + e2.x >= 0.0f);
-        if (pass) leaf_test(recs, __float_as_int(e2.z), o, d, t_min, best);
+        if (cand_covers(ra, rb, px, py)) leaf_test(recs, cand_leaf(ra), o, d, t_min, best);
     }
     return best;
 }
@@ -323,15 +345,12 @@ __device__ __forceinline__ void probe_step(ProbeScan& s, const TriRec* __restric
     }
     ++s.j;
     CDR_PSTAT(6, 1);
-    const float4 e2 = s.cand[k].e2, e0 = s.cand[k].e0, e1 = s.cand[k].e1;
-    if (double(e2.y) > s.best.t) {  // every remaining candidate is farther
+    const float4 ra = s.cand[k].a, rb = s.cand[k].b;
+    if (double(ra.x) > s.best.t) {  // every remaining candidate is farther
         s.mode = 0;
         return;
     }
-    const bool pass = (__float_as_int(e2.w) & 1) ||
-                      (e0.x * s.lx + e0.y * s.ly + e0.z >= 0.0f && e0.w * s.lx + e1.x * s.ly + e1.y >= 0.0f &&
-                       e1.z * s.lx + e1.w * s.ly + e2.x >= 0.0f);
-    if (pass) leaf_test(recs, __float_as_int(e2.z), o, d, t_min, s.best);
+    if (cand_covers(ra, rb, s.lx, s.ly)) leaf_test(recs, cand_leaf(ra), o, d, t_min, s.best);
 }
 
 __device__ __forceinline__ void trace_points2(const BeamView& bv, int vi, const DevCamera& cam, const BNode* nodes,

@@ -278,18 +278,26 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
         const double area2 = (sx[1] - sx[0]) * (sy[2] - sy[0]) - (sx[2] - sx[0]) * (sy[1] - sy[0]);
         if (!(fabs(area2) > 1e-9)) flags = 1;
         const double sg = area2 < 0 ? -1.0 : 1.0;
-        float E[9];
-        for (int k = 0; k < 3; ++k) {  // E = cross(edge, point - start) >= -0.01 px * |edge|
+        unsigned ab[3] = {0, 0, 0};
+        float cc[3] = {0, 0, 0};
+        for (int k = 0; k < 3 && !flags; ++k) {
+            // E = cross(edge, point - start) / |edge| >= -0.01 px: a signed
+            // distance in pixels (|A|, |B| <= 1), so fp16 A, B lose < 2.5e-4
+            // each; that rounding over the tile is added to C (rounded up)
             const int j = k == 2 ? 0 : k + 1;
             const double dx = sx[j] - sx[k], dy = sy[j] - sy[k];
-            E[3 * k] = float(-dy * sg);
-            E[3 * k + 1] = float(dx * sg);
-            E[3 * k + 2] = float((dy * sx[k] - dx * sy[k]) * sg + 0.01 * sqrt(dx * dx + dy * dy));
+            const double len = sqrt(dx * dx + dy * dy);  // > 0: area2 > 1e-9 here
+            const double A = -dy * sg / len, B = dx * sg / len;
+            const __half ha = __double2half(A), hb = __double2half(B);
+            const double slack = fabs(A - double(__half2float(ha))) * double(p.TW) +
+                                 fabs(B - double(__half2float(hb))) * double(p.TH);
+            ab[k] = unsigned(__half_as_ushort(ha)) | (unsigned(__half_as_ushort(hb)) << 16);
+            cc[k] = __double2float_ru((dy * sx[k] - dx * sy[k]) * sg / len + 0.01 + slack);
         }
         BeamCand bc;
-        bc.e0 = make_float4(E[0], E[1], E[2], E[3]);
-        bc.e1 = make_float4(E[4], E[5], E[6], E[7]);
-        bc.e2 = make_float4(E[8], di, __int_as_float(leaf), __int_as_float(flags));
+        bc.a = make_float4(di, __int_as_float(leaf | (flags ? int(0x80000000u) : 0)), __uint_as_float(ab[0]),
+                           __uint_as_float(ab[1]));
+        bc.b = make_float4(__uint_as_float(ab[2]), cc[0], cc[1], cc[2]);
         s_cand[rank] = bc;
     }
     __syncwarp();  // orders the lanes' pool writes for the per-pixel pass

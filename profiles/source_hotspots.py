@@ -40,7 +40,31 @@ def hotspots(rep, kern, top=25):
     return res
 
 
+def stall_totals(rep, kern):
+    """Kernel-wide warp-stall samples by reason (sums of the SASS rows)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}", "--print-source",
+                          "sass"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = next(r for r in rows if r and r[0] == "Address")
+    tot = {}
+    for r in rows[rows.index(hdr) + 1:]:
+        if len(r) != len(hdr):
+            continue
+        for h, v in zip(hdr, r):
+            if h.startswith("stall_"):
+                try:
+                    tot[h] = tot.get(h, 0) + int(v or 0)
+                except ValueError:
+                    pass
+    s = sum(tot.values()) or 1
+    return {k: round(100 * v / s, 1) for k, v in sorted(tot.items(), key=lambda x: -x[1]) if v}
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 3 and sys.argv[3] == "--stalls":
+        for k, v in stall_totals(sys.argv[1], sys.argv[2]).items():
+            print(f"{v:5.1f}%  {k}")
+        sys.exit(0)
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
     for x in hotspots(sys.argv[1], sys.argv[2], top):
         print(f"{x['pct']:5.1f}%  {x['file']}:{x['line']:<5d} {x['source']}")
