@@ -286,13 +286,13 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
             // each; that rounding over the tile is added to C (rounded up)
             const int j = k == 2 ? 0 : k + 1;
             const double dx = sx[j] - sx[k], dy = sy[j] - sy[k];
-            const double len = sqrt(dx * dx + dy * dy);  // > 0: area2 > 1e-9 here
-            const double A = -dy * sg / len, B = dx * sg / len;
+            const double inv = sg / sqrt(dx * dx + dy * dy);  // |edge| > 0: area2 > 1e-9 here
+            const double A = -dy * inv, B = dx * inv;
             const __half ha = __double2half(A), hb = __double2half(B);
             const double slack = fabs(A - double(__half2float(ha))) * double(p.TW) +
                                  fabs(B - double(__half2float(hb))) * double(p.TH);
             ab[k] = unsigned(__half_as_ushort(ha)) | (unsigned(__half_as_ushort(hb)) << 16);
-            cc[k] = __double2float_ru((dy * sx[k] - dx * sy[k]) * sg / len + 0.01 + slack);
+            cc[k] = __double2float_ru((dy * sx[k] - dx * sy[k]) * inv + 0.01 + slack);
         }
         BeamCand bc;
         bc.a = make_float4(di, __int_as_float(leaf | (flags ? int(0x80000000u) : 0)), __uint_as_float(ab[0]),
@@ -475,10 +475,6 @@ __global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_l
     const bool fits = build_tile_list<kBeamCap, kFrontCap, kPixCap>(
         p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], nullptr, -1, share ? s_top : nullptr,
         share ? s_ntop : 0, 0, 0, 1 << 20, 1 << 20, nullptr, p.fast_cap);
-    if (lane == 0 && p.tile_queue) {  // every tile that can be hit (lane 0 wrote the header)
-        if (!fits || p.tile_hdr[size_t(vc.tile_base) + b].cnt != 0)
-            p.tile_queue[atomicAdd(p.tile_queue_count, 1)] = make_int2(int(blockIdx.y), b);
-    }
     if (fits) return;
     if (lane == 0) {
         p.tile_hdr[size_t(vc.tile_base) + b] = TileHdr{0, -1, -1, 0};
@@ -861,6 +857,81 @@ __device__ __forceinline__ double pixel_loss_adjoint(const Params& p, const View
     }
     p.adj[3 * qi + c] = a;
     return a;
+}
+
+// Tile queue by stream compaction of the final tile headers (after the list
+// passes): every tile with cnt != 0 (candidates, split, or per-ray) in tile
+// order — raster order per view, views in call order, as the full grid — so
+// the shading kernel keeps the full grid's locality. Three small kernels:
+// per-block counts of 1,024 tiles, one scan, in-order writes.
+constexpr int kQBlock = 1024;
+__global__ void __launch_bounds__(256) k_queue_count(const TileHdr* __restrict__ hdr, int n, int* __restrict__ cnt) {
+    int c = 0;
+    for (int k = 0; k < 4; ++k) {
+        const int t = int(blockIdx.x) * kQBlock + k * 256 + int(threadIdx.x);
+        c += t < n && hdr[t].cnt != 0;
+    }
+    __shared__ int s[8];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) cnt[blockIdx.x] = s[0] + s[1] + s[2] + s[3] + s[4] + s[5] + s[6] + s[7];
+}
+
+__global__ void __launch_bounds__(1024) k_queue_scan(int* __restrict__ cnt, int nb, int* __restrict__ total) {
+    __shared__ int ws[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int carry = 0;
+    for (int base = 0; base < nb; base += 1024) {
+        const int i = base + int(threadIdx.x);
+        const int v = i < nb ? cnt[i] : 0;
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) ws[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int t = ws[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, t, o);
+                if (lane >= o) t += y;
+            }
+            ws[lane] = t;
+        }
+        __syncthreads();
+        if (i < nb) cnt[i] = carry + (w > 0 ? ws[w - 1] : 0) + x - v;  // exclusive
+        carry += ws[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(256) k_queue_write(Params p, int n, int n_calls, const int* __restrict__ off) {
+    __shared__ int s[8];
+    int base = off[blockIdx.x];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int k = 0; k < 4; ++k) {
+        const int t = int(blockIdx.x) * kQBlock + k * 256 + int(threadIdx.x);
+        const bool on = t < n && p.tile_hdr[t].cnt != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, on);
+        if (lane == 0) s[w] = __popc(bal);
+        __syncthreads();
+        int before = base;
+        for (int j = 0; j < w; ++j) before += s[j];
+        if (on) {
+            int lo = 0, hi = n_calls - 1;  // the call whose tiles hold t
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (p.calls[mid].tile_base <= t) lo = mid;
+                else hi = mid - 1;
+            }
+            p.tile_queue[before + __popc(bal & ((1u << lane) - 1u))] = make_int2(lo, t - p.calls[lo].tile_base);
+        }
+        for (int j = 0; j < 8; ++j) base += s[j];
+        __syncthreads();
+    }
 }
 
 // The pixels of empty beam tiles in a queue-mode loss call (spp 16): no
@@ -1439,12 +1510,11 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     const bool queue = p.skip_empty_hits && n_chunks == 1 && !std::getenv("CDR_NO_QUEUE");
     if (queue) {
         c->tile_queue.ensure(std::max(1, tile_total));
-        c->tile_queue_count.ensure(1);
+        c->tile_queue_count.ensure(1 + (tile_total + kQBlock - 1) / kQBlock);  // [0] total, then per-block offsets
         if (!c->tile_queue_host) CDR_CUDA_CHECK(cudaHostAlloc(&c->tile_queue_host, sizeof(int), cudaHostAllocDefault));
         if (!c->tile_queue_ev) CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->tile_queue_ev, cudaEventDisableTiming));
         p.tile_queue = c->tile_queue.p;
         p.tile_queue_count = c->tile_queue_count.p;
-        CDR_CUDA_CHECK(cudaMemsetAsync(p.tile_queue_count, 0, sizeof(int), c->stream));
     }
     if (timed) {
         while (c->chunk_ev.size() < size_t(2 * n_chunks + 1)) {
@@ -1477,6 +1547,12 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             }
         }
         if (queue) {
+            const int nb = (tile_total + kQBlock - 1) / kQBlock;
+            int* blk = pc.tile_queue_count + 1;
+            c->launches += 3;
+            k_queue_count<<<nb, 256, 0, c->stream>>>(pc.tile_hdr, tile_total, blk);
+            k_queue_scan<<<1, 1024, 0, c->stream>>>(blk, nb, pc.tile_queue_count);
+            k_queue_write<<<nb, 256, 0, c->stream>>>(pc, tile_total, nv, blk);
             CDR_CUDA_CHECK(cudaMemcpyAsync(c->tile_queue_host, p.tile_queue_count, sizeof(int), cudaMemcpyDeviceToHost,
                                            c->stream));
             CDR_CUDA_CHECK(cudaEventRecord(c->tile_queue_ev, c->stream));
