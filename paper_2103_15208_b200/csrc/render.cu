@@ -633,6 +633,62 @@ using RedT = float;
 using RedT = double;
 #endif
 
+// ---- group sums on the fp64 tensor core ------------------------------------
+// Per warp, the scatter sums kC weighted copies of a kV-vector u (kV <= 8) over
+// the lanes of each group (lanes sharing a texel quad or a triangle): corner c
+// of group m receives sum_s [gid(s) == m] w_c(s) u(s). With ng <= 8 groups that
+// is, per corner, S_c[8 x 8] = A_c[8 x 32] U[32 x 8] with A_c = group membership
+// times the corner weight: eight m8n8k4 fp64 MMAs (exact fp64 products and
+// sums), the kC corners as independent accumulator chains sharing U's B
+// fragments — instead of log-depth shuffle trees over every value (2 SHFL per
+// double per round). U goes through the warp's dead shared memory (column n =
+// 32 doubles, rotated by 4n so a fragment load hits 16 bank pairs); lane l ends
+// with S_c[l >> 2][2 (l & 3)] and S_c[l >> 2][2 (l & 3) + 1].
+__device__ __forceinline__ void mma_f64_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// column n of this warp's U: s_rad's slice for n < 3, s_ray[n - 3]'s after
+template <int kRT>
+__device__ __forceinline__ double* ucol(double (&s_rad)[kRT][3], double (&s_ray)[5][kRT], int w32, int n) {
+    return n < 3 ? &s_rad[w32][0] + 32 * n : &s_ray[n - 3][w32];
+}
+
+template <int kV, int kC, int kRT, typename Wf>
+__device__ __forceinline__ void group_sum_mma(double (&s_rad)[kRT][3], double (&s_ray)[5][kRT], int w32,
+                                              const double (&u)[kV], int gid, int lane, Wf weight,
+                                              double (&s0)[kC], double (&s1)[kC]) {
+    __syncwarp();  // the lanes' earlier reads of these slices are done
+#pragma unroll
+    for (int n = 0; n < kV; ++n) ucol<kRT>(s_rad, s_ray, w32, n)[(lane + 4 * n) & 31] = u[n];
+    __syncwarp();
+    const int m = lane >> 2, k = lane & 3;
+    const double* col = m < kV ? ucol<kRT>(s_rad, s_ray, w32, m) : nullptr;
+#pragma unroll
+    for (int c = 0; c < kC; ++c) s0[c] = s1[c] = 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+        const int src = 4 * t + k;
+        const bool in = __shfl_sync(0xffffffffu, gid, src) == m;  // A: membership of sample src in group m
+        const double b = col ? col[(src + 4 * m) & 31] : 0.0;     // B: U[src][m]
+#pragma unroll
+        for (int c = 0; c < kC; ++c) mma_f64_8x8x4(s0[c], s1[c], in ? weight(c, src) : 0.0, b);
+    }
+    __syncwarp();  // U is rewritten by the next call
+}
+
+// Dense group ids of a match_any grouping over the active lanes: gid in
+// [0, ng) by leader order, 15 for inactive lanes; ng > 8 -> the caller falls
+// back to the shuffle reduction. leader_of(m) = lane of group m's leader.
+__device__ __forceinline__ int group_ids(bool act, unsigned peers, int lane, unsigned& leaders, int& ng) {
+    const int leader = __ffs(peers) - 1;
+    leaders = __ballot_sync(0xffffffffu, act && leader == lane);
+    ng = __popc(leaders);
+    return act ? __popc(leaders & ((1u << leader) - 1u)) : 15;
+}
+
 // Phase 3 of k_render: the interior adjoint of one sample (diff_render.cpp:78-184).
 // The 4 bilinear weights of the texel scatter, staged per thread in shared
 // memory (transposed: lane-consecutive, conflict-free). The scatter loop
@@ -644,7 +700,8 @@ constexpr int kTexState = 4;
 template <int kRT>
 __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x, int y, int spp, int tri, double t,
                                               double b1, double b2, D3 dir, D3 a, bool act,
-                                              double (&s_ts)[kTexState][kRT], const double (&s_ray)[5][kRT]) {
+                                              double (&s_ts)[kTexState][kRT], double (&s_ray)[5][kRT],
+                                              double (&s_rad)[kRT][3]) {
     a = (spp & (spp - 1)) == 0 ? a * (1.0 / spp) : a / double(spp);  // diff_render.cpp:82 (x/2^n exact as x*2^-n)
 
     // Compute everything the scatter needs first, so the large temporaries
@@ -776,7 +833,44 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
     }
     // intersection response + normal-chain input, per triangle corner
     // (diff_render.cpp:170-184; the chain itself is applied in finalize.cu)
+#if !defined(CDR_SCATTER_SHFL) && !defined(CDR_REDUCE_F32)
+    // U columns for group_sum_mma: this warp's slices of s_rad (dead after
+    // phase 2) and s_ray[0..2] (the direction, dead now); s_ray[3..4] (b1, b2)
+    // are the position corners' weights and become U's 7th column afterwards
+    const int w32 = tid & ~31;
+    unsigned pleaders = 0, tleaders = 0;
+    int png = 0, tng = 0;
+    const int pkey = pact ? tri : -1 - lane, tkey = act ? tex0 : -1 - lane;
+    const unsigned ppeers = __match_any_sync(0xffffffffu, pkey), tpeers = __match_any_sync(0xffffffffu, tkey);
+    const int pgid = group_ids(pact, ppeers, lane, pleaders, png);
+    const int tgid = group_ids(act, tpeers, lane, tleaders, tng);
+    const int gm = lane >> 2, n0 = 2 * (lane & 3);
+    __syncwarp();  // every lane is past its s_ray[0..2] reads before U overwrites them
+#endif
 #ifndef CDR_EXP_NO_POS
+#if !defined(CDR_SCATTER_SHFL) && !defined(CDR_REDUCE_F32)
+    if (png <= 8) {  // warp-uniform
+        const int ltri = __shfl_sync(0xffffffffu, tri, gm < png ? __fns(pleaders, 0, gm + 1) : 0);
+        double u[6] = {gc.x, gc.y, gc.z, hm.x, hm.y, hm.z};
+        if (!pact)
+            for (int i = 0; i < 6; ++i) u[i] = 0;
+        const double* sb1 = &s_ray[3][w32];
+        const double* sb2 = &s_ray[4][w32];
+        auto bw = [&](int j, int src) {  // barycentric of corner j (b0 as computed above)
+            const double r1 = sb1[src], r2 = sb2[src];
+            return j == 0 ? 1.0 - r1 - r2 : (j == 1 ? r1 : r2);
+        };
+        double s0[3], s1[3];
+        group_sum_mma<6, 3, kRT>(s_rad, s_ray, w32, u, pgid, lane, bw, s0, s1);
+        if (gm < png && n0 < 6)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                double* dst = p.corner + (size_t(ltri) * 3 + j) * 6 + n0;
+                if (s0[j] != 0) atomicAdd(dst, s0[j]);
+                if (s1[j] != 0) atomicAdd(dst + 1, s1[j]);
+            }
+    } else
+#endif
     {
         const int key = pact ? tri : -1 - lane;
         const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -799,6 +893,33 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
     }
 #endif
 #ifndef CDR_EXP_NO_TEXEL
+#if !defined(CDR_SCATTER_SHFL) && !defined(CDR_REDUCE_F32)
+    if (tng <= 8) {  // warp-uniform
+        const int ltex = __shfl_sync(0xffffffffu, tex0, gm < tng ? __fns(tleaders, 0, gm + 1) : 0);
+        const int tw = p.sc.tw, th = p.sc.th;
+        const int x0 = ltex % tw, y0 = ltex / tw;
+        const int x1 = x0 + 1 == tw ? 0 : x0 + 1, y1 = y0 + 1 == th ? 0 : y0 + 1;
+        double u[7] = {0, 0, 0, 0, 0, 0, 0};
+        if (act) {
+            for (int c = 0; c < 3; ++c) {
+                u[c] = aL[c] * wd0;
+                u[3 + c] = aL[c] * ws0;
+            }
+            u[6] = wr0;
+        }
+        auto tw4 = [&](int kq, int src) { return s_ts[kq][w32 + src]; };  // bilinear weight of corner kq
+        double s0[4], s1[4];
+        group_sum_mma<7, 4, kRT>(s_rad, s_ray, w32, u, tgid, lane, tw4, s0, s1);
+        if (gm < tng && n0 < 7)
+#pragma unroll
+            for (int kq = 0; kq < 4; ++kq) {
+                const int64_t tx = int64_t((kq < 2 ? y0 : y1)) * tw + ((kq & 1) ? x1 : x0);
+                TexAcc* dst = p.texacc + tx;
+                if (s0[kq] != 0) atomicAdd(&dst->v[n0], TexAccT(s0[kq]));
+                if (n0 + 1 < 7 && s1[kq] != 0) atomicAdd(&dst->v[n0 + 1], TexAccT(s1[kq]));
+            }
+    } else
+#endif
     {
         // texel scatter through the bilinear weights (diff_render.cpp:110-128)
         const int key = act ? tex0 : -1 - lane;
@@ -1147,7 +1268,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
 
     // ---------------- phase 3: interior adjoint scatter
     if constexpr (kInterior) {
-        if (__any_sync(0xffffffffu, act)) interior_scatter<kRT>(p, tid, x, y, spp, tri, t, b1, b2, dir, a, act, s_ts, s_ray);
+        if (__any_sync(0xffffffffu, act)) interior_scatter<kRT>(p, tid, x, y, spp, tri, t, b1, b2, dir, a, act, s_ts, s_ray, s_rad);
     }
 
     // ---------------- publish the CTA's tallies (warp 0 waits for the others)
