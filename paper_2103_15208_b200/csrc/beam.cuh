@@ -89,19 +89,36 @@ struct TileHdr {
 
 // A tile whose big-pass list overflows (> 255 candidates: silhouette-dense
 // tiles of thin geometry) is split into its four pixel quadrants, each with
-// its own candidate list (off, cnt; cnt -1: that quadrant traverses per ray).
-// The pixel lists of all four stay in the tile's big slot (pixel q's list
-// indexes its own quadrant's candidates), and the edge functions stay relative
-// to the tile origin, so a consumer only swaps the (off, cnt) it scans.
-__device__ __forceinline__ int tile_quadrant(int q, int TW, int TH) {
-    return (q / TW >= TH / 2 ? 2 : 0) + (q % TW >= TW / 2 ? 1 : 0);
-}
-
+// its own candidate list (off, cnt; cnt -1: that quadrant traverses per ray,
+// -2: split once more into its own quadrants, off = their group). The pixel
+// lists of every level stay in the tile's big slot (pixel q's list indexes
+// its own list's candidates), and the edge functions stay relative to the
+// tile origin, so a consumer only swaps the (off, cnt) it scans.
 // (first candidate, count) of the list pixel q of tile header h scans.
 __device__ __forceinline__ int2 pixel_tile_list(const TileHdr& h, const int2* __restrict__ split, int q, int TW,
                                                 int TH) {
     if (h.cnt != -2) return make_int2(h.off, h.cnt);
-    return split[4 * h.off + tile_quadrant(q, TW, TH)];
+    const int qx = q % TW, qy = q / TW;
+    int rx = 0, ry = 0, rw = TW, rh = TH, g = h.off;
+    while (true) {  // descend the quadrant splits (k_tile_lists_split): at most two levels
+        const int hw = rw / 2, hh = rh / 2;
+        const bool bx = qx - rx >= hw, by = qy - ry >= hh;
+        const int2 e = split[4 * g + (by ? 2 : 0) + (bx ? 1 : 0)];
+        if (e.y != -2) return e;
+        g = e.x;
+        if (bx) {
+            rx += hw;
+            rw -= hw;
+        } else {
+            rw = hw;
+        }
+        if (by) {
+            ry += hh;
+            rh -= hh;
+        } else {
+            rh = hh;
+        }
+    }
 }
 
 struct FrustumPlanes {

@@ -136,8 +136,8 @@ struct cdr_ctx {
     cdr::DBuf<int> beam_tile_base;
     cdr::DBuf<int2> beam_big_queue;  // tiles rebuilt with the big candidate cap
     cdr::DBuf<int> beam_big_count;   // [0] big queue, [1] split queue
-    cdr::DBuf<int> beam_split_queue;  // big-queue index of each split tile
-    cdr::DBuf<int2> beam_split_hdr;   // 4 quadrant lists per split tile
+    cdr::DBuf<int4> beam_split_queue;  // split work items (levels 0 and 1)
+    cdr::DBuf<int2> beam_split_hdr;    // groups of 4 quadrant lists
     cdr::DBuf<unsigned char> beam_big_pix_list, beam_big_pix_cnt;      // per view index of the last render call
     cdr::DBuf<int2> tile_queue;         // non-empty tiles (call, tile) of a queue-mode loss call
     cdr::DBuf<int> tile_queue_count;

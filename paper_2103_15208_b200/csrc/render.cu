@@ -70,14 +70,15 @@ struct Params {
     int use_beam;
     int fast_cap;     // candidate cap of the fast pass (kBeamCap; lower only to test the big pass)
     int big_list_cap;  // the same for the big pass (kBigCap; lower only to test the split pass)
+    int split_list_cap;  // the same for the level-0 quadrants (kBigCap; lower only to test level 1)
     int no_shared_top;  // 1: every tile walks the BVH from the root (A/B and tests)
     int2* big_queue;  // (call, tile) of the tiles over kBeamCap candidates
     int* big_count;
     int big_cap;
-    int* split_queue;  // big-queue index of the tiles over kBigCap candidates (split into quadrants)
-    int* split_count;
-    int split_cap;
-    int2* split_hdr;  // per split tile: 4 quadrant lists (first candidate, count; -1 = per ray)
+    int4* split_queue;  // split work: (big slot, packed rect, list group, level); level 0 = the big-pass overflows
+    int* split_count;   // [0] level-0 items, [1] level-1 items, [2] level-1 groups allocated
+    int split_cap;      // items per level
+    int2* split_hdr;    // groups of 4 quadrant lists (first candidate, count; -1 = per ray, -2 = split again)
     // tile queue (loss calls at spp 16): k_tile_lists appends every non-empty
     // tile (call, tile); k_render then runs over the queue only and
     // k_background writes the empty tiles' pixels
@@ -504,7 +505,7 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
                                                              p.big_list_cap) &&
             lane == 0) {
             const int j = atomicAdd(p.split_count, 1);  // split into quadrants (k_tile_lists_split)
-            if (j < p.split_cap) p.split_queue[j] = i;
+            if (j < p.split_cap) p.split_queue[j] = make_int4(i, p.TW << 16 | p.TH << 24, j, 0);
             else atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
         }
         __syncwarp();
@@ -512,33 +513,55 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_big(Params p) {
 }
 
 // Split pass: the tiles still over kBigCap candidates, one warp per
-// (tile, quadrant); the quadrants share the tile's big pixel-list slot. A
-// quadrant that still overflows is traced per ray (beam_fallback_tiles counts
-// such quadrants).
-__global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_split(Params p) {
+// (item, quadrant); every list of a tile shares the tile's big pixel-list slot.
+// Level 0 splits the tile into its 4 quadrants (list group j = the item's queue
+// position); a quadrant of more than one pixel that still overflows is split
+// once more by the level-1 launch (its entry {group, -2}, the 4 sub-quadrant
+// lists in a group allocated past the level-0 ones). What overflows after that
+// is traced per ray (beam_fallback_tiles counts those lists).
+__device__ __forceinline__ int4 split_item(int slot, int sx0, int sy0, int sw, int sh, int group, int level) {
+    return make_int4(slot, sx0 | sy0 << 8 | sw << 16 | sh << 24, group, level);
+}
+
+__global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_split(Params p, int level) {
     __shared__ __align__(8) int s_front[kBigWarps][2][kBigFront];
     __shared__ int s_leaf[kBigWarps][kBigCap];
     __shared__ float s_d[kBigWarps][kBigCap];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n = min(*p.split_count, p.split_cap);
-    const int hw = p.TW / 2, hh = p.TH / 2;
+    const int n = min(p.split_count[level], p.split_cap);
+    const int4* queue = p.split_queue + size_t(level) * p.split_cap;
     for (int it = blockIdx.x * kBigWarps + w; it < 4 * n; it += gridDim.x * kBigWarps) {
-        const int j = it >> 2, qd = it & 3;  // quadrant bits as tile_quadrant (beam.cuh)
-        const int i = p.split_queue[j];
+        const int4 item = queue[it >> 2];
+        const int qd = it & 3;  // quadrant bits as pixel_tile_list (beam.cuh)
+        const int i = item.x, g = item.z;
+        const int rx = item.y & 0xff, ry = (item.y >> 8) & 0xff, rw = (item.y >> 16) & 0xff, rh = item.y >> 24;
+        const int hw = rw / 2, hh = rh / 2;
+        const int sx0 = rx + ((qd & 1) ? hw : 0), sw = (qd & 1) ? rw - hw : hw;
+        const int sy0 = ry + ((qd & 2) ? hh : 0), sh = (qd & 2) ? rh - hh : hh;
         const int2 e = p.big_queue[i];
         const ViewCall vc = p.calls[e.x];
         const DevCamera& cam = p.cams[vc.slot];
-        const int sx0 = (qd & 1) ? hw : 0, sw = (qd & 1) ? p.TW - hw : hw;
-        const int sy0 = (qd & 2) ? hh : 0, sh = (qd & 2) ? p.TH - hh : hh;
-        int2* out = p.split_hdr + 4 * j + qd;
+        int2* out = p.split_hdr + 4 * size_t(g) + qd;
         if (!build_tile_list<kBigCap, kBigFront, kBigPixCap>(p, vc, cam, e.y, lane, s_front[w], s_leaf[w], s_d[w],
                                                              reinterpret_cast<unsigned long long*>(s_front[w]), i,
-                                                             nullptr, 0, sx0, sy0, sw, sh, out) &&
+                                                             nullptr, 0, sx0, sy0, sw, sh, out,
+                                                             level == 0 ? p.split_list_cap : kBigCap) &&
             lane == 0) {
-            *out = make_int2(0, -1);
-            atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+            int j2 = -1;
+            if (level == 0 && sw * sh > 1) {  // split this quadrant once more
+                j2 = atomicAdd(p.split_count + 1, 1);
+                if (j2 >= p.split_cap) j2 = -1;
+            }
+            if (j2 >= 0) {
+                const int g2 = p.split_cap + j2;
+                *out = make_int2(g2, -2);
+                p.split_queue[size_t(p.split_cap) + j2] = split_item(i, sx0, sy0, sw, sh, g2, 1);
+            } else {
+                *out = make_int2(0, -1);
+                atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+            }
         }
-        if (qd == 0 && lane == 0) p.tile_hdr[size_t(vc.tile_base) + e.y] = TileHdr{j, -2, i, 0};
+        if (level == 0 && qd == 0 && lane == 0) p.tile_hdr[size_t(vc.tile_base) + e.y] = TileHdr{g, -2, i, 0};
         __syncwarp();
     }
 }
@@ -1561,6 +1584,8 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     if (const char* e = std::getenv("CDR_BEAM_FAST_CAP")) p.fast_cap = std::max(0, std::min(kBeamCap, std::atoi(e)));
     p.big_list_cap = kBigCap;  // CDR_BEAM_BIG_CAP < kBigCap pushes big tiles to the split pass (tests)
     if (const char* e = std::getenv("CDR_BEAM_BIG_CAP")) p.big_list_cap = std::max(0, std::min(kBigCap, std::atoi(e)));
+    p.split_list_cap = kBigCap;
+    if (const char* e = std::getenv("CDR_BEAM_SPLIT_CAP")) p.split_list_cap = std::max(0, std::min(kBigCap, std::atoi(e)));
     c->beam_view.valid = 0;
     p.skip_empty_hits = p.use_beam && loss && a.spp == 16;
     if (c->beam_used_host) c->beam_used_last = *c->beam_used_host;  // previous call has completed
@@ -1585,11 +1610,11 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         // fit k_trace's staging buffer (P <= 64, spp >= 4)
         const int big_cap = P * kBigPixCap <= kThreads * kPixCap ? std::max(64, tile_total / 16) : 0;
         c->beam_big_queue.ensure(std::max(1, big_cap));
-        c->beam_big_count.ensure(2);  // big queue, split queue
+        c->beam_big_count.ensure(4);  // big queue, split queues of levels 0 and 1
         // CDR_NO_SPLIT (A/B): no split pass, its tiles traced per ray (and counted so)
         const int split_cap = big_cap > 0 && !std::getenv("CDR_NO_SPLIT") ? std::max(64, big_cap / 8) : 0;
-        c->beam_split_queue.ensure(std::max(1, split_cap));
-        c->beam_split_hdr.ensure(std::max<size_t>(4, 4 * size_t(split_cap)));
+        c->beam_split_queue.ensure(std::max<size_t>(1, 2 * size_t(split_cap)));  // two levels
+        c->beam_split_hdr.ensure(std::max<size_t>(4, 8 * size_t(split_cap)));    // 4 lists per group, 2 levels
         p.split_queue = c->beam_split_queue.p;
         p.split_count = c->beam_big_count.p + 1;
         p.split_cap = split_cap;
@@ -1657,14 +1682,15 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
 #else
             dim3 lgrid((tiles + kListWarps - 1) / kListWarps, nv);
 #endif
-            CDR_CUDA_CHECK(cudaMemsetAsync(pc.big_count, 0, 2 * sizeof(int), c->stream));
+            CDR_CUDA_CHECK(cudaMemsetAsync(pc.big_count, 0, 4 * sizeof(int), c->stream));
             ++c->launches;
             k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(pc);
             ++c->launches;
             k_tile_lists_big<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
             if (p.split_cap > 0) {
-                ++c->launches;
-                k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc);
+                c->launches += 2;
+                k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc, 0);
+                k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc, 1);
             }
         }
         if (queue) {

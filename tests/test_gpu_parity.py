@@ -344,8 +344,9 @@ def test_fp32_targets_equal_widened_fp64(sphere):
     assert rel_l2(out[0][1], out[1][1]) <= 1e-12
 
 
-@pytest.mark.parametrize("fast_cap,big_cap", [("0", None), ("3", None), ("3", "8"), ("0", "0")])
-def test_big_tile_lists_exact(sphere, monkeypatch, fast_cap, big_cap):
+@pytest.mark.parametrize("fast_cap,big_cap,split_cap", [("0", None, None), ("3", None, None), ("3", "8", None),
+                                                         ("0", "0", None), ("2", "4", "1"), ("0", "0", "0")])
+def test_big_tile_lists_exact(sphere, monkeypatch, fast_cap, big_cap, split_cap):
     """Tiles over the fast pass's candidate cap are rebuilt by the big pass
     (255 candidates, 128-entry pixel lists); tiles over that are split into
     quadrant lists (k_tile_lists_split). Forcing (almost) every tile through
@@ -354,6 +355,8 @@ def test_big_tile_lists_exact(sphere, monkeypatch, fast_cap, big_cap):
     monkeypatch.setenv("CDR_BEAM_FAST_CAP", fast_cap)
     if big_cap is not None:
         monkeypatch.setenv("CDR_BEAM_BIG_CAP", big_cap)
+    if split_cap is not None:  # level-0 quadrants overflow too: split once more (pixel lists)
+        monkeypatch.setenv("CDR_BEAM_SPLIT_CAP", split_cap)
     blob = blob_scene(freq=8, tex=32, views=2, image=48)
     for sc in (sphere, blob):
         r, o = _pair(sc)
@@ -425,7 +428,7 @@ def _silhouette_probe_points(o, v, rng, per_seg=8):
 
 
 @pytest.mark.parametrize("spp", [4, 16])
-@pytest.mark.parametrize("fast_cap", [None, "0", "split"])
+@pytest.mark.parametrize("fast_cap", [None, "0", "split", "split2"])
 def test_probe_points_through_lists_bit_exact(monkeypatch, spp, fast_cap):
     """The boundary probes of the fused loss call trace through the per-pixel
     candidate lists (trace_points2, beam.cuh), not per-ray traversal. After a
@@ -436,6 +439,10 @@ def test_probe_points_through_lists_bit_exact(monkeypatch, spp, fast_cap):
     if fast_cap == "split":  # every tile through the big pass, most of them split into quadrants
         monkeypatch.setenv("CDR_BEAM_FAST_CAP", "0")
         monkeypatch.setenv("CDR_BEAM_BIG_CAP", "6")
+    elif fast_cap == "split2":  # and most quadrants split once more
+        monkeypatch.setenv("CDR_BEAM_FAST_CAP", "0")
+        monkeypatch.setenv("CDR_BEAM_BIG_CAP", "6")
+        monkeypatch.setenv("CDR_BEAM_SPLIT_CAP", "2")
     elif fast_cap is not None:
         monkeypatch.setenv("CDR_BEAM_FAST_CAP", fast_cap)
     sc = blob_scene(freq=8, tex=16, views=2, image=64)
