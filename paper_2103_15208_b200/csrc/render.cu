@@ -673,43 +673,54 @@ __device__ __forceinline__ void mma_f64_8x8x4(double& d0, double& d1, double a, 
                  : "d"(a), "d"(b));
 }
 
+#ifndef CDR_MMA_UNROLL
+#define CDR_MMA_UNROLL 8
+#endif
+constexpr int kMmaUnroll = CDR_MMA_UNROLL;  // k-steps per unrolled body (code size vs loop overhead)
+
+
 // column n of this warp's U: s_rad's slice for n < 3, s_ray[n - 3]'s after
 template <int kRT>
 __device__ __forceinline__ double* ucol(double (&s_rad)[kRT][3], double (&s_ray)[5][kRT], int w32, int n) {
     return n < 3 ? &s_rad[w32][0] + 32 * n : &s_ray[n - 3][w32];
 }
 
+// mbase: this call sums groups mbase .. mbase + 7 (a second call with
+// mbase 8 and write_u false covers warps of up to 16 groups)
 template <int kV, int kC, int kRT, typename Wf>
 __device__ __forceinline__ void group_sum_mma(double (&s_rad)[kRT][3], double (&s_ray)[5][kRT], int w32,
                                               const double (&u)[kV], int gid, int lane, Wf weight,
-                                              double (&s0)[kC], double (&s1)[kC]) {
-    __syncwarp();  // the lanes' earlier reads of these slices are done
+                                              double (&s0)[kC], double (&s1)[kC], int mbase = 0,
+                                              bool write_u = true) {
+    if (write_u) {
+        __syncwarp();  // the lanes' earlier reads of these slices are done
 #pragma unroll
-    for (int n = 0; n < kV; ++n) ucol<kRT>(s_rad, s_ray, w32, n)[(lane + 4 * n) & 31] = u[n];
-    __syncwarp();
+        for (int n = 0; n < kV; ++n) ucol<kRT>(s_rad, s_ray, w32, n)[(lane + 4 * n) & 31] = u[n];
+        __syncwarp();
+    }
     const int m = lane >> 2, k = lane & 3;
     const double* col = m < kV ? ucol<kRT>(s_rad, s_ray, w32, m) : nullptr;
 #pragma unroll
     for (int c = 0; c < kC; ++c) s0[c] = s1[c] = 0.0;
-#pragma unroll
+#pragma unroll kMmaUnroll
     for (int t = 0; t < 8; ++t) {
         const int src = 4 * t + k;
-        const bool in = __shfl_sync(0xffffffffu, gid, src) == m;  // A: membership of sample src in group m
+        const bool in = __shfl_sync(0xffffffffu, gid, src) == m + mbase;  // A: sample src in group mbase + m
         const double b = col ? col[(src + 4 * m) & 31] : 0.0;     // B: U[src][m]
 #pragma unroll
         for (int c = 0; c < kC; ++c) mma_f64_8x8x4(s0[c], s1[c], in ? weight(c, src) : 0.0, b);
     }
-    __syncwarp();  // U is rewritten by the next call
+    __syncwarp();  // U is rewritten by the next call (the caller's reads of col are done)
 }
 
 // Dense group ids of a match_any grouping over the active lanes: gid in
-// [0, ng) by leader order, 15 for inactive lanes; ng > 8 -> the caller falls
+// [0, ng) by leader order, -1 for inactive lanes; ng > kMmaGroups -> the caller falls
 // back to the shuffle reduction. leader_of(m) = lane of group m's leader.
 __device__ __forceinline__ int group_ids(bool act, unsigned peers, int lane, unsigned& leaders, int& ng) {
     const int leader = __ffs(peers) - 1;
     leaders = __ballot_sync(0xffffffffu, act && leader == lane);
     ng = __popc(leaders);
-    return act ? __popc(leaders & ((1u << leader) - 1u)) : 15;
+    return act ? __popc(leaders & ((1u << leader) - 1u)) : -1;
 }
 
 // Phase 3 of k_render: the interior adjoint of one sample (diff_render.cpp:78-184).
@@ -872,8 +883,7 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
 #endif
 #ifndef CDR_EXP_NO_POS
 #if !defined(CDR_SCATTER_SHFL) && !defined(CDR_REDUCE_F32)
-    if (png <= 8) {  // warp-uniform
-        const int ltri = __shfl_sync(0xffffffffu, tri, gm < png ? __fns(pleaders, 0, gm + 1) : 0);
+    {  // groups of 8 per pass: a warp has <= 32 (4 passes at most, 1 in the common case)
         double u[6] = {gc.x, gc.y, gc.z, hm.x, hm.y, hm.z};
         if (!pact)
             for (int i = 0; i < 6; ++i) u[i] = 0;
@@ -883,17 +893,22 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             const double r1 = sb1[src], r2 = sb2[src];
             return j == 0 ? 1.0 - r1 - r2 : (j == 1 ? r1 : r2);
         };
-        double s0[3], s1[3];
-        group_sum_mma<6, 3, kRT>(s_rad, s_ray, w32, u, pgid, lane, bw, s0, s1);
-        if (gm < png && n0 < 6)
+#pragma unroll 1
+        for (int mb = 0; mb < png; mb += 8) {
+            const int g = mb + gm;
+            const int ltri = __shfl_sync(0xffffffffu, tri, g < png ? __fns(pleaders, 0, g + 1) : 0);
+            double s0[3], s1[3];
+            group_sum_mma<6, 3, kRT>(s_rad, s_ray, w32, u, pgid, lane, bw, s0, s1, mb, mb == 0);
+            if (g < png && n0 < 6)
 #pragma unroll
-            for (int j = 0; j < 3; ++j) {
-                double* dst = p.corner + (size_t(ltri) * 3 + j) * 6 + n0;
-                if (s0[j] != 0) atomicAdd(dst, s0[j]);
-                if (s1[j] != 0) atomicAdd(dst + 1, s1[j]);
-            }
-    } else
-#endif
+                for (int j = 0; j < 3; ++j) {
+                    double* dst = p.corner + (size_t(ltri) * 3 + j) * 6 + n0;
+                    if (s0[j] != 0) atomicAdd(dst, s0[j]);
+                    if (s1[j] != 0) atomicAdd(dst + 1, s1[j]);
+                }
+        }
+    }
+#else
     {
         const int key = pact ? tri : -1 - lane;
         const unsigned peers = __match_any_sync(0xffffffffu, key);
@@ -915,13 +930,11 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
         }
     }
 #endif
+#endif
 #ifndef CDR_EXP_NO_TEXEL
 #if !defined(CDR_SCATTER_SHFL) && !defined(CDR_REDUCE_F32)
-    if (tng <= 8) {  // warp-uniform
-        const int ltex = __shfl_sync(0xffffffffu, tex0, gm < tng ? __fns(tleaders, 0, gm + 1) : 0);
+    {  // groups of 8 per pass, as above
         const int tw = p.sc.tw, th = p.sc.th;
-        const int x0 = ltex % tw, y0 = ltex / tw;
-        const int x1 = x0 + 1 == tw ? 0 : x0 + 1, y1 = y0 + 1 == th ? 0 : y0 + 1;
         double u[7] = {0, 0, 0, 0, 0, 0, 0};
         if (act) {
             for (int c = 0; c < 3; ++c) {
@@ -931,18 +944,25 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             u[6] = wr0;
         }
         auto tw4 = [&](int kq, int src) { return s_ts[kq][w32 + src]; };  // bilinear weight of corner kq
-        double s0[4], s1[4];
-        group_sum_mma<7, 4, kRT>(s_rad, s_ray, w32, u, tgid, lane, tw4, s0, s1);
-        if (gm < tng && n0 < 7)
+#pragma unroll 1
+        for (int mb = 0; mb < tng; mb += 8) {
+            const int g = mb + gm;
+            const int ltex = __shfl_sync(0xffffffffu, tex0, g < tng ? __fns(tleaders, 0, g + 1) : 0);
+            const int x0 = ltex % tw, y0 = ltex / tw;
+            const int x1 = x0 + 1 == tw ? 0 : x0 + 1, y1 = y0 + 1 == th ? 0 : y0 + 1;
+            double s0[4], s1[4];
+            group_sum_mma<7, 4, kRT>(s_rad, s_ray, w32, u, tgid, lane, tw4, s0, s1, mb, mb == 0);
+            if (g < tng && n0 < 7)
 #pragma unroll
-            for (int kq = 0; kq < 4; ++kq) {
-                const int64_t tx = int64_t((kq < 2 ? y0 : y1)) * tw + ((kq & 1) ? x1 : x0);
-                TexAcc* dst = p.texacc + tx;
-                if (s0[kq] != 0) atomicAdd(&dst->v[n0], TexAccT(s0[kq]));
-                if (n0 + 1 < 7 && s1[kq] != 0) atomicAdd(&dst->v[n0 + 1], TexAccT(s1[kq]));
-            }
-    } else
-#endif
+                for (int kq = 0; kq < 4; ++kq) {
+                    const int64_t tx = int64_t((kq < 2 ? y0 : y1)) * tw + ((kq & 1) ? x1 : x0);
+                    TexAcc* dst = p.texacc + tx;
+                    if (s0[kq] != 0) atomicAdd(&dst->v[n0], TexAccT(s0[kq]));
+                    if (n0 + 1 < 7 && s1[kq] != 0) atomicAdd(&dst->v[n0 + 1], TexAccT(s1[kq]));
+                }
+        }
+    }
+#else
     {
         // texel scatter through the bilinear weights (diff_render.cpp:110-128)
         const int key = act ? tex0 : -1 - lane;
@@ -972,6 +992,7 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             }
         }
     }
+#endif
 #endif
 }
 
