@@ -893,8 +893,7 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             const double r1 = sb1[src], r2 = sb2[src];
             return j == 0 ? 1.0 - r1 - r2 : (j == 1 ? r1 : r2);
         };
-#pragma unroll 1
-        for (int mb = 0; mb < png; mb += 8) {
+        auto pass = [&](int mb) {
             const int g = mb + gm;
             const int ltri = __shfl_sync(0xffffffffu, tri, g < png ? __fns(pleaders, 0, g + 1) : 0);
             double s0[3], s1[3];
@@ -906,7 +905,10 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                     if (s0[j] != 0) atomicAdd(dst, s0[j]);
                     if (s1[j] != 0) atomicAdd(dst + 1, s1[j]);
                 }
-        }
+        };
+        pass(0);  // the common case: <= 8 triangles per warp
+#pragma unroll 1
+        for (int mb = 8; mb < png; mb += 8) pass(mb);
     }
 #else
     {
@@ -944,8 +946,7 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             u[6] = wr0;
         }
         auto tw4 = [&](int kq, int src) { return s_ts[kq][w32 + src]; };  // bilinear weight of corner kq
-#pragma unroll 1
-        for (int mb = 0; mb < tng; mb += 8) {
+        auto pass = [&](int mb) {
             const int g = mb + gm;
             const int ltex = __shfl_sync(0xffffffffu, tex0, g < tng ? __fns(tleaders, 0, g + 1) : 0);
             const int x0 = ltex % tw, y0 = ltex / tw;
@@ -960,7 +961,10 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                     if (s0[kq] != 0) atomicAdd(&dst->v[n0], TexAccT(s0[kq]));
                     if (n0 + 1 < 7 && s1[kq] != 0) atomicAdd(&dst->v[n0 + 1], TexAccT(s1[kq]));
                 }
-        }
+        };
+        pass(0);  // the common case: <= 8 texel quads per warp
+#pragma unroll 1
+        for (int mb = 8; mb < tng; mb += 8) pass(mb);
     }
 #else
     {
