@@ -525,12 +525,6 @@ def main(argv=None):
                 regs["cpu_ms"] = None
                 regs["cpu_kind"] = f"unavailable: {e}"
 
-    cpu = None
-    cb = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_baseline_sample(scene, spp, seed, lay, os.cpu_count() or 1, label=args.config)
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-
     # ---- ms per optimisation iteration (the metric's second half), resident:
     # total_loss with all six terms (LossWeights defaults) -> adam_step ->
     # robust_evolve, every step on the device, only scalars back to the host
@@ -569,6 +563,13 @@ def main(argv=None):
                      "iterations": len(parts), "timing": "host wall clock around each synchronous call",
                      "what": "total_loss (rendering + Laplacian + 4 regularisers, LossWeights defaults) -> "
                              "adam_step + apply -> robust_evolve, resident on the device"}
+        iteration["ms_each"] = [round(x, 3) for x in tot]
+    cpu = None
+    cb = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline_sample(scene, spp, seed, lay, os.cpu_count() or 1, label=args.config)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    if iteration is not None:
         if cb is not None:  # the reference's iteration, extrapolated from the bounded sample
             per_view_s = cb["seconds"] * (cfg["image"] ** 2 * spp) / cb["samples"]
             ref_ms = per_view_s * total_views * 1e3 + ((regs or {}).get("cpu_ms") or 0.0)
