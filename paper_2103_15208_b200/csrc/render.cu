@@ -1139,7 +1139,9 @@ __global__ void __launch_bounds__(256) k_background(Params p) {
     }
 }
 
-template <bool kShade, bool kLoss, bool kInterior, int kSPP>
+// kQ: the queue-mode instance (CTAs from the tile queue; no empty-tile path,
+// so the hot instance carries no dead code for the instruction cache)
+template <bool kShade, bool kLoss, bool kInterior, int kSPP, bool kQ = false>
 __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
                                   kSPP == 16 ? CDR_RENDER_CTAS16
                                              : CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
@@ -1154,9 +1156,9 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     __shared__ double s_ts[kTexState][kRT];  // interior_scatter's texel state
     __shared__ double s_ray[kInterior ? 5 : 1][kRT];  // dir, b1, b2 of the sample, for the scatter's late uses
 
-    constexpr bool kQueue = kSPP == 16 && kShade && kLoss;  // may run over the tile queue
+    static_assert(!kQ || (kSPP == 16 && kShade && kLoss), "queue mode is the spp-16 loss call");
     int cx = int(blockIdx.x), cy = int(blockIdx.y), cz = int(blockIdx.z);
-    if (kQueue && p.queue_mode) {  // CTA = (non-empty tile, pixel-row group) from k_tile_lists' queue
+    if (kQ) {  // CTA = (non-empty tile, pixel-row group) from the tile queue
         constexpr int kCPT = 4 / (kRT / 64);  // CTAs per 4 x 4 tile
         const int2 e = p.tile_queue[int(blockIdx.x) / kCPT];
         cz = e.x;
@@ -1184,7 +1186,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     // Empty beam tile (no candidate at all: k_trace wrote a miss for every
     // sample): warp 0 writes the 8 pixels' background mean, mask, loss and
     // adjoint straight away; no hit loads, no staging, no barrier.
-    if (kSPP == 16 && kShade && kLoss && p.use_beam && !p.queue_mode) {
+    if (!kQ && kSPP == 16 && kShade && kLoss && p.use_beam) {
         const TileHdr th = p.tile_hdr[size_t(vc.tile_base) + (Y0 / 4) * vc.tiles_x + cx];
         if (th.cnt == 0) {
 #ifdef CDR_EXP_EMPTY_RETURN  // measurement only (wrong output): cost of the empty-tile path
@@ -1738,7 +1740,11 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             constexpr int kCPT = 4 / (kRenderThreads16 / 64);
             if (nq > 0) {
                 ++c->launches;
-                launch_render_kernel_t<16>(pc, dim3(unsigned(nq) * kCPT, 1, 1), c, trace, loss, interior);
+                const dim3 qgrid(unsigned(nq) * kCPT, 1, 1);
+                if (interior)
+                    k_render<true, true, true, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
+                else
+                    k_render<true, true, false, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
             }
             ++c->launches;
             k_background<<<dim3((maxW * maxH + 255) / 256, nv), 256, 0, c->stream>>>(pc);
