@@ -70,13 +70,13 @@ struct Params {
     int use_beam;
     int fast_cap;     // candidate cap of the fast pass (kBeamCap; lower only to test the big pass)
     int big_list_cap;  // the same for the big pass (kBigCap; lower only to test the split pass)
-    int split_list_cap;  // the same for the level-0 quadrants (kBigCap; lower only to test level 1)
+    int split_list_cap;  // the same for the split levels (kBigCap; lower only to test level 1 and the huge pass)
     int no_shared_top;  // 1: every tile walks the BVH from the root (A/B and tests)
     int2* big_queue;  // (call, tile) of the tiles over kBeamCap candidates
     int* big_count;
     int big_cap;
     int4* split_queue;  // split work: (big slot, packed rect, list group, level); level 0 = the big-pass overflows
-    int* split_count;   // [0] level-0 items, [1] level-1 items, [2] level-1 groups allocated
+    int* split_count;   // [0] level-0 items, [1] level-1 items, [2] huge-pass items
     int split_cap;      // items per level
     int2* split_hdr;    // groups of 4 quadrant lists (first candidate, count; -1 = per ray, -2 = split again)
     // tile queue (loss calls at spp 16): k_tile_lists appends every non-empty
@@ -246,7 +246,7 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
     if (s_key) {  // big tiles: sort (distance bits, list position): the same order as the ranks below
         for (int i = lane; i < nl; i += 32)
             s_key[i] = (static_cast<unsigned long long>(__float_as_uint(s_d[i])) << 32) | unsigned(i);
-        warp_bitonic_sort<256>(s_key, nl, lane);
+        warp_bitonic_sort<(kCap > 255 ? 1024 : 256)>(s_key, nl, lane);
     }
     for (int i = lane; i < nl; i += 32) {
         int rank = 0;  // distance order, ties by list position
@@ -308,6 +308,15 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
         const int qx = q % p.TW - sx0, qy = q / p.TW - sy0;
         return qx >= 0 && qx < sw && qy >= 0 && qy < sh;
     };
+    if (kCap > 255 && nl > 255) {  // candidates beyond a byte index: the rect's pixels scan the whole list
+        for (int q = lane; q < P; q += 32)
+            if (in_rect(q)) (big >= 0 ? p.big_pix_cnt : p.pix_cnt)[big >= 0 ? size_t(big) * P + q : tile * P + q] = 255;
+        if (lane == 0) {
+            if (sub_out) *sub_out = make_int2(off, nl);
+            else *hdr = TileHdr{off, nl, big, 0};
+        }
+        return true;
+    }
     if (P <= 32) {
         // lane = candidate: a mask of the tile pixels its triangle may cover
         // (the same test as cand_overlaps_pixel), then one ballot per pixel
@@ -545,23 +554,65 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_split(Params p, i
         if (!build_tile_list<kBigCap, kBigFront, kBigPixCap>(p, vc, cam, e.y, lane, s_front[w], s_leaf[w], s_d[w],
                                                              reinterpret_cast<unsigned long long*>(s_front[w]), i,
                                                              nullptr, 0, sx0, sy0, sw, sh, out,
-                                                             level == 0 ? p.split_list_cap : kBigCap) &&
+                                                             p.split_list_cap) &&
             lane == 0) {
             int j2 = -1;
             if (level == 0 && sw * sh > 1) {  // split this quadrant once more
                 j2 = atomicAdd(p.split_count + 1, 1);
                 if (j2 >= p.split_cap) j2 = -1;
             }
+            int jh = -1;
+            if (level == 1 || sw * sh == 1) {  // the list itself, with up to kHugeCap candidates (k_tile_lists_huge)
+                jh = atomicAdd(p.split_count + 2, 1);
+                if (jh >= p.split_cap) jh = -1;
+            }
             if (j2 >= 0) {
                 const int g2 = p.split_cap + j2;
                 *out = make_int2(g2, -2);
                 p.split_queue[size_t(p.split_cap) + j2] = split_item(i, sx0, sy0, sw, sh, g2, 1);
+            } else if (jh >= 0) {
+                *out = make_int2(0, -1);  // per ray unless the huge pass fits it
+                p.split_queue[2 * size_t(p.split_cap) + jh] =
+                    split_item(i, sx0, sy0, sw, sh, int(out - p.split_hdr), 2);
             } else {
                 *out = make_int2(0, -1);
                 atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
             }
         }
         if (level == 0 && qd == 0 && lane == 0) p.tile_hdr[size_t(vc.tile_base) + e.y] = TileHdr{g, -2, i, 0};
+        __syncwarp();
+    }
+}
+
+// Huge pass: the lists that still overflow after the splits (at spp 16
+// single pixels: grazing rays along a thin tube see hundreds of triangles),
+// rebuilt with up to kHugeCap candidates; the pixels scan the whole list (no
+// byte-indexed pixel lists). One warp per CTA, 20 KB of shared memory.
+constexpr int kHugeCap = 1023;
+constexpr int kHugeFront = 1024;
+__global__ void __launch_bounds__(32) k_tile_lists_huge(Params p) {
+    __shared__ __align__(8) int s_front[2][kHugeFront];
+    __shared__ int s_leaf[kHugeCap];
+    __shared__ float s_d[kHugeCap];
+    static_assert(2 * kHugeFront * sizeof(int) >= 1024 * sizeof(unsigned long long), "key space");
+    const int lane = threadIdx.x & 31;
+    const int n = min(p.split_count[2], p.split_cap);
+    const int4* queue = p.split_queue + 2 * size_t(p.split_cap);
+    for (int it = blockIdx.x; it < n; it += gridDim.x) {
+        const int4 item = queue[it];
+        const int i = item.x;
+        const int rx = item.y & 0xff, ry = (item.y >> 8) & 0xff, rw = (item.y >> 16) & 0xff, rh = item.y >> 24;
+        const int2 e = p.big_queue[i];
+        const ViewCall vc = p.calls[e.x];
+        const DevCamera& cam = p.cams[vc.slot];
+        int2* out = p.split_hdr + item.z;
+        if (!build_tile_list<kHugeCap, kHugeFront, kBigPixCap>(p, vc, cam, e.y, lane, s_front, s_leaf, s_d,
+                                                               reinterpret_cast<unsigned long long*>(s_front), i,
+                                                               nullptr, 0, rx, ry, rw, rh, out) &&
+            lane == 0) {
+            *out = make_int2(0, -1);
+            atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+        }
         __syncwarp();
     }
 }
@@ -1640,7 +1691,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         c->beam_big_count.ensure(4);  // big queue, split queues of levels 0 and 1
         // CDR_NO_SPLIT (A/B): no split pass, its tiles traced per ray (and counted so)
         const int split_cap = big_cap > 0 && !std::getenv("CDR_NO_SPLIT") ? std::max(64, big_cap / 8) : 0;
-        c->beam_split_queue.ensure(std::max<size_t>(1, 2 * size_t(split_cap)));  // two levels
+        c->beam_split_queue.ensure(std::max<size_t>(1, 3 * size_t(split_cap)));  // two levels + the huge pass
         c->beam_split_hdr.ensure(std::max<size_t>(4, 8 * size_t(split_cap)));    // 4 lists per group, 2 levels
         p.split_queue = c->beam_split_queue.p;
         p.split_count = c->beam_big_count.p + 1;
@@ -1718,6 +1769,10 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
                 c->launches += 2;
                 k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc, 0);
                 k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc, 1);
+                if (!std::getenv("CDR_NO_HUGE")) {
+                    ++c->launches;
+                    k_tile_lists_huge<<<148 * 4, 32, 0, c->stream>>>(pc);
+                }
             }
         }
         if (queue) {

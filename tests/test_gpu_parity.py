@@ -355,7 +355,7 @@ def test_big_tile_lists_exact(sphere, monkeypatch, fast_cap, big_cap, split_cap)
     monkeypatch.setenv("CDR_BEAM_FAST_CAP", fast_cap)
     if big_cap is not None:
         monkeypatch.setenv("CDR_BEAM_BIG_CAP", big_cap)
-    if split_cap is not None:  # level-0 quadrants overflow too: split once more (pixel lists)
+    if split_cap is not None:  # quadrants overflow too: split once more, then the huge pass
         monkeypatch.setenv("CDR_BEAM_SPLIT_CAP", split_cap)
     blob = blob_scene(freq=8, tex=32, views=2, image=48)
     for sc in (sphere, blob):
@@ -394,7 +394,8 @@ def test_odd_image_sizes_exact(wh):
     _loss_grad_check(sc, 16, 3, param_layout(sc))
 
 
-@pytest.mark.parametrize("knob", ["CDR_NO_BEAM", "CDR_CHUNK_MB", "CDR_NO_SHARED_TOP", "CDR_NO_SPLIT", "CDR_NO_QUEUE"])
+@pytest.mark.parametrize("knob", ["CDR_NO_BEAM", "CDR_CHUNK_MB", "CDR_NO_SHARED_TOP", "CDR_NO_SPLIT", "CDR_NO_QUEUE",
+                                  "CDR_NO_HUGE"])
 def test_alternate_paths_exact(sphere, monkeypatch, knob):
     """The A/B switches kept in the code (per-ray traversal only; view chunks
     through lists -> trace -> shade; every tile from the BVH root) stay exact."""
