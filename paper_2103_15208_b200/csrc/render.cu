@@ -70,6 +70,7 @@ struct Params {
     int use_beam;
     int fast_cap;     // candidate cap of the fast pass (kBeamCap; lower only to test the big pass)
     int big_list_cap;  // the same for the big pass (kBigCap; lower only to test the split pass)
+    int huge_on;         // lists overflowing both splits go to k_tile_lists_huge (CDR_NO_HUGE: per ray)
     int split_list_cap;  // the same for the split levels (kBigCap; lower only to test level 1 and the huge pass)
     int no_shared_top;  // 1: every tile walks the BVH from the root (A/B and tests)
     int2* big_queue;  // (call, tile) of the tiles over kBeamCap candidates
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(32 * kBigWarps) k_tile_lists_split(Params p, i
                 if (j2 >= p.split_cap) j2 = -1;
             }
             int jh = -1;
-            if (level == 1 || sw * sh == 1) {  // the list itself, with up to kHugeCap candidates (k_tile_lists_huge)
+            if (p.huge_on && (level == 1 || sw * sh == 1)) {  // the list itself, up to kHugeCap candidates (k_tile_lists_huge)
                 jh = atomicAdd(p.split_count + 2, 1);
                 if (jh >= p.split_cap) jh = -1;
             }
@@ -1696,6 +1697,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         p.split_queue = c->beam_split_queue.p;
         p.split_count = c->beam_big_count.p + 1;
         p.split_cap = split_cap;
+        p.huge_on = !std::getenv("CDR_NO_HUGE");
         p.split_hdr = c->beam_split_hdr.p;
         c->beam_big_pix_list.ensure(std::max<size_t>(16, size_t(big_cap) * P * kBigPixCap));
         c->beam_big_pix_cnt.ensure(std::max<size_t>(1, size_t(big_cap) * P));
@@ -1769,7 +1771,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
                 c->launches += 2;
                 k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc, 0);
                 k_tile_lists_split<<<148 * 16 / kBigWarps, 32 * kBigWarps, 0, c->stream>>>(pc, 1);
-                if (!std::getenv("CDR_NO_HUGE")) {
+                if (pc.huge_on) {
                     ++c->launches;
                     k_tile_lists_huge<<<148 * 4, 32, 0, c->stream>>>(pc);
                 }
