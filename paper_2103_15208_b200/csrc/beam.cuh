@@ -178,41 +178,6 @@ __device__ __forceinline__ bool cand_overlaps_pixel(const BeamCand& c, float x0,
     return true;
 }
 
-// Sub-cell coverage of a candidate inside pixel (x0, y0) (tile-relative):
-// bit (i + 4 j) set when the margined triangle may overlap the 0.25-px cell
-// (i, j). Conservative like cand_overlaps_pixel (corner maximum per edge),
-// with a slack far above the fp32 rounding of the point test, so a point the
-// point test accepts always lies in a set cell. Big-tile pixel lists store it
-// beside each entry: a scan skips candidates whose cell bit is clear without
-// loading their record (the scans are L1-bandwidth bound).
-__device__ __forceinline__ unsigned cand_subcell_mask(const BeamCand& c, float x0, float y0) {
-    if (cand_always(c.a)) return 0xffffu;
-    float A[3], B[3], C[3];
-    cand_edges(c.a, c.b, A, B, C);
-    unsigned m = 0xffffu;
-#pragma unroll
-    for (int e = 0; e < 3; ++e) {
-        const float ax = A[e] > 0 ? 0.25f : 0.0f, by = B[e] > 0 ? 0.25f : 0.0f;
-        const float base = A[e] * x0 + B[e] * y0 + C[e] + 1e-4f;  // cell (0, 0)'s lower corner + slack
-        unsigned me = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const float v = base + A[e] * (0.25f * i + ax) + B[e] * (0.25f * j + by);
-                me |= unsigned(!(v < 0.0f)) << (i + 4 * j);
-            }
-        m &= me;
-    }
-    return m;
-}
-
-// the sub-cell bit of tile-relative point (x, y) in pixel (px, py)
-__device__ __forceinline__ unsigned subcell_bit(float x, float y, int px, int py) {
-    const int i = min(3, max(0, int((x - float(px)) * 4.0f))), j = min(3, max(0, int((y - float(py)) * 4.0f)));
-    return 1u << (i + 4 * j);
-}
-
 // cand_overlaps_pixel for every pixel of a tile of P <= 32 pixels, TW wide:
 // bit q set when pixel (q % TW, q / TW) may be covered. Same arithmetic per
 // pixel as cand_overlaps_pixel, so the same decisions.
@@ -258,21 +223,13 @@ __device__ __forceinline__ Hit trace_beam(const BeamCand* __restrict__ cand, int
 }
 
 // Same scan over an index list (a pixel's candidates, in distance order).
-// masks (big-tile lists): each entry's sub-cell coverage; entries whose cell
-// bit `bit` is clear are skipped without loading their record.
 __device__ __forceinline__ Hit trace_beam_list(const BeamCand* __restrict__ cand, const unsigned char* __restrict__ idx,
                                                int n, const TriRec* __restrict__ recs, D3 o, D3 d, double t_min,
-                                               float px, float py, const unsigned short* __restrict__ masks = nullptr,
-                                               unsigned bit = 0) {
+                                               float px, float py) {
     Hit best{-1, 1e300, 0.0, 0.0};
     unsigned iw = 0;  // four list entries per load (lists are 4-byte aligned, kPix % 4 == 0)
-    uint2 mw = make_uint2(0, 0);  // four masks per load
     for (int j = 0; j < n; ++j) {
-        if ((j & 3) == 0) {
-            iw = __ldg(reinterpret_cast<const unsigned*>(idx + j));
-            if (masks) mw = __ldg(reinterpret_cast<const uint2*>(masks + j));
-        }
-        if (masks && !((((j & 2) ? mw.y : mw.x) >> (16 * (j & 1))) & bit)) continue;
+        if ((j & 3) == 0) iw = __ldg(reinterpret_cast<const unsigned*>(idx + j));
         const int k = int((iw >> (8 * (j & 3))) & 0xffu);
         CDR_DCHECK(k < 255);
         const float4 ra = cand[k].a, rb = cand[k].b;
@@ -292,7 +249,6 @@ struct BeamView {
     const unsigned char* pix_cnt;
     const unsigned char* big_pix_list;
     const unsigned char* big_pix_cnt;
-    const unsigned short* big_pix_mask;  // sub-cell masks beside big_pix_list
     const int* tile_base;  // per view index of the call
     const int2* split;     // quadrant lists of split tiles (4 per split tile)
     int TW, TH, P;
@@ -322,10 +278,7 @@ __device__ __forceinline__ Hit trace_point(const BeamView& bv, int vi, const Dev
                 const float lx = float(x.x - tx * bv.TW), ly = float(x.y - ty * bv.TH);
                 if (cnt == 0) return Hit{-1, 1e300, 0.0, 0.0};
                 if (cnt == 255) return trace_beam(bv.pool + tl.x, tl.y, recs, o, d, t_min, lx, ly);
-                const int qx = px - tx * bv.TW, qy = py - ty * bv.TH;
-                return trace_beam_list(bv.pool + tl.x, lst, cnt, recs, o, d, t_min, lx, ly,
-                                       h.big >= 0 && bv.big_pix_mask ? bv.big_pix_mask + li * kBigPixCap : nullptr,
-                                       subcell_bit(lx, ly, qx, qy));
+                return trace_beam_list(bv.pool + tl.x, lst, cnt, recs, o, d, t_min, lx, ly);
             }
         }
     }
@@ -350,9 +303,6 @@ struct ProbeScan {
     const BeamCand* cand;
     const unsigned char* lst;  // nullptr: scan the whole tile list
     unsigned iw;               // the current 4-entry word of lst
-    const unsigned short* msk; // big lists: sub-cell masks beside lst (nullptr: none)
-    unsigned bit;              // the probe's sub-cell bit
-    uint2 mw;                  // the current 4-mask word
     int n, j;
     float lx, ly;
     int mode;  // 0 done, 1 scanning, 2 per-ray traversal
@@ -388,17 +338,12 @@ __device__ __forceinline__ void probe_setup(const BeamView& bv, int vi, const De
     s.cand = bv.pool + tl.x;
     s.lx = float(x.x - tx * bv.TW);
     s.ly = float(x.y - ty * bv.TH);
-    s.msk = nullptr;
     if (cnt == 255) {
         s.lst = nullptr;
         s.n = tl.y;
     } else {
         s.lst = h.big >= 0 ? bv.big_pix_list + li * kBigPixCap : bv.pix_list + li * kPixCap;
         s.n = cnt;
-        if (h.big >= 0 && bv.big_pix_mask) {
-            s.msk = bv.big_pix_mask + li * kBigPixCap;
-            s.bit = subcell_bit(s.lx, s.ly, px - tx * bv.TW, py - ty * bv.TH);
-        }
     }
     s.mode = s.n > 0 ? 1 : 0;
     CDR_PSTAT(s.n == 0 ? 7 : (cnt == 255 ? (h.big >= 0 ? 5 : 4) : (h.big >= 0 ? 3 : 2)), 1);
@@ -412,15 +357,7 @@ __device__ __forceinline__ void probe_step(ProbeScan& s, const TriRec* __restric
     }
     int k = s.j;
     if (s.lst) {  // four list entries per load: no dependent byte load on most steps
-        if ((s.j & 3) == 0) {
-            s.iw = __ldg(reinterpret_cast<const unsigned*>(s.lst + s.j));
-            if (s.msk) s.mw = __ldg(reinterpret_cast<const uint2*>(s.msk + s.j));
-        }
-        // big-tile lists: skip a candidate whose sub-cell bit is clear, no record load
-        if (s.msk && !((((s.j & 2) ? s.mw.y : s.mw.x) >> (16 * (s.j & 1))) & s.bit)) {
-            ++s.j;
-            return;
-        }
+        if ((s.j & 3) == 0) s.iw = __ldg(reinterpret_cast<const unsigned*>(s.lst + s.j));
         k = int((s.iw >> (8 * (s.j & 3))) & 0xffu);
     }
     ++s.j;

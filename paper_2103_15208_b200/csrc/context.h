@@ -139,7 +139,6 @@ struct cdr_ctx {
     cdr::DBuf<int4> beam_split_queue;  // split work items (levels 0 and 1)
     cdr::DBuf<int2> beam_split_hdr;    // groups of 4 quadrant lists
     cdr::DBuf<unsigned char> beam_big_pix_list, beam_big_pix_cnt;      // per view index of the last render call
-    cdr::DBuf<unsigned short> beam_big_pix_mask;  // sub-cell coverage beside each big-list entry
     cdr::DBuf<int2> tile_queue;         // non-empty tiles (call, tile) of a queue-mode loss call
     cdr::DBuf<int> tile_queue_count;
     int* tile_queue_host = nullptr;     // pinned: its length, read back during k_trace

@@ -67,12 +67,10 @@ struct Params {
     unsigned char* pix_cnt;   // per (tile, pixel): count, 255 = scan the tile list
     unsigned char* big_pix_list;  // per (big tile, pixel): kBigPixCap indices
     unsigned char* big_pix_cnt;
-    unsigned short* big_pix_mask;  // beside big_pix_list: each entry's sub-cell coverage (cand_subcell_mask)
     int use_beam;
     int fast_cap;     // candidate cap of the fast pass (kBeamCap; lower only to test the big pass)
     int big_list_cap;  // the same for the big pass (kBigCap; lower only to test the split pass)
     int huge_on;         // lists overflowing both splits go to k_tile_lists_huge (CDR_NO_HUGE: per ray)
-    int use_masks;       // scans use the big lists' sub-cell masks (CDR_NO_SUBCELL: not)
     int split_list_cap;  // the same for the split levels (kBigCap; lower only to test level 1 and the huge pass)
     int no_shared_top;  // 1: every tile walks the BVH from the root (A/B and tests)
     int2* big_queue;  // (call, tile) of the tiles over kBeamCap candidates
@@ -337,12 +335,7 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
                 if (!bal) continue;  // warp-uniform
                 const int cq = __shfl_sync(0xffffffffu, my_cnt, q);
                 const int pos = cq + __popc(bal & lt);
-                if (on && pos < kPix) {
-                    lst0[size_t(q) * kPix + pos] = (unsigned char)k;
-                    if (big >= 0)
-                        p.big_pix_mask[(size_t(big) * P + q) * kPix + pos] =
-                            (unsigned short)cand_subcell_mask(s_cand[k], float(q % p.TW), float(q / p.TW));
-                }
+                if (on && pos < kPix) lst0[size_t(q) * kPix + pos] = (unsigned char)k;
                 if (lane == q) my_cnt += __popc(bal);
             }
         }
@@ -364,10 +357,7 @@ __device__ bool build_tile_list(const Params& p, const ViewCall& vc, const DevCa
         int cnt = 0;
         for (int k = 0; k < nl; ++k)
             if (cand_overlaps_pixel(s_cand[k], qx, qy)) {
-                if (cnt < kPix) {
-                    lst[cnt] = (unsigned char)k;
-                    if (big >= 0) p.big_pix_mask[li * kPix + cnt] = (unsigned short)cand_subcell_mask(s_cand[k], qx, qy);
-                }
+                if (cnt < kPix) lst[cnt] = (unsigned char)k;
                 ++cnt;
             }
         (big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li] = (unsigned char)(cnt > kPix ? 255 : cnt);
@@ -681,9 +671,7 @@ __device__ __forceinline__ void trace_item(const Params& p, const ViewCall& vc, 
             h = cnt == 255 ? trace_beam(cands, tl.y, p.sc.recs, org, dir, p.info->t_min, fx, fy)
                            : trace_beam_list(cands,
                                              (th.big >= 0 ? p.big_pix_list + li * kBigPixCap : p.pix_list + li * kPixCap),
-                                             cnt, p.sc.recs, org, dir, p.info->t_min, fx, fy,
-                                             th.big >= 0 && p.use_masks ? p.big_pix_mask + li * kBigPixCap : nullptr,
-                                             subcell_bit(fx, fy, pix % TW, pix / TW));
+                                             cnt, p.sc.recs, org, dir, p.info->t_min, fx, fy);
         }
     } else {
         D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
@@ -1710,12 +1698,9 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         p.split_count = c->beam_big_count.p + 1;
         p.split_cap = split_cap;
         p.huge_on = !std::getenv("CDR_NO_HUGE");
-        p.use_masks = !std::getenv("CDR_NO_SUBCELL");
         p.split_hdr = c->beam_split_hdr.p;
         c->beam_big_pix_list.ensure(std::max<size_t>(16, size_t(big_cap) * P * kBigPixCap));
         c->beam_big_pix_cnt.ensure(std::max<size_t>(1, size_t(big_cap) * P));
-        c->beam_big_pix_mask.ensure(std::max<size_t>(16, size_t(big_cap) * P * kBigPixCap));
-        p.big_pix_mask = c->beam_big_pix_mask.p;
         p.big_queue = c->beam_big_queue.p;
         p.big_count = c->beam_big_count.p;
         p.big_cap = big_cap;
@@ -1727,10 +1712,8 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         c->beam_tile_base.ensure(n_views);
         CDR_CUDA_CHECK(cudaMemcpyAsync(c->beam_tile_base.p, bases.data(), sizeof(int) * n_views,
                                        cudaMemcpyHostToDevice, c->stream));
-        c->beam_view = BeamView{p.tile_hdr,          p.pool,          p.pix_list,        p.pix_cnt, p.big_pix_list,
-                                p.big_pix_cnt,       p.use_masks ? p.big_pix_mask : nullptr,
-                                c->beam_tile_base.p, p.split_hdr,     TW,                TH,        P,
-                                1};
+        c->beam_view = BeamView{p.tile_hdr,          p.pool,      p.pix_list, p.pix_cnt, p.big_pix_list, p.big_pix_cnt,
+                                c->beam_tile_base.p, p.split_hdr, TW,         TH,        P,              1};
         c->beam_slots.assign(view_slots, view_slots + n_views);
     }
     // Views can go through lists -> trace -> shade in chunks whose hit cache
