@@ -370,6 +370,14 @@ __device__ __forceinline__ void probe_step(ProbeScan& s, const TriRec* __restric
     if (cand_covers(ra, rb, s.lx, s.ly)) leaf_test(recs, cand_leaf(ra), o, d, t_min, s.best);
 }
 
+// Per-ray traversal for the rare probe without a usable list (off-image
+// points, lists that overflowed every pass): out of line, so its stack and
+// registers do not weigh on the list scans around it.
+static __device__ __noinline__ Hit trace_out_of_line(const BNode* nodes, const TriRec* recs, int n_tris, D3 o, D3 d,
+                                              double t_min) {
+    return trace(nodes, recs, n_tris, o, d, t_min);
+}
+
 __device__ __forceinline__ void trace_points2(const BeamView& bv, int vi, const DevCamera& cam, const BNode* nodes,
                                               const TriRec* recs, int n_tris, D2 xa, D3 da, D2 xb, D3 db,
                                               double t_min, Hit& ha, Hit& hb) {
@@ -381,8 +389,8 @@ __device__ __forceinline__ void trace_points2(const BeamView& bv, int vi, const 
         if (a.mode == 1) probe_step(a, recs, o, da, t_min);
         if (b.mode == 1) probe_step(b, recs, o, db, t_min);
     }
-    ha = a.mode == 2 ? trace(nodes, recs, n_tris, o, da, t_min) : a.best;
-    hb = b.mode == 2 ? trace(nodes, recs, n_tris, o, db, t_min) : b.best;
+    ha = a.mode == 2 ? trace_out_of_line(nodes, recs, n_tris, o, da, t_min) : a.best;
+    hb = b.mode == 2 ? trace_out_of_line(nodes, recs, n_tris, o, db, t_min) : b.best;
 }
 
 }  // namespace cdr

@@ -447,8 +447,10 @@ __device__ __forceinline__ int boundary_samples(const BParams& p, int vi, const 
             delta = lo3 - hi3;
         } else {
             D3 org{cam.o[0], cam.o[1], cam.o[2]};
-            double cm = trace(p.sc.nodes, p.sc.recs, p.sc.n_tris, org, primary_dir(cam, xm), t_min).tri >= 0 ? 1.0 : 0.0;
-            double cp = trace(p.sc.nodes, p.sc.recs, p.sc.n_tris, org, primary_dir(cam, xp), t_min).tri >= 0 ? 1.0 : 0.0;
+            double cm = trace_out_of_line(p.sc.nodes, p.sc.recs, p.sc.n_tris, org, primary_dir(cam, xm), t_min).tri >= 0
+                            ? 1.0 : 0.0;
+            double cp = trace_out_of_line(p.sc.nodes, p.sc.recs, p.sc.n_tris, org, primary_dir(cam, xp), t_min).tri >= 0
+                            ? 1.0 : 0.0;
             delta = D3{cm - cp, cm - cp, cm - cp};
         }
         weighted = dot(b.adj, delta);
