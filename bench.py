@@ -434,6 +434,10 @@ def main(argv=None):
             roof["traffic"] = 1e6 * (kr["dram_read_MB"] + kr["dram_write_MB"])
             roof["traffic_source"] = (f"ncu dram__bytes_read.sum + dram__bytes_write.sum of k_render<1,1,1,16> at "
                                       f"{args.config}, {os.path.relpath(traffic_file, ROOT)}")
+            # what HBM actually moved per launch, over this run's kernel time: the
+            # algorithmic fraction above is served mostly from L2 (mesh, BVH, maps)
+            roof["dram_GBps"] = roof["traffic"] / (ms_shade / 1e3) / 1e9
+            roof["dram_frac"] = roof["dram_GBps"] / pk["hbm_gbs"]
         except Exception as e:  # noqa: BLE001
             roof["traffic_source"] = f"unreadable capture: {e}"
 
