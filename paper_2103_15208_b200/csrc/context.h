@@ -135,6 +135,7 @@ struct cdr_ctx {
     cdr::DBuf<unsigned char> beam_pix_list, beam_pix_cnt;
     cdr::DBuf<int> beam_tile_base;
     cdr::DBuf<int2> beam_big_queue;  // tiles rebuilt with the big candidate cap
+    cdr::DBuf<int> beam_top;         // k_top_walk: per tile block, the shared top frontier
     cdr::DBuf<int> beam_big_count;   // [0] big queue, [1] split queue
     cdr::DBuf<int4> beam_split_queue;  // split work items (levels 0 and 1)
     cdr::DBuf<int2> beam_split_hdr;    // groups of 4 quadrant lists

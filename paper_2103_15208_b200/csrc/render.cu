@@ -86,6 +86,8 @@ struct Params {
     int2* tile_queue;
     int* tile_queue_count;
     int queue_mode;  // k_render: CTAs from tile_queue instead of the full tile grid
+    int* top_nodes;  // k_top_walk's output: per 2 x 2 block, [count, <= kTopCap frontier nodes]
+    int top_stride;  // blocks per view slot in top_nodes
 };
 
 constexpr int kThreads = 256;
@@ -436,12 +438,32 @@ __device__ int shared_top_levels(const Params& p, const DevCamera& cam, int X0, 
     return nf;
 }
 
+// The shared top levels of every 2 x 2 tile block, one warp per block, ahead
+// of the list builder: the builder's warps then start from
+// the stored frontier instead of waiting at a barrier for one of them to walk.
+__global__ void __launch_bounds__(128) k_top_walk(Params p) {
+    __shared__ int s_front[4][2][kFrontCap];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const ViewCall vc = p.calls[blockIdx.y];
+    const DevCamera cam = p.cams[vc.slot];
+    const int bx = (vc.tiles_x + 1) / 2, by = (vc.tiles_y + 1) / 2;
+    const int blk = int(blockIdx.x) * 4 + w;
+    if (blk >= bx * by) return;
+    const int cx = blk % bx, cy = blk / bx;
+    const int X0 = 2 * cx * p.TW, X1 = min(X0 + 2 * p.TW, cam.W);
+    const int Y0 = 2 * cy * p.TH, Y1 = min(Y0 + 2 * p.TH, cam.H);
+    int* out = p.top_nodes + (size_t(blockIdx.y) * p.top_stride + blk) * (kTopCap + 1);
+    const int n = shared_top_levels(p, cam, X0, X1, Y0, Y1, lane, s_front[w], out + 1);
+    if (lane == 0) out[0] = n;
+}
+
 __global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_lists(Params p) {
     __shared__ int s_front[kListWarps][2][kFrontCap];
     __shared__ int s_leaf[kListWarps][kBeamCap];
     __shared__ float s_d[kListWarps][kBeamCap];
     __shared__ int s_top[kTopCap];
     __shared__ int s_ntop;
+    __shared__ int s_top_w[kListWarps][kTopCap];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const ViewCall vc = p.calls[blockIdx.y];
     const DevCamera cam = p.cams[vc.slot];
@@ -455,6 +477,24 @@ __global__ void __launch_bounds__(32 * kListWarps, CDR_LIST_MIN_BLOCKS) k_tile_l
     const bool mine = tx < vc.tiles_x && ty < vc.tiles_y;
     const int b = ty * vc.tiles_x + tx;
     const bool share = p.sc.n_tris > 1 && !p.no_shared_top;
+    if (share && p.top_nodes) {  // the prepass stored the block's frontier
+        if (!mine) return;
+        const int* src = p.top_nodes + (size_t(blockIdx.y) * p.top_stride + blockIdx.x) * (kTopCap + 1);
+        const int n = src[0];
+        for (int i = lane; i < n; i += 32) s_top_w[w][i] = src[1 + i];
+        __syncwarp();
+        if (build_tile_list<kBeamCap, kFrontCap, kPixCap>(p, vc, cam, b, lane, s_front[w], s_leaf[w], s_d[w], nullptr,
+                                                           -1, s_top_w[w], n, 0, 0, 1 << 20, 1 << 20, nullptr,
+                                                           p.fast_cap))
+            return;
+        if (lane == 0) {
+            p.tile_hdr[size_t(vc.tile_base) + b] = TileHdr{0, -1, -1, 0};
+            const int i = atomicAdd(p.big_count, 1);
+            if (i < p.big_cap) p.big_queue[i] = make_int2(int(blockIdx.y), b);
+            else atomicAdd(&p.counters->beam_fallback_tiles, 1ull);
+        }
+        return;
+    }
     if (share) {
         if (w == 0) {
             const int X0 = 2 * cx * p.TW, X1 = min(X0 + 2 * p.TW, cam.W);
@@ -1763,6 +1803,17 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             dim3 lgrid((tiles + kListWarps - 1) / kListWarps, nv);
 #endif
             CDR_CUDA_CHECK(cudaMemsetAsync(pc.big_count, 0, 4 * sizeof(int), c->stream));
+            // the blocks' shared top levels in a prepass (its warps do not hold
+            // three builder warps at a barrier): lists 7.2 -> 6.5 ms at cfg2,
+            // 22.6 -> 20.7 ms at cfg4 (CDR_NO_TOP_PREPASS: the in-kernel walk)
+            if (!std::getenv("CDR_NO_TOP_PREPASS") && pc.sc.n_tris > 1 && !pc.no_shared_top) {
+                const int nblk = ((maxW + TW - 1) / TW + 1) / 2 * (((maxH + TH - 1) / TH + 1) / 2);
+                c->beam_top.ensure(size_t(nv) * nblk * (kTopCap + 1));
+                pc.top_nodes = c->beam_top.p;
+                pc.top_stride = nblk;
+                ++c->launches;
+                k_top_walk<<<dim3((nblk + 3) / 4, nv), 128, 0, c->stream>>>(pc);
+            }
             ++c->launches;
             k_tile_lists<<<lgrid, 32 * kListWarps, 0, c->stream>>>(pc);
             ++c->launches;
