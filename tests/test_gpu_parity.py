@@ -395,7 +395,8 @@ def test_odd_image_sizes_exact(wh):
 
 
 @pytest.mark.parametrize("knob", ["CDR_NO_BEAM", "CDR_CHUNK_MB", "CDR_NO_SHARED_TOP", "CDR_NO_SPLIT", "CDR_NO_QUEUE",
-                                  "CDR_NO_HUGE", "CDR_NO_TOP_PREPASS"])
+                                  "CDR_NO_HUGE", "CDR_NO_TOP_PREPASS",
+                                  "CDR_TRACE_QUEUE", "CDR_NO_TRACE_QUEUE"])
 def test_alternate_paths_exact(sphere, monkeypatch, knob):
     """The A/B switches kept in the code (per-ray traversal only; view chunks
     through lists -> trace -> shade; every tile from the BVH root) stay exact."""
