@@ -144,6 +144,7 @@ struct cdr_ctx {
     cdr::DBuf<int> tile_queue_count;
     int* tile_queue_host = nullptr;     // pinned: its length, read back during k_trace
     cudaEvent_t tile_queue_ev = nullptr;
+    double queue_frac_last = 1.0;       // non-empty tile fraction of the last queue-mode call
     cdr::BeamView beam_view{};          // lists of the last render call (valid flag)
     std::vector<int> beam_slots;        // view slots of that call, in call order (beam_view's view index)
     int* beam_used_host = nullptr;   // pinned; previous call's pool use

@@ -1864,12 +1864,16 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         // (cfg4: 90 %, visibility 21.2 -> 20.5 ms); over the full grid otherwise
         // (cfg2: 67 % empty, the grid's 8-column CTAs measured 0.4 ms faster).
         // Deciding needs the queue length first: a ~10 us host round trip.
+        // The previous loss call's non-empty fraction picks the path, so the
+        // grid path never waits for the queue length before launching.
         int nq = -1;
-        if (queue && trace && !std::getenv("CDR_NO_TRACE_QUEUE")) {
+        const bool qtrace = queue && trace && !std::getenv("CDR_NO_TRACE_QUEUE") &&
+                            (c->queue_frac_last < 0.25 || std::getenv("CDR_TRACE_QUEUE"));
+        if (qtrace) {
             CDR_CUDA_CHECK(cudaEventSynchronize(c->tile_queue_ev));
             nq = *c->tile_queue_host;
         }
-        if (nq >= 0 && (size_t(nq) * 4 < size_t(tile_total) || std::getenv("CDR_TRACE_QUEUE"))) {
+        if (qtrace) {
             Params pt = pc;
             pt.queue_mode = 1;
             pt.queue_len = nq;
@@ -1888,6 +1892,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
                 CDR_CUDA_CHECK(cudaEventSynchronize(c->tile_queue_ev));
                 nq = *c->tile_queue_host;
             }
+            c->queue_frac_last = double(nq) / double(std::max(1, tile_total));
             pc.queue_mode = 1;
             constexpr int kCPT = 4 / (kRenderThreads16 / 64);
             if (nq > 0) {
