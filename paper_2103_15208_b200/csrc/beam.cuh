@@ -299,6 +299,9 @@ static __device__ unsigned long long g_probe_stats[8];
 #define CDR_PSTAT(i, v)
 #endif
 
+// The scan keeps only the best hit's triangle, t and leaf; its barycentrics
+// are recomputed once at the end by the same ray_triangle (identical values),
+// which keeps two doubles per probe out of the scan's register set.
 struct ProbeScan {
     const BeamCand* cand;
     const unsigned char* lst;  // nullptr: scan the whole tile list
@@ -306,11 +309,45 @@ struct ProbeScan {
     int n, j;
     float lx, ly;
     int mode;  // 0 done, 1 scanning, 2 per-ray traversal
-    Hit best;
+    int tri, leaf;
+    double t;
 };
 
+__device__ __forceinline__ void probe_leaf_test(const TriRec* __restrict__ recs, int leaf, D3 o, D3 d, double t_min,
+                                                ProbeScan& s) {
+    const TriRec* p = recs + leaf;
+    const double2 a = __ldg(&p->a), b = __ldg(&p->b), c = __ldg(&p->c), dd = __ldg(&p->d);
+    const double e = __ldg(&p->e);
+    const int tri = __ldg(&p->tri);
+    double t, b1, b2;
+    if (ray_triangle(o, d, D3{a.x, a.y, b.x}, D3{b.y, c.x, c.y}, D3{dd.x, dd.y, e}, t, b1, b2) && t > t_min &&
+        (t < s.t || (t == s.t && tri < s.tri))) {
+        s.t = t;
+        s.tri = tri;
+        s.leaf = leaf;
+    }
+}
+
+// the Hit of a finished scan (barycentrics of its triangle, as leaf_test had them)
+__device__ __forceinline__ Hit probe_hit(const TriRec* __restrict__ recs, D3 o, D3 d, const ProbeScan& s) {
+    Hit h{-1, 1e300, 0.0, 0.0};
+    if (s.tri < 0) return h;
+    const TriRec* p = recs + s.leaf;
+    const double2 a = __ldg(&p->a), b = __ldg(&p->b), c = __ldg(&p->c), dd = __ldg(&p->d);
+    const double e = __ldg(&p->e);
+    double t, b1, b2;
+    ray_triangle(o, d, D3{a.x, a.y, b.x}, D3{b.y, c.x, c.y}, D3{dd.x, dd.y, e}, t, b1, b2);
+    h.tri = s.tri;
+    h.t = t;
+    h.b1 = b1;
+    h.b2 = b2;
+    return h;
+}
+
 __device__ __forceinline__ void probe_setup(const BeamView& bv, int vi, const DevCamera& cam, D2 x, ProbeScan& s) {
-    s.best = Hit{-1, 1e300, 0.0, 0.0};
+    s.tri = -1;
+    s.leaf = 0;
+    s.t = 1e300;
     s.mode = 2;
     s.j = 0;
     if (!bv.valid) {
@@ -363,11 +400,11 @@ __device__ __forceinline__ void probe_step(ProbeScan& s, const TriRec* __restric
     ++s.j;
     CDR_PSTAT(6, 1);
     const float4 ra = s.cand[k].a, rb = s.cand[k].b;
-    if (double(ra.x) > s.best.t) {  // every remaining candidate is farther
+    if (double(ra.x) > s.t) {  // every remaining candidate is farther
         s.mode = 0;
         return;
     }
-    if (cand_covers(ra, rb, s.lx, s.ly)) leaf_test(recs, cand_leaf(ra), o, d, t_min, s.best);
+    if (cand_covers(ra, rb, s.lx, s.ly)) probe_leaf_test(recs, cand_leaf(ra), o, d, t_min, s);
 }
 
 // Per-ray traversal for the rare probe without a usable list (off-image
@@ -389,8 +426,8 @@ __device__ __forceinline__ void trace_points2(const BeamView& bv, int vi, const 
         if (a.mode == 1) probe_step(a, recs, o, da, t_min);
         if (b.mode == 1) probe_step(b, recs, o, db, t_min);
     }
-    ha = a.mode == 2 ? trace_out_of_line(nodes, recs, n_tris, o, da, t_min) : a.best;
-    hb = b.mode == 2 ? trace_out_of_line(nodes, recs, n_tris, o, db, t_min) : b.best;
+    ha = a.mode == 2 ? trace_out_of_line(nodes, recs, n_tris, o, da, t_min) : probe_hit(recs, o, da, a);
+    hb = b.mode == 2 ? trace_out_of_line(nodes, recs, n_tris, o, db, t_min) : probe_hit(recs, o, db, b);
 }
 
 }  // namespace cdr
