@@ -862,6 +862,7 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
             set_view_calls(c, slots.data(), samples.data(), n);
             launch_silhouettes(c, n);
             launch_cdf(c, n);
+            launch_boundary_sampling(c, n, max_samples, st->seed);  // beside the render as well
         }
         CDR_CUDA_CHECK(cudaEventRecord(c->ev_sil, c->stream));
         CDR_CUDA_CHECK(cudaMemsetAsync(c->reg_vals.p, 0, sizeof(double) * 4, c->stream));
@@ -882,7 +883,7 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
     CDR_CUDA_CHECK(cudaEventRecord(ev[3], s));
     stage.emplace("cdr.boundary");
     if (st->boundary_term)  // the render above built candidate lists for exactly these views
-        launch_boundary(c, n, max_samples, st->seed, CDR_PROBE_RADIANCE, lay->positions, /*use_beam=*/true);
+        launch_boundary_probes(c, n, max_samples, st->seed, CDR_PROBE_RADIANCE, lay->positions, /*use_beam=*/true);
     CDR_CUDA_CHECK(cudaEventRecord(ev[4], s));
     stage.emplace("cdr.finalize (texel flush, normal chain, Laplacian)");
     launch_texel_flush(c, lay->diffuse, lay->specular, lay->roughness);

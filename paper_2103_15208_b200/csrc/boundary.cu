@@ -235,6 +235,7 @@ struct BParams {
     int m_stride;  // per-view stride of the sample arrays (max M)
     uint64_t seed;
     int probe;
+    int sample_adj;  // k_bsample drops zero-adjoint samples (else k_boundary does, before its probes)
     const double* adj;
     double* grad;
     int64_t lay_pos;
@@ -287,6 +288,7 @@ __device__ __forceinline__ bool boundary_setup(const BParams& p, int vi, int64_t
     if (b.sg->length_px < 1e-12) return false;
     b.s = rng.next_double();
     const cdr_segment* sg = b.sg;
+    if (!p.sample_adj) return true;  // the adjoint is not known yet: k_boundary checks it
     b.xq = D2{sg->q0[0] + (sg->q1[0] - sg->q0[0]) * b.s, sg->q0[1] + (sg->q1[1] - sg->q0[1]) * b.s};
     int px = int(floor(b.xq.x)), py = int(floor(b.xq.y));
     px = px < 0 ? 0 : (px > cam.W - 1 ? cam.W - 1 : px);
@@ -419,6 +421,7 @@ __device__ __forceinline__ int boundary_samples(const BParams& p, int vi, const 
         px = px < 0 ? 0 : (px > cam.W - 1 ? cam.W - 1 : px);
         py = py < 0 ? 0 : (py > cam.H - 1 ? cam.H - 1 : py);
         b.adj = ld3(p.adj + 3 * (p.pix_off[p.calls[vi].slot] + size_t(py) * cam.W + px));
+        if (b.adj.x == 0 && b.adj.y == 0 && b.adj.z == 0) act = false;  // diff_render.cpp:243-244: no probes
     }
     const int samples = p.calls[vi].samples;
     const double total_len = p.totals[3 * vi];
@@ -608,16 +611,9 @@ void launch_cdf(cdr_ctx* c, int n_views) {
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int probe,
-                     int64_t lay_pos, bool use_beam) {
-    if (n_views <= 0 || samples <= 0) return;
+static BParams boundary_params(cdr_ctx* c, int n_views, int samples, uint64_t seed, int probe, int64_t lay_pos,
+                               bool use_beam) {
     BStatics& st = bstatics(c);
-    size_t nslots = c->views.size();
-    std::vector<size_t> offs(nslots);
-    for (size_t i = 0; i < nslots; ++i) offs[i] = c->views[i].pix_off;
-    st.pix_off.ensure(nslots);
-    CDR_CUDA_CHECK(cudaMemcpyAsync(st.pix_off.p, offs.data(), sizeof(size_t) * nslots,
-                                   cudaMemcpyHostToDevice, c->stream));
     const int E = c->seg_stride;  // set_view_calls
     const size_t nm = size_t(n_views) * samples;
     const size_t nbins = size_t(n_views) * E * kSBins;
@@ -662,9 +658,50 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     p.s_param = c->b_s.p;
     p.sorted_si = c->b_sorted_si.p;
     p.sorted_s = c->b_sorted_s.p;
+    return p;
+}
+
+static void upload_pix_off(cdr_ctx* c) {
+    BStatics& st = bstatics(c);
+    const size_t nslots = c->views.size();
+    std::vector<size_t> offs(nslots);
+    for (size_t i = 0; i < nslots; ++i) offs[i] = c->views[i].pix_off;
+    st.pix_off.ensure(std::max<size_t>(1, nslots));
+    // pageable source: the copy is staged before cudaMemcpyAsync returns
+    CDR_CUDA_CHECK(cudaMemcpyAsync(st.pix_off.p, offs.data(), sizeof(size_t) * nslots, cudaMemcpyHostToDevice,
+                                   c->stream));
+}
+
+void launch_boundary_sampling(cdr_ctx* c, int n_views, int samples, uint64_t seed) {
+    if (n_views <= 0 || samples <= 0) return;
+    BParams p = boundary_params(c, n_views, samples, seed, CDR_PROBE_RADIANCE, 0, false);
+    p.sample_adj = 0;
     dim3 grid((samples + kBlock - 1) / kBlock, n_views);
     { ++c->launches; k_bsample<<<grid, kBlock, 0, c->stream>>>(p); }
-    { ++c->launches; k_bscan<<<n_views, 1024, 0, c->stream>>>(p.seg_count, p.count, E, p.seg_off, p.n_active); }
+    { ++c->launches; k_bscan<<<n_views, 1024, 0, c->stream>>>(p.seg_count, p.count, p.E, p.seg_off, p.n_active); }
+    { ++c->launches; k_bscatter<<<grid, kBlock, 0, c->stream>>>(p); }
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_boundary_probes(cdr_ctx* c, int n_views, int samples, uint64_t seed, int probe, int64_t lay_pos,
+                            bool use_beam) {
+    if (n_views <= 0 || samples <= 0) return;
+    upload_pix_off(c);
+    BParams p = boundary_params(c, n_views, samples, seed, probe, lay_pos, use_beam);
+    dim3 bgrid((samples + kBndBlock - 1) / kBndBlock, n_views);
+    { ++c->launches; k_boundary<<<bgrid, kBndBlock, 0, c->stream>>>(p); }
+    CDR_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int probe,
+                     int64_t lay_pos, bool use_beam) {
+    if (n_views <= 0 || samples <= 0) return;
+    upload_pix_off(c);
+    BParams p = boundary_params(c, n_views, samples, seed, probe, lay_pos, use_beam);
+    p.sample_adj = 1;  // the adjoint is on the device: sampling drops zero-adjoint samples itself
+    dim3 grid((samples + kBlock - 1) / kBlock, n_views);
+    { ++c->launches; k_bsample<<<grid, kBlock, 0, c->stream>>>(p); }
+    { ++c->launches; k_bscan<<<n_views, 1024, 0, c->stream>>>(p.seg_count, p.count, p.E, p.seg_off, p.n_active); }
     { ++c->launches; k_bscatter<<<grid, kBlock, 0, c->stream>>>(p); }
     dim3 bgrid((samples + kBndBlock - 1) / kBndBlock, n_views);
     { ++c->launches; k_boundary<<<bgrid, kBndBlock, 0, c->stream>>>(p); }

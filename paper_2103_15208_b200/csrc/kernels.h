@@ -87,6 +87,13 @@ void launch_cdf(cdr_ctx* c, int n_views);
 // for the same view list (cdr_loss_grad); otherwise per-ray traversal
 void launch_boundary(cdr_ctx* c, int n_views, int max_samples, uint64_t seed, int probe,
                      int64_t lay_pos, bool use_beam = false);
+// The same in two stages for the fused loss call: the edge samples' RNG picks,
+// CDF searches and binning need only the segments and the CDF, so they run on
+// the side stream beside the render; the probes and deposits follow the
+// render (they need its adjoint and candidate lists).
+void launch_boundary_sampling(cdr_ctx* c, int n_views, int max_samples, uint64_t seed);
+void launch_boundary_probes(cdr_ctx* c, int n_views, int max_samples, uint64_t seed, int probe, int64_t lay_pos,
+                            bool use_beam);
 // The boundary probes' visibility on its own (cdr_probe_points): n points of
 // the view at index vi of the last render call, traced in pairs through that
 // call's candidate lists exactly as k_boundary traces x -/+ n/2 (rgb nullable).
