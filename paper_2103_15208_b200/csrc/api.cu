@@ -271,6 +271,8 @@ int cdr_create(int device, cdr_ctx** out) {
         CDR_CUDA_CHECK(cudaSetDevice(device));
         CDR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
         CDR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        CDR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->bg, cudaStreamNonBlocking));
+        CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_bg, cudaEventDisableTiming));
         CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_sil, cudaEventDisableTiming));
         CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_reg, cudaEventDisableTiming));
@@ -293,6 +295,7 @@ void cdr_destroy(cdr_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->side) cudaStreamSynchronize(c->side);
+    if (c->bg) cudaStreamSynchronize(c->bg);
     free_render_statics(c);
     free_boundary_statics(c);
     if (c->nccl_comm && nccl().ok) nccl().commDestroy(c->nccl_comm);
@@ -304,6 +307,8 @@ void cdr_destroy(cdr_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_sil) cudaEventDestroy(c->ev_sil);
     if (c->ev_reg) cudaEventDestroy(c->ev_reg);
+    if (c->ev_bg) cudaEventDestroy(c->ev_bg);
+    if (c->bg) cudaStreamDestroy(c->bg);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;  // every DBuf member frees its device allocation (context.h)

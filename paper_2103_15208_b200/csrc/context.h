@@ -84,6 +84,8 @@ struct cdr_ctx {
     int device = 0;
     cudaStream_t side = nullptr;  // silhouettes + CDF and the regularisers run here, beside the render
     cudaEvent_t ev_fork = nullptr, ev_sil = nullptr, ev_reg = nullptr;
+    cudaStream_t bg = nullptr;  // k_background of a queue-mode render, beside k_trace / k_render
+    cudaEvent_t ev_bg = nullptr;
     cdr_ctx* geo = nullptr;  // geometry-only context of cdr_self_intersects / cdr_evolve (lazy)
     // Per-context scratch (device memory of this context's GPU): used inside one
     // synchronous entry point at a time, never across calls.

@@ -1795,6 +1795,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     // shading grid is exact and the GPU does not idle. Cuts the launch and
     // prologue of ~2/3 (cfg2) to ~9/10 (cfg4) of the shading CTAs.
     const bool queue = p.skip_empty_hits && n_chunks == 1 && !std::getenv("CDR_NO_QUEUE");
+    const bool bg_side = c->bg && !std::getenv("CDR_BG_INLINE");  // CDR_BG_INLINE: k_background after k_render
     if (queue) {
         c->tile_queue.ensure(std::max(1, tile_total));
         c->tile_queue_count.ensure(1 + (tile_total + kQBlock - 1) / kQBlock);  // [0] total, then per-block offsets
@@ -1859,6 +1860,14 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             CDR_CUDA_CHECK(cudaMemcpyAsync(c->tile_queue_host, p.tile_queue_count, sizeof(int), cudaMemcpyDeviceToHost,
                                            c->stream));
             CDR_CUDA_CHECK(cudaEventRecord(c->tile_queue_ev, c->stream));
+            if (bg_side) {
+                // the empty tiles' pixels (HBM-bound) beside k_trace and
+                // k_render (latency-bound); joined at the end of this call
+                CDR_CUDA_CHECK(cudaStreamWaitEvent(c->bg, c->tile_queue_ev, 0));
+                ++c->launches;
+                k_background<<<dim3((maxW * maxH + 255) / 256, nv), 256, 0, c->bg>>>(pc);
+                CDR_CUDA_CHECK(cudaEventRecord(c->ev_bg, c->bg));
+            }
         }
         // k_trace over the (tile-ordered) queue when most tiles are empty
         // (cfg4: 90 %, visibility 21.2 -> 20.5 ms); over the full grid otherwise
@@ -1903,13 +1912,16 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
                 else
                     k_render<true, true, false, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
             }
-            ++c->launches;
-            k_background<<<dim3((maxW * maxH + 255) / 256, nv), 256, 0, c->stream>>>(pc);
+            if (!bg_side) {
+                ++c->launches;
+                k_background<<<dim3((maxW * maxH + 255) / 256, nv), 256, 0, c->stream>>>(pc);
+            }
         } else {
             launch_render_kernel(pc, grid, c, trace, loss, interior);
         }
     }
     if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * n_chunks], c->stream));
+    if (queue && bg_side) CDR_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_bg, 0));
     if (p.use_beam) {
         if (!c->beam_used_host) CDR_CUDA_CHECK(cudaHostAlloc(&c->beam_used_host, sizeof(int), cudaHostAllocDefault));
         CDR_CUDA_CHECK(cudaMemcpyAsync(c->beam_used_host, c->beam_used.p, sizeof(int), cudaMemcpyDeviceToHost,
