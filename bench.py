@@ -19,7 +19,9 @@ silhouettes + boundary edge sampling, normal chain, cotangent Laplacian.
           before each step), inputs resident in HBM, gradient left on device.
   e2e   : the same step through the C-ABI with HOST buffers: positions and the
           three texture maps uploaded from pinned memory and the gradient
-          downloaded every step (wall clock around the blocking C-ABI call);
+          downloaded every step (wall clock around the blocking C-ABI calls:
+          cdr_stage_params + cdr_loss_grad, which overlaps the copies with its
+          kernels; e2e.separate_uploads = synchronous uploads before the call);
           e2e.with_rendered_images adds total_loss's K rendered images + masks
           (TotalLossResult::rendered, losses.cpp:259) to the download.
   cpu_baseline : the reference library compiled from its own sources
@@ -450,7 +452,7 @@ def main(argv=None):
                  "primary_rays": s0["shaded_samples"], "ms_visibility": ms_trace,
                  "probe_Mrays_per_s": 2 * s0["boundary_active"] / (ms_bnd / 1e3) / 1e6,
                  "probe_rays": 2 * s0["boundary_active"], "ms_boundary": ms_bnd,
-                 "note": "per rank; visibility = candidate lists + trace; boundary = sampling + probes + deposits"}
+                 "note": "per rank; visibility = candidate lists + trace; boundary = probes + deposits (the sampling kernels run on the side stream beside the render)"}
 
     # ---- e2e: host buffers through the C-ABI
     e2e = None
@@ -459,42 +461,45 @@ def main(argv=None):
         pos_h = pin(scene.mesh.positions)
         d_h, s_h, r_h = pin(scene.diffuse), pin(scene.specular), pin(scene.roughness)
         g_h = pin(np.zeros(lay["total"]))
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            r.update_positions(pos_h)
-            r.set_textures(d_h, s_h, r_h)
-            r.loss_grad(views, st, lay, grad=g_h, overwrite=True)  # fresh gradient, as total_loss
-        barrier()
-        dt = time.perf_counter() - t0
-        te = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
-        if dist is not None:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        # positions + maps up; the step's gradient (and the two loss terms) down
-        h2d = pos_h.nbytes + d_h.nbytes + s_h.nbytes + r_h.nbytes
-        d2h = g_h.nbytes + 16
-        e2e = {"value": total_samples / float(te.item()) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * float(te.item()) / args.steps,
-               "what": "cdr_loss_grad with host buffers: positions + 3 maps up, gradient + loss down"}
-        # the same with total_loss's rendered images and masks (the K Images of
-        # TotalLossResult, losses.cpp:259) downloaded into pinned buffers too
         npx = sum(c.width * c.height for c in scene.cameras)
         rgb_h, msk_h = pin(np.zeros(3 * npx)), pin(np.zeros(npx))
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            r.update_positions(pos_h)
-            r.set_textures(d_h, s_h, r_h)
-            r.loss_grad(views, st, lay, grad=g_h, overwrite=True, rendered_out=rgb_h, mask_out=msk_h)
-        barrier()
-        dt = time.perf_counter() - t0
-        te = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
-        if dist is not None:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+
+        def timed_e2e(staged, images):
+            # one step = positions + 3 maps up, the loss call, the gradient
+            # (+ the K rendered images and masks) and the loss terms down
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                if staged:  # cdr_stage_params: read by the loss call, copies overlapped with its kernels
+                    r.stage_params(pos_h, (d_h, s_h, r_h))
+                else:       # separate synchronous uploads before the call
+                    r.update_positions(pos_h)
+                    r.set_textures(d_h, s_h, r_h)
+                r.loss_grad(views, st, lay, grad=g_h, overwrite=True,  # fresh gradient, as total_loss
+                            rendered_out=rgb_h if images else None, mask_out=msk_h if images else None)
+            barrier()
+            te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=f"cuda:{local}")
+            if dist is not None:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            return float(te.item())
+
+        h2d = pos_h.nbytes + d_h.nbytes + s_h.nbytes + r_h.nbytes
+        d2h = g_h.nbytes + 16
+        dt = timed_e2e(True, False)
+        e2e = {"value": total_samples / dt / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": 1e3 * dt / args.steps,
+               "what": "cdr_stage_params + cdr_loss_grad with pinned host buffers: positions + 3 maps up, "
+                       "gradient + loss down (maps up beside the visibility pass, map gradient down beside "
+                       "the boundary pass)"}
+        dt = timed_e2e(False, False)
+        e2e["separate_uploads"] = {"value": total_samples / dt / 1e6, "ms_per_step": 1e3 * dt / args.steps,
+                                   "what": "cdr_update_positions + cdr_set_textures, then cdr_loss_grad"}
+        # the same with total_loss's rendered images and masks (the K Images of
+        # TotalLossResult, losses.cpp:259) downloaded into pinned buffers too
+        dt = timed_e2e(True, True)
         e2e["with_rendered_images"] = {
-            "value": total_samples / float(te.item()) / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h + rgb_h.nbytes + msk_h.nbytes),
-            "ms_per_step": 1e3 * float(te.item()) / args.steps}
+            "value": total_samples / dt / 1e6, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h + rgb_h.nbytes + msk_h.nbytes), "ms_per_step": 1e3 * dt / args.steps}
 
     # ---- the four mesh/material regularisers of total_loss (losses.cpp:272-292)
     # at the reference's default weights: texture-size work, not per sample, so

@@ -160,6 +160,20 @@ int cdr_get_edges(cdr_ctx* ctx, int32_t* edges_out /* E x 4 */, int32_t* n_edges
 /* MaterialMaps (material.hpp:22-26). */
 int cdr_set_textures(cdr_ctx* ctx, const double* diffuse, const double* specular,
                      const double* roughness, int32_t width, int32_t height);
+/* The next cdr_loss_grad / cdr_total_loss's parameters, read during that
+ * call: positions (3V, NULL = unchanged) and the three maps (all or none,
+ * as cdr_set_textures). The call uploads the maps on a copy stream beside
+ * its visibility pass, and with CDR_FLAG_GRAD_OVERWRITE on one rank it
+ * downloads the map/light gradient and the rendered images beside its
+ * boundary pass. Same results as cdr_update_positions + cdr_set_textures
+ * just before the call; the buffers must stay valid and unchanged until it
+ * returns (pinned buffers overlap; pageable ones are copied at its start).
+ * Any other entry point applies staged parameters first, synchronously.
+ * Replaces the per-iteration `apply` + `total_loss(mesh, material, ...)`
+ * hand-off of the reference optimiser (coarse_to_fine.cpp:157-158,
+ * losses.hpp:94-96). */
+int cdr_stage_params(cdr_ctx* ctx, const double* positions, const double* diffuse, const double* specular,
+                     const double* roughness, int32_t width, int32_t height);
 /* CollocatedLight::intensity, Scene::background (scene.hpp:13-23). */
 int cdr_set_light(cdr_ctx* ctx, const double intensity[3], const double background[3]);
 /* Scene::views (scene.hpp:21). global_ids may be NULL (= 0..n-1). */

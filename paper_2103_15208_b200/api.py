@@ -133,6 +133,7 @@ def load_library(path: str = LIB_PATH):
     L.cdr_update_positions.argtypes = [_vp, _d]
     L.cdr_get_edges.argtypes = [_vp, _i, _i]
     L.cdr_set_textures.argtypes = [_vp, _d, _d, _d, C.c_int32, C.c_int32]
+    L.cdr_stage_params.argtypes = [_vp, _d, _d, _d, _d, C.c_int32, C.c_int32]
     L.cdr_set_light.argtypes = [_vp, _d, _d]
     L.cdr_set_views.argtypes = [_vp, _vp, _i, C.c_int32]
     L.cdr_set_target.argtypes = [_vp, C.c_int32, _d, _d]
@@ -330,6 +331,23 @@ class Renderer:
         r = np.ascontiguousarray(roughness, dtype=np.float64)
         h, w = r.shape[:2]
         self._chk(self.L.cdr_set_textures(self.h, _dp(d), _dp(s), _dp(r), w, h))
+
+    def stage_params(self, positions=None, maps=None):
+        """Parameters read by the next loss_grad / total_loss call
+        (cdr_stage_params): positions (V x 3) and/or maps = (diffuse,
+        specular, roughness). With pinned arrays the maps' upload and the
+        gradient/image downloads overlap that call's kernels. The arrays are
+        kept referenced here until then (the library reads them in the call)."""
+        pos = None if positions is None else np.ascontiguousarray(positions, dtype=np.float64)
+        d = s = r = None
+        w = h = 0
+        if maps is not None:
+            if len(maps) != 3 or any(m is None for m in maps):
+                raise ValueError("maps = (diffuse, specular, roughness), all three")
+            d, s, r = (np.ascontiguousarray(m, dtype=np.float64) for m in maps)
+            h, w = r.shape[:2]
+        self._staged = (pos, d, s, r)
+        self._chk(self.L.cdr_stage_params(self.h, _dp(pos), _dp(d), _dp(s), _dp(r), w, h))
 
     def set_light(self, intensity, background=(0.0, 0.0, 0.0)):
         a = np.asarray(intensity, dtype=np.float64)

@@ -16,6 +16,7 @@
 #include <memory>
 #include <new>
 #include <optional>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -34,20 +35,41 @@ struct ApiErr : std::runtime_error {
     ApiErr(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 
-int handle(cdr_ctx* c, const std::function<void()>& fn);
+int handle(cdr_ctx* c, const std::function<void()>& fn, bool staged_consumer = false);
 
 #define API_BEGIN(ctx)                                            \
     if (!(ctx)) return CDR_ERR_INVALID_ARG;                       \
     return handle((ctx), [&]() {
 #define API_END \
     });
+// the loss entry points consume cdr_stage_params' parameters themselves
+#define API_BEGIN_STAGED(ctx)                                     \
+    if (!(ctx)) return CDR_ERR_INVALID_ARG;                       \
+    return handle((ctx), [&]() {
+#define API_END_STAGED \
+    }, true);
 
-int handle(cdr_ctx* c, const std::function<void()>& fn) {
+void apply_staged_sync(cdr_ctx* c);
+int handle_error(cdr_ctx* c);
+
+int handle(cdr_ctx* c, const std::function<void()>& fn, bool staged_consumer) {
     try {
         if (cudaSetDevice(c->device) != cudaSuccess) throw ApiErr(CDR_ERR_NO_DEVICE, "cudaSetDevice failed");
+        if (!staged_consumer) apply_staged_sync(c);  // as cdr_update_positions + cdr_set_textures now
         fn();
         c->err.clear();
         return CDR_OK;
+    } catch (...) {
+        // no copy may still read a caller's buffer once the call has returned
+        if (c->copy) cudaStreamSynchronize(c->copy);
+        c->staged = cdr_ctx::Staged{};
+        return handle_error(c);
+    }
+}
+
+int handle_error(cdr_ctx* c) {
+    try {
+        throw;
     } catch (const SizeMismatchErr& e) {
         c->err = e.what();
         return CDR_ERR_SIZE_MISMATCH;
@@ -62,6 +84,9 @@ int handle(cdr_ctx* c, const std::function<void()>& fn) {
         return CDR_ERR_CUDA;
     } catch (const std::exception& e) {
         c->err = e.what();
+        return CDR_ERR_ERROR;
+    } catch (...) {
+        c->err = "unknown error";
         return CDR_ERR_ERROR;
     }
 }
@@ -122,9 +147,9 @@ RenderArgs render_args(const cdr_ctx* c, const cdr_settings* s, const cdr_layout
     return a;
 }
 
-void check_layout(const cdr_ctx* c, const cdr_layout* lay) {
+void check_layout(const cdr_ctx* c, const cdr_layout* lay, int tw = -1, int th = -1) {
     if (!lay) throw ApiErr(CDR_ERR_INVALID_ARG, "layout is null");
-    int64_t n = int64_t(c->tw) * c->th;
+    int64_t n = tw >= 0 ? int64_t(tw) * th : int64_t(c->tw) * c->th;
     auto seg = [&](int64_t off, int64_t size, const char* name) {
         if (off < 0 || off + size > lay->total)
             throw SizeMismatchErr(std::string("gradient layout segment ") + name + " out of range");
@@ -238,6 +263,35 @@ void nccl_check(int r, const char* what) {
 
 constexpr int kNcclFloat64 = 8, kNcclSum = 0;
 
+// Enqueues the maps' upload and the texel packing on c->stream (no sync).
+void set_textures_impl(cdr_ctx* c, const double* diffuse, const double* specular, const double* roughness,
+                              int32_t w, int32_t h) {
+    if (w <= 0 || h <= 0 || !diffuse || !specular || !roughness)
+        throw ApiErr(CDR_ERR_INVALID_ARG, "bad texture arguments");
+    size_t n = size_t(w) * h;
+    c->tw = w;
+    c->th = h;
+    c->tex.ensure(n);
+    // fp64 maps stay resident (regularisers); shading reads fp32 texel records
+    h2d(c->map_d, diffuse, 3 * n, c->stream);
+    h2d(c->map_s, specular, 3 * n, c->stream);
+    h2d(c->map_r, roughness, n, c->stream);
+    launch_pack_textures(c, c->map_d.p, c->map_s.p, c->map_r.p, int(n));
+}
+
+// Staged parameters applied now, as cdr_update_positions + cdr_set_textures
+// would have (any entry point other than the loss calls).
+void apply_staged_sync(cdr_ctx* c) {
+    if (!c->staged.pos && !c->staged.d) return;
+    const cdr_ctx::Staged sp = std::exchange(c->staged, cdr_ctx::Staged{});
+    if (sp.pos && c->V > 0) {
+        CDR_CUDA_CHECK(cudaMemcpyAsync(c->pos.p, sp.pos, sizeof(double) * 3 * size_t(c->V), cudaMemcpyHostToDevice,
+                                       c->stream));
+        c->geometry_dirty = true;
+    }
+    if (sp.d) set_textures_impl(c, sp.d, sp.s, sp.r, sp.w, sp.h);
+    sync(c);
+}
 }  // namespace
 
 extern "C" {
@@ -273,6 +327,9 @@ int cdr_create(int device, cdr_ctx** out) {
         CDR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         CDR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->bg, cudaStreamNonBlocking));
         CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_bg, cudaEventDisableTiming));
+        CDR_CUDA_CHECK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+        CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming));
+        CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_maps, cudaEventDisableTiming));
         CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_sil, cudaEventDisableTiming));
         CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_reg, cudaEventDisableTiming));
@@ -296,6 +353,7 @@ void cdr_destroy(cdr_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->side) cudaStreamSynchronize(c->side);
     if (c->bg) cudaStreamSynchronize(c->bg);
+    if (c->copy) cudaStreamSynchronize(c->copy);
     free_render_statics(c);
     free_boundary_statics(c);
     if (c->nccl_comm && nccl().ok) nccl().commDestroy(c->nccl_comm);
@@ -308,6 +366,9 @@ void cdr_destroy(cdr_ctx* c) {
     if (c->ev_sil) cudaEventDestroy(c->ev_sil);
     if (c->ev_reg) cudaEventDestroy(c->ev_reg);
     if (c->ev_bg) cudaEventDestroy(c->ev_bg);
+    if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+    if (c->ev_maps) cudaEventDestroy(c->ev_maps);
+    if (c->copy) cudaStreamDestroy(c->copy);
     if (c->bg) cudaStreamDestroy(c->bg);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -459,6 +520,7 @@ int cdr_update_positions(cdr_ctx* c, const double* positions) {
         CDR_CUDA_CHECK(cudaMemcpyAsync(c->pos.p, positions, sizeof(double) * 3 * size_t(c->V),
                                        cudaMemcpyHostToDevice, c->stream));
     c->geometry_dirty = true;
+    sync(c);  // a pinned buffer is read asynchronously: done before the caller can reuse it
     API_END
 }
 
@@ -472,18 +534,26 @@ int cdr_get_edges(cdr_ctx* c, int32_t* out, int32_t* n) {
 int cdr_set_textures(cdr_ctx* c, const double* diffuse, const double* specular, const double* roughness,
                      int32_t w, int32_t h) {
     API_BEGIN(c)
-    if (w <= 0 || h <= 0 || !diffuse || !specular || !roughness)
-        throw ApiErr(CDR_ERR_INVALID_ARG, "bad texture arguments");
-    size_t n = size_t(w) * h;
-    c->tw = w;
-    c->th = h;
-    c->tex.ensure(n);
-    // fp64 maps stay resident (regularisers); shading reads fp32 texel records
-    h2d(c->map_d, diffuse, 3 * n, c->stream);
-    h2d(c->map_s, specular, 3 * n, c->stream);
-    h2d(c->map_r, roughness, n, c->stream);
-    launch_pack_textures(c, c->map_d.p, c->map_s.p, c->map_r.p, int(n));
+    set_textures_impl(c, diffuse, specular, roughness, w, h);
     sync(c);
+    API_END
+}
+
+
+int cdr_stage_params(cdr_ctx* c, const double* positions, const double* diffuse, const double* specular,
+                     const double* roughness, int32_t w, int32_t h) {
+    API_BEGIN(c)  // (applies anything staged before)
+    const bool maps = diffuse || specular || roughness;
+    if (maps && (!diffuse || !specular || !roughness || w <= 0 || h <= 0))
+        throw ApiErr(CDR_ERR_INVALID_ARG, "bad texture arguments");
+    c->staged.pos = positions;
+    if (maps) {
+        c->staged.d = diffuse;
+        c->staged.s = specular;
+        c->staged.r = roughness;
+        c->staged.w = w;
+        c->staged.h = h;
+    }
     API_END
 }
 
@@ -810,6 +880,56 @@ struct OnSideStream {
     explicit OnSideStream(cdr_ctx* ctx) : c(ctx) { std::swap(c->stream, c->side); }
     ~OnSideStream() { std::swap(c->stream, c->side); }
 };
+struct OnCopyStream {
+    cdr_ctx* c;
+    explicit OnCopyStream(cdr_ctx* ctx) : c(ctx) { std::swap(c->stream, c->copy); }
+    ~OnCopyStream() { std::swap(c->stream, c->copy); }
+};
+
+// Page-locked host memory (cudaHostAlloc / cudaHostRegister): a copy into it
+// on the copy stream runs asynchronously. Pageable destinations are copied
+// at the end of the call as before (a pageable device-to-host copy blocks the
+// host, which would hold back the launches behind it).
+static bool is_pinned(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// [off, off + n) pieces of a gradient layout
+struct Span {
+    int64_t off, n;
+};
+// The map and light segments of `lay` (final once the render and the texel
+// flush are done, while the boundary pass still adds to the positions) when
+// all segments are pairwise disjoint; empty otherwise.
+static std::vector<Span> early_spans(const cdr_ctx* c, const cdr_layout* lay) {
+    const int64_t nt = int64_t(c->tw) * c->th;
+    std::vector<Span> all{{lay->positions, 3 * int64_t(c->V)}, {lay->diffuse, 3 * nt}, {lay->specular, 3 * nt},
+                          {lay->roughness, nt}};
+    if (lay->light >= 0) all.push_back({lay->light, 3});
+    std::vector<Span> sorted = all;
+    std::sort(sorted.begin(), sorted.end(), [](const Span& a, const Span& b) { return a.off < b.off; });
+    for (size_t i = 1; i < sorted.size(); ++i)
+        if (sorted[i - 1].off + sorted[i - 1].n > sorted[i].off) return {};
+    return std::vector<Span>(all.begin() + 1, all.end());
+}
+// [0, total) minus the (disjoint) spans
+static std::vector<Span> complement(std::vector<Span> sp, int64_t total) {
+    std::sort(sp.begin(), sp.end(), [](const Span& a, const Span& b) { return a.off < b.off; });
+    std::vector<Span> out;
+    int64_t at = 0;
+    for (const Span& x : sp) {
+        if (x.off > at) out.push_back({at, x.off - at});
+        at = std::max(at, x.off + x.n);
+    }
+    if (total > at) out.push_back({at, total - at});
+    return out;
+}
 
 // The fused total_loss pipeline (losses.cpp:244-297). terms[6] = rend, lap,
 // normal, edge, spec, roug; reg == nullptr leaves the last four at 0.
@@ -818,7 +938,10 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
                     const cdr_layout* lay, double* terms_out, double* grad, double* rendered_rgb,
                     double* rendered_mask, cdr_stats* stats) {
     if (!st || n < 0 || (n > 0 && !views)) throw ApiErr(CDR_ERR_INVALID_ARG, "bad arguments");
-    check_layout(c, lay);
+    // parameters staged by cdr_stage_params: uploaded below, after every check
+    const cdr_ctx::Staged sp = std::exchange(c->staged, cdr_ctx::Staged{});
+    if (sp.d) check_layout(c, lay, sp.w, sp.h);
+    else check_layout(c, lay);
     check_ready(c);
     const int spp = spp_of(st);
     check_spp(spp);
@@ -840,6 +963,23 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
     cudaStream_t s = c->stream;
     auto& ev = c->ev;
     c->launches = 0;
+    if (sp.pos && c->V > 0) {  // needed first (normals, LBVH): on the main stream
+        CDR_CUDA_CHECK(cudaMemcpyAsync(c->pos.p, sp.pos, sizeof(double) * 3 * size_t(c->V), cudaMemcpyHostToDevice, s));
+        c->geometry_dirty = true;
+    }
+    // staged maps: upload + texel packing on the copy stream, beside the
+    // LBVH, silhouettes and visibility; joined before the regularisers and
+    // the shading (pinned buffers overlap; pageable ones block here)
+    const bool maps_pending = sp.d != nullptr;
+    if (maps_pending) {
+        CDR_CUDA_CHECK(cudaEventRecord(c->ev_copy, s));
+        CDR_CUDA_CHECK(cudaStreamWaitEvent(c->copy, c->ev_copy, 0));
+        {
+            OnCopyStream cs(c);
+            set_textures_impl(c, sp.d, sp.s, sp.r, sp.w, sp.h);
+        }
+        CDR_CUDA_CHECK(cudaEventRecord(c->ev_maps, c->copy));
+    }
     std::optional<NvtxRange> stage(std::in_place, "cdr.prepare (normals, LBVH)");
     CDR_CUDA_CHECK(cudaEventRecord(ev[0], s));
     zero_grad(c, lay->total);  // fresh GradVector (losses.cpp:250)
@@ -872,6 +1012,7 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
         CDR_CUDA_CHECK(cudaEventRecord(c->ev_sil, c->stream));
         CDR_CUDA_CHECK(cudaMemsetAsync(c->reg_vals.p, 0, sizeof(double) * 4, c->stream));
         if (reg_here) {
+            if (maps_pending) CDR_CUDA_CHECK(cudaStreamWaitEvent(c->stream, c->ev_maps, 0));
             c->reg_grad.ensure(std::max<int64_t>(1, lay->total));
             CDR_CUDA_CHECK(cudaMemsetAsync(c->reg_grad.p, 0, sizeof(double) * std::max<int64_t>(1, lay->total),
                                            c->stream));
@@ -882,8 +1023,48 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
     RenderArgs a = render_args(c, st, lay);
     a.use_mask = use_mask;
     stage.emplace("cdr.render (lists, trace, shade+loss+interior)");
+    if (maps_pending) {  // the list builders and k_trace read no texel: join just before the shading
+        a.wait_before_shade = c->ev_maps;
+    }
     launch_render(c, slots.data(), n, a, true, true, true, scales.data(), ev[7]);
     CDR_CUDA_CHECK(cudaEventRecord(ev[2], s));
+    // Downloads that need only the render run on the copy stream beside the
+    // boundary pass: the K images, then (one rank, overwrite) the map and
+    // light segments of the gradient once the texel flush has written them.
+    const bool out_images = (rendered_rgb || rendered_mask) && (!rendered_rgb || is_pinned(rendered_rgb)) &&
+                            (!rendered_mask || is_pinned(rendered_mask));
+    if (out_images) {
+        CDR_CUDA_CHECK(cudaEventRecord(c->ev_copy, s));
+        CDR_CUDA_CHECK(cudaStreamWaitEvent(c->copy, c->ev_copy, 0));
+        size_t ro = 0, mo = 0;
+        for (int i = 0; i < n; ++i) {
+            const ViewData& v = c->views[slots[i]];
+            size_t np = size_t(v.cam.W) * v.cam.H;
+            if (rendered_rgb)
+                CDR_CUDA_CHECK(cudaMemcpyAsync(rendered_rgb + ro, c->img.p + 3 * v.pix_off, sizeof(double) * 3 * np,
+                                               cudaMemcpyDeviceToHost, c->copy));
+            if (rendered_mask)
+                CDR_CUDA_CHECK(cudaMemcpyAsync(rendered_mask + mo, c->mask.p + v.pix_off, sizeof(double) * np,
+                                               cudaMemcpyDeviceToHost, c->copy));
+            ro += 3 * np;
+            mo += np;
+        }
+    }
+    launch_texel_flush(c, lay->diffuse, lay->specular, lay->roughness);  // independent of the boundary pass
+    const std::vector<Span> early =
+        (grad && (st->flags & CDR_FLAG_GRAD_OVERWRITE) && !c->nccl_comm && is_pinned(grad)) ? early_spans(c, lay)
+                                                                                             : std::vector<Span>{};
+    if (!early.empty()) {
+        CDR_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_reg, 0));  // the regularisers' map gradient
+        if (reg_here)
+            for (const Span& x : early) launch_axpy(c, c->grad.p + x.off, c->reg_grad.p + x.off, x.n);
+        CDR_CUDA_CHECK(cudaEventRecord(c->ev_copy, s));
+        CDR_CUDA_CHECK(cudaStreamWaitEvent(c->copy, c->ev_copy, 0));
+        for (const Span& x : early)
+            if (x.n > 0)
+                CDR_CUDA_CHECK(cudaMemcpyAsync(grad + x.off, c->grad.p + x.off, sizeof(double) * x.n,
+                                               cudaMemcpyDeviceToHost, c->copy));
+    }
     CDR_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_sil, 0));  // segments + CDF for the boundary pass
     CDR_CUDA_CHECK(cudaEventRecord(ev[3], s));
     stage.emplace("cdr.boundary");
@@ -891,11 +1072,12 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
         launch_boundary_probes(c, n, max_samples, st->seed, CDR_PROBE_RADIANCE, lay->positions, /*use_beam=*/true);
     CDR_CUDA_CHECK(cudaEventRecord(ev[4], s));
     stage.emplace("cdr.finalize (texel flush, normal chain, Laplacian)");
-    launch_texel_flush(c, lay->diffuse, lay->specular, lay->roughness);
     launch_finalize_positions(c, lay->positions);
     if (lap_here) launch_laplacian(c, lap_mode, lambda_lap, c->grad.p + lay->positions);
     CDR_CUDA_CHECK(cudaStreamWaitEvent(s, c->ev_reg, 0));  // the regularisers' gradient and values
-    if (reg_here) launch_axpy(c, c->grad.p, c->reg_grad.p, lay->total);  // grad += reg_grad
+    const std::vector<Span> late = early.empty() ? std::vector<Span>{{0, lay->total}} : complement(early, lay->total);
+    if (reg_here)  // grad += reg_grad (the early segments got theirs above)
+        for (const Span& x : late) launch_axpy(c, c->grad.p + x.off, c->reg_grad.p + x.off, x.n);
     CDR_CUDA_CHECK(cudaEventRecord(ev[5], s));
     stage.emplace("cdr.allreduce + download");
     if (c->nccl_comm)
@@ -909,24 +1091,31 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
         CDR_CUDA_CHECK(cudaMemcpyAsync(&lap_sq, c->lap_partial.p, sizeof(double), cudaMemcpyDeviceToHost, s));
     double regv[4] = {0, 0, 0, 0};
     CDR_CUDA_CHECK(cudaMemcpyAsync(regv, c->reg_vals.p, sizeof(regv), cudaMemcpyDeviceToHost, s));
-    if (grad && (st->flags & CDR_FLAG_GRAD_OVERWRITE))
-        CDR_CUDA_CHECK(cudaMemcpyAsync(grad, c->grad.p, sizeof(double) * lay->total, cudaMemcpyDeviceToHost, s));
-    else if (grad)
+    if (grad && (st->flags & CDR_FLAG_GRAD_OVERWRITE)) {
+        for (const Span& x : late)
+            if (x.n > 0)
+                CDR_CUDA_CHECK(cudaMemcpyAsync(grad + x.off, c->grad.p + x.off, sizeof(double) * x.n,
+                                               cudaMemcpyDeviceToHost, s));
+    } else if (grad) {
         add_grad_to_host(c, grad, 0, lay->total);
-    size_t ro = 0, mo = 0;
-    for (int i = 0; i < n; ++i) {
-        const ViewData& v = c->views[slots[i]];
-        size_t np = size_t(v.cam.W) * v.cam.H;
-        if (rendered_rgb)
-            CDR_CUDA_CHECK(cudaMemcpyAsync(rendered_rgb + ro, c->img.p + 3 * v.pix_off, sizeof(double) * 3 * np,
-                                           cudaMemcpyDeviceToHost, s));
-        if (rendered_mask)
-            CDR_CUDA_CHECK(cudaMemcpyAsync(rendered_mask + mo, c->mask.p + v.pix_off, sizeof(double) * np,
-                                           cudaMemcpyDeviceToHost, s));
-        ro += 3 * np;
-        mo += np;
+    }
+    if (!out_images) {  // pageable (or no) image buffers: at the end, on the main stream
+        size_t ro = 0, mo = 0;
+        for (int i = 0; i < n; ++i) {
+            const ViewData& v = c->views[slots[i]];
+            size_t np = size_t(v.cam.W) * v.cam.H;
+            if (rendered_rgb)
+                CDR_CUDA_CHECK(cudaMemcpyAsync(rendered_rgb + ro, c->img.p + 3 * v.pix_off, sizeof(double) * 3 * np,
+                                               cudaMemcpyDeviceToHost, s));
+            if (rendered_mask)
+                CDR_CUDA_CHECK(cudaMemcpyAsync(rendered_mask + mo, c->mask.p + v.pix_off, sizeof(double) * np,
+                                               cudaMemcpyDeviceToHost, s));
+            ro += 3 * np;
+            mo += np;
+        }
     }
     sync(c);
+    CDR_CUDA_CHECK(cudaStreamSynchronize(c->copy));
     raise_device_error(c);
     // rendering term in view order, each view scale * Σ m|d| (losses.cpp:44-47, :257)
     double terms[6] = {0.0, lap_here ? lambda_lap * lap_sq : 0.0, regv[0], regv[1], regv[2], regv[3]};
@@ -986,7 +1175,7 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
 int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_settings* st, double lambda_rend,
                   double lambda_lap, int32_t lap_mode, int32_t use_mask, const cdr_layout* lay, double* loss_out,
                   double* grad, double* rendered_rgb, double* rendered_mask, cdr_stats* stats) {
-    API_BEGIN(c)
+    API_BEGIN_STAGED(c)
     double terms[6];
     loss_grad_impl(c, views, n, st, lambda_rend, lambda_lap, nullptr, lap_mode, use_mask, lay, terms, grad,
                    rendered_rgb, rendered_mask, stats);
@@ -994,14 +1183,14 @@ int cdr_loss_grad(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_setting
         loss_out[0] = terms[0];
         loss_out[1] = terms[1];
     }
-    API_END
+    API_END_STAGED
 }
 
 int cdr_total_loss(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_settings* st, double lambda_rend,
                    double lambda_lap, const cdr_reg_weights* reg, int32_t lap_mode, int32_t use_mask,
                    const cdr_layout* lay, double* breakdown, double* grad, double* rendered_rgb,
                    double* rendered_mask, cdr_stats* stats) {
-    API_BEGIN(c)
+    API_BEGIN_STAGED(c)
     if (!reg) throw ApiErr(CDR_ERR_INVALID_ARG, "reg weights are required");
     double t[6];
     loss_grad_impl(c, views, n, st, lambda_rend, lambda_lap, reg, lap_mode, use_mask, lay, t, grad, rendered_rgb,
@@ -1010,7 +1199,7 @@ int cdr_total_loss(cdr_ctx* c, const int32_t* views, int32_t n, const cdr_settin
         breakdown[0] = t[0] + t[1] + t[2] + t[3] + t[4] + t[5];
         for (int i = 0; i < 6; ++i) breakdown[1 + i] = t[i];
     }
-    API_END
+    API_END_STAGED
 }
 
 int cdr_regularisers(cdr_ctx* c, const cdr_reg_weights* reg, const cdr_layout* lay, double* values,

@@ -86,6 +86,16 @@ struct cdr_ctx {
     cudaEvent_t ev_fork = nullptr, ev_sil = nullptr, ev_reg = nullptr;
     cudaStream_t bg = nullptr;  // k_background of a queue-mode render, beside k_trace / k_render
     cudaEvent_t ev_bg = nullptr;
+    // cdr_stage_params: host parameters read by the next loss call (maps
+    // uploaded on `copy` beside the visibility pass; gradient pieces and
+    // images downloaded on `copy` beside the boundary pass)
+    struct Staged {
+        const double* pos = nullptr;
+        const double *d = nullptr, *s = nullptr, *r = nullptr;
+        int w = 0, h = 0;
+    } staged;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_copy = nullptr, ev_maps = nullptr;
     cdr_ctx* geo = nullptr;  // geometry-only context of cdr_self_intersects / cdr_evolve (lazy)
     // Per-context scratch (device memory of this context's GPU): used inside one
     // synchronous entry point at a time, never across calls.

@@ -64,6 +64,7 @@ struct RenderArgs {
     int use_mask;
     int write_hits;
     int64_t lay_diffuse, lay_specular, lay_roughness, lay_light;  // -1 = absent
+    cudaEvent_t wait_before_shade = nullptr;  // joined after the visibility pass, before the shading
 };
 void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a,
                    bool trace, bool loss, bool interior, const double* loss_scales,

@@ -1896,6 +1896,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             launch_trace_kernel(pc, grid, c);
         }
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k + 1], c->stream));
+        if (a.wait_before_shade && k == 0) CDR_CUDA_CHECK(cudaStreamWaitEvent(c->stream, a.wait_before_shade, 0));
         if (queue) {
             if (nq < 0) {
                 CDR_CUDA_CHECK(cudaEventSynchronize(c->tile_queue_ev));
