@@ -705,7 +705,7 @@ __device__ __forceinline__ void trace_item(const Params& p, const ViewCall& vc, 
         const size_t li = th.big >= 0 ? size_t(th.big) * P + pix : tile * P + pix;
         const int cnt = (th.big >= 0 ? p.big_pix_cnt : p.pix_cnt)[li];
         if (cnt != 0) {  // an empty pixel list means no triangle can cover the pixel: no ray needed
-            D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
+            D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, kSPP == 16 ? 4 : p.k, kSPP == 16 ? 0.25 : p.inv_k);
             D3 dir = primary_dir(cam, ps);
             const float fx = float(ps.x - X0), fy = float(ps.y - Y0);
             const BeamCand* cands = p.pool + tl.x;
@@ -715,7 +715,7 @@ __device__ __forceinline__ void trace_item(const Params& p, const ViewCall& vc, 
                                              cnt, p.sc.recs, org, dir, p.info->t_min, fx, fy);
         }
     } else {
-        D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
+        D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, kSPP == 16 ? 4 : p.k, kSPP == 16 ? 0.25 : p.inv_k);
         D3 dir = primary_dir(cam, ps);
         h = trace(p.sc_bin, p.sc.recs, p.sc.n_tris, org, dir, p.info->t_min);
     }
@@ -1019,9 +1019,14 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                     if (s1[j] != 0) atomicAdd(dst + 1, s1[j]);
                 }
         };
+#ifdef CDR_NO_PEEL
+#pragma unroll 1
+        for (int mb = 0; mb == 0 || mb < png; mb += 8) pass(mb);
+#else
         pass(0);  // the common case: <= 8 triangles per warp
 #pragma unroll 1
         for (int mb = 8; mb < png; mb += 8) pass(mb);
+#endif
     }
 #else
     {
@@ -1075,9 +1080,14 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                     if (n0 + 1 < 7 && s1[kq] != 0) atomicAdd(&dst->v[n0 + 1], TexAccT(s1[kq]));
                 }
         };
+#ifdef CDR_NO_PEEL
+#pragma unroll 1
+        for (int mb = 0; mb == 0 || mb < tng; mb += 8) pass(mb);
+#else
         pass(0);  // the common case: <= 8 texel quads per warp
 #pragma unroll 1
         for (int mb = 8; mb < tng; mb += 8) pass(mb);
+#endif
     }
 #else
     {
@@ -1337,7 +1347,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     if (!__syncthreads_or(tri >= 0)) return;
 #endif
     if (tri >= 0) {  // misses need no ray: their radiance is the background
-        D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, p.k, p.inv_k);
+        D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, kSPP == 16 ? 4 : p.k, kSPP == 16 ? 0.25 : p.inv_k);
         dir = primary_dir(cam, ps);
         {
             int a = p.sc.tris[3 * tri], b = p.sc.tris[3 * tri + 1], c = p.sc.tris[3 * tri + 2];

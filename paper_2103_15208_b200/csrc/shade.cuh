@@ -20,6 +20,11 @@ struct ShadeScene {
     double L[3], bg[3];
 };
 
+// the degenerate-normal fallback of shade_hit, out of line (cold)
+static __device__ __noinline__ D3 unit_face_normal(const double* fnormal, int tri) {
+    return normalize(ld3(fnormal + 3 * tri));
+}
+
 __device__ __forceinline__ D3 shade_hit(const ShadeScene& sc, const Hit& h, D3 dir) {
     const double b1 = h.b1, b2 = h.b2;
     const double b0 = 1.0 - b1 - b2;
@@ -32,7 +37,11 @@ __device__ __forceinline__ D3 shade_hit(const ShadeScene& sc, const Hit& h, D3 d
     }
     D3 n = ld3(sc.normals + 3 * va) * b0 + ld3(sc.normals + 3 * vb) * b1 + ld3(sc.normals + 3 * vc) * b2;
     double len = length(n);
+#ifdef CDR_FNORMAL_INLINE
     n = len > 1e-14 ? n / len : normalize(ld3(sc.fnormal + 3 * h.tri));
+#else
+    n = len > 1e-14 ? n / len : unit_face_normal(sc.fnormal, h.tri);
+#endif
     double mu = dot(n, -dir);
     TexSample3 ts = sample_maps(sc.tex, sc.tw, sc.th, uv, false);
     Brdf br = eval_brdf(ts.dv, ts.sv, ts.rv, mu, false);
