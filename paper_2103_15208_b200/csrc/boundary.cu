@@ -445,6 +445,7 @@ __device__ __forceinline__ int boundary_samples(const BParams& p, int vi, const 
             trace_points2(p.beam, vi, cam, p.sc.nodes, p.sc.recs, p.sc.n_tris, xm, dm, xp, dp, t_min, hm, hp);
 #endif
             const D3 bg{p.sc.bg[0], p.sc.bg[1], p.sc.bg[2]};
+            // (one shade_hit call in a loop over the two probes: smaller code, slower at cfg4)
             D3 lo3 = hm.tri >= 0 ? shade_hit(p.sc, hm, dm) : bg;
             D3 hi3 = hp.tri >= 0 ? shade_hit(p.sc, hp, dp) : bg;
             delta = lo3 - hi3;

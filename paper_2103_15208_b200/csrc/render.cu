@@ -709,6 +709,8 @@ __device__ __forceinline__ void trace_item(const Params& p, const ViewCall& vc, 
             D3 dir = primary_dir(cam, ps);
             const float fx = float(ps.x - X0), fy = float(ps.y - Y0);
             const BeamCand* cands = p.pool + tl.x;
+            // (one loop for both, or one trace_item call site for the queue
+            // and grid paths: smaller code, but slower at cfg2; measured)
             h = cnt == 255 ? trace_beam(cands, tl.y, p.sc.recs, org, dir, p.info->t_min, fx, fy)
                            : trace_beam_list(cands,
                                              (th.big >= 0 ? p.big_pix_list + li * kBigPixCap : p.pix_list + li * kPixCap),
@@ -717,7 +719,9 @@ __device__ __forceinline__ void trace_item(const Params& p, const ViewCall& vc, 
     } else {
         D2 ps = pixel_sample_position(vc.h_view, x, y, W, s, spp, kSPP == 16 ? 4 : p.k, kSPP == 16 ? 0.25 : p.inv_k);
         D3 dir = primary_dir(cam, ps);
-        h = trace(p.sc_bin, p.sc.recs, p.sc.n_tris, org, dir, p.info->t_min);
+        // per-ray traversal: the whole pass without lists, or (rare) a tile whose lists overflowed
+        h = kBeam ? trace_out_of_line(p.sc_bin, p.sc.recs, p.sc.n_tris, org, dir, p.info->t_min)
+                  : trace(p.sc_bin, p.sc.recs, p.sc.n_tris, org, dir, p.info->t_min);
     }
     p.hit[pidx * spp + s] = h.tri;
 }
