@@ -361,6 +361,8 @@ void cdr_destroy(cdr_ctx* c) {
     for (auto& e : c->chunk_ev) cudaEventDestroy(e);
     if (c->beam_used_host) cudaFreeHost(c->beam_used_host);
     if (c->tile_queue_host) cudaFreeHost(c->tile_queue_host);
+    if (c->tex_flag_host) cudaFreeHost(c->tex_flag_host);
+    if (c->ev_texflag) cudaEventDestroy(c->ev_texflag);
     if (c->tile_queue_ev) cudaEventDestroy(c->tile_queue_ev);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_sil) cudaEventDestroy(c->ev_sil);

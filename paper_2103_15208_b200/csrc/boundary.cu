@@ -405,6 +405,7 @@ constexpr int kBndBlock = CDR_BND_BLOCK;  // a CTA waits for its slowest warp, y
 // One warp-wide step: sample j (< n_act: active) of view vi, lanes holding
 // consecutive grouped samples. Returns the warp's count of samples with a
 // non-zero contribution (uniform across the warp).
+template <bool kT64>
 __device__ __forceinline__ int boundary_samples(const BParams& p, int vi, const DevCamera& cam, int64_t j, bool act,
                                                 int lane) {
     // the RNG pick and lower_bound were done in pass 1: read the grouped result
@@ -446,8 +447,8 @@ __device__ __forceinline__ int boundary_samples(const BParams& p, int vi, const 
 #endif
             const D3 bg{p.sc.bg[0], p.sc.bg[1], p.sc.bg[2]};
             // (one shade_hit call in a loop over the two probes: smaller code, slower at cfg4)
-            D3 lo3 = hm.tri >= 0 ? shade_hit(p.sc, hm, dm) : bg;
-            D3 hi3 = hp.tri >= 0 ? shade_hit(p.sc, hp, dp) : bg;
+            D3 lo3 = hm.tri >= 0 ? shade_hit<kT64>(p.sc, hm, dm) : bg;
+            D3 hi3 = hp.tri >= 0 ? shade_hit<kT64>(p.sc, hp, dp) : bg;
             delta = lo3 - hi3;
         } else {
             D3 org{cam.o[0], cam.o[1], cam.o[2]};
@@ -493,6 +494,7 @@ __device__ __forceinline__ int boundary_samples(const BParams& p, int vi, const 
     return na;
 }
 
+template <bool kT64>
 __global__ void __launch_bounds__(kBndBlock, CDR_BOUNDARY_MIN_BLOCKS * 256 / kBndBlock) k_boundary(BParams p) {
     const int vi = blockIdx.y;
     const int lane = threadIdx.x & 31;
@@ -500,12 +502,13 @@ __global__ void __launch_bounds__(kBndBlock, CDR_BOUNDARY_MIN_BLOCKS * 256 / kBn
     const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
     const int n_act = p.n_active[vi];
     if (int64_t(blockIdx.x) * blockDim.x >= n_act) return;  // whole CTA idle (uniform)
-    const int na = boundary_samples(p, vi, cam, j, j < n_act, lane);
+    const int na = boundary_samples<kT64>(p, vi, cam, j, j < n_act, lane);
     if (lane == 0 && na) atomicAdd(&p.counters->boundary_active, (unsigned long long)na);
 }
 
 // cdr_probe_points: point pairs (2i, 2i+1) through trace_points2, the odd last
 // point through trace_point, then shade_hit / background as the probes do.
+template <bool kT64>
 __global__ void k_probe_points(ShadeScene sc, const SceneInfo* __restrict__ info, DevCamera cam, BeamView bv,
                                int vi, int n, const double* __restrict__ xy, double* __restrict__ rgb,
                                int32_t* __restrict__ tri) {
@@ -531,7 +534,7 @@ __global__ void k_probe_points(ShadeScene sc, const SceneInfo* __restrict__ info
         const Hit& h = k == 0 ? ha : hb;
         if (tri) tri[j] = h.tri;
         if (rgb) {
-            const D3 r = h.tri >= 0 ? shade_hit(sc, h, k == 0 ? da : db) : bg;
+            const D3 r = h.tri >= 0 ? shade_hit<kT64>(sc, h, k == 0 ? da : db) : bg;
             rgb[3 * j] = r.x;
             rgb[3 * j + 1] = r.y;
             rgb[3 * j + 2] = r.z;
@@ -684,13 +687,20 @@ void launch_boundary_sampling(cdr_ctx* c, int n_views, int samples, uint64_t see
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
+static void launch_k_boundary(cdr_ctx* c, dim3 bgrid, const BParams& p) {
+    tex64_resolve(c);
+    ++c->launches;
+    if (c->tex64_on) k_boundary<true><<<bgrid, kBndBlock, 0, c->stream>>>(p);
+    else k_boundary<false><<<bgrid, kBndBlock, 0, c->stream>>>(p);
+}
+
 void launch_boundary_probes(cdr_ctx* c, int n_views, int samples, uint64_t seed, int probe, int64_t lay_pos,
                             bool use_beam) {
     if (n_views <= 0 || samples <= 0) return;
     upload_pix_off(c);
     BParams p = boundary_params(c, n_views, samples, seed, probe, lay_pos, use_beam);
     dim3 bgrid((samples + kBndBlock - 1) / kBndBlock, n_views);
-    { ++c->launches; k_boundary<<<bgrid, kBndBlock, 0, c->stream>>>(p); }
+    launch_k_boundary(c, bgrid, p);
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -705,7 +715,7 @@ void launch_boundary(cdr_ctx* c, int n_views, int samples, uint64_t seed, int pr
     { ++c->launches; k_bscan<<<n_views, 1024, 0, c->stream>>>(p.seg_count, p.count, p.E, p.seg_off, p.n_active); }
     { ++c->launches; k_bscatter<<<grid, kBlock, 0, c->stream>>>(p); }
     dim3 bgrid((samples + kBndBlock - 1) / kBndBlock, n_views);
-    { ++c->launches; k_boundary<<<bgrid, kBndBlock, 0, c->stream>>>(p); }
+    launch_k_boundary(c, bgrid, p);
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -713,9 +723,14 @@ void launch_probe_points(cdr_ctx* c, int vi, int n, const double* xy, double* rg
     if (n <= 0) return;
     const int pairs = (n + 1) / 2;
     const DevCamera cam = c->views[c->beam_slots[vi]].cam;
+    tex64_resolve(c);
     ++c->launches;
-    k_probe_points<<<(pairs + 127) / 128, 128, 0, c->stream>>>(shade_scene(c), c->info.p, cam, c->beam_view, vi, n,
-                                                               xy, rgb, tri);
+    if (c->tex64_on)
+        k_probe_points<true><<<(pairs + 127) / 128, 128, 0, c->stream>>>(shade_scene(c), c->info.p, cam, c->beam_view,
+                                                                         vi, n, xy, rgb, tri);
+    else
+        k_probe_points<false><<<(pairs + 127) / 128, 128, 0, c->stream>>>(shade_scene(c), c->info.p, cam,
+                                                                          c->beam_view, vi, n, xy, rgb, tri);
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -165,7 +165,13 @@ struct cdr_ctx {
 
     // materials, light
     int tw = 0, th = 0;
-    cdr::DBuf<cdr::Texel> tex;
+    cdr::DBuf<cdr::Texel> tex;      // fp32 texel records (maps on the fp32 grid)
+    cdr::DBuf<cdr::Texel64> tex64;  // fp64 texel records (any maps)
+    cdr::DBuf<int> tex_flag;        // k_pack_textures: 1 = some value off the fp32 grid
+    int* tex_flag_host = nullptr;   // pinned copy of it
+    cudaEvent_t ev_texflag = nullptr;
+    bool tex_flag_pending = false;  // the copy is in flight: tex64_resolve reads it
+    bool tex64_on = false;          // shading kernels read tex64
     cdr::DBuf<double> map_d, map_s, map_r;  // fp64 maps, resident (the regularisers read them)
     cdr::DBuf<double> reg_part, reg_lum, reg_stats, reg_vals, reg_grad;
     double light[3] = {1, 1, 1};

@@ -20,6 +20,7 @@ inline ShadeScene shade_scene(const cdr_ctx* c) {
     sc.normals = c->normals.p;
     sc.fnormal = c->fnormal.p;
     sc.tex = c->tex.p;
+    sc.tex64 = c->tex64.p;
     sc.tw = c->tw;
     sc.th = c->th;
     for (int i = 0; i < 3; ++i) {
@@ -117,6 +118,7 @@ void launch_texel_flush(cdr_ctx* c, int64_t lay_d, int64_t lay_s, int64_t lay_r)
 void launch_radiance_points(cdr_ctx* c, int slot, int n, const double* xy, double* rgb, int32_t* tri);
 // pack diffuse/specular/roughness (fp64, device) into 32-byte fp32 texel records
 void launch_pack_textures(cdr_ctx* c, const double* d, const double* s, const double* r, int n);
+void tex64_resolve(cdr_ctx* c);  // the texel record choice of the last packed maps (host)
 
 void launch_view_loss(cdr_ctx* c, int W, int H, const double* rendered, const double* target,
                       const double* tmask, double scale, double gamma, int masked, double* adj,

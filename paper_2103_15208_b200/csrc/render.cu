@@ -848,7 +848,7 @@ __device__ __forceinline__ int group_ids(bool act, unsigned peers, int lane, uns
 // scatter scalars this way was slower at cfg4: 16 KB per CTA shrinks L1.
 constexpr int kTexState = 4;
 
-template <int kRT>
+template <int kRT, bool kT64>
 __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x, int y, int spp, int tri, double t,
                                               double b1, double b2, D3 dir, D3 a, bool act,
                                               double (&s_ts)[kTexState][kRT], double (&s_ray)[5][kRT],
@@ -902,7 +902,9 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             }
             const double du1 = uv1.x - uv0.x, dv1 = uv1.y - uv0.y, du2 = uv2.x - uv0.x, dv2 = uv2.y - uv0.y;
             const double dn1 = dot(hv, N1) - dot(hv, N0), dn2 = dot(hv, N2) - dot(hv, N0);
-            TexSample3 ts = sample_maps(p.sc.tex, p.sc.tw, p.sc.th, uv, true);
+            TexSample3 ts;
+            if constexpr (kT64) ts = sample_maps(p.sc.tex64, p.sc.tw, p.sc.th, uv, true);
+            else ts = sample_maps(p.sc.tex, p.sc.tw, p.sc.th, uv, true);
             Brdf br = eval_brdf_grad(ts.dv, ts.sv, ts.rv, mu);
             const double inv_r2 = rcp(t * t);
             const double Lc[3] = {p.sc.L[0], p.sc.L[1], p.sc.L[2]};
@@ -1268,7 +1270,7 @@ __global__ void __launch_bounds__(256) k_background(Params p) {
 
 // kQ: the queue-mode instance (CTAs from the tile queue; no empty-tile path,
 // so the hot instance carries no dead code for the instruction cache)
-template <bool kShade, bool kLoss, bool kInterior, int kSPP, bool kQ = false>
+template <bool kShade, bool kLoss, bool kInterior, int kSPP, bool kQ = false, bool kT64 = false>
 __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
                                   kSPP == 16 ? CDR_RENDER_CTAS16
                                              : CDR_RENDER_MIN_BLOCKS) k_render(Params p) {
@@ -1361,7 +1363,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     }
     if (kShade) {
         D3 rad{p.sc.bg[0], p.sc.bg[1], p.sc.bg[2]};
-        if (tri >= 0) rad = shade_hit(p.sc, Hit{tri, t, b1, b2}, dir);
+        if (tri >= 0) rad = shade_hit<kT64>(p.sc, Hit{tri, t, b1, b2}, dir);
         s_rad[tid][0] = rad.x;
         s_rad[tid][1] = rad.y;
         s_rad[tid][2] = rad.z;
@@ -1445,7 +1447,7 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
 
     // ---------------- phase 3: interior adjoint scatter
     if constexpr (kInterior) {
-        if (__any_sync(0xffffffffu, act)) interior_scatter<kRT>(p, tid, x, y, spp, tri, t, b1, b2, dir, a, act, s_ts, s_ray, s_rad);
+        if (__any_sync(0xffffffffu, act)) interior_scatter<kRT, kT64>(p, tid, x, y, spp, tri, t, b1, b2, dir, a, act, s_ts, s_ray, s_rad);
     }
 
     // ---------------- publish the CTA's tallies (warp 0 waits for the others)
@@ -1520,6 +1522,7 @@ __global__ void k_view_loss(int n, const double* __restrict__ r, const double* _
     if ((threadIdx.x & 31) == 0 && part != 0) atomicAdd(sum, part);
 }
 
+template <bool kT64>
 __global__ void k_radiance_points(ShadeScene sc, const SceneInfo* __restrict__ info,
                                   const DevCamera* __restrict__ cams, int slot, int n,
                                   const double* __restrict__ xy, double* __restrict__ rgb,
@@ -1527,36 +1530,77 @@ __global__ void k_radiance_points(ShadeScene sc, const SceneInfo* __restrict__ i
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int t = -1;
-    D3 r = radiance_at(sc, cams[slot], D2{xy[2 * i], xy[2 * i + 1]}, info->t_min, &t);
+    D3 r = radiance_at<kT64>(sc, cams[slot], D2{xy[2 * i], xy[2 * i + 1]}, info->t_min, &t);
     rgb[3 * i] = r.x;
     rgb[3 * i + 1] = r.y;
     rgb[3 * i + 2] = r.z;
     if (tri) tri[i] = t;
 }
 
+// Both texel records, and flag = 1 if any map value is off the fp32 grid
+// (then the shading kernels read the fp64 records: images stay bit-exact).
 __global__ void k_pack_textures(const double* __restrict__ d, const double* __restrict__ s,
-                                const double* __restrict__ r, int n, Texel* __restrict__ out) {
+                                const double* __restrict__ r, int n, Texel* __restrict__ out,
+                                Texel64* __restrict__ out64, int* __restrict__ flag) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    Texel t;
-    t.a = make_float4(float(d[3 * i]), float(d[3 * i + 1]), float(d[3 * i + 2]), float(s[3 * i]));
-    t.b = make_float4(float(s[3 * i + 1]), float(s[3 * i + 2]), float(r[i]), 0.0f);
-    out[i] = t;
+    bool off = false;
+    if (i < n) {
+        const double v[7] = {d[3 * i], d[3 * i + 1], d[3 * i + 2], s[3 * i], s[3 * i + 1], s[3 * i + 2], r[i]};
+        Texel t;
+        t.a = make_float4(float(v[0]), float(v[1]), float(v[2]), float(v[3]));
+        t.b = make_float4(float(v[4]), float(v[5]), float(v[6]), 0.0f);
+        out[i] = t;
+        Texel64 q;
+        q.a0 = make_double2(v[0], v[1]);
+        q.a1 = make_double2(v[2], v[3]);
+        q.b0 = make_double2(v[4], v[5]);
+        q.b1 = make_double2(v[6], 0.0);
+        out64[i] = q;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) off |= double(float(v[k])) != v[k] && v[k] == v[k];  // NaN: either record
+    }
+    if (__any_sync(0xffffffffu, off) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
 }  // namespace
 
 void launch_radiance_points(cdr_ctx* c, int slot, int n, const double* xy, double* rgb, int32_t* tri) {
     if (n <= 0) return;
-    { ++c->launches; k_radiance_points<<<(n + 255) / 256, 256, 0, c->stream>>>(shade_scene(c), c->info.p, c->d_cams.p, slot, n,
-                                                              xy, rgb, tri); }
+    tex64_resolve(c);
+    ++c->launches;
+    if (c->tex64_on)
+        k_radiance_points<true><<<(n + 255) / 256, 256, 0, c->stream>>>(shade_scene(c), c->info.p, c->d_cams.p, slot, n,
+                                                                        xy, rgb, tri);
+    else
+        k_radiance_points<false><<<(n + 255) / 256, 256, 0, c->stream>>>(shade_scene(c), c->info.p, c->d_cams.p, slot,
+                                                                         n, xy, rgb, tri);
     CDR_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_pack_textures(cdr_ctx* c, const double* d, const double* s, const double* r, int n) {
     if (n <= 0) return;
-    { ++c->launches; k_pack_textures<<<(n + 255) / 256, 256, 0, c->stream>>>(d, s, r, n, c->tex.p); }
+    c->tex64.ensure(size_t(n));
+    c->tex_flag.ensure(1);
+    if (!c->tex_flag_host) CDR_CUDA_CHECK(cudaHostAlloc(&c->tex_flag_host, sizeof(int), cudaHostAllocDefault));
+    CDR_CUDA_CHECK(cudaMemsetAsync(c->tex_flag.p, 0, sizeof(int), c->stream));
+    ++c->launches;
+    k_pack_textures<<<(n + 255) / 256, 256, 0, c->stream>>>(d, s, r, n, c->tex.p, c->tex64.p, c->tex_flag.p);
     CDR_CUDA_CHECK(cudaGetLastError());
+    CDR_CUDA_CHECK(cudaMemcpyAsync(c->tex_flag_host, c->tex_flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (!c->ev_texflag) CDR_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_texflag, cudaEventDisableTiming));
+    CDR_CUDA_CHECK(cudaEventRecord(c->ev_texflag, c->stream));
+    c->tex_flag_pending = true;
+}
+
+// The record choice of the last packed maps, on the host, before the first
+// launch that shades (waits for the flag's copy if it is still in flight:
+// a staged upload finishes long before the shading is launched).
+// CDR_TEXEL_F64 forces the fp64 records.
+void tex64_resolve(cdr_ctx* c) {
+    if (!c->tex_flag_pending) return;
+    CDR_CUDA_CHECK(cudaEventSynchronize(c->ev_texflag));
+    c->tex64_on = *c->tex_flag_host != 0 || std::getenv("CDR_TEXEL_F64") != nullptr;
+    c->tex_flag_pending = false;
 }
 
 void launch_widen(cdr_ctx* c, const float* in, int64_t n, double* out) {
@@ -1611,19 +1655,25 @@ static RenderStatics& statics(cdr_ctx* c) {  // owned by the context (free_rende
     return *static_cast<RenderStatics*>(c->render_statics);
 }
 
-template <int kSPP>
-static void launch_render_kernel_t(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
+template <int kSPP, bool kT64>
+static void launch_render_kernel_tt(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
     constexpr int bs = kSPP == 16 ? kRenderThreads16 : kThreads;
     if (trace && loss && interior)
-        k_render<true, true, true, kSPP><<<grid, bs, 0, c->stream>>>(p);
+        k_render<true, true, true, kSPP, false, kT64><<<grid, bs, 0, c->stream>>>(p);
     else if (trace && !loss && !interior)
-        k_render<true, false, false, kSPP><<<grid, bs, 0, c->stream>>>(p);
+        k_render<true, false, false, kSPP, false, kT64><<<grid, bs, 0, c->stream>>>(p);
     else if (!trace && !loss && interior)
-        k_render<false, false, true, kSPP><<<grid, bs, 0, c->stream>>>(p);
+        k_render<false, false, true, kSPP, false, kT64><<<grid, bs, 0, c->stream>>>(p);
     else if (trace && loss && !interior)
-        k_render<true, true, false, kSPP><<<grid, bs, 0, c->stream>>>(p);
+        k_render<true, true, false, kSPP, false, kT64><<<grid, bs, 0, c->stream>>>(p);
     else
         throw std::runtime_error("unsupported render mode");
+}
+
+template <int kSPP>
+static void launch_render_kernel_t(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
+    if (c->tex64_on) launch_render_kernel_tt<kSPP, true>(p, grid, c, trace, loss, interior);
+    else launch_render_kernel_tt<kSPP, false>(p, grid, c, trace, loss, interior);
 }
 
 static void launch_render_kernel(const Params& p, dim3 grid, cdr_ctx* c, bool trace, bool loss, bool interior) {
@@ -1911,6 +1961,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         }
         if (timed) CDR_CUDA_CHECK(cudaEventRecord(c->chunk_ev[2 * k + 1], c->stream));
         if (a.wait_before_shade && k == 0) CDR_CUDA_CHECK(cudaStreamWaitEvent(c->stream, a.wait_before_shade, 0));
+        tex64_resolve(c);  // fp32 or fp64 texel records for the shading kernels
         if (queue) {
             if (nq < 0) {
                 CDR_CUDA_CHECK(cudaEventSynchronize(c->tile_queue_ev));
@@ -1922,8 +1973,12 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             if (nq > 0) {
                 ++c->launches;
                 const dim3 qgrid(unsigned(nq) * kCPT, 1, 1);
-                if (interior)
+                if (interior && c->tex64_on)
+                    k_render<true, true, true, 16, true, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
+                else if (interior)
                     k_render<true, true, true, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
+                else if (c->tex64_on)
+                    k_render<true, true, false, 16, true, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
                 else
                     k_render<true, true, false, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
             }

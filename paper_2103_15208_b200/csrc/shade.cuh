@@ -15,7 +15,8 @@ struct ShadeScene {
     const double* uv;  // nullptr: uvs absent -> uv = (0, 0)
     const double* normals;
     const double* fnormal;
-    const Texel* tex;
+    const Texel* tex;      // fp32 records (maps on the fp32 grid)
+    const Texel64* tex64;  // fp64 records (any maps); kernels pick one at compile time (kT64)
     int tw, th;
     double L[3], bg[3];
 };
@@ -25,6 +26,7 @@ static __device__ __noinline__ D3 unit_face_normal(const double* fnormal, int tr
     return normalize(ld3(fnormal + 3 * tri));
 }
 
+template <bool kT64>
 __device__ __forceinline__ D3 shade_hit(const ShadeScene& sc, const Hit& h, D3 dir) {
     const double b1 = h.b1, b2 = h.b2;
     const double b0 = 1.0 - b1 - b2;
@@ -43,19 +45,22 @@ __device__ __forceinline__ D3 shade_hit(const ShadeScene& sc, const Hit& h, D3 d
     n = len > 1e-14 ? n / len : unit_face_normal(sc.fnormal, h.tri);
 #endif
     double mu = dot(n, -dir);
-    TexSample3 ts = sample_maps(sc.tex, sc.tw, sc.th, uv, false);
+    TexSample3 ts;
+    if constexpr (kT64) ts = sample_maps(sc.tex64, sc.tw, sc.th, uv, false);
+    else ts = sample_maps(sc.tex, sc.tw, sc.th, uv, false);
     Brdf br = eval_brdf(ts.dv, ts.sv, ts.rv, mu, false);
     return hadamard(D3{sc.L[0], sc.L[1], sc.L[2]}, br.value) / (h.t * h.t);
 }
 
 // radiance_at for a continuous pixel position (render.cpp:24-33)
+template <bool kT64>
 __device__ __forceinline__ D3 radiance_at(const ShadeScene& sc, const DevCamera& cam, D2 x,
                                           double t_min, int* tri_out) {
     D3 dir = primary_dir(cam, x);
     Hit h = trace(sc.nodes, sc.recs, sc.n_tris, D3{cam.o[0], cam.o[1], cam.o[2]}, dir, t_min);
     if (tri_out) *tri_out = h.tri;
     if (h.tri < 0) return D3{sc.bg[0], sc.bg[1], sc.bg[2]};
-    return shade_hit(sc, h, dir);
+    return shade_hit<kT64>(sc, h, dir);
 }
 
 }  // namespace cdr
