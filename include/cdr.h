@@ -298,6 +298,13 @@ int cdr_lbvh_keys(cdr_ctx* ctx, uint64_t* keys_out, int32_t n);
  * buffers (either may be NULL). */
 int cdr_get_rendered(cdr_ctx* ctx, int32_t view, double* rgb_out, double* mask_out);
 
+/* Page-locked host memory (cudaHostAlloc) for the caller's per-iteration
+ * buffers: the loss calls overlap their downloads into such buffers with the
+ * boundary pass, and cdr_stage_params' uploads with the visibility pass.
+ * (new; the drop-in shim stages total_loss's rendered images in one.) */
+int cdr_host_alloc(size_t bytes, void** out);
+void cdr_host_free(void* p);
+
 /* self_intersects (mesh.hpp:67, mesh.cpp:184-214) on an arbitrary mesh (it
  * need not be the context's render mesh, nor manifold): result = 1 iff two
  * triangles sharing no vertex overlap (triangles_intersect, tol 1e-10). With

@@ -105,6 +105,20 @@ struct Device {
     uint64_t view_key = 0;
     std::vector<int32_t> tris, edges;
     std::vector<double> buf;
+    double* pin = nullptr;  // page-locked staging of total_loss's rendered images (cdr_host_alloc)
+    size_t pin_n = 0;
+    double* staging(size_t n) {
+        if (n > pin_n) {
+            cdr_host_free(pin);
+            pin = nullptr;
+            pin_n = 0;
+            void* p = nullptr;
+            check(cdr_host_alloc(n * sizeof(double), &p));
+            pin = static_cast<double*>(p);
+            pin_n = n;
+        }
+        return pin;
+    }
 
     explicit Device(int device) {
         if (cdr_abi_version() != CDR_ABI_VERSION)  // cdr_stats and friends follow the header's layout
@@ -626,6 +640,7 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
     const int32_t lap_mode = options.laplacian_mode == LaplacianMode::Uniform ? CDR_LAPLACIAN_UNIFORM
                                                                                : CDR_LAPLACIAN_COTANGENT;
     const bool single = g.devs.size() == 1;
+    const bool want_rendered = !std::getenv("CDR_SKIP_RENDERED");
     std::vector<std::array<double, 7>> bd(g.devs.size(), std::array<double, 7>{});
     std::vector<std::vector<double>> part(single || g.nccl ? 0 : g.devs.size());
     std::vector<std::exception_ptr> err(g.devs.size());
@@ -648,9 +663,21 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
                 part[k].assign(res.grad.values.size(), 0.0);
                 gout = part[k].data();
             }
+            // the rendered images come down into page-locked staging during
+            // the call (beside its boundary pass); the Images are filled below
+            double *srgb = nullptr, *smask = nullptr;
+            if (want_rendered) {
+                size_t npx = 0;
+                for (int i = 0; i < n; ++i) {
+                    const Camera& c = scene.views[single ? i : size_t(gids[k][i])];
+                    npx += size_t(c.width) * c.height;
+                }
+                srgb = d.staging(4 * npx);
+                smask = srgb + 3 * npx;
+            }
             ShimTimer t2(2);
             d.check(cdr_total_loss(d.ctx, slots.data(), n, &st, weights.rend, weights.lap, &reg, lap_mode,
-                                   options.use_target_masks ? 1 : 0, &lay, bd[k].data(), gout, nullptr, nullptr,
+                                   options.use_target_masks ? 1 : 0, &lay, bd[k].data(), gout, srgb, smask,
                                    nullptr));
         } catch (...) {
             err[k] = std::current_exception();
@@ -682,20 +709,39 @@ TotalLossResult total_loss(const Scene& scene, const std::vector<Image>& targets
     res.breakdown.edge = t[4];
     res.breakdown.spec = t[5];
     res.breakdown.roug = t[6];
-    if (!std::getenv("CDR_SKIP_RENDERED")) {  // straight from the device arenas into the returned images
+    if (want_rendered) {  // the Images from the staging buffers, views spread over host threads
         ShimTimer t3(3);
-        res.rendered.reserve(scene.views.size());
+        std::vector<const double*> src(K);
+        std::vector<size_t> off(g.devs.size(), 0), tot(g.devs.size(), 0);
         for (int v = 0; v < K; ++v) {
             const size_t k = single ? 0 : size_t(v / per);
-            const int slot = single ? v : v - int(k) * per;
-            const Camera& c = scene.views[v];
-            std::optional<ShimTimer> t6(std::in_place, 6);
-            Image img(c.width, c.height, true);
-            t6.reset();
-            Device& d = *g.devs[k];
-            d.check(cdr_get_rendered(d.ctx, slot, reinterpret_cast<double*>(img.pixels.data()), img.mask.data()));
-            res.rendered.push_back(std::move(img));
+            tot[k] += size_t(scene.views[v].width) * scene.views[v].height;
         }
+        for (int v = 0; v < K; ++v) {
+            const size_t k = single ? 0 : size_t(v / per);
+            src[v] = g.devs[k]->pin + 3 * off[k];
+            off[k] += size_t(scene.views[v].width) * scene.views[v].height;
+        }
+        std::vector<std::optional<Image>> imgs(K);
+        auto fill = [&](int t, int nt) {
+            for (int v = t; v < K; v += nt) {
+                const size_t k = single ? 0 : size_t(v / per);
+                const Camera& c = scene.views[v];
+                const size_t np = size_t(c.width) * c.height;
+                imgs[v].emplace(c.width, c.height, true);
+                std::memcpy(imgs[v]->pixels.data(), src[v], sizeof(double) * 3 * np);
+                // the masks follow the rgb blocks of this device's views
+                const double* m = g.devs[k]->pin + 3 * tot[k] + (src[v] - g.devs[k]->pin) / 3;
+                std::memcpy(imgs[v]->mask.data(), m, sizeof(double) * np);
+            }
+        };
+        const int nt = std::max(1, std::min<int>(K, int(std::thread::hardware_concurrency())));
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) th.emplace_back(fill, t, nt);
+        fill(0, nt);
+        for (auto& t : th) t.join();
+        res.rendered.reserve(K);
+        for (auto& im : imgs) res.rendered.push_back(std::move(*im));
     }
     return res;
 }

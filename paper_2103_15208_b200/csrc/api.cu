@@ -1323,6 +1323,21 @@ int cdr_get_rendered(cdr_ctx* c, int32_t view, double* rgb, double* mask) {
     API_END
 }
 
+int cdr_host_alloc(size_t bytes, void** out) {
+    if (!out) return CDR_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return CDR_ERR_CUDA;
+    }
+    return CDR_OK;
+}
+
+void cdr_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 namespace {
 // The geometry-only context (lazy): an arbitrary mesh for the query entry
 // points, its LBVH built; the render mesh stays untouched. The topology is
