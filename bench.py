@@ -424,18 +424,21 @@ def main(argv=None):
             "storage_frac": stored_bytes / (ms_shade / 1e3) / 1e9 / pk["hbm_gbs"],
             "ms_per_launch": ms_shade, "share_of_step": ms_shade / statistics.mean(ms_steps)}
     # DRAM traffic of the same kernel at THIS config, from the committed ncu
-    # capture of one iteration (profiles/profile_step.py, profiles/r2/per_kernel_<cfg>.json);
+    # capture of this step (profiles/profile_step.py --bench-step,
+    # profiles/r2/per_kernel_<cfg>_step.json);
     # configs without a capture report null rather than a scaled figure
-    traffic_file = os.path.join(ROOT, "profiles", "r2", f"per_kernel_{args.config}.json")
+    traffic_file = os.path.join(ROOT, "profiles", "r2", f"per_kernel_{args.config}_step.json")
     roof["traffic"] = None
     roof["traffic_source"] = f"no ncu capture of {args.config}"
     if os.path.exists(traffic_file) and args.views is None and world == 1:
         try:
             kern = json.load(open(traffic_file))["kernels"]
-            kr = next(v for k, v in kern.items() if k.startswith("k_render<1, 1, 1"))
+            # the step's fused instance (fp32 texel records: synthetic maps)
+            kr = max((v for k, v in kern.items() if k.startswith("k_render<1, 1, 1,") and k.endswith(", 0>")),
+                     key=lambda v: v["ms"])
             roof["traffic"] = 1e6 * (kr["dram_read_MB"] + kr["dram_write_MB"])
-            roof["traffic_source"] = (f"ncu dram__bytes_read.sum + dram__bytes_write.sum of k_render<1,1,1,16> at "
-                                      f"{args.config}, {os.path.relpath(traffic_file, ROOT)}")
+            roof["traffic_source"] = (f"ncu dram__bytes_read.sum + dram__bytes_write.sum of the fused k_render "
+                                      f"in this step at {args.config}, {os.path.relpath(traffic_file, ROOT)}")
             # what HBM actually moved per launch, over this run's kernel time: the
             # algorithmic fraction above is served mostly from L2 (mesh, BVH, maps)
             roof["dram_GBps"] = roof["traffic"] / (ms_shade / 1e3) / 1e9

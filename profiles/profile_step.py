@@ -23,6 +23,9 @@ def main():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--views", type=int, default=None)
     ap.add_argument("--loss-only", action="store_true", help="bracket only the loss call")
+    ap.add_argument("--bench-step", action="store_true",
+                    help="bracket bench.py's timed step instead: cdr_loss_grad over the synthetic maps "
+                         "(fp32 texel records), no regularisers, no optimiser step")
     a = ap.parse_args()
     import torch
     import bench
@@ -42,6 +45,17 @@ def main():
     diag = float(np.linalg.norm(np.ptp(scene.mesh.positions, axis=0)))
     r.adam_init(api.AdamConfig(lr_positions=1e-3 * diag), lay)
     lw = api.LossWeights()
+
+    if a.bench_step:
+        r.loss_grad(views, st, lay, device_only=True)  # warm-up
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        _, _, stats, _ = r.loss_grad(views, st, lay, device_only=True)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        print({"config": a.config, "views": len(views), "bench_step": True, "launches": stats.kernel_launches})
+        r.close()
+        return
 
     def iteration():
         bd, stats = r.total_loss_device(views, st, lay, lw)
