@@ -77,21 +77,20 @@ def test_drop_in_demo_matches_reference():
     """The reference's unmodified run_coarse_to_fine, linked against the shim,
     against the reference alone: the first total_loss breakdown and the loss
     after the optimisation steps. The demo's constant maps (0.6, 0.45, ...)
-    are not fp32-representable and the GPU keeps texels as fp32 records
-    (SURVEY §8(d)), so the rendering term agrees to ~1e-8, not bit for bit;
-    the mesh terms are exact."""
+    are not fp32-representable, so the GPU shades from its fp64 texel
+    records: every term agrees to the order of fp64 atomic sums (~1e-15;
+    round 1's fp32 records left the rendering term at ~1e-8)."""
     args = "2 64 4 2 3 32"  # views image spp iters subdiv tex
     ref = _demo(_need("demo_ref"), args)
     b200 = _demo(_need("demo_b200"), args)
     for k in ("lap0", "edge0", "normal0"):
         assert b200[k] == pytest.approx(ref[k], rel=1e-12, abs=1e-300), k
     for k in ("loss0", "rend0", "spec0", "roug0"):
-        assert b200[k] == pytest.approx(ref[k], rel=1e-6, abs=1e-12), k
+        assert b200[k] == pytest.approx(ref[k], rel=1e-12, abs=1e-300), k
     assert b200["iterations"] == ref["iterations"] == 2
-    # after the steps only loosely: Adam's first update is ~lr * sign(g), so
-    # gradients that cancel to ~0 can flip sign on a 1e-8 perturbation (as
-    # between the reference's own thread counts, whose merge order differs)
-    assert b200["loss_last"] == pytest.approx(ref["loss_last"], rel=1e-2)
+    # after the Adam steps too (a gradient that cancels to ~0 could still
+    # flip sign on the atomic-order noise, hence not bit-level)
+    assert b200["loss_last"] == pytest.approx(ref["loss_last"], rel=1e-9)
     assert b200["tris_final"] == ref["tris_final"]
 
 
@@ -112,10 +111,13 @@ def test_drop_in_demo_coarse_to_fine_stages():
     for k in ("lap0", "edge0", "normal0"):
         assert b200[k] == pytest.approx(ref[k], rel=1e-12, abs=1e-300), k
     for k in ("loss0", "rend0", "spec0", "roug0"):
-        assert b200[k] == pytest.approx(ref[k], rel=1e-6, abs=1e-12), k
-    # remeshed twice: the final topology follows the same remesh decisions
-    assert b200["tris_final"] == pytest.approx(ref["tris_final"], rel=0.02)
-    assert b200["loss_last"] == pytest.approx(ref["loss_last"], rel=5e-2)
+        assert b200[k] == pytest.approx(ref[k], rel=1e-12, abs=1e-300), k
+    # remeshed twice: the same remesh decisions and final topology; the final
+    # loss to 1e-6 (the remeshes and uv_transfer amplify the ~1e-15 sum-order
+    # noise of six steps: measured 1.2e-8 on this small plan, 4e-15 on the
+    # 81,920-tri profile run, profiles/r2/demo_*_stages3.json)
+    assert b200["tris_final"] == ref["tris_final"]
+    assert b200["loss_last"] == pytest.approx(ref["loss_last"], rel=1e-6)
 
 
 @pytest.mark.gpu
