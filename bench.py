@@ -446,6 +446,30 @@ def main(argv=None):
         except Exception as e:  # noqa: BLE001
             roof["traffic_source"] = f"unreadable capture: {e}"
 
+    # the boundary stage against the same roofline: SURVEY §8(d)'s 970 B per
+    # active boundary sample (segment record, CDF search, adjoint, two probe
+    # shadings, vertex RMW) over the stage's event-timed window. The window
+    # holds the probes and deposits (k_boundary); the sampling kernels
+    # (k_bsample / k_bscan / k_bscatter) run on the side stream beside the
+    # render, so `frac` is an upper bound and `frac_serial` adds their
+    # serialised ncu time from this config's step capture when there is one.
+    ms_bnd_stage = statistics.mean(x["ms_boundary"] for x in stats)
+    bnd_bytes = 970 * s0["boundary_active"]
+    bnd = {"kernel": "k_boundary (probes + deposits)", "bound": "hbm", "unit": "GB/s",
+           "bytes_per_active_sample": 970, "active_samples": s0["boundary_active"],
+           "algorithmic_bytes": bnd_bytes, "ms": ms_bnd_stage,
+           "achieved": bnd_bytes / (ms_bnd_stage / 1e3) / 1e9 if ms_bnd_stage > 0 else None,
+           "peak": pk["hbm_gbs"]}
+    bnd["frac"] = bnd["achieved"] / pk["hbm_gbs"] if bnd["achieved"] else None
+    try:
+        kern = json.load(open(traffic_file))["kernels"] if os.path.exists(traffic_file) else {}
+        ms_samp = sum(kern[k]["ms"] for k in ("k_bsample", "k_bscan", "k_bscatter") if k in kern)
+        if ms_samp > 0 and args.views is None and world == 1:
+            bnd["ms_sampling_serial"] = ms_samp
+            bnd["frac_serial"] = bnd_bytes / ((ms_bnd_stage + ms_samp) / 1e3) / 1e9 / pk["hbm_gbs"]
+    except Exception:  # noqa: BLE001
+        pass
+
     # traversal throughput (latency-bound, reported as Mrays/s):
     # primary rays = samples of non-empty beam tiles (k_tile_lists + k_trace),
     # boundary probe rays = 2 per active edge sample (k_bsample..k_boundary)
@@ -600,7 +624,7 @@ def main(argv=None):
                            "views_per_gpu": len(scene.cameras), "spp": spp,
                            "samples_per_step": samples_all, "parallelism": f"views sharded x{world}",
                            "l2": "flushed (256 MB write) before every timed step; step working set ~2 GB"},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "regularisers": regs, "iteration": iteration,
+                "roofline": roof, "boundary_roofline": bnd, "cpu_baseline": cpu, "e2e": e2e, "regularisers": regs, "iteration": iteration,
                 "traversal": traversal,
                 "gpu_launches": int(sum(x["kernel_launches"] for x in stats)),
                 "clocks": clk, "stages_ms": stages,
