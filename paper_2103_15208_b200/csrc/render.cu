@@ -1025,14 +1025,9 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                     if (s1[j] != 0) atomicAdd(dst + 1, s1[j]);
                 }
         };
-#ifdef CDR_NO_PEEL
-#pragma unroll 1
-        for (int mb = 0; mb == 0 || mb < png; mb += 8) pass(mb);
-#else
         pass(0);  // the common case: <= 8 triangles per warp
 #pragma unroll 1
         for (int mb = 8; mb < png; mb += 8) pass(mb);
-#endif
     }
 #else
     {
@@ -1086,14 +1081,9 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
                     if (n0 + 1 < 7 && s1[kq] != 0) atomicAdd(&dst->v[n0 + 1], TexAccT(s1[kq]));
                 }
         };
-#ifdef CDR_NO_PEEL
-#pragma unroll 1
-        for (int mb = 0; mb == 0 || mb < tng; mb += 8) pass(mb);
-#else
         pass(0);  // the common case: <= 8 texel quads per warp
 #pragma unroll 1
         for (int mb = 8; mb < tng; mb += 8) pass(mb);
-#endif
     }
 #else
     {

@@ -39,11 +39,7 @@ __device__ __forceinline__ D3 shade_hit(const ShadeScene& sc, const Hit& h, D3 d
     }
     D3 n = ld3(sc.normals + 3 * va) * b0 + ld3(sc.normals + 3 * vb) * b1 + ld3(sc.normals + 3 * vc) * b2;
     double len = length(n);
-#ifdef CDR_FNORMAL_INLINE
-    n = len > 1e-14 ? n / len : normalize(ld3(sc.fnormal + 3 * h.tri));
-#else
     n = len > 1e-14 ? n / len : unit_face_normal(sc.fnormal, h.tri);
-#endif
     double mu = dot(n, -dir);
     TexSample3 ts;
     if constexpr (kT64) ts = sample_maps(sc.tex64, sc.tw, sc.th, uv, false);
