@@ -395,7 +395,7 @@ __global__ void k_bscatter(BParams p) {
 // pass 4: the two radiance probes and the vertex deposit, in segment order so a
 // warp traces neighbouring rays along one silhouette edge (diff_render.cpp:246-277)
 #ifndef CDR_BOUNDARY_MIN_BLOCKS
-#define CDR_BOUNDARY_MIN_BLOCKS 4  // 8 x 128-thread CTAs / SM, 64 regs: cfg4 boundary 37.7 -> 35.6 ms vs 5, cfg2 equal
+#define CDR_BOUNDARY_MIN_BLOCKS 5  // 5 x 256-thread CTAs / SM, 48 regs: cfg4 boundary 17.41 -> 16.54 ms vs 4 (3, 6, 7 slower)
 #endif
 #ifndef CDR_BND_BLOCK
 #define CDR_BND_BLOCK 256  // 4 x 256-thread CTAs per SM: boundary cfg2 4.05 -> 3.90 ms vs 128, cfg4 35.6 -> 35.2
