@@ -1,5 +1,5 @@
 // Bit-exactness of the shared-reciprocal fp64 division (common.cuh,
-// operator/(D3, double)) against the compiler's `/`: random numerators and
+// operator/(D3, double)) and of div_pi (x / pi) against the compiler's `/`: random numerators and
 // divisors over and around its fast-path range [2^-500, 2^501) (outside it the
 // operator takes the plain divisions), plus exact and near-1 quotients.
 // Built and run by tests/test_division_exact.py.
@@ -34,12 +34,13 @@ __global__ void k(uint64_t seed, long long n, int emin, int emax, unsigned long 
         if ((h1 & 0xff) == 1) b = 1.0 + double(h2 & 0xffff) * 0x1p-52;       // near-1 divisors
         if ((h1 & 0xff) == 2) a.y = 0.0;                                      // a zero numerator
         const D3 q = a / b;
-        const double r[3] = {a.x / b, a.y / b, a.z / b}, g[3] = {q.x, q.y, q.z};
-        for (int c = 0; c < 3; ++c)
+        const double r[4] = {a.x / b, a.y / b, a.z / b, a.x / cdr::kPiD};
+        const double g[4] = {q.x, q.y, q.z, cdr::div_pi(a.x)};
+        for (int c = 0; c < 4; ++c)
             if (__double_as_longlong(g[c]) != __double_as_longlong(r[c]) && !(r[c] != r[c] && g[c] != g[c])) {
                 if (atomicAdd(bad, 1ull) == 0) {
-                    ex[0] = c == 0 ? a.x : (c == 1 ? a.y : a.z);
-                    ex[1] = b;
+                    ex[0] = c == 0 || c == 3 ? a.x : (c == 1 ? a.y : a.z);
+                    ex[1] = c == 3 ? cdr::kPiD : b;
                     ex[2] = g[c];
                     ex[3] = r[c];
                 }
@@ -61,7 +62,7 @@ int main(int argc, char** argv) {
             printf("CUDA error\n");
             return 2;
         }
-        printf("range [2^%d, 2^%d]: %lld x 3 quotients, %llu differ", ranges[t][0], ranges[t][1], n, *bad);
+        printf("range [2^%d, 2^%d]: %lld x 4 quotients, %llu differ", ranges[t][0], ranges[t][1], n, *bad);
         if (*bad) printf(" (e.g. %a / %a = %a, '/' gives %a)", ex[0], ex[1], ex[2], ex[3]);
         printf("\n");
         total += *bad;
