@@ -430,7 +430,9 @@ __device__ __forceinline__ int boundary_samples(const BParams& p, int vi, const 
     D2 n2{0, 0};
     if (act) {
         const cdr_segment* sg = b.sg;
-        D2 tg{(sg->q1[0] - sg->q0[0]) / sg->length_px, (sg->q1[1] - sg->q0[1]) / sg->length_px};
+        // the two quotients with one reciprocal (common.cuh operator/(D3, double): bit-identical)
+        const D3 tq = D3{sg->q1[0] - sg->q0[0], sg->q1[1] - sg->q0[1], 1.0} / sg->length_px;
+        D2 tg{tq.x, tq.y};
         n2 = D2{-tg.y, tg.x};
         D2 xm{b.xq.x - n2.x * 0.5, b.xq.y - n2.y * 0.5}, xp{b.xq.x + n2.x * 0.5, b.xq.y + n2.y * 0.5};
         const double t_min = p.info->t_min;
