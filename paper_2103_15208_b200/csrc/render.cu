@@ -791,7 +791,7 @@ __device__ __forceinline__ void mma_f64_8x8x4(double& d0, double& d1, double a, 
 }
 
 #ifndef CDR_MMA_UNROLL
-#define CDR_MMA_UNROLL 8
+#define CDR_MMA_UNROLL 2  // k-steps per unrolled body: 2 measured best (cfg2 shading 10.76 -> 10.55 ms, cfg4 23.45 -> 22.75; 1, 4, 8 slower)
 #endif
 constexpr int kMmaUnroll = CDR_MMA_UNROLL;  // k-steps per unrolled body (code size vs loop overhead)
 
