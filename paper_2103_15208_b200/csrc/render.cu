@@ -859,6 +859,7 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
     // (texture sample, BRDF partials, vertex data) are dead before the
     // warp-aggregation loops; only a compact state crosses them.
     int tex0 = 0;           // texel quad key (texel[0] determines all four)
+    int tcol = 0, trow = 0;  // its column and row (the scatter's addresses without a division)
     double wd0 = 0, ws0 = 0, wr0 = 0;  // d_diffuse/r^2, d_specular/r^2, Σ a L d_rough / r^2
     double aL[3] = {0, 0, 0};
     double lv[3] = {0, 0, 0};          // light gradient (diff_render.cpp:129-131)
@@ -910,6 +911,8 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
             const double Lc[3] = {p.sc.L[0], p.sc.L[1], p.sc.L[2]};
             const double ac[3] = {a.x, a.y, a.z};
             tex0 = ts.texel[0];
+            tcol = ts.x0;
+            trow = ts.y0;
             for (int k = 0; k < 4; ++k) s_ts[k][tid] = ts.w[k];
             wd0 = br.d_diffuse * inv_r2;
             ws0 = br.d_specular * inv_r2;
@@ -1067,8 +1070,8 @@ __device__ __forceinline__ void interior_scatter(const Params& p, int tid, int x
         auto tw4 = [&](int kq, int src) { return s_ts[kq][w32 + src]; };  // bilinear weight of corner kq
         auto pass = [&](int mb) {
             const int g = mb + gm;
-            const int ltex = __shfl_sync(0xffffffffu, tex0, g < tng ? __fns(tleaders, 0, g + 1) : 0);
-            const int x0 = ltex % tw, y0 = ltex / tw;
+            const int lsrc = g < tng ? __fns(tleaders, 0, g + 1) : 0;  // the group's leader lane
+            const int x0 = __shfl_sync(0xffffffffu, tcol, lsrc), y0 = __shfl_sync(0xffffffffu, trow, lsrc);
             const int x1 = x0 + 1 == tw ? 0 : x0 + 1, y1 = y0 + 1 == th ? 0 : y0 + 1;
             double s0[4], s1[4];
             group_sum_mma<7, 4, kRT>(s_rad, s_ray, w32, u, tgid, lane, tw4, s0, s1, mb, mb == 0);
