@@ -362,6 +362,9 @@ void cdr_destroy(cdr_ctx* c) {
     if (c->beam_used_host) cudaFreeHost(c->beam_used_host);
     if (c->tile_queue_host) cudaFreeHost(c->tile_queue_host);
     if (c->tex_flag_host) cudaFreeHost(c->tex_flag_host);
+    if (c->queue_starts_host) cudaFreeHost(c->queue_starts_host);
+    for (auto& e : c->img_ev)
+        if (e) cudaEventDestroy(e);
     if (c->ev_texflag) cudaEventDestroy(c->ev_texflag);
     if (c->tile_queue_ev) cudaEventDestroy(c->tile_queue_ev);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -1024,6 +1027,14 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
     }
     RenderArgs a = render_args(c, st, lay);
     a.use_mask = use_mask;
+    // page-locked image destinations: downloaded on the copy stream, group by
+    // group during the shading when the call runs in queue mode, else after it
+    const bool out_images = (rendered_rgb || rendered_mask) && (!rendered_rgb || is_pinned(rendered_rgb)) &&
+                            (!rendered_mask || is_pinned(rendered_mask));
+    if (out_images) {
+        a.img_rgb_host = rendered_rgb;
+        a.img_mask_host = rendered_mask;
+    }
     stage.emplace("cdr.render (lists, trace, shade+loss+interior)");
     if (maps_pending) {  // the list builders and k_trace read no texel: join just before the shading
         a.wait_before_shade = c->ev_maps;
@@ -1033,9 +1044,7 @@ static void loss_grad_impl(cdr_ctx* c, const int32_t* views, int32_t n, const cd
     // Downloads that need only the render run on the copy stream beside the
     // boundary pass: the K images, then (one rank, overwrite) the map and
     // light segments of the gradient once the texel flush has written them.
-    const bool out_images = (rendered_rgb || rendered_mask) && (!rendered_rgb || is_pinned(rendered_rgb)) &&
-                            (!rendered_mask || is_pinned(rendered_mask));
-    if (out_images) {
+    if (out_images && !c->images_downloaded) {
         CDR_CUDA_CHECK(cudaEventRecord(c->ev_copy, s));
         CDR_CUDA_CHECK(cudaStreamWaitEvent(c->copy, c->ev_copy, 0));
         size_t ro = 0, mo = 0;

@@ -96,6 +96,11 @@ struct cdr_ctx {
     } staged;
     cudaStream_t copy = nullptr;
     cudaEvent_t ev_copy = nullptr, ev_maps = nullptr;
+    cudaEvent_t img_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // per shading group (launch_render)
+    cdr::DBuf<int> queue_starts;           // per call: first tile-queue entry
+    int* queue_starts_host = nullptr;      // pinned copy of it
+    int queue_starts_cap = 0;
+    bool images_downloaded = false;        // the last launch_render downloaded its images itself
     cdr_ctx* geo = nullptr;  // geometry-only context of cdr_self_intersects / cdr_evolve (lazy)
     // Per-context scratch (device memory of this context's GPU): used inside one
     // synchronous entry point at a time, never across calls.

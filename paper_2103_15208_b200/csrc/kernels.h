@@ -66,6 +66,12 @@ struct RenderArgs {
     int write_hits;
     int64_t lay_diffuse, lay_specular, lay_roughness, lay_light;  // -1 = absent
     cudaEvent_t wait_before_shade = nullptr;  // joined after the visibility pass, before the shading
+    // page-locked destinations of the call's images and masks (views in call
+    // order): a queue-mode call shades view group by view group and downloads
+    // each group's images on the copy stream while the next group shades
+    // (sets c->images_downloaded)
+    double* img_rgb_host = nullptr;
+    double* img_mask_host = nullptr;
 };
 void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderArgs& a,
                    bool trace, bool loss, bool interior, const double* loss_scales,

@@ -87,6 +87,7 @@ struct Params {
     int* tile_queue_count;
     int queue_mode;  // k_render: CTAs from tile_queue instead of the full tile grid
     int queue_len;   // its length (host-read)
+    int queue_off;   // k_render: CTA offset into the queue (a launch over a range of it)
     int* top_nodes;  // k_top_walk's output: per 2 x 2 block, [count, <= kTopCap frontier nodes]
     int top_stride;  // blocks per view slot in top_nodes
 };
@@ -1225,6 +1226,21 @@ __global__ void __launch_bounds__(256) k_queue_write(Params p, int n, int n_call
     }
 }
 
+// starts[v] = the first queue entry of call v (the queue is in tile order, so
+// call-major): the shading can then be launched view group by view group
+__global__ void k_queue_view_starts(const int2* __restrict__ queue, const int* __restrict__ total, int n_calls,
+                                    int* __restrict__ starts) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v > n_calls) return;
+    int lo = 0, hi = *total;  // lower_bound of v over queue[].x
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (queue[mid].x < v) lo = mid + 1;
+        else hi = mid;
+    }
+    starts[v] = lo;
+}
+
 // The pixels of empty beam tiles in a queue-mode loss call (spp 16): no
 // triangle can cover them, so every sample misses (k_trace wrote no hits) and
 // the pixel is the background mean, mask 0, with its loss and adjoint — the
@@ -1282,11 +1298,12 @@ __global__ void __launch_bounds__(kSPP == 16 ? kRenderThreads16 : kThreads,
     int cx = int(blockIdx.x), cy = int(blockIdx.y), cz = int(blockIdx.z);
     if (kQ) {  // CTA = (non-empty tile, pixel-row group) from the tile queue
         constexpr int kCPT = 4 / (kRT / 64);  // CTAs per 4 x 4 tile
-        const int2 e = p.tile_queue[int(blockIdx.x) / kCPT];
+        const int it = int(blockIdx.x) + p.queue_off;
+        const int2 e = p.tile_queue[it / kCPT];
         cz = e.x;
         const int tiles_x = p.calls[cz].tiles_x;
         cx = e.y % tiles_x;
-        cy = (e.y / tiles_x) * kCPT + int(blockIdx.x) % kCPT;
+        cy = (e.y / tiles_x) * kCPT + it % kCPT;
     }
     const ViewCall vc = p.calls[cz];
     const DevCamera& cam = p.cams[vc.slot];
@@ -1853,6 +1870,21 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     // prologue of ~2/3 (cfg2) to ~9/10 (cfg4) of the shading CTAs.
     const bool queue = p.skip_empty_hits && n_chunks == 1 && !std::getenv("CDR_NO_QUEUE");
     const bool bg_side = c->bg && !std::getenv("CDR_BG_INLINE");  // CDR_BG_INLINE: k_background after k_render
+    // shading in view groups with the images downloaded group by group (the
+    // empty tiles' pixels come from k_background on the bg stream, which each
+    // download waits for)
+    const bool grouped = queue && bg_side && (a.img_rgb_host || a.img_mask_host) && !std::getenv("CDR_NO_IMG_OVERLAP");
+    c->images_downloaded = false;
+    if (grouped) {
+        c->queue_starts.ensure(size_t(n_views) + 1);
+        if (c->queue_starts_cap < n_views + 1) {
+            if (c->queue_starts_host) CDR_CUDA_CHECK(cudaFreeHost(c->queue_starts_host));
+            CDR_CUDA_CHECK(cudaHostAlloc(&c->queue_starts_host, sizeof(int) * (n_views + 1), cudaHostAllocDefault));
+            c->queue_starts_cap = n_views + 1;
+        }
+        for (auto& e : c->img_ev)
+            if (!e) CDR_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     if (queue) {
         c->tile_queue.ensure(std::max(1, tile_total));
         c->tile_queue_count.ensure(1 + (tile_total + kQBlock - 1) / kQBlock);  // [0] total, then per-block offsets
@@ -1914,6 +1946,13 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             k_queue_count<<<nb, 256, 0, c->stream>>>(pc.tile_hdr, tile_total, blk);
             k_queue_scan<<<1, 1024, 0, c->stream>>>(blk, nb, pc.tile_queue_count);
             k_queue_write<<<nb, 256, 0, c->stream>>>(pc, tile_total, nv, blk);
+            if (grouped) {
+                ++c->launches;
+                k_queue_view_starts<<<(nv + 1 + 127) / 128, 128, 0, c->stream>>>(pc.tile_queue, pc.tile_queue_count, nv,
+                                                                                 c->queue_starts.p);
+                CDR_CUDA_CHECK(cudaMemcpyAsync(c->queue_starts_host, c->queue_starts.p, sizeof(int) * (nv + 1),
+                                               cudaMemcpyDeviceToHost, c->stream));
+            }
             CDR_CUDA_CHECK(cudaMemcpyAsync(c->tile_queue_host, p.tile_queue_count, sizeof(int), cudaMemcpyDeviceToHost,
                                            c->stream));
             CDR_CUDA_CHECK(cudaEventRecord(c->tile_queue_ev, c->stream));
@@ -1963,17 +2002,50 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
             c->queue_frac_last = double(nq) / double(std::max(1, tile_total));
             pc.queue_mode = 1;
             constexpr int kCPT = 4 / (kRenderThreads16 / 64);
-            if (nq > 0) {
+            auto shade = [&](int q0, int q1) {  // the queue range [q0, q1)
+                if (q1 <= q0) return;
                 ++c->launches;
-                const dim3 qgrid(unsigned(nq) * kCPT, 1, 1);
+                Params pq = pc;
+                pq.queue_off = q0 * kCPT;
+                const dim3 qgrid(unsigned(q1 - q0) * kCPT, 1, 1);
                 if (interior && c->tex64_on)
-                    k_render<true, true, true, 16, true, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
+                    k_render<true, true, true, 16, true, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pq);
                 else if (interior)
-                    k_render<true, true, true, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
+                    k_render<true, true, true, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pq);
                 else if (c->tex64_on)
-                    k_render<true, true, false, 16, true, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
+                    k_render<true, true, false, 16, true, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pq);
                 else
-                    k_render<true, true, false, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pc);
+                    k_render<true, true, false, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pq);
+            };
+            if (grouped && n_chunks == 1) {
+                // up to 4 view groups: each group's images come down on the copy
+                // stream while the next group shades (and the last one during
+                // the boundary pass of a loss call)
+                const int* qs = c->queue_starts_host;
+                const int G = std::min(4, nv);
+                size_t ro = 0, mo = 0;
+                for (int g = 0; g < G; ++g) {
+                    const int va = g * nv / G, vb = (g + 1) * nv / G;
+                    shade(qs[va], qs[vb]);
+                    CDR_CUDA_CHECK(cudaEventRecord(c->img_ev[g], c->stream));
+                    CDR_CUDA_CHECK(cudaStreamWaitEvent(c->copy, c->img_ev[g], 0));
+                    CDR_CUDA_CHECK(cudaStreamWaitEvent(c->copy, c->ev_bg, 0));  // the empty tiles' pixels
+                    for (int v = va; v < vb; ++v) {
+                        const ViewData& vd = c->views[view_slots[v]];
+                        const size_t np = size_t(vd.cam.W) * vd.cam.H;
+                        if (a.img_rgb_host)
+                            CDR_CUDA_CHECK(cudaMemcpyAsync(a.img_rgb_host + ro, c->img.p + 3 * vd.pix_off,
+                                                           sizeof(double) * 3 * np, cudaMemcpyDeviceToHost, c->copy));
+                        if (a.img_mask_host)
+                            CDR_CUDA_CHECK(cudaMemcpyAsync(a.img_mask_host + mo, c->mask.p + vd.pix_off,
+                                                           sizeof(double) * np, cudaMemcpyDeviceToHost, c->copy));
+                        ro += 3 * np;
+                        mo += np;
+                    }
+                }
+                c->images_downloaded = true;
+            } else {
+                shade(0, nq);
             }
             if (!bg_side) {
                 ++c->launches;

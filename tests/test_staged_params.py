@@ -158,3 +158,30 @@ def test_staged_params_cleared_on_error():
     with pytest.raises(ValueError):
         r.stage_params(None, (d, None, ro))
     r.close()
+
+
+@pytest.mark.parametrize("nviews", [1, 3, 5])
+def test_grouped_shading_image_downloads(nviews):
+    """Queue-mode loss calls (spp 16) with page-locked image destinations
+    shade in up to four view groups and download each group's images and
+    masks while the next group shades: the same images, masks, loss and
+    gradient as with pageable destinations (downloaded after the call)."""
+    sc = S.make_scene(S.blob(3), 32, nviews, 48)
+    lay = api.param_layout(sc)
+    views = np.arange(nviews, dtype=np.int32)
+    st = RenderSettings(spp=16, seed=7)
+    npx = sum(c.width * c.height for c in sc.cameras)
+    a, b = _renderer(sc), _renderer(sc)
+    for _ in range(2):  # the second call runs with the sizes of the first (queue mode either way)
+        rga, mka = np.zeros(3 * npx), np.zeros(npx)
+        la, ga, _, _ = a.loss_grad(views, st, lay, overwrite=True, rendered_out=rga, mask_out=mka)
+        rgb, mkb, gb = _pinned(3 * npx), _pinned(npx), _pinned(lay["total"])
+        rgb[:] = np.nan
+        mkb[:] = np.nan
+        lb, _, _, _ = b.loss_grad(views, st, lay, grad=gb, overwrite=True, rendered_out=rgb, mask_out=mkb)
+        np.testing.assert_array_equal(rgb, rga)
+        np.testing.assert_array_equal(mkb, mka)
+        np.testing.assert_allclose(lb, la, rtol=1e-13)
+        np.testing.assert_allclose(gb, ga, rtol=1e-12, atol=1e-300)
+    a.close()
+    b.close()
