@@ -96,7 +96,7 @@ struct cdr_ctx {
     } staged;
     cudaStream_t copy = nullptr;
     cudaEvent_t ev_copy = nullptr, ev_maps = nullptr;
-    cudaEvent_t img_ev[4] = {nullptr, nullptr, nullptr, nullptr};  // per shading group (launch_render)
+    cudaEvent_t img_ev[16] = {};  // per shading group (launch_render)
     cdr::DBuf<int> queue_starts;           // per call: first tile-queue entry
     int* queue_starts_host = nullptr;      // pinned copy of it
     int queue_starts_cap = 0;

@@ -2018,11 +2018,12 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
                     k_render<true, true, false, 16, true><<<qgrid, kRenderThreads16, 0, c->stream>>>(pq);
             };
             if (grouped && n_chunks == 1) {
-                // up to 4 view groups: each group's images come down on the copy
-                // stream while the next group shades (and the last one during
-                // the boundary pass of a loss call)
+                // up to 16 view groups (CDR_IMG_GROUPS; 2 / 4 / 8 measured slower):
+                // each group's images come down on the copy stream while the
+                // next group shades (and the last one during the boundary pass)
                 const int* qs = c->queue_starts_host;
-                const int G = std::min(4, nv);
+                static const int kGroups = std::getenv("CDR_IMG_GROUPS") ? std::max(1, std::min(16, std::atoi(std::getenv("CDR_IMG_GROUPS")))) : 16;
+                const int G = std::min(kGroups, nv);
                 size_t ro = 0, mo = 0;
                 for (int g = 0; g < G; ++g) {
                     const int va = g * nv / G, vb = (g + 1) * nv / G;

@@ -163,7 +163,7 @@ def test_staged_params_cleared_on_error():
 @pytest.mark.parametrize("nviews", [1, 3, 5])
 def test_grouped_shading_image_downloads(nviews):
     """Queue-mode loss calls (spp 16) with page-locked image destinations
-    shade in up to four view groups and download each group's images and
+    shade in up to 16 view groups and download each group's images and
     masks while the next group shades: the same images, masks, loss and
     gradient as with pageable destinations (downloaded after the call)."""
     sc = S.make_scene(S.blob(3), 32, nviews, 48)
