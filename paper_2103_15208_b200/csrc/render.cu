@@ -15,6 +15,9 @@
 // group is summed with log-depth shuffles, and one lane issues the atomics.
 // The one-ring normal chain is deferred: per-corner sums of coeff_mu*b_j*h feed
 // the finalize kernels (finalize.cu), which apply it once per iteration.
+#include <chrono>
+#include <cstdio>
+
 #include "kernels.h"
 #include "beam.cuh"
 #include "shade.cuh"
@@ -1807,7 +1810,17 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
         // candidate pool sized from the previous call's use (overflowing tiles
         // fall back to per-ray traversal, so the size only affects speed)
         size_t want = std::max<size_t>(size_t(tile_total) * 24, size_t(c->beam_used_last) * 3 / 2 + 1024);
-        if (c->beam_pool.n < want) c->beam_pool.ensure(want);
+        if (c->beam_pool.n < want) {
+            // geometric growth: the use creeps up as an optimisation moves
+            // the mesh, and every reallocation (free + malloc of ~GB) stalls
+            // the call (measured up to ~0.9 s)
+            want = std::max(want, c->beam_pool.n + c->beam_pool.n / 2);
+            const auto t0 = std::chrono::steady_clock::now();
+            c->beam_pool.ensure(want);
+            if (std::getenv("CDR_DEBUG_ALLOC"))
+                std::fprintf(stderr, "[cdr] beam pool -> %zu candidates (%.1f MB) in %.1f ms\n", want, want * 32.0 / 1e6,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        }
         c->beam_hdr.ensure(std::max(1, tile_total));
         c->beam_used.ensure(1);
         CDR_CUDA_CHECK(cudaMemsetAsync(c->beam_used.p, 0, sizeof(int), c->stream));
