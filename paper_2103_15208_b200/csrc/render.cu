@@ -44,6 +44,7 @@ struct Params {
     double inv_k;
     uint64_t seed;
     double gamma;
+    double inv_gamma;  // 1 / gamma (host)
     int use_mask, write_hits;
     int skip_empty_hits;  // loss calls at spp 16: no hit-cache writes for empty beam tiles (k_render skips them too)
     double* img;
@@ -1143,11 +1144,12 @@ __device__ __forceinline__ double pixel_loss_adjoint(const Params& p, const View
     double a = 0;
     if (m != 0) {
         // Φ'(r) = Φ(r) / (γ r) for r in (0, 1); Φ(0) = pow(0, 1/γ) = +0 exactly: skip pow on background
-        const double tr = mean <= 0.0 ? 0.0 : tone_map(mean, p.gamma);
+        const double tr = mean <= 0.0 ? 0.0 : tone_map_inv(mean, p.inv_gamma);
         const double d = tr - p.target_tone[3 * qi + c];
         loss_part += m * fabs(d);
         const double sg = double((d > 0) - (d < 0));
-        const double der = (mean <= 0.0 || mean >= 1.0) ? 0.0 : tr / (p.gamma * mean);
+        // the adjoint path (tolerance, as the interior pass): a reciprocal
+        const double der = (mean <= 0.0 || mean >= 1.0) ? 0.0 : tr * rcp(p.gamma * mean);
         a = vc.scale * m * sg * der;
     }
     p.adj[3 * qi + c] = a;
@@ -1773,6 +1775,7 @@ void launch_render(cdr_ctx* c, const int* view_slots, int n_views, const RenderA
     p.sc_bin = c->nodes.p;
     p.seed = a.seed;
     p.gamma = a.gamma;
+    p.inv_gamma = 1.0 / a.gamma;
     p.use_mask = a.use_mask;
     p.write_hits = a.write_hits;
     p.img = c->img.p;
