@@ -153,6 +153,8 @@ struct cdr_ctx {
     cdr::DBuf<int> beam_tile_base;
     cdr::DBuf<int2> beam_big_queue;  // tiles rebuilt with the big candidate cap
     cdr::DBuf<int> beam_top;         // k_top_walk: per tile block, the shared top frontier
+    cdr::DBuf<int2> beam_blk_queue;  // k_top_walk: the non-empty tile blocks (the list builder's queue)
+    cdr::DBuf<int> beam_blk_count;
     cdr::DBuf<int> beam_big_count;   // [0] big queue, [1] split queue
     cdr::DBuf<int4> beam_split_queue;  // split work items (levels 0 and 1)
     cdr::DBuf<int2> beam_split_hdr;    // groups of 4 quadrant lists

@@ -373,6 +373,38 @@ def test_big_tile_lists_exact(sphere, monkeypatch, fast_cap, big_cap, split_cap)
     _loss_grad_check(sphere, 16, 2, param_layout(sphere))
 
 
+@pytest.mark.parametrize("fast_cap", [None, "3"])
+def test_block_queue_lists_exact(monkeypatch, fast_cap):
+    """The list builder over k_top_walk's queue of non-empty 2 x 2 tile blocks
+    (the empty blocks' tiles written by k_top_walk itself), with and without
+    tiles forced through the big pass: hit caches, images, the loss call and
+    the probes through its lists exact."""
+    monkeypatch.setenv("CDR_BLOCK_QUEUE", "1")
+    if fast_cap is not None:
+        monkeypatch.setenv("CDR_BEAM_FAST_CAP", fast_cap)
+    sc = blob_scene(freq=8, tex=16, views=2, image=64)
+    r, o = _pair(sc)
+    for spp in (4, 16):
+        st = RenderSettings(spp=spp, seed=8)
+        for v in range(len(sc.cameras)):
+            rgb, mask, hit = r.render(v, st)
+            ro, mo, ho = o.render(v, spp, 8)
+            np.testing.assert_array_equal(hit, ho)
+            np.testing.assert_array_equal(rgb, ro)
+    _loss_grad_check(sc, 16, 8, param_layout(sc))
+    tg = targets_for(sc, 16, 8, Oracle)
+    for k in range(len(sc.cameras)):
+        r.set_target(k, tg[k])
+    r.loss_grad(np.arange(len(sc.cameras)), RenderSettings(spp=16, seed=8), param_layout(sc))
+    rng = np.random.default_rng(17)
+    for v in range(len(sc.cameras)):
+        xy = _silhouette_probe_points(o, v, rng)
+        cg, tgp = r.probe_points(v, xy)
+        co, to = o.radiance_at(v, xy)
+        np.testing.assert_array_equal(tgp, to)
+        np.testing.assert_array_equal(cg, co)
+
+
 @pytest.mark.parametrize("wh", [(37, 29), (29, 37)])
 def test_odd_image_sizes_exact(wh):
     """Partial tiles at the right and bottom edges, odd tile counts (the 2x2
@@ -396,7 +428,7 @@ def test_odd_image_sizes_exact(wh):
 
 @pytest.mark.parametrize("knob", ["CDR_NO_BEAM", "CDR_CHUNK_MB", "CDR_NO_SHARED_TOP", "CDR_NO_SPLIT", "CDR_NO_QUEUE",
                                   "CDR_NO_HUGE", "CDR_NO_TOP_PREPASS",
-                                  "CDR_TRACE_QUEUE", "CDR_NO_TRACE_QUEUE"])
+                                  "CDR_TRACE_QUEUE", "CDR_NO_TRACE_QUEUE", "CDR_BLOCK_QUEUE", "CDR_NO_BLOCK_QUEUE"])
 def test_alternate_paths_exact(sphere, monkeypatch, knob):
     """The A/B switches kept in the code (per-ray traversal only; view chunks
     through lists -> trace -> shade; every tile from the BVH root) stay exact."""
