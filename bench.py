@@ -21,7 +21,9 @@ silhouettes + boundary edge sampling, normal chain, cotangent Laplacian.
           three texture maps uploaded from pinned memory and the gradient
           downloaded every step (wall clock around the blocking C-ABI calls:
           cdr_stage_params + cdr_loss_grad, which overlaps the copies with its
-          kernels; e2e.separate_uploads = synchronous uploads before the call);
+          kernels; e2e.separate_uploads = synchronous uploads before the call;
+          no L2 flush between e2e steps, so with the copies hidden e2e can
+          exceed the L2-flushed device value);
           e2e.with_rendered_images adds total_loss's K rendered images + masks
           (TotalLossResult::rendered, losses.cpp:259) to the download.
   cpu_baseline : the reference library compiled from its own sources
